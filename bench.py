@@ -1,0 +1,311 @@
+"""bench.py -- SOR voxel-updates/s of the 4D SUBSURF time step on B200.
+
+Contract:
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config config1]
+
+A *step* is one semi-implicit time step of segment() (solver.cpp:428-438):
+assemble_step + red-black SOR to relative residual 1e-8 + local_rescale, on
+BASELINE config 1 (64^4, two moving blobs; the largest config that is quoted
+for 1 GPU).  value = interior doxels x completed red+black sweeps / device time
+of the K timed steps (all ranks summed), inputs resident in HBM.  e2e = the same
+metric through the public session API with the step's input u copied H2D from
+pinned host memory and the result u copied D2H inside the timed region.
+
+--impl reference times the UNMODIFIED reference CPU solver (oracle/_ref, built
+from /root/reference/proj/src) through its own public calls on the same
+workload, on the host cores (rank 0 only under torchrun).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SOR voxel-updates/s (4D grid, red+black sweep = 1 update/doxel)"
+UNIT = "voxel-updates/s"
+SURVEY_BYTES_PER_SWEEP = 56.0  # 8 fp32 coeff + rhs + u read + u write
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline_sample(wl, sweeps=40):
+    """The reference's own redblack_sor (oracle/_ref) on the workload's grid, all host
+    threads it can use (it parallelises over l only): `sweeps` red-black sweeps of the
+    first time step's system (assemble_step at u0 with G == 1), timed around
+    redblack_sor; the reference throws SolverError at max_iter, caught as intended."""
+    from oracle import oracle_py as op
+    if not op.ref_available():
+        return None
+    R = op.ref()
+    g = op.Grid.make(wl.dims, wl.h)
+    workers = min(R.lib.ref_hardware_threads(), wl.dims[3])
+    st, off, _, _ = R.assemble_step(g, wl.u0, None, wl.params["tau"], wl.params["epsilon"], workers)
+    t0 = time.perf_counter()
+    st, u, it, res = R.redblack_sor(g, off, wl.u0, wl.u0, wl.params["omega"], 1e-300, sweeps, workers)
+    dt = time.perf_counter() - t0
+    return {"value": wl.n_interior * it / dt, "unit": UNIT, "cores": workers, "kind": "reference",
+            "sample": f"{it} red-black sweeps of redblack_sor on the {wl.dims} system "
+                      f"(oracle/_ref = unmodified reference, {workers} std::thread workers), {dt:.2f} s"}
+
+
+def run_reference(args, wl):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    from oracle import oracle_py as op
+    base = {"metric": METRIC, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl.name, "dims": list(wl.dims), "sor_rel_tol": 1e-8,
+                       "omega": wl.params["omega"]}}
+    if not op.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
+        return 0
+    R = op.ref()
+    g = op.Grid.make(wl.dims, wl.h)
+    workers = min(R.lib.ref_hardware_threads(), wl.dims[3])
+    n = args.warmup + args.steps
+    p = op.seg_params(**{**wl.params, "n_steps": n})
+    t0 = time.perf_counter()
+    st, u, info = R.segment(g, wl.image, wl.rows, p, wl.u0, workers)
+    wall = time.perf_counter() - t0
+    if st != 0:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference segment failed: {R.lib.ref_last_error()}"}))
+        return 0
+    its = [d["iterations"] for d in info["diags"]][args.warmup:]
+    secs = info["step_seconds"][args.warmup:]
+    value = wl.n_interior * sum(its) / sum(secs)
+    line = dict(base)
+    line.update({
+        "value": value, "ms_per_step": 1e3 * sum(secs) / len(secs), "vs_baseline": None,
+        "sor_iterations": its,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
+                         "sample": f"time steps {args.warmup + 1}..{n} of segment() on {wl.dims} "
+                                   f"(setup {info['times'][0]:.1f} s untimed; total wall {wall:.1f} s)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    })
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="config1")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--loop-mode", type=int, default=1)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    import workloads
+    wl = workloads.CONFIGS[args.config]()
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import paper_2111_11866_b200 as ss
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+
+    g = ss.Grid.make(wl.dims, wl.h)
+    p = ss.seg_params(**{**wl.params, "n_steps": args.warmup + args.steps})
+    sess = ss.Session(g, device=local)
+    sess.set_loop_mode(args.loop_mode)
+    stream = torch.cuda.ExternalStream(sess.stream, device=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- value: device-resident steps
+    sess.prepare(wl.image, wl.rows, p, wl.u0)
+    for _ in range(args.warmup):
+        sess.step_nodiag()
+    sess.profile()  # reset counters
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    l0 = ss.launch_count()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            sess.step_nodiag()
+        e1.record(stream)
+        e1.synchronize()
+    launches = ss.launch_count() - l0
+    barrier()
+    ms = e0.elapsed_time(e1)
+    prof = sess.profile()
+    sweeps = prof["sweeps"]
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * wl.n_interior * sweeps / (ms_max * 1e-3)
+
+    # ---------------- e2e: same steps through the public API with host buffers
+    P = g.padded_size()
+    host_in = torch.empty(P, dtype=torch.float64, pin_memory=True)
+    host_out = torch.empty(P, dtype=torch.float64, pin_memory=True)
+    sess.prepare(wl.image, wl.rows, p, wl.u0)
+    for _ in range(args.warmup):
+        sess.step_nodiag()
+    sess.get_u_ptr(host_in.data_ptr())
+    sess.profile()
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        sess.set_u_ptr(host_in.data_ptr())     # H2D of the step's input u^{n-1}
+        sess.step_nodiag()
+        sess.get_u_ptr(host_out.data_ptr())    # D2H of the step's result u^n
+        host_in, host_out = host_out, host_in
+    f1.record(stream)
+    f1.synchronize()
+    barrier()
+    ms_e2e = f0.elapsed_time(f1)
+    sweeps_e2e = sess.profile()["sweeps"]
+    t = torch.tensor([ms_e2e], device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = world * wl.n_interior * sweeps_e2e / (float(t.item()) * 1e-3)
+
+    # ---------------- roofline of the dominant kernel (SOR colour pass), event-timed
+    sess.prepare(wl.image, wl.rows, p, wl.u0)
+    for _ in range(args.warmup):
+        sess.step_nodiag()
+    sess.set_profiling(True)
+    sess.profile()
+    for _ in range(2):
+        sess.step_nodiag()
+    pr = sess.profile()
+    sess.set_profiling(False)
+    pass_ms = (pr["red_ms"] + pr["black_ms"]) / max(1, pr["red_n"] + pr["black_n"])
+    bytes_per_pass = SURVEY_BYTES_PER_SWEEP * wl.n_interior / 2.0
+    achieved = bytes_per_pass / (pass_ms * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.config, {}).get("sor_pass_bytes")
+        except Exception:
+            traffic = None
+    sor_share = (pr["red_ms"] + pr["black_ms"]) / max(1e-9, pr["red_ms"] + pr["black_ms"] + pr["assemble_ms"] + pr["rescale_ms"])
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl.name, "dims": list(wl.dims), "sor_rel_tol": 1e-8,
+                       "omega": wl.params["omega"], "parallelism": "replicas" if world > 1 else "1 GPU",
+                       "sweeps_timed": int(sweeps), "l2": "inputs larger than L2 (state+rhs+coef+G ~2.5 GB)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * P,
+                    "d2h_bytes_per_step": 8 * P},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "sor_pass (one colour half-sweep)",
+                         "bytes_per_launch": bytes_per_pass, "avg_launch_ms": pass_ms,
+                         "peak_source": peak_src, "sor_share_of_step": sor_share},
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline_sample(wl)
+            except Exception as e:  # reported, not fatal
+                line["cpu_baseline"] = {"error": str(e)}
+        print(json.dumps(line))
+    sess.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,167 @@
+/*
+ * subsurf_b200.h -- C ABI of the B200-native SUBSURF time step.
+ *
+ * Plain pointers and sizes only.  Host arrays use the reference's ghost-padded
+ * fp64 layout (Field4D, grid.hpp:91-119): P = (n1+2)(n2+2)(n3+2)(n4+2) doubles,
+ *   idx = ((l*kMax + k)*jMax + j)*iMax + i,
+ * per-face arrays hold 8 doubles per padded doxel in kFaceOffsets order
+ * (grid.cpp:67-80, f = 2*axis + (sign > 0)).
+ *
+ * Every entry point replaces one reference function (cited below, file:line in
+ * /root/reference/proj).  Errors: the reference throws; here a status code is
+ * returned and ss_last_error() holds the message.  The C++ mirror
+ * (include/subsurf_b200/subsurf.hpp) maps the codes back onto the reference's
+ * exception types (errors.hpp:9-39).
+ *
+ * There is no CPU fallback: without a usable CUDA device every compute entry
+ * point returns SS_ERR_CUDA.
+ */
+#ifndef SUBSURF_B200_H
+#define SUBSURF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_API __attribute__((visibility("default")))
+
+typedef enum {
+    SS_OK = 0,
+    SS_ERR_VALIDATION = 1, /* ValidationError  (errors.hpp:15-18)            */
+    SS_ERR_NOCONVERGE = 2, /* SolverError      (errors.hpp:26-33)            */
+    SS_ERR_NONFINITE = 3,  /* NumericalError   (errors.hpp:36-39)            */
+    SS_ERR_CUDA = 4,       /* device missing / CUDA runtime failure          */
+    SS_ERR_NCCL = 5,       /* multi-GPU transport failure                    */
+    SS_ERR_STATE = 6       /* API misuse (session not prepared, ...)         */
+} ss_status;
+
+/* GridSpec (grid.hpp:16-46) */
+typedef struct {
+    int n1, n2, n3, n4;
+    double h1, h2, h3, h4;
+} ss_grid;
+
+/* CenterRow (io.hpp:23-27): frame 0-based, x,y,z 0-based doxel coordinates */
+typedef struct {
+    int frame;
+    double x, y, z, radius;
+} ss_center;
+
+/* SegmentationParams (solver.hpp:77-85) flattened: SolverParams, SmoothingParams,
+ * ThresholdParams, EdgeParams, InitParams, rescale_radius.  Field order is the
+ * ABI; defaults are the reference's (cli.cpp:73-107). */
+typedef struct {
+    double tau, epsilon, omega, sor_tol;
+    int sor_max_iter, n_steps, rescale_each_step;
+    double sor_rel_tol;   /* extension: > 0 => sor_tol = rel * ||u^{n-1}||_2 per step */
+    double sigma;
+    int smooth_steps;
+    double smooth_tol;
+    int smooth_max_iter;
+    double smooth_omega;
+    double lambda, background;
+    double K, delta, vartheta;
+    double init_v, init_R;
+    int init_profile;     /* 0 = peak, 1 = linear (seedinit.hpp:10) */
+    double rescale_radius;/* <= 0 => per-row radii (std::nullopt) */
+} ss_seg_params;
+
+/* per-step diagnostics line (solver.cpp:433-438) */
+typedef struct {
+    int iterations;
+    double residual, tol, umin, umax;
+} ss_step_diag;
+
+SS_API const char* ss_last_error(void);
+SS_API int ss_abi_version(void);
+/* number of this library's kernel launches since load (process-wide) */
+SS_API unsigned long long ss_launch_count(void);
+/* 1 if a CUDA device is usable, else 0 (sets ss_last_error) */
+SS_API int ss_device_available(void);
+
+/* ---------------- per-call API: the reference's free functions ---------------- */
+
+/* assemble_step (solver.hpp:50-51, solver.cpp:23-77).  G may be NULL (G == 1).
+ * offdiag: 8*P, diag: P, abar: P (ghost rows zero, like the reference). */
+SS_API ss_status ss_assemble_step(const ss_grid* g, const double* u_prev, const double* G,
+                                  double tau, double epsilon, double* offdiag, double* diag,
+                                  double* abar);
+/* assemble_heat_step (solver.hpp:55, solver.cpp:79-116) */
+SS_API ss_status ss_assemble_heat_step(const ss_grid* g, double dt, double* offdiag,
+                                       double* diag, double* abar);
+/* redblack_sor (solver.hpp:69-70, solver.cpp:379-397).  u: in = u_guess (its
+ * ghosts are the Dirichlet data), out = result.  On SS_ERR_NOCONVERGE u holds
+ * the last iterate and *iterations / *residual are set (SolverError fields).
+ * workers > 1 is accepted and ignored (results are worker-count invariant,
+ * solver.cpp:144-156). */
+SS_API ss_status ss_redblack_sor(const ss_grid* g, const double* offdiag, const double* rhs,
+                                 double* u, double omega, double sor_tol, int sor_max_iter,
+                                 int workers, int* iterations, double* residual);
+/* face_coefficients (edge.hpp:95-97, edge.cpp:73-99); G: 8*P, ghosts = 1 */
+SS_API ss_status ss_face_coefficients(const ss_grid* g, const double* I0s, const double* ITs,
+                                      double K, double delta, double vartheta, double* G);
+/* heat_smooth (preprocess.hpp:23, preprocess.cpp:25-51) */
+SS_API ss_status ss_heat_smooth(const ss_grid* g, const double* image, double sigma, int steps,
+                                double omega, double sor_tol, int sor_max_iter, double* out);
+/* local_threshold (preprocess.hpp:36-37, preprocess.cpp:53-102) */
+SS_API ss_status ss_local_threshold(const ss_grid* g, const double* image, const ss_center* c,
+                                    int n, double lambda, double background, double* out);
+/* build_initial (seedinit.hpp:25-26, seedinit.cpp:42-66) */
+SS_API ss_status ss_build_initial(const ss_grid* g, const ss_center* c, int n, double v,
+                                  double R, int profile, double* u);
+/* local_rescale (seedinit.hpp:32-33, seedinit.cpp:68-99); radius <= 0 => per-row */
+SS_API ss_status ss_local_rescale(const ss_grid* g, double* u, const ss_center* c, int n,
+                                  double radius);
+/* extract_mask (tracking.hpp:55, tracking.cpp:35-52): n4 frames of n1*n2*n3 bytes */
+SS_API ss_status ss_extract_mask(const ss_grid* g, const double* u, double level,
+                                 uint8_t* mask);
+/* segment (solver.hpp:91-92, solver.cpp:405-441).  u0 may be NULL
+ * (build_initial); diags: n_steps entries or NULL. */
+SS_API ss_status ss_segment(const ss_grid* g, const double* image, const ss_center* c, int n,
+                            const ss_seg_params* p, const double* u0, double* u_out,
+                            ss_step_diag* diags);
+
+/* ---------------- device-resident session (the performance boundary) ---------------- */
+typedef struct ss_session ss_session;
+
+SS_API ss_status ss_session_create(const ss_grid* g, int device, ss_session** out);
+SS_API ss_status ss_session_destroy(ss_session* s);
+/* the cudaStream_t every kernel of this session is launched on */
+SS_API void* ss_session_stream(ss_session* s);
+/* segment() preamble (solver.cpp:408-426): u0 (or build_initial) + local_rescale,
+ * local_threshold, heat_smooth x2, face_coefficients, apply_dirichlet. */
+SS_API ss_status ss_session_prepare(ss_session* s, const double* image, const ss_center* c,
+                                    int n, const ss_seg_params* p, const double* u0);
+/* one time step of the loop body (solver.cpp:428-438): assemble_step,
+ * redblack_sor (rhs = guess = u), local_rescale.  diag may be NULL. */
+SS_API ss_status ss_session_step(ss_session* s, ss_step_diag* diag);
+/* host <-> device copies of u (padded fp64, ghosts included) */
+SS_API ss_status ss_session_set_u(ss_session* s, const double* host_u);
+SS_API ss_status ss_session_get_u(ss_session* s, double* host_u);
+SS_API ss_status ss_session_get_mask(ss_session* s, double level, uint8_t* mask);
+/* fixed-sweep mode (BASELINE config 4): assemble at the current u, then exactly
+ * n_sweeps red+black sweeps with no stopping test; *residual = last residual. */
+SS_API ss_status ss_session_fixed_sweeps(ss_session* s, int n_sweeps, double* residual);
+/* 0 = host-driven chunked loop, 1 = CUDA-graph conditional loop (default) */
+SS_API ss_status ss_session_set_loop_mode(ss_session* s, int mode);
+/* per-pass CUDA-event timing of the SOR kernels (forces the host-driven loop) */
+SS_API ss_status ss_session_set_profiling(ss_session* s, int enable);
+/* accumulated since the last call (then reset): total ms in red passes, black
+ * passes, assembly kernels and rescale, and the number of each */
+typedef struct {
+    double red_ms, black_ms, assemble_ms, rescale_ms;
+    long long red_n, black_n, assemble_n, rescale_n;
+    long long sweeps; /* completed red+black sweeps */
+} ss_profile;
+SS_API ss_status ss_session_profile(ss_session* s, ss_profile* out);
+/* algorithmic bytes of one SOR colour pass: 28 B x interior doxels (SURVEY 8(d):
+ * 56 B per doxel per red+black sweep) */
+SS_API double ss_sor_pass_bytes(const ss_grid* g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

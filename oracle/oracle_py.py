@@ -129,7 +129,7 @@ class _Lib:
         self._eoc = sig("eoc_row", [C.c_int, C.c_double, C.c_double, C.c_int] + W + [_D])
         seg_args = [_G, _D, _CEN, C.c_int, C.POINTER(SegParams), _D] + W + [_D, C.POINTER(StepDiag)]
         if with_workers:
-            seg_args += [_D, C.POINTER(C.c_longlong)]
+            seg_args += [_D, C.POINTER(C.c_longlong), _D]
         self._seg = sig("segment", seg_args)
 
     def _wk(self, workers):
@@ -214,15 +214,16 @@ class _Lib:
         extra = []
         times = np.zeros(4)
         sweeps = C.c_longlong(0)
+        step_s = np.zeros(params.n_steps)
         if self.w:
-            extra = [_p(times), C.byref(sweeps)]
+            extra = [_p(times), C.byref(sweeps), _p(step_s)]
         st = self._seg(C.byref(g), _p(image), arr, n, C.byref(params), _p(u0), *self._wk(workers),
                        _p(out), diags, *extra)
         d = [dict(iterations=x.iterations, residual=x.residual, tol=x.tol, umin=x.umin,
                   umax=x.umax) for x in diags]
         info = dict(diags=d)
         if self.w:
-            info.update(times=times.tolist(), sweeps=sweeps.value)
+            info.update(times=times.tolist(), sweeps=sweeps.value, step_seconds=step_s.tolist())
         return st, out, info
 
 

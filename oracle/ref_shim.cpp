@@ -269,10 +269,11 @@ int ref_eoc_row(int n, double omega, double sor_tol, int max_iter, int workers, 
 // Otherwise the harness loop of SURVEY.md section 8(d): the same sequence of
 // public reference calls with a per-step sor_tol = rel_tol * ||u^{n-1}||_2
 // and/or a caller-built u0.  Per-step diagnostics and phase timings go to
-// diags / times (seconds: [setup, assemble_total, sor_total, rescale_total]).
+// diags / times (seconds: [setup, assemble_total, sor_total, rescale_total]);
+// step_seconds[n] is the wall time of time step n+1 (assemble + SOR + rescale).
 int ref_segment(const or_grid* g, const double* image, const or_center* c, int n,
                 const or_seg_params* p, const double* u0, int workers, double* u_out,
-                or_step_diag* diags, double* times, long long* sor_sweeps) {
+                or_step_diag* diags, double* times, long long* sor_sweeps, double* step_seconds) {
     using clk = std::chrono::steady_clock;
     return guarded([&] {
         SegmentationParams sp;
@@ -301,7 +302,7 @@ int ref_segment(const or_grid* g, const double* image, const or_center* c, int n
 
         const Field4D image_f = field_of(g, image);
         const CentersTable centers = table_of(c, n);
-        if (p->sor_rel_tol <= 0.0 && !u0 && !diags && !times) {
+        if (p->sor_rel_tol <= 0.0 && !u0 && !diags && !times && !step_seconds) {
             store(segment(image_f, centers, sp), u_out);
             return;
         }
@@ -336,6 +337,7 @@ int ref_segment(const or_grid* g, const double* image, const or_center* c, int n
             t_asm += std::chrono::duration<double>(a1 - a0).count();
             t_sor += std::chrono::duration<double>(a2 - a1).count();
             t_resc += std::chrono::duration<double>(a3 - a2).count();
+            if (step_seconds) step_seconds[step - 1] = std::chrono::duration<double>(a3 - a0).count();
             sweeps += sor.iterations;
             if (diags) {
                 diags[step - 1].iterations = sor.iterations;

@@ -1,0 +1,440 @@
+"""B200-native SUBSURF time step (arXiv 2111.11866 hot path).
+
+Python host mirror of the reference's solver API (namespace ``subsurf`` in
+/root/reference/proj/include/subsurf/*.hpp) over the C ABI of
+``libsubsurf_b200.so`` (include/subsurf_b200.h).  Same function names, the same
+argument meaning and the same error taxonomy (errors.hpp:9-39):
+
+=======================  ==============================================
+reference                this module
+=======================  ==============================================
+assemble_step            :func:`assemble_step`      solver.hpp:50-51
+assemble_heat_step       :func:`assemble_heat_step` solver.hpp:55
+redblack_sor             :func:`redblack_sor`       solver.hpp:69-70
+face_coefficients        :func:`face_coefficients`  edge.hpp:95-97
+heat_smooth              :func:`heat_smooth`        preprocess.hpp:23
+local_threshold          :func:`local_threshold`    preprocess.hpp:36-37
+build_initial            :func:`build_initial`      seedinit.hpp:25-26
+local_rescale            :func:`local_rescale`      seedinit.hpp:32-33
+extract_mask             :func:`extract_mask`       tracking.hpp:55
+segment                  :func:`segment`            solver.hpp:91-92
+=======================  ==============================================
+
+Fields are numpy fp64 arrays in the reference's ghost-padded layout, shape
+``(n4+2, n3+2, n2+2, n1+2)`` (i fastest); per-face arrays add a trailing axis
+of 8 (kFaceOffsets order).  Everything runs on the GPU; there is no CPU path:
+without the built library or a CUDA device every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsubsurf_b200.so")
+
+SS_OK, SS_ERR_VALIDATION, SS_ERR_NOCONVERGE, SS_ERR_NONFINITE, SS_ERR_CUDA, SS_ERR_NCCL, SS_ERR_STATE = range(7)
+
+
+# ----------------------------------------------------------------------------- errors (errors.hpp)
+class SubsurfError(RuntimeError):
+    """Base of the reference's exception taxonomy."""
+
+
+class ValidationError(SubsurfError):
+    """errors.hpp:15-18"""
+
+
+class SolverError(SubsurfError):
+    """errors.hpp:26-33: carries ``last_residual`` and ``iterations``."""
+
+    def __init__(self, msg: str, last_residual: float = 0.0, iterations: int = 0):
+        super().__init__(msg)
+        self.last_residual = last_residual
+        self.iterations = iterations
+
+
+class NumericalError(SubsurfError):
+    """errors.hpp:36-39"""
+
+
+class DeviceError(SubsurfError):
+    """No usable CUDA device / CUDA failure (the library has no CPU fallback)."""
+
+
+class StateError(SubsurfError):
+    """API misuse."""
+
+
+# ----------------------------------------------------------------------------- ABI structs
+class Grid(C.Structure):
+    """GridSpec (grid.hpp:16-46)."""
+    _fields_ = [("n1", C.c_int), ("n2", C.c_int), ("n3", C.c_int), ("n4", C.c_int),
+                ("h1", C.c_double), ("h2", C.c_double), ("h3", C.c_double), ("h4", C.c_double)]
+
+    @classmethod
+    def make(cls, dims, h) -> "Grid":
+        hs = (h,) * 4 if np.isscalar(h) else tuple(h)
+        return cls(*[int(d) for d in dims], *[float(x) for x in hs])
+
+    @property
+    def shape(self):
+        return (self.n4 + 2, self.n3 + 2, self.n2 + 2, self.n1 + 2)
+
+    @property
+    def interior(self):
+        return (slice(1, self.n4 + 1), slice(1, self.n3 + 1), slice(1, self.n2 + 1),
+                slice(1, self.n1 + 1))
+
+    def padded_size(self) -> int:
+        return int(np.prod(self.shape))
+
+
+class Center(C.Structure):
+    """CenterRow (io.hpp:23-27)."""
+    _fields_ = [("frame", C.c_int), ("x", C.c_double), ("y", C.c_double), ("z", C.c_double),
+                ("radius", C.c_double)]
+
+
+class SegParams(C.Structure):
+    """SegmentationParams (solver.hpp:77-85), flattened as ss_seg_params."""
+    _fields_ = [("tau", C.c_double), ("epsilon", C.c_double), ("omega", C.c_double),
+                ("sor_tol", C.c_double), ("sor_max_iter", C.c_int), ("n_steps", C.c_int),
+                ("rescale_each_step", C.c_int), ("sor_rel_tol", C.c_double),
+                ("sigma", C.c_double), ("smooth_steps", C.c_int), ("smooth_tol", C.c_double),
+                ("smooth_max_iter", C.c_int), ("smooth_omega", C.c_double),
+                ("lambda_", C.c_double), ("background", C.c_double),
+                ("K", C.c_double), ("delta", C.c_double), ("vartheta", C.c_double),
+                ("init_v", C.c_double), ("init_R", C.c_double), ("init_profile", C.c_int),
+                ("rescale_radius", C.c_double)]
+
+
+class StepDiag(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("residual", C.c_double), ("tol", C.c_double),
+                ("umin", C.c_double), ("umax", C.c_double)]
+
+
+class Profile(C.Structure):
+    _fields_ = [("red_ms", C.c_double), ("black_ms", C.c_double), ("assemble_ms", C.c_double),
+                ("rescale_ms", C.c_double), ("red_n", C.c_longlong), ("black_n", C.c_longlong),
+                ("assemble_n", C.c_longlong), ("rescale_n", C.c_longlong),
+                ("sweeps", C.c_longlong)]
+
+
+def seg_params(**kw) -> SegParams:
+    """Defaults of the reference (cli.cpp:73-107, solver.hpp:19-29, preprocess.hpp:10-30,
+    edge.hpp:12-18, seedinit.hpp:14-20).  ``lam`` is accepted for ``lambda``."""
+    d = dict(tau=1.0, epsilon=1e-4, omega=1.85, sor_tol=1e-8, sor_max_iter=10000, n_steps=10,
+             rescale_each_step=1, sor_rel_tol=0.0, sigma=0.0, smooth_steps=1, smooth_tol=1e-10,
+             smooth_max_iter=10000, smooth_omega=1.85, lambda_=0.5, background=0.0, K=1.0,
+             delta=1.0, vartheta=0.0, init_v=1.0, init_R=10.0, init_profile=0,
+             rescale_radius=0.0)
+    if "lam" in kw:
+        kw["lambda_"] = kw.pop("lam")
+    d.update(kw)
+    return SegParams(**d)
+
+
+# ----------------------------------------------------------------------------- library
+_lib = None
+_D = C.POINTER(C.c_double)
+_GP = C.POINTER(Grid)
+_CP = C.POINTER(Center)
+
+
+def library() -> C.CDLL:
+    """Load libsubsurf_b200.so (raises ImportError when it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`"
+                          " (there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+
+    def sig(name, args, res=C.c_int):
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+
+    sig("ss_last_error", [], C.c_char_p)
+    sig("ss_abi_version", [])
+    sig("ss_launch_count", [], C.c_ulonglong)
+    sig("ss_device_available", [])
+    sig("ss_sor_pass_bytes", [_GP], C.c_double)
+    sig("ss_assemble_step", [_GP, _D, _D, C.c_double, C.c_double, _D, _D, _D])
+    sig("ss_assemble_heat_step", [_GP, C.c_double, _D, _D, _D])
+    sig("ss_redblack_sor", [_GP, _D, _D, _D, C.c_double, C.c_double, C.c_int, C.c_int,
+                            C.POINTER(C.c_int), _D])
+    sig("ss_face_coefficients", [_GP, _D, _D, C.c_double, C.c_double, C.c_double, _D])
+    sig("ss_heat_smooth", [_GP, _D, C.c_double, C.c_int, C.c_double, C.c_double, C.c_int, _D])
+    sig("ss_local_threshold", [_GP, _D, _CP, C.c_int, C.c_double, C.c_double, _D])
+    sig("ss_build_initial", [_GP, _CP, C.c_int, C.c_double, C.c_double, C.c_int, _D])
+    sig("ss_local_rescale", [_GP, _D, _CP, C.c_int, C.c_double])
+    sig("ss_extract_mask", [_GP, _D, C.c_double, C.POINTER(C.c_uint8)])
+    sig("ss_segment", [_GP, _D, _CP, C.c_int, C.POINTER(SegParams), _D, _D, C.POINTER(StepDiag)])
+    sig("ss_session_create", [_GP, C.c_int, C.POINTER(C.c_void_p)])
+    sig("ss_session_destroy", [C.c_void_p])
+    sig("ss_session_stream", [C.c_void_p], C.c_void_p)
+    sig("ss_session_prepare", [C.c_void_p, _D, _CP, C.c_int, C.POINTER(SegParams), _D])
+    sig("ss_session_step", [C.c_void_p, C.POINTER(StepDiag)])
+    sig("ss_session_set_u", [C.c_void_p, _D])
+    sig("ss_session_get_u", [C.c_void_p, _D])
+    sig("ss_session_get_mask", [C.c_void_p, C.c_double, C.POINTER(C.c_uint8)])
+    sig("ss_session_fixed_sweeps", [C.c_void_p, C.c_int, _D])
+    sig("ss_session_set_loop_mode", [C.c_void_p, C.c_int])
+    sig("ss_session_set_profiling", [C.c_void_p, C.c_int])
+    sig("ss_session_profile", [C.c_void_p, C.POINTER(Profile)])
+    _lib = L
+    return L
+
+
+def _check(status: int, iterations: int = 0, residual: float = 0.0) -> None:
+    if status == SS_OK:
+        return
+    msg = library().ss_last_error().decode(errors="replace")
+    if status == SS_ERR_VALIDATION:
+        raise ValidationError(msg)
+    if status == SS_ERR_NOCONVERGE:
+        raise SolverError(msg, residual, iterations)
+    if status == SS_ERR_NONFINITE:
+        raise NumericalError(msg)
+    if status == SS_ERR_STATE:
+        raise StateError(msg)
+    raise DeviceError(msg)
+
+
+def launch_count() -> int:
+    """Kernels launched by the library so far (process-wide)."""
+    return int(library().ss_launch_count())
+
+
+def device_available() -> bool:
+    return bool(library().ss_device_available())
+
+
+def sor_pass_bytes(g: Grid) -> float:
+    return float(library().ss_sor_pass_bytes(C.byref(g)))
+
+
+def _dp(a: Optional[np.ndarray]):
+    if a is None:
+        return None
+    return a.ctypes.data_as(_D)
+
+
+def _field(g: Grid, a, name: str, per_face: bool = False) -> np.ndarray:
+    shape = g.shape + ((8,) if per_face else ())
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.shape != shape:
+        raise ValidationError(f"{name}: shape {a.shape} does not match grid {shape}")
+    return a
+
+
+def _centers(rows) -> tuple:
+    rows = list(rows)
+    arr = (Center * max(1, len(rows)))()
+    for n, r in enumerate(rows):
+        if isinstance(r, Center):
+            arr[n] = r
+        else:
+            arr[n] = Center(int(r[0]), float(r[1]), float(r[2]), float(r[3]), float(r[4]))
+    return arr, len(rows)
+
+
+# ----------------------------------------------------------------------------- reference API
+@dataclass
+class StepCoefficients:
+    """solver.hpp:36-45 (padded indexing; ghost rows zero)."""
+    offdiag: np.ndarray
+    diag: np.ndarray
+    abar: np.ndarray
+
+
+@dataclass
+class SorResult:
+    """solver.hpp:57-61"""
+    u: np.ndarray
+    iterations: int = 0
+    residual: float = 0.0
+
+
+def assemble_step(u_prev, G, tau: float, epsilon: float, g: Grid) -> StepCoefficients:
+    u = _field(g, u_prev, "u_prev")
+    Gf = None if G is None else _field(g, G, "G", per_face=True)
+    off = np.empty(g.shape + (8,))
+    dg = np.empty(g.shape)
+    ab = np.empty(g.shape)
+    _check(library().ss_assemble_step(C.byref(g), _dp(u), _dp(Gf), tau, epsilon, _dp(off), _dp(dg), _dp(ab)))
+    return StepCoefficients(off, dg, ab)
+
+
+def assemble_heat_step(g: Grid, dt: float) -> StepCoefficients:
+    off = np.empty(g.shape + (8,))
+    dg = np.empty(g.shape)
+    ab = np.empty(g.shape)
+    _check(library().ss_assemble_heat_step(C.byref(g), dt, _dp(off), _dp(dg), _dp(ab)))
+    return StepCoefficients(off, dg, ab)
+
+
+def redblack_sor(coeff, rhs, u_guess, omega: float, sor_tol: float, sor_max_iter: int, g: Grid,
+                 workers: int = 1) -> SorResult:
+    off = _field(g, coeff.offdiag if isinstance(coeff, StepCoefficients) else coeff, "offdiag", True)
+    r = _field(g, rhs, "rhs")
+    u = np.array(_field(g, u_guess, "u_guess"), copy=True)  # u_guess is taken by value
+    it = C.c_int(0)
+    res = C.c_double(0.0)
+    st = library().ss_redblack_sor(C.byref(g), _dp(off), _dp(r), _dp(u), omega, sor_tol,
+                                   sor_max_iter, workers, C.byref(it), C.byref(res))
+    _check(st, it.value, res.value)
+    return SorResult(u, it.value, res.value)
+
+
+def face_coefficients(I0s, ITs, K: float, delta: float, vartheta: float, g: Grid) -> np.ndarray:
+    a = _field(g, I0s, "smoothed_image")
+    b = _field(g, ITs, "smoothed_threshold")
+    G = np.empty(g.shape + (8,))
+    _check(library().ss_face_coefficients(C.byref(g), _dp(a), _dp(b), K, delta, vartheta, _dp(G)))
+    return G
+
+
+def heat_smooth(image, g: Grid, sigma: float, steps: int = 1, omega: float = 1.85,
+                sor_tol: float = 1e-10, sor_max_iter: int = 10000) -> np.ndarray:
+    a = _field(g, image, "image")
+    out = np.empty(g.shape)
+    _check(library().ss_heat_smooth(C.byref(g), _dp(a), sigma, steps, omega, sor_tol, sor_max_iter, _dp(out)))
+    return out
+
+
+def local_threshold(image, centers, g: Grid, lam: float = 0.5, background: float = 0.0) -> np.ndarray:
+    a = _field(g, image, "image")
+    arr, n = _centers(centers)
+    out = np.empty(g.shape)
+    _check(library().ss_local_threshold(C.byref(g), _dp(a), arr, n, lam, background, _dp(out)))
+    return out
+
+
+def build_initial(centers, g: Grid, v: float = 1.0, R: float = 10.0, profile: int = 0) -> np.ndarray:
+    arr, n = _centers(centers)
+    out = np.empty(g.shape)
+    _check(library().ss_build_initial(C.byref(g), arr, n, v, R, profile, _dp(out)))
+    return out
+
+
+def local_rescale(u, centers, g: Grid, radius: Optional[float] = None) -> np.ndarray:
+    """Returns the rescaled copy (the reference rescales in place)."""
+    out = np.array(_field(g, u, "u"), copy=True)
+    arr, n = _centers(centers)
+    _check(library().ss_local_rescale(C.byref(g), _dp(out), arr, n, 0.0 if radius is None else radius))
+    return out
+
+
+def extract_mask(u, g: Grid, level: float = 0.5) -> np.ndarray:
+    a = _field(g, u, "u")
+    m = np.empty((g.n4, g.n3, g.n2, g.n1), dtype=np.uint8)
+    _check(library().ss_extract_mask(C.byref(g), _dp(a), level, m.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return m
+
+
+def segment(image, centers, params: SegParams, g: Grid, u0=None):
+    """solver.cpp:405-441. Returns (u, per-step diagnostics)."""
+    a = _field(g, image, "image")
+    u0a = None if u0 is None else _field(g, u0, "u0")
+    arr, n = _centers(centers)
+    out = np.empty(g.shape)
+    diags = (StepDiag * params.n_steps)()
+    _check(library().ss_segment(C.byref(g), _dp(a), arr, n, C.byref(params), _dp(u0a), _dp(out), diags))
+    return out, [dict(iterations=d.iterations, residual=d.residual, tol=d.tol, umin=d.umin,
+                      umax=d.umax) for d in diags]
+
+
+# ----------------------------------------------------------------------------- device session
+class Session:
+    """Device-resident segment() state (the performance boundary).
+
+    ``prepare`` runs segment()'s preamble on the GPU; ``step`` one time step;
+    u stays in HBM between steps unless ``get_u`` / ``set_u`` move it.
+    """
+
+    def __init__(self, g: Grid, device: int = 0):
+        self.g = g
+        h = C.c_void_p()
+        _check(library().ss_session_create(C.byref(g), device, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            library().ss_session_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def stream(self) -> int:
+        return int(library().ss_session_stream(self._h) or 0)
+
+    def prepare(self, image, centers, params: SegParams, u0=None):
+        a = _field(self.g, image, "image")
+        u0a = None if u0 is None else _field(self.g, u0, "u0")
+        arr, n = _centers(centers)
+        self.params = params
+        _check(library().ss_session_prepare(self._h, _dp(a), arr, n, C.byref(params), _dp(u0a)))
+
+    def step(self) -> dict:
+        d = StepDiag()
+        _check(library().ss_session_step(self._h, C.byref(d)))
+        return dict(iterations=d.iterations, residual=d.residual, tol=d.tol, umin=d.umin, umax=d.umax)
+
+    def step_nodiag(self) -> None:
+        _check(library().ss_session_step(self._h, None))
+
+    def set_u(self, u) -> None:
+        a = _field(self.g, u, "u")
+        _check(library().ss_session_set_u(self._h, _dp(a)))
+
+    def set_u_ptr(self, ptr: int) -> None:
+        _check(library().ss_session_set_u(self._h, C.cast(C.c_void_p(ptr), _D)))
+
+    def get_u(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        out = np.empty(self.g.shape) if out is None else out
+        _check(library().ss_session_get_u(self._h, _dp(out)))
+        return out
+
+    def get_u_ptr(self, ptr: int) -> None:
+        _check(library().ss_session_get_u(self._h, C.cast(C.c_void_p(ptr), _D)))
+
+    def get_mask(self, level: float = 0.5) -> np.ndarray:
+        g = self.g
+        m = np.empty((g.n4, g.n3, g.n2, g.n1), dtype=np.uint8)
+        _check(library().ss_session_get_mask(self._h, level, m.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return m
+
+    def fixed_sweeps(self, n: int) -> float:
+        r = C.c_double(0.0)
+        _check(library().ss_session_fixed_sweeps(self._h, n, C.byref(r)))
+        return r.value
+
+    def set_loop_mode(self, mode: int) -> None:
+        _check(library().ss_session_set_loop_mode(self._h, mode))
+
+    def set_profiling(self, on: bool) -> None:
+        _check(library().ss_session_set_profiling(self._h, 1 if on else 0))
+
+    def profile(self) -> dict:
+        p = Profile()
+        _check(library().ss_session_profile(self._h, C.byref(p)))
+        return {k: getattr(p, k) for k, _ in Profile._fields_}

@@ -1,0 +1,98 @@
+// common.cuh -- shared layout, error handling and launch bookkeeping of the
+// B200 SUBSURF library.
+//
+// Device layout ("colour-packed"): the ghost-padded box of the reference
+// (grid.hpp:91-119) is split by red/black colour, colour(i,j,k,l) = (i+j+k+l)&1
+// (red = 0 = even, solver.cpp:244/291/341, 1-based padded GLOBAL indices).
+// Each colour is a dense array of rows; row r = (l*kMax + k)*jMax + j holds the
+// doxels of that colour at packed position m = i >> 1 (W = (n1+3)/2 slots per
+// row).  For any doxel the j/k/l neighbours sit at the same m in the other
+// colour's array one row stride away, and the i-1 / i+1 neighbours at
+// m' = (i-1)>>1 and (i+1)>>1.  A colour half-sweep therefore reads and writes
+// whole 32-byte sectors only (no half-used sectors as with the interleaved
+// Field4D layout).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "subsurf_b200.h"
+
+namespace ssb {
+
+struct Layout {
+    int n1, n2, n3, n4;
+    int iMax, jMax, kMax, lMax;
+    int W;            // packed slots per row
+    long long rows;   // jMax * kMax * lMax
+    long long cs;     // elements per colour array = rows * W
+    long long sj, sk, sl;  // packed row strides for j, k, l neighbours
+    long long P;      // padded doxels of the reference layout
+
+    static Layout make(const ss_grid& g) {
+        Layout L;
+        L.n1 = g.n1; L.n2 = g.n2; L.n3 = g.n3; L.n4 = g.n4;
+        L.iMax = g.n1 + 2; L.jMax = g.n2 + 2; L.kMax = g.n3 + 2; L.lMax = g.n4 + 2;
+        L.W = (L.iMax + 1) / 2;
+        L.rows = (long long)L.jMax * L.kMax * L.lMax;
+        L.cs = L.rows * L.W;
+        L.sj = L.W;
+        L.sk = (long long)L.W * L.jMax;
+        L.sl = (long long)L.W * L.jMax * L.kMax;
+        L.P = (long long)L.iMax * L.rows;
+        return L;
+    }
+    __host__ __device__ __forceinline__ long long row(int j, int k, int l) const {
+        return ((long long)l * kMax + k) * jMax + j;
+    }
+    __host__ __device__ __forceinline__ long long padded(int i, int j, int k, int l) const {
+        return row(j, k, l) * iMax + i;
+    }
+    __host__ __device__ __forceinline__ long long packed(int i, int j, int k, int l) const {
+        return row(j, k, l) * W + (i >> 1);
+    }
+    __host__ __device__ __forceinline__ static int colour(int i, int j, int k, int l) {
+        return (i + j + k + l) & 1;
+    }
+};
+
+// A colour-packed scalar field: two device arrays (red, black).
+struct PField {
+    double* c[2] = {nullptr, nullptr};
+};
+
+// Error plumbing: internal failures throw ssb::Error, the C ABI catches and
+// converts to a status code + message (ss_last_error()).
+struct Error : std::runtime_error {
+    ss_status code;
+    Error(ss_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+extern std::atomic<unsigned long long> g_launches;
+
+inline void count_launch(unsigned long long n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+#define SSB_CUDA(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            throw ::ssb::Error(SS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define SSB_LAUNCHED()                                                                      \
+    do {                                                                                    \
+        ::ssb::count_launch();                                                              \
+        cudaError_t _e = cudaGetLastError();                                                \
+        if (_e != cudaSuccess)                                                              \
+            throw ::ssb::Error(SS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+    } while (0)
+
+inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+}  // namespace ssb

@@ -1,0 +1,274 @@
+// field.cu -- layout conversion and whole-field kernels: pack/unpack between
+// the reference's ghost-padded Field4D layout and the colour-packed device
+// layout, Dirichlet / mirror ghosts (grid.cpp:126-156), deterministic interior
+// reductions (grid.cpp:158-171) and the 0.5-superlevel mask (tracking.cpp:35-52).
+#include "kernels.cuh"
+
+namespace ssb {
+
+namespace {
+
+struct Pos {
+    int i, j, k, l;
+    long long row;
+};
+
+__device__ __forceinline__ Pos decode_padded(const Layout& L, long long e) {
+    Pos p;
+    p.i = (int)(e % L.iMax);
+    p.row = e / L.iMax;
+    p.j = (int)(p.row % L.jMax);
+    p.k = (int)((p.row / L.jMax) % L.kMax);
+    p.l = (int)(p.row / ((long long)L.jMax * L.kMax));
+    return p;
+}
+
+__device__ __forceinline__ Pos decode_interior(const Layout& L, long long e) {
+    Pos p;
+    p.i = (int)(e % L.n1) + 1;
+    long long r = e / L.n1;
+    p.j = (int)(r % L.n2) + 1;
+    r /= L.n2;
+    p.k = (int)(r % L.n3) + 1;
+    p.l = (int)(r / L.n3) + 1;
+    p.row = L.row(p.j, p.k, p.l);
+    return p;
+}
+
+__device__ __forceinline__ double* at(const Layout& L, PField f, int i, int j, int k, int l) {
+    return f.c[Layout::colour(i, j, k, l)] + L.packed(i, j, k, l);
+}
+
+__global__ void pack_kernel(const Layout L, const double* __restrict__ src, PField dst, PField t0,
+                            PField t1) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= L.P) return;
+    const Pos p = decode_padded(L, e);
+    const int c = Layout::colour(p.i, p.j, p.k, p.l);
+    const long long q = p.row * L.W + (p.i >> 1);
+    const double v = src[e];
+    dst.c[c][q] = v;
+    const bool ghost = p.i == 0 || p.i > L.n1 || p.j == 0 || p.j > L.n2 || p.k == 0 ||
+                       p.k > L.n3 || p.l == 0 || p.l > L.n4;
+    if (ghost && t0.c[c]) t0.c[c][q] = v;
+    if (ghost && t1.c[c]) t1.c[c][q] = v;
+}
+
+__global__ void unpack_kernel(const Layout L, PField src, double* __restrict__ dst) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= L.P) return;
+    const Pos p = decode_padded(L, e);
+    dst[e] = src.c[Layout::colour(p.i, p.j, p.k, p.l)][p.row * L.W + (p.i >> 1)];
+}
+
+__global__ void fill_kernel(const Layout L, PField f, double v, int ghosts_only) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= L.P) return;
+    const Pos p = decode_padded(L, e);
+    const bool ghost = p.i == 0 || p.i > L.n1 || p.j == 0 || p.j > L.n2 || p.k == 0 ||
+                       p.k > L.n3 || p.l == 0 || p.l > L.n4;
+    if (ghosts_only && !ghost) return;
+    f.c[Layout::colour(p.i, p.j, p.k, p.l)][p.row * L.W + (p.i >> 1)] = v;
+}
+
+// grid.cpp:138-156, one launch per axis (axis order 0..3 carries edges/corners)
+__global__ void mirror_kernel(const Layout L, PField f, int axis) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= L.P) return;
+    const Pos p = decode_padded(L, e);
+    int c[4] = {p.i, p.j, p.k, p.l};
+    const int hi[4] = {L.n1 + 1, L.n2 + 1, L.n3 + 1, L.n4 + 1};
+    if (c[axis] != 0 && c[axis] != hi[axis]) return;
+    const int dst[4] = {c[0], c[1], c[2], c[3]};
+    c[axis] += c[axis] == 0 ? 1 : -1;
+    *at(L, f, dst[0], dst[1], dst[2], dst[3]) = *at(L, f, c[0], c[1], c[2], c[3]);
+}
+
+__global__ void fill_raw_kernel(double* p, long long n, double v) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x)
+        p[e] = v;
+}
+
+__global__ void copy_ghosts_kernel(const Layout L, PField dst, PField src) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= L.P) return;
+    const Pos p = decode_padded(L, e);
+    const bool ghost = p.i == 0 || p.i > L.n1 || p.j == 0 || p.j > L.n2 || p.k == 0 ||
+                       p.k > L.n3 || p.l == 0 || p.l > L.n4;
+    if (!ghost) return;
+    const int c = Layout::colour(p.i, p.j, p.k, p.l);
+    const long long q = p.row * L.W + (p.i >> 1);
+    dst.c[c][q] = src.c[c][q];
+}
+
+__global__ void copy_kernel(long long n, double* __restrict__ d, const double* __restrict__ s) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x)
+        d[e] = s[e];
+}
+
+__device__ __forceinline__ double bsum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    __shared__ double ws[32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    }
+    return v;
+}
+
+__device__ __forceinline__ void bminmax(double& lo, double& hi) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_down_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_down_sync(0xffffffffu, hi, o));
+    }
+    __shared__ double wl[32], wh[32];
+    if ((threadIdx.x & 31) == 0) {
+        wl[threadIdx.x >> 5] = lo;
+        wh[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const bool ok = threadIdx.x < (blockDim.x >> 5);
+        lo = ok ? wl[threadIdx.x] : INFINITY;
+        hi = ok ? wh[threadIdx.x] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fmin(lo, __shfl_down_sync(0xffffffffu, lo, o));
+            hi = fmax(hi, __shfl_down_sync(0xffffffffu, hi, o));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) norm_part_kernel(const Layout L, PField f, double* part) {
+    const long long N = (long long)L.n1 * L.n2 * L.n3 * L.n4;
+    double s = 0.0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < N;
+         e += (long long)gridDim.x * blockDim.x) {
+        const Pos p = decode_interior(L, e);
+        const double v = *at(L, f, p.i, p.j, p.k, p.l);
+        s += v * v;
+    }
+    s = bsum(s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) sum_final_kernel(const double* part, int n, double* out) {
+    double s = 0.0;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) s += part[q];
+    s = bsum(s);
+    if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void __launch_bounds__(256) minmax_part_kernel(const Layout L, PField f, double* part) {
+    const long long N = (long long)L.n1 * L.n2 * L.n3 * L.n4;
+    double lo = INFINITY, hi = -INFINITY;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < N;
+         e += (long long)gridDim.x * blockDim.x) {
+        const Pos p = decode_interior(L, e);
+        const double v = *at(L, f, p.i, p.j, p.k, p.l);
+        lo = fmin(lo, v);
+        hi = fmax(hi, v);
+    }
+    bminmax(lo, hi);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = lo;
+        part[2 * blockIdx.x + 1] = hi;
+    }
+}
+
+__global__ void __launch_bounds__(256) minmax_final_kernel(const double* part, int n, double* out) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        lo = fmin(lo, part[2 * q]);
+        hi = fmax(hi, part[2 * q + 1]);
+    }
+    bminmax(lo, hi);
+    if (threadIdx.x == 0) {
+        out[0] = lo;
+        out[1] = hi;
+    }
+}
+
+__global__ void mask_kernel(const Layout L, PField f, double level, uint8_t* mask) {
+    const long long N = (long long)L.n1 * L.n2 * L.n3 * L.n4;
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= N) return;
+    const Pos p = decode_interior(L, e);
+    mask[e] = *at(L, f, p.i, p.j, p.k, p.l) >= level ? 1 : 0;
+}
+
+}  // namespace
+
+void launch_pack(cudaStream_t s, const Layout& L, const double* src, PField dst, PField t0,
+                 PField t1) {
+    pack_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, src, dst, t0, t1);
+    SSB_LAUNCHED();
+}
+
+void launch_fill_raw(cudaStream_t s, double* p, long long n, double v) {
+    fill_raw_kernel<<<kReduceBlocks * 2, 256, 0, s>>>(p, n, v);
+    SSB_LAUNCHED();
+}
+
+void launch_copy_ghosts(cudaStream_t s, const Layout& L, PField dst, PField src) {
+    copy_ghosts_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, dst, src);
+    SSB_LAUNCHED();
+}
+
+void launch_unpack(cudaStream_t s, const Layout& L, PField src, double* dst) {
+    unpack_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, src, dst);
+    SSB_LAUNCHED();
+}
+
+void launch_fill(cudaStream_t s, const Layout& L, PField f, double v) {
+    fill_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, f, v, 0);
+    SSB_LAUNCHED();
+}
+
+void launch_set_ghosts(cudaStream_t s, const Layout& L, PField f, double v) {
+    fill_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, f, v, 1);
+    SSB_LAUNCHED();
+}
+
+void launch_mirror_ghosts(cudaStream_t s, const Layout& L, PField f) {
+    for (int axis = 0; axis < 4; ++axis) {
+        mirror_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, f, axis);
+        SSB_LAUNCHED();
+    }
+}
+
+void launch_copy_field(cudaStream_t s, const Layout& L, PField dst, PField src) {
+    for (int c = 0; c < 2; ++c) {
+        copy_kernel<<<kReduceBlocks * 2, 256, 0, s>>>(L.cs, dst.c[c], src.c[c]);
+        SSB_LAUNCHED();
+    }
+}
+
+void launch_norm_sq(cudaStream_t s, const Layout& L, PField f, double* scratch, double* out) {
+    norm_part_kernel<<<kReduceBlocks, 256, 0, s>>>(L, f, scratch);
+    SSB_LAUNCHED();
+    sum_final_kernel<<<1, 256, 0, s>>>(scratch, kReduceBlocks, out);
+    SSB_LAUNCHED();
+}
+
+void launch_minmax(cudaStream_t s, const Layout& L, PField f, double* scratch, double* out2) {
+    minmax_part_kernel<<<kReduceBlocks, 256, 0, s>>>(L, f, scratch);
+    SSB_LAUNCHED();
+    minmax_final_kernel<<<1, 256, 0, s>>>(scratch, kReduceBlocks, out2);
+    SSB_LAUNCHED();
+}
+
+void launch_mask(cudaStream_t s, const Layout& L, PField f, double level, uint8_t* mask) {
+    const long long N = (long long)L.n1 * L.n2 * L.n3 * L.n4;
+    mask_kernel<<<ceil_div(N, 256), 256, 0, s>>>(L, f, level, mask);
+    SSB_LAUNCHED();
+}
+
+}  // namespace ssb

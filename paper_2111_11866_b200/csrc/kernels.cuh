@@ -1,0 +1,120 @@
+// kernels.cuh -- device data structures and host launchers of every kernel.
+#pragma once
+
+#include "common.cuh"
+
+namespace ssb {
+
+// ---------------------------------------------------------------- SOR solve
+// Device-resident loop control of one redblack_sor call (solver.cpp:163-214).
+// The red pass of iteration n reads n_red, the black pass n_black; the
+// finalize kernel between them decides convergence of iteration n-1 and
+// advances the counters, so every kernel has fixed launch arguments and the
+// loop body can live in a CUDA-graph conditional WHILE node.
+struct SorState {
+    int n_red, n_black;
+    int done, converged;
+    int iterations, max_iter;
+    int fixed, pad;
+    unsigned int counter, pad2;
+    double tol, residual;
+};
+
+struct SorArgs {
+    Layout L;
+    // [buffer][colour].  Buffer 0 holds the initial guess and is never written;
+    // iteration n writes buffer out(n) = n odd ? 1 : 2 and reads in(n) = n == 1 ? 0
+    // : out(n-1), so the rhs may alias buffer 0 and the iterate of the stopping
+    // iteration survives the (lagged-residual) red pass that follows it.
+    double* U[3][2];
+    const double* rhs[2];   // colour-packed rhs
+    const float* coef[2];   // colour-packed fp32 off-diagonals, 8 per doxel (kFaceOffsets order)
+    double* part[2];        // per-block squared-residual partials of the red / black pass
+    double* slice_res;      // per-slice residual (solver.cpp:195-199 slice_residual_sq_)
+    SorState* st;
+    double omega, keep;
+    double hc[4];           // heat stencil constants float(-dt/h_a^2) (solver.cpp:100-110)
+    int bps;                // blocks per l-slice of one pass
+    int use_cond;
+    cudaGraphConditionalHandle cond;
+};
+
+constexpr int kPassBX = 32;  // doxels of one colour along a row
+constexpr int kPassBY = 8;   // rows (j) per block
+
+dim3 pass_grid(const Layout& L);
+void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_sq,
+                     double rel, int max_iter, int fixed);
+void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* ev /*4 or null*/);
+
+// ---------------------------------------------------------------- assembly
+struct AsmArgs {
+    Layout L;
+    const double* u[2];     // colour-packed u_prev (ghosts = previous boundary data)
+    const double* G[2];     // colour-packed 8 x fp64 per doxel, or null (G == 1)
+    float* coef[2];         // output, colour-packed
+    double t_h2[4];         // tau / h_a^2 (solver.cpp:36-38)
+    double eps;
+    double h[4];
+    int* bad;               // set when a diag is non-finite (solver.cpp:71-75)
+    // export (per-call API): padded outputs, may be null
+    double* off_out;        // 8 per padded doxel
+    double* diag_out;
+    double* abar_out;
+};
+void launch_assemble(cudaStream_t s, const AsmArgs& a);
+
+struct EdgeArgs {
+    Layout L;
+    const double* I0[2];
+    const double* IT[2];
+    double* G[2];           // colour-packed output
+    double* G_out;          // padded export (8 per doxel), may be null
+    double K, delta, vartheta;
+    double h[4];
+};
+void launch_face_coefficients(cudaStream_t s, const EdgeArgs& a);
+
+// padded fp64 off-diagonals (8 per doxel) -> colour-packed fp32 rows
+// (pack_coefficients, solver.cpp:233-249)
+void launch_pack_coef(cudaStream_t s, const Layout& L, const double* off, float* coef0,
+                      float* coef1);
+// padded 8-vector field -> colour-packed
+void launch_pack8(cudaStream_t s, const Layout& L, const double* src, double* d0, double* d1);
+// heat-step export (assemble_heat_step, solver.cpp:79-116)
+void launch_heat_export(cudaStream_t s, const Layout& L, double dt_h2[4], double* off,
+                        double* diag, double* abar);
+
+// ---------------------------------------------------------------- fields
+// src (padded) -> dst; ghost doxels are also written into twin0/twin1 (null members skipped)
+void launch_pack(cudaStream_t s, const Layout& L, const double* src, PField dst, PField twin0,
+                 PField twin1);
+void launch_fill_raw(cudaStream_t s, double* p, long long n, double v);
+void launch_unpack(cudaStream_t s, const Layout& L, PField src, double* dst);
+void launch_fill(cudaStream_t s, const Layout& L, PField f, double v);
+void launch_set_ghosts(cudaStream_t s, const Layout& L, PField f, double v);
+// ghost doxels of src copied into dst
+void launch_copy_ghosts(cudaStream_t s, const Layout& L, PField dst, PField src);
+void launch_mirror_ghosts(cudaStream_t s, const Layout& L, PField f);
+void launch_copy_field(cudaStream_t s, const Layout& L, PField dst, PField src);
+// deterministic interior reductions; out[0] = sum of squares or (min,max)
+void launch_norm_sq(cudaStream_t s, const Layout& L, PField f, double* scratch, double* out);
+void launch_minmax(cudaStream_t s, const Layout& L, PField f, double* scratch, double* out2);
+void launch_mask(cudaStream_t s, const Layout& L, PField f, double level, uint8_t* mask);
+constexpr int kReduceBlocks = 592;  // 4 x 148 SMs; fixed => deterministic order
+
+// ---------------------------------------------------------------- balls
+struct Ball {
+    int l, i0, i1, j0, j1, k0, k1, pad;
+    double x, y, z, r, r_sq;
+};
+// threshold: per-ball alpha/beta over the raw image (preprocess.cpp:77-88)
+void launch_ball_minmax(cudaStream_t s, const Layout& L, PField f, const Ball* balls, int n,
+                        double* ab, int* empty_flag);
+void launch_threshold_write(cudaStream_t s, const Layout& L, PField img, PField out,
+                            const Ball* balls, int n, const double* ab, double lambda);
+void launch_rescale(cudaStream_t s, const Layout& L, PField u, const Ball* balls, int n);
+void launch_initial(cudaStream_t s, const Layout& L, PField u, const Ball* balls, int n,
+                    double v, double R, int profile);
+
+}  // namespace ssb
