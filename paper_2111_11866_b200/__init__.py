@@ -35,7 +35,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsubsurf_b200.so")
+LIB_PATH = os.environ.get("SUBSURF_B200_LIB") or os.path.join(_HERE, "libsubsurf_b200.so")
 
 SS_OK, SS_ERR_VALIDATION, SS_ERR_NOCONVERGE, SS_ERR_NONFINITE, SS_ERR_CUDA, SS_ERR_NCCL, SS_ERR_STATE = range(7)
 

@@ -34,14 +34,28 @@ struct SorArgs {
     SorState* st;
     double omega, keep;
     double hc[4];           // heat stencil constants float(-dt/h_a^2) (solver.cpp:100-110)
-    int bps;                // blocks per l-slice of one pass
+    int bps;                // residual partials (tiles) per l-slice of one pass
+    int tx, ty, tk;         // tile grid of one slice (pass_tiles)
+    long long tiles;
     int use_cond;
     cudaGraphConditionalHandle cond;
 };
 
 constexpr int kPassBX = 32;  // doxels of one colour along a row
 constexpr int kPassBY = 8;   // rows (j) per block
+#ifndef SSB_PASS_KC
+#define SSB_PASS_KC 4
+#endif
+#ifndef SSB_PASS_BATCH
+#define SSB_PASS_BATCH 1
+#endif
+#ifndef SSB_PASS_MINB
+#define SSB_PASS_MINB 4
+#endif
+constexpr int kPassKC = SSB_PASS_KC;        // planes (k) per tile
+constexpr int kPassBatch = SSB_PASS_BATCH;  // doxels whose loads a thread issues together
 
+void pass_tiles(const Layout& L, SorArgs& a);
 dim3 pass_grid(const Layout& L);
 void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_sq,
                      double rel, int max_iter, int fixed);

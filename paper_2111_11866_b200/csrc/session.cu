@@ -249,10 +249,10 @@ struct Session {
         for (auto& f : S) f.alloc(L);
         coef[0].alloc(L.cs * 8);
         coef[1].alloc(L.cs * 8);
-        const dim3 pg = pass_grid(L);
-        const size_t nparts = (size_t)pg.x * pg.y * pg.z;
-        part[0].alloc(nparts);
-        part[1].alloc(nparts);
+        SorArgs tmp{};
+        pass_tiles(L, tmp);
+        part[0].alloc((size_t)tmp.tiles * kPassBY);
+        part[1].alloc((size_t)tmp.tiles * kPassBY);
         slice_res.alloc(L.n4);
         st.alloc(1);
         scratch.alloc(2 * kReduceBlocks);
@@ -340,8 +340,7 @@ struct Session {
         a.omega = omega;
         a.keep = 1.0 - omega;
         for (int q = 0; q < 4; ++q) a.hc[q] = heat ? hc[q] : 0.0;
-        const dim3 pg = pass_grid(L);
-        a.bps = (int)(pg.x * pg.y * (unsigned)L.n3);
+        pass_tiles(L, a);
         a.use_cond = 0;
         return a;
     }
@@ -740,7 +739,6 @@ struct Session {
 };
 
 // ------------------------------------------------------------------ session cache (per-call API)
-static std::mutex g_cache_mu;
 static std::unique_ptr<Session> g_cached;
 
 static bool same_grid(const ss_grid& a, const ss_grid& b) {

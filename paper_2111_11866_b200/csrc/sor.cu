@@ -17,6 +17,8 @@
 // as the rhs (segment() solves with rhs = guess = u^{n-1}, solver.cpp:430).
 // Per-doxel arithmetic is the reference's expression order compiled with
 // -fmad=false: iterates are bit-identical to the oracle.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace ssb {
@@ -40,8 +42,99 @@ __device__ __forceinline__ double block_sum(double v) {
     return v;  // valid in thread 0
 }
 
+// Operands of one doxel update; loads are split from the arithmetic so a
+// thread can put the loads of several doxels in flight before the first store.
+struct DoxelIn {
+    float c[8];  // heat: exact float values of float(-dt/h^2), so nothing is lost
+    double rhs, u0, nb[8];
+    long long p;
+};
+
 template <int C, bool HEAT>
-__global__ void __launch_bounds__(kPassBX * kPassBY) sor_pass(const SorArgs a) {
+__device__ __forceinline__ void load_doxel(const SorArgs& a, const float* __restrict__ cf,
+                                           const double* __restrict__ rh,
+                                           const double* __restrict__ uc,
+                                           const double* __restrict__ uo, int i, int j, int k,
+                                           int l, DoxelIn& d) {
+    const Layout& L = a.L;
+    const long long rb = L.row(j, k, l) * L.W;
+    const long long p = rb + (i >> 1);
+    d.p = p;
+    if constexpr (HEAT) {
+        // assemble_heat_step: couplings into ghosts are dropped (solver.cpp:100-103)
+        d.c[0] = i > 1 ? (float)a.hc[0] : 0.f;
+        d.c[1] = i < L.n1 ? (float)a.hc[0] : 0.f;
+        d.c[2] = j > 1 ? (float)a.hc[1] : 0.f;
+        d.c[3] = j < L.n2 ? (float)a.hc[1] : 0.f;
+        d.c[4] = k > 1 ? (float)a.hc[2] : 0.f;
+        d.c[5] = k < L.n3 ? (float)a.hc[2] : 0.f;
+        d.c[6] = l > 1 ? (float)a.hc[3] : 0.f;
+        d.c[7] = l < L.n4 ? (float)a.hc[3] : 0.f;
+    } else {
+        const float4* cp = reinterpret_cast<const float4*>(cf + p * 8);
+        const float4 lo = __ldcs(cp);
+        const float4 hi = __ldcs(cp + 1);
+        d.c[0] = lo.x; d.c[1] = lo.y; d.c[2] = lo.z; d.c[3] = lo.w;
+        d.c[4] = hi.x; d.c[5] = hi.y; d.c[6] = hi.z; d.c[7] = hi.w;
+    }
+    d.rhs = __ldcs(rh + p);
+    d.u0 = __ldg(uc + p);
+    d.nb[0] = __ldg(uo + rb + ((i - 1) >> 1));
+    d.nb[1] = __ldg(uo + rb + ((i + 1) >> 1));
+    d.nb[2] = __ldg(uo + p - L.sj);
+    d.nb[3] = __ldg(uo + p + L.sj);
+    d.nb[4] = __ldg(uo + p - L.sk);
+    d.nb[5] = __ldg(uo + p + L.sk);
+    d.nb[6] = __ldg(uo + p - L.sl);
+    d.nb[7] = __ldg(uo + p + L.sl);
+}
+
+// The update of solver.cpp:292-313; returns the squared residual contribution
+// (black: in-sweep, :309-312; red: of the incoming state, :347-356).
+template <int C>
+__device__ __forceinline__ double compute_doxel(const SorArgs& a, const DoxelIn& d,
+                                                double* __restrict__ ucw) {
+    const double c0 = (double)d.c[0], c1 = (double)d.c[1], c2 = (double)d.c[2];
+    const double c3 = (double)d.c[3], c4 = (double)d.c[4], c5 = (double)d.c[5];
+    const double c6 = (double)d.c[6], c7 = (double)d.c[7];
+    const double dg = 1.0 - (c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7);
+    double acc = d.rhs;
+    acc -= c0 * d.nb[0];
+    acc -= c1 * d.nb[1];
+    acc -= c2 * d.nb[2];
+    acc -= c3 * d.nb[3];
+    acc -= c4 * d.nb[4];
+    acc -= c5 * d.nb[5];
+    acc -= c6 * d.nb[6];
+    acc -= c7 * d.nb[7];
+    const double ubar = acc / dg;
+    const double unew = a.omega * ubar + a.keep * d.u0;
+    ucw[d.p] = unew;
+    if constexpr (C == 1) {
+        const double res = dg * (unew - ubar);
+        return res * res;
+    } else {
+        double res = dg * d.u0 - d.rhs;
+        res += c0 * d.nb[0];
+        res += c1 * d.nb[1];
+        res += c2 * d.nb[2];
+        res += c3 * d.nb[3];
+        res += c4 * d.nb[4];
+        res += c5 * d.nb[5];
+        res += c6 * d.nb[6];
+        res += c7 * d.nb[7];
+        return res * res;
+    }
+}
+
+// Persistent colour pass: a resident grid walks the tiles (kPassBX doxels of one
+// colour along i) x (kPassBY rows j) x (kPassKC planes k) of one slice l.  Each
+// warp (one row j of a tile) reduces its squared residuals with shuffles and
+// writes one partial; the partials of a slice are contiguous and indexed by
+// (tile, warp), so the per-slice sums do not depend on the grid size, and no
+// block barrier stalls the load pipeline between tiles.
+template <int C, bool HEAT>
+__global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(const SorArgs a) {
     const SorState* st = a.st;
     if (*(volatile const int*)&st->done) return;
     const int n = C == 0 ? *(volatile const int*)&st->n_red : *(volatile const int*)&st->n_black;
@@ -52,79 +145,40 @@ __global__ void __launch_bounds__(kPassBX * kPassBY) sor_pass(const SorArgs a) {
     const double* __restrict__ uo = C == 0 ? a.U[bin][1] : a.U[bout][0];
     double* __restrict__ ucw = a.U[bout][C];
 
-    const int z = blockIdx.z;
-    const int k = z % L.n3 + 1;
-    const int l = z / L.n3 + 1;
-    const int j = blockIdx.y * kPassBY + threadIdx.y + 1;
-    const int i = 1 + ((1 + j + k + l + C) & 1) + 2 * (int)(blockIdx.x * kPassBX + threadIdx.x);
-
-    double r2 = 0.0;
-    if (j <= L.n2 && i <= L.n1) {
-        const long long rb = L.row(j, k, l) * L.W;
-        const long long p = rb + (i >> 1);
-        double c0, c1, c2, c3, c4, c5, c6, c7;
-        if constexpr (HEAT) {
-            // assemble_heat_step: couplings into ghosts are dropped (solver.cpp:100-103)
-            c0 = i > 1 ? a.hc[0] : 0.0;
-            c1 = i < L.n1 ? a.hc[0] : 0.0;
-            c2 = j > 1 ? a.hc[1] : 0.0;
-            c3 = j < L.n2 ? a.hc[1] : 0.0;
-            c4 = k > 1 ? a.hc[2] : 0.0;
-            c5 = k < L.n3 ? a.hc[2] : 0.0;
-            c6 = l > 1 ? a.hc[3] : 0.0;
-            c7 = l < L.n4 ? a.hc[3] : 0.0;
-        } else {
-            const float4* cp = reinterpret_cast<const float4*>(a.coef[C] + p * 8);
-            const float4 lo = __ldcs(cp);
-            const float4 hi = __ldcs(cp + 1);
-            c0 = lo.x; c1 = lo.y; c2 = lo.z; c3 = lo.w;
-            c4 = hi.x; c5 = hi.y; c6 = hi.z; c7 = hi.w;
+    const float* __restrict__ cf = a.coef[C];
+    const double* __restrict__ rh = a.rhs[C];
+    for (long long t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+        const int bx = (int)(t % a.tx);
+        long long r = t / a.tx;
+        const int by = (int)(r % a.ty);
+        r /= a.ty;
+        const int bk = (int)(r % a.tk);
+        const int l = (int)(r / a.tk) + 1;
+        const int j = by * kPassBY + threadIdx.y + 1;
+        const int q = bx * kPassBX + threadIdx.x;
+        const int k0 = bk * kPassKC + 1;
+        double r2 = 0.0;
+        if (j <= L.n2) {
+#pragma unroll
+            for (int kb = 0; kb < kPassKC; kb += kPassBatch) {
+                DoxelIn d[kPassBatch];
+                bool ok[kPassBatch];
+#pragma unroll
+                for (int b = 0; b < kPassBatch; ++b) {  // all loads of the batch first
+                    const int k = k0 + kb + b;
+                    const int i = 1 + ((1 + j + k + l + C) & 1) + 2 * q;
+                    ok[b] = k <= L.n3 && i <= L.n1;
+                    if (ok[b]) load_doxel<C, HEAT>(a, cf, rh, uc, uo, i, j, k, l, d[b]);
+                }
+#pragma unroll
+                for (int b = 0; b < kPassBatch; ++b)
+                    if (ok[b]) r2 += compute_doxel<C>(a, d[b], ucw);
+            }
         }
-        const double rhs = __ldcs(a.rhs[C] + p);
-        const double u0 = __ldg(uc + p);
-        const double n0 = __ldg(uo + rb + ((i - 1) >> 1));
-        const double n1 = __ldg(uo + rb + ((i + 1) >> 1));
-        const double n2 = __ldg(uo + p - L.sj);
-        const double n3 = __ldg(uo + p + L.sj);
-        const double n4 = __ldg(uo + p - L.sk);
-        const double n5 = __ldg(uo + p + L.sk);
-        const double n6 = __ldg(uo + p - L.sl);
-        const double n7 = __ldg(uo + p + L.sl);
-
-        // solver.cpp:296-312
-        const double dg = 1.0 - (c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7);
-        double acc = rhs;
-        acc -= c0 * n0;
-        acc -= c1 * n1;
-        acc -= c2 * n2;
-        acc -= c3 * n3;
-        acc -= c4 * n4;
-        acc -= c5 * n5;
-        acc -= c6 * n6;
-        acc -= c7 * n7;
-        const double ubar = acc / dg;
-        const double unew = a.omega * ubar + a.keep * u0;
-        ucw[p] = unew;
-        if constexpr (C == 1) {
-            const double res = dg * (unew - ubar);
-            r2 = res * res;
-        } else {
-            // red residual of the incoming state (solver.cpp:347-356)
-            double res = dg * u0 - rhs;
-            res += c0 * n0;
-            res += c1 * n1;
-            res += c2 * n2;
-            res += c3 * n3;
-            res += c4 * n4;
-            res += c5 * n5;
-            res += c6 * n6;
-            res += c7 * n7;
-            r2 = res * res;
-        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
+        if (threadIdx.x == 0) a.part[C][t * kPassBY + threadIdx.y] = r2;
     }
-    r2 = block_sum(r2);
-    if (threadIdx.x == 0 && threadIdx.y == 0)
-        a.part[C][((long long)z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = r2;
 }
 
 // grid = n4 blocks (one per local l-slice), 256 threads
@@ -195,6 +249,28 @@ dim3 pass_grid(const Layout& L) {
     return dim3(ceil_div(nq, kPassBX), ceil_div(L.n2, kPassBY), (unsigned)(L.n3 * L.n4));
 }
 
+void pass_tiles(const Layout& L, SorArgs& a) {
+    const int nq = (L.n1 + 1) / 2;
+    a.tx = (int)ceil_div(nq, kPassBX);
+    a.ty = (int)ceil_div(L.n2, kPassBY);
+    a.tk = (int)ceil_div(L.n3, kPassKC);
+    a.tiles = (long long)a.tx * a.ty * a.tk * L.n4;
+    a.bps = a.tx * a.ty * a.tk * kPassBY;  // one partial per warp-row of a tile
+}
+
+static int resident_blocks() {
+    static int blocks = 0;
+    if (!blocks) {
+        int dev = 0, sms = 0, per = 0;
+        SSB_CUDA(cudaGetDevice(&dev));
+        SSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sor_pass<0, false>,
+                                                               kPassBX * kPassBY, 0));
+        blocks = sms * std::max(1, per);
+    }
+    return blocks;
+}
+
 void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_sq, double rel,
                      int max_iter, int fixed) {
     sor_init<<<1, 1, 0, s>>>(st, tol, norm_sq, rel, max_iter, fixed);
@@ -202,7 +278,7 @@ void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* nor
 }
 
 void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* ev) {
-    const dim3 grid = pass_grid(a.L);
+    const unsigned grid = (unsigned)std::min<long long>(a.tiles, resident_blocks());
     const dim3 block(kPassBX, kPassBY);
     if (ev) SSB_CUDA(cudaEventRecord(ev[0], s));
     if (heat)
