@@ -115,6 +115,11 @@ SS_API ss_status ss_build_initial(const ss_grid* g, const ss_center* c, int n, d
 /* local_rescale (seedinit.hpp:32-33, seedinit.cpp:68-99); radius <= 0 => per-row */
 SS_API ss_status ss_local_rescale(const ss_grid* g, double* u, const ss_center* c, int n,
                                   double radius);
+/* apply_dirichlet (grid.cpp:126-136), apply_mirror_ghosts (grid.cpp:138-156),
+ * interior_minmax (grid.cpp:158-171) on a padded host field */
+SS_API ss_status ss_apply_dirichlet(const ss_grid* g, double* f, double value);
+SS_API ss_status ss_apply_mirror_ghosts(const ss_grid* g, double* f);
+SS_API ss_status ss_interior_minmax(const ss_grid* g, const double* f, double* lo, double* hi);
 /* extract_mask (tracking.hpp:55, tracking.cpp:35-52): n4 frames of n1*n2*n3 bytes */
 SS_API ss_status ss_extract_mask(const ss_grid* g, const double* u, double level,
                                  uint8_t* mask);

@@ -176,6 +176,9 @@ def library() -> C.CDLL:
     sig("ss_build_initial", [_GP, _CP, C.c_int, C.c_double, C.c_double, C.c_int, _D])
     sig("ss_local_rescale", [_GP, _D, _CP, C.c_int, C.c_double])
     sig("ss_extract_mask", [_GP, _D, C.c_double, C.POINTER(C.c_uint8)])
+    sig("ss_apply_dirichlet", [_GP, _D, C.c_double])
+    sig("ss_apply_mirror_ghosts", [_GP, _D])
+    sig("ss_interior_minmax", [_GP, _D, _D, _D])
     sig("ss_segment", [_GP, _D, _CP, C.c_int, C.POINTER(SegParams), _D, _D, C.POINTER(StepDiag)])
     sig("ss_session_create", [_GP, C.c_int, C.POINTER(C.c_void_p)])
     sig("ss_session_destroy", [C.c_void_p])
@@ -338,6 +341,28 @@ def extract_mask(u, g: Grid, level: float = 0.5) -> np.ndarray:
     m = np.empty((g.n4, g.n3, g.n2, g.n1), dtype=np.uint8)
     _check(library().ss_extract_mask(C.byref(g), _dp(a), level, m.ctypes.data_as(C.POINTER(C.c_uint8))))
     return m
+
+
+def apply_dirichlet(f, g: Grid, value: float) -> np.ndarray:
+    """grid.cpp:126-136 (returns a copy)."""
+    out = np.array(_field(g, f, "field"), copy=True)
+    _check(library().ss_apply_dirichlet(C.byref(g), _dp(out), value))
+    return out
+
+
+def apply_mirror_ghosts(f, g: Grid) -> np.ndarray:
+    """grid.cpp:138-156 (returns a copy)."""
+    out = np.array(_field(g, f, "field"), copy=True)
+    _check(library().ss_apply_mirror_ghosts(C.byref(g), _dp(out)))
+    return out
+
+
+def interior_minmax(f, g: Grid):
+    """grid.cpp:158-171"""
+    a = _field(g, f, "field")
+    lo, hi = C.c_double(0.0), C.c_double(0.0)
+    _check(library().ss_interior_minmax(C.byref(g), _dp(a), C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
 
 
 def segment(image, centers, params: SegParams, g: Grid, u0=None):

@@ -981,6 +981,48 @@ ss_status ss_local_rescale(const ss_grid* g, double* u, const ss_center* c, int 
     });
 }
 
+ss_status ss_apply_dirichlet(const ss_grid* g, double* f, double value) {
+    return guard([&] {
+        validate_grid(g);
+        require(f != nullptr, "null field");
+        Session& s = cached_session(*g);
+        s.prepared = false;
+        s.upload_field(f, s.S[0].pf());
+        launch_set_ghosts(s.stream, s.L, s.S[0].pf(), value);
+        s.download_field(s.S[0].pf(), f);
+        s.sync();
+    });
+}
+
+ss_status ss_apply_mirror_ghosts(const ss_grid* g, double* f) {
+    return guard([&] {
+        validate_grid(g);
+        require(f != nullptr, "null field");
+        Session& s = cached_session(*g);
+        s.prepared = false;
+        s.upload_field(f, s.S[0].pf());
+        launch_mirror_ghosts(s.stream, s.L, s.S[0].pf());
+        s.download_field(s.S[0].pf(), f);
+        s.sync();
+    });
+}
+
+ss_status ss_interior_minmax(const ss_grid* g, const double* f, double* lo, double* hi) {
+    return guard([&] {
+        validate_grid(g);
+        require(f && lo && hi, "null argument");
+        Session& s = cached_session(*g);
+        s.prepared = false;
+        s.upload_field(f, s.S[0].pf());
+        launch_minmax(s.stream, s.L, s.S[0].pf(), s.scratch.p, s.scal.p + 1);
+        SSB_CUDA(cudaMemcpyAsync(s.scal_host + 1, s.scal.p + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                                 s.stream));
+        s.sync();
+        *lo = s.scal_host[1];
+        *hi = s.scal_host[2];
+    });
+}
+
 ss_status ss_extract_mask(const ss_grid* g, const double* u, double level, uint8_t* mask) {
     return guard([&] {
         validate_grid(g);

@@ -279,3 +279,17 @@ def test_fixed_sweeps_and_launch_count(gpu):
         r = s.fixed_sweeps(50)
         assert np.isfinite(r)
         assert gpu.launch_count() - n0 >= 150  # 50 x (red, finalize, black)
+
+
+def test_grid_helpers(gpu, oracle):
+    dims = (7, 5, 4, 3)
+    g = gpu.Grid.make(dims, 0.5)
+    og = cs.grid(dims, 0.5)
+    f = cs.rand_field(dims, 17)
+    assert_bits(gpu.apply_mirror_ghosts(f, g), oracle.apply_mirror_ghosts(og, f), "mirror ghosts")
+    d = gpu.apply_dirichlet(f, g, 0.25)
+    ghost = np.ones(g.shape, bool)
+    ghost[g.interior] = False
+    assert np.all(d[ghost] == 0.25) and np.array_equal(d[~ghost], f[~ghost])
+    lo, hi = gpu.interior_minmax(f, g)
+    assert lo == f[g.interior].min() and hi == f[g.interior].max()
