@@ -133,6 +133,19 @@ SS_API ss_status ss_segment(const ss_grid* g, const double* image, const ss_cent
 typedef struct ss_session ss_session;
 
 SS_API ss_status ss_session_create(const ss_grid* g, int device, ss_session** out);
+/* the grid split along l into n_slabs slabs on ONE device (Partition::create
+ * semantics, parallel.cpp:9-19), exchanging halo planes by device copies:
+ * the multi-GPU decomposition exercised on a single GPU (bit-identical to 1 slab) */
+SS_API ss_status ss_session_create_group(const ss_grid* g, int n_slabs, int device, ss_session** out);
+/* multi-GPU: one process per GPU.  Rank 0 calls ss_nccl_unique_id and shares the
+ * 128 bytes (e.g. torch.distributed broadcast); every rank then creates its slab
+ * session.  Host arrays of a distributed session are the rank's padded slab:
+ * global planes l_begin-1 .. l_begin+l_count (ss_session_slab). */
+SS_API ss_status ss_nccl_unique_id(uint8_t out[128]);
+SS_API ss_status ss_session_create_dist(const ss_grid* g, int rank, int world, const uint8_t uid[128],
+                                        int device, ss_session** out);
+/* 1-based first owned slice, owned slice count (whole grid unless distributed), world size */
+SS_API ss_status ss_session_slab(ss_session* s, int* l_begin, int* l_count, int* world);
 SS_API ss_status ss_session_destroy(ss_session* s);
 /* the cudaStream_t every kernel of this session is launched on */
 SS_API void* ss_session_stream(ss_session* s);

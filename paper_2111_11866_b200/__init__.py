@@ -181,6 +181,10 @@ def library() -> C.CDLL:
     sig("ss_interior_minmax", [_GP, _D, _D, _D])
     sig("ss_segment", [_GP, _D, _CP, C.c_int, C.POINTER(SegParams), _D, _D, C.POINTER(StepDiag)])
     sig("ss_session_create", [_GP, C.c_int, C.POINTER(C.c_void_p)])
+    sig("ss_session_create_group", [_GP, C.c_int, C.c_int, C.POINTER(C.c_void_p)])
+    sig("ss_nccl_unique_id", [C.POINTER(C.c_uint8)])
+    sig("ss_session_create_dist", [_GP, C.c_int, C.c_int, C.POINTER(C.c_uint8), C.c_int, C.POINTER(C.c_void_p)])
+    sig("ss_session_slab", [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)])
     sig("ss_session_destroy", [C.c_void_p])
     sig("ss_session_stream", [C.c_void_p], C.c_void_p)
     sig("ss_session_prepare", [C.c_void_p, _D, _CP, C.c_int, C.POINTER(SegParams), _D])
@@ -378,18 +382,40 @@ def segment(image, centers, params: SegParams, g: Grid, u0=None):
 
 
 # ----------------------------------------------------------------------------- device session
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(library().ss_nccl_unique_id(buf))
+    return bytes(buf)
+
+
 class Session:
     """Device-resident segment() state (the performance boundary).
 
     ``prepare`` runs segment()'s preamble on the GPU; ``step`` one time step;
     u stays in HBM between steps unless ``get_u`` / ``set_u`` move it.
+
+    ``n_slabs > 1`` splits the grid along l into slabs on the same device (the
+    multi-GPU decomposition with device-copy halo exchange); ``dist=(rank,
+    world, uid)`` makes this process's slab of an NCCL job, whose host arrays
+    are the rank's padded slab (see :mod:`paper_2111_11866_b200.dist`).
     """
 
-    def __init__(self, g: Grid, device: int = 0):
+    def __init__(self, g: Grid, device: int = 0, n_slabs: int = 1, dist=None):
         self.g = g
         h = C.c_void_p()
-        _check(library().ss_session_create(C.byref(g), device, C.byref(h)))
+        if dist is not None:
+            rank, world, uid = dist
+            ub = (C.c_uint8 * 128).from_buffer_copy(uid)
+            _check(library().ss_session_create_dist(C.byref(g), rank, world, ub, device, C.byref(h)))
+        else:
+            _check(library().ss_session_create_group(C.byref(g), n_slabs, device, C.byref(h)))
         self._h = h
+        lb, lc, w = C.c_int(0), C.c_int(0), C.c_int(0)
+        _check(library().ss_session_slab(h, C.byref(lb), C.byref(lc), C.byref(w)))
+        self.l_begin, self.l_count, self.world = lb.value, lc.value, w.value
+        self.distributed = dist is not None
+        # host arrays: whole padded grid, or the rank's padded slab
+        self.host_shape = (self.l_count + 2,) + g.shape[1:] if self.distributed else g.shape
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
@@ -412,9 +438,15 @@ class Session:
     def stream(self) -> int:
         return int(library().ss_session_stream(self._h) or 0)
 
+    def _host(self, a, name):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.shape != self.host_shape:
+            raise ValidationError(f"{name}: shape {a.shape} does not match {self.host_shape}")
+        return a
+
     def prepare(self, image, centers, params: SegParams, u0=None):
-        a = _field(self.g, image, "image")
-        u0a = None if u0 is None else _field(self.g, u0, "u0")
+        a = self._host(image, "image")
+        u0a = None if u0 is None else self._host(u0, "u0")
         arr, n = _centers(centers)
         self.params = params
         _check(library().ss_session_prepare(self._h, _dp(a), arr, n, C.byref(params), _dp(u0a)))
@@ -428,14 +460,14 @@ class Session:
         _check(library().ss_session_step(self._h, None))
 
     def set_u(self, u) -> None:
-        a = _field(self.g, u, "u")
+        a = self._host(u, "u")
         _check(library().ss_session_set_u(self._h, _dp(a)))
 
     def set_u_ptr(self, ptr: int) -> None:
         _check(library().ss_session_set_u(self._h, C.cast(C.c_void_p(ptr), _D)))
 
     def get_u(self, out: Optional[np.ndarray] = None) -> np.ndarray:
-        out = np.empty(self.g.shape) if out is None else out
+        out = np.zeros(self.host_shape) if out is None else out
         _check(library().ss_session_get_u(self._h, _dp(out)))
         return out
 
@@ -444,7 +476,7 @@ class Session:
 
     def get_mask(self, level: float = 0.5) -> np.ndarray:
         g = self.g
-        m = np.empty((g.n4, g.n3, g.n2, g.n1), dtype=np.uint8)
+        m = np.empty((self.l_count if self.distributed else g.n4, g.n3, g.n2, g.n1), dtype=np.uint8)
         _check(library().ss_session_get_mask(self._h, level, m.ctypes.data_as(C.POINTER(C.c_uint8))))
         return m
 

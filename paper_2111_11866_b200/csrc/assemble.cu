@@ -73,7 +73,7 @@ __device__ __forceinline__ Site site(const Layout& L, int C) {
     s.k = z % L.n3 + 1;
     s.l = z / L.n3 + 1;
     s.j = blockIdx.y * kPassBY + threadIdx.y + 1;
-    s.i = 1 + ((1 + s.j + s.k + s.l + C) & 1) + 2 * (int)(blockIdx.x * kPassBX + threadIdx.x);
+    s.i = 1 + ((1 + s.j + s.k + s.l + L.lpar + C) & 1) + 2 * (int)(blockIdx.x * kPassBX + threadIdx.x);
     s.valid = s.j <= L.n2 && s.i <= L.n1;
     return s;
 }
@@ -213,7 +213,7 @@ __global__ void pack_coef_kernel(const Layout L, const double* __restrict__ off,
     const int k = (int)((r / L.jMax) % L.kMax);
     const int l = (int)(r / ((long long)L.jMax * L.kMax));
     if (i < 1 || i > L.n1 || j < 1 || j > L.n2 || k < 1 || k > L.n3 || l < 1 || l > L.n4) return;
-    float* dst = (Layout::colour(i, j, k, l) ? c1 : c0) + (r * L.W + (i >> 1)) * 8;
+    float* dst = (L.colour(i, j, k, l) ? c1 : c0) + (r * L.W + (i >> 1)) * 8;
 #pragma unroll
     for (int f = 0; f < 8; ++f) dst[f] = (float)off[e * 8 + f];
 }
@@ -227,7 +227,7 @@ __global__ void pack8_kernel(const Layout L, const double* __restrict__ src, dou
     const int j = (int)(r % L.jMax);
     const int k = (int)((r / L.jMax) % L.kMax);
     const int l = (int)(r / ((long long)L.jMax * L.kMax));
-    double* dst = (Layout::colour(i, j, k, l) ? d1 : d0) + (r * L.W + (i >> 1)) * 8;
+    double* dst = (L.colour(i, j, k, l) ? d1 : d0) + (r * L.W + (i >> 1)) * 8;
 #pragma unroll
     for (int f = 0; f < 8; ++f) dst[f] = src[e * 8 + f];
 }

@@ -34,7 +34,7 @@ __device__ __forceinline__ void box_pos(const Ball& b, long long t, int& i, int&
 }
 
 __device__ __forceinline__ double* at(const Layout& L, PField f, int i, int j, int k, int l) {
-    return f.c[Layout::colour(i, j, k, l)] + L.packed(i, j, k, l);
+    return f.c[L.colour(i, j, k, l)] + L.packed(i, j, k, l);
 }
 
 // block-wide (min, max); result broadcast to all threads

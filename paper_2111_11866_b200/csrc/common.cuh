@@ -26,7 +26,11 @@
 namespace ssb {
 
 struct Layout {
-    int n1, n2, n3, n4;
+    int n1, n2, n3, n4;   // local extents (n4 = slices owned by this slab)
+    int l0;               // global l of local plane 0 (slab offset; 0 for a whole grid)
+    int n4g;              // global number of slices
+    int lpar;             // l0 & 1: colour parity uses GLOBAL l (solver.cpp:244)
+    int glo, ghi;         // local planes 0 / n4+1 are global ghosts (else: halos)
     int iMax, jMax, kMax, lMax;
     int W;            // packed slots per row
     long long rows;   // jMax * kMax * lMax
@@ -34,9 +38,14 @@ struct Layout {
     long long sj, sk, sl;  // packed row strides for j, k, l neighbours
     long long P;      // padded doxels of the reference layout
 
-    static Layout make(const ss_grid& g) {
+    static Layout make(const ss_grid& g, int l0 = 0, int n4g = -1) {
         Layout L;
         L.n1 = g.n1; L.n2 = g.n2; L.n3 = g.n3; L.n4 = g.n4;
+        L.l0 = l0;
+        L.n4g = n4g < 0 ? g.n4 : n4g;
+        L.lpar = l0 & 1;
+        L.glo = l0 == 0;
+        L.ghi = l0 + g.n4 == L.n4g;
         L.iMax = g.n1 + 2; L.jMax = g.n2 + 2; L.kMax = g.n3 + 2; L.lMax = g.n4 + 2;
         L.W = (L.iMax + 1) / 2;
         L.rows = (long long)L.jMax * L.kMax * L.lMax;
@@ -56,9 +65,11 @@ struct Layout {
     __host__ __device__ __forceinline__ long long packed(int i, int j, int k, int l) const {
         return row(j, k, l) * W + (i >> 1);
     }
-    __host__ __device__ __forceinline__ static int colour(int i, int j, int k, int l) {
-        return (i + j + k + l) & 1;
+    // red = 0 <=> (i + j + k + l_global) even
+    __host__ __device__ __forceinline__ int colour(int i, int j, int k, int l) const {
+        return (i + j + k + l + lpar) & 1;
     }
+    long long plane() const { return (long long)jMax * kMax * W; }  // one colour, one l-plane
 };
 
 // A colour-packed scalar field: two device arrays (red, black).

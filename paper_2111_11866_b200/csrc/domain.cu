@@ -1,0 +1,869 @@
+// domain.cu -- slabs, the in-process transport and the device-resident
+// segment() domain (solver.cpp:405-441) with its red-black SOR driver
+// (solver.cpp:124-397).  See domain.cuh for the structure.
+#include "domain.cuh"
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+namespace ssb {
+
+std::atomic<unsigned long long> g_launches{0};
+
+// ------------------------------------------------------------------ validation
+// (solver.cpp:13-21, preprocess.cpp:11-23, edge.cpp:9-14, seedinit.cpp:9-12, io.cpp:128-140)
+void require(bool ok, const std::string& msg) {
+    if (!ok) throw Error(SS_ERR_VALIDATION, msg);
+}
+void validate_grid(const ss_grid* g) {
+    require(g != nullptr, "null grid");
+    require(g->n1 >= 1 && g->n2 >= 1 && g->n3 >= 1 && g->n4 >= 1, "GridSpec: doxel counts must be >= 1");
+    require(g->h1 > 0.0 && g->h2 > 0.0 && g->h3 > 0.0 && g->h4 > 0.0, "GridSpec: spacings must be > 0");
+}
+void validate_solver(double tau, double eps, double omega, double tol, int max_iter, int n_steps) {
+    require(!(tau < 0.0), "SolverParams: tau must be >= 0");
+    require(eps > 0.0, "SolverParams: epsilon must be > 0");
+    require(omega > 0.0 && omega < 2.0, "SolverParams: omega must lie in (0,2)");
+    require(tol > 0.0, "SolverParams: sor_tol must be > 0");
+    require(max_iter >= 1, "SolverParams: sor_max_iter must be >= 1");
+    require(n_steps >= 1, "SolverParams: n_steps must be >= 1");
+}
+void validate_smoothing(double sigma, int steps, double tol, int max_iter, double omega) {
+    require(!(sigma < 0.0), "SmoothingParams: sigma must be >= 0");
+    require(steps >= 1, "SmoothingParams: steps must be >= 1");
+    require(tol > 0.0, "SmoothingParams: sor_tol must be > 0");
+    require(max_iter >= 1, "SmoothingParams: sor_max_iter must be >= 1");
+    require(omega > 0.0 && omega < 2.0, "SmoothingParams: omega must lie in (0,2)");
+}
+void validate_edge(double K, double delta, double vartheta) {
+    require(!(K < 0.0), "EdgeParams: K must be >= 0");
+    require(!(delta < 0.0 || delta > 1.0), "EdgeParams: delta must be in [0,1]");
+    require(!(vartheta < 0.0 || vartheta > 1.0), "EdgeParams: vartheta must be in [0,1]");
+}
+void validate_centers(const ss_grid& g, const ss_center* c, int n) {
+    require(n == 0 || c != nullptr, "null centres table");
+    for (int m = 0; m < n; ++m) {
+        const std::string where = "centers row " + std::to_string(m + 1);
+        require(c[m].frame >= 0 && c[m].frame < g.n4,
+                where + ": frame " + std::to_string(c[m].frame) + " out of range [0," +
+                    std::to_string(g.n4 - 1) + "]");
+        require(c[m].radius > 0.0, where + ": radius must be > 0");
+        require(!(c[m].x < 0.0 || c[m].x > g.n1 - 1 || c[m].y < 0.0 || c[m].y > g.n2 - 1 ||
+                  c[m].z < 0.0 || c[m].z > g.n3 - 1),
+                where + ": center outside volume bounds");
+    }
+}
+void validate_seg_params(const ss_seg_params& p) {
+    validate_solver(p.tau, p.epsilon, p.omega, p.sor_tol, p.sor_max_iter, p.n_steps);
+    validate_smoothing(p.sigma, p.smooth_steps, p.smooth_tol, p.smooth_max_iter, p.smooth_omega);
+    require(!(p.lambda < 0.0 || p.lambda > 1.0), "ThresholdParams: lambda must be in [0,1]");
+    validate_edge(p.K, p.delta, p.vartheta);
+    require(p.init_v > 0.0, "InitParams: v must be > 0");
+    require(p.init_R > 0.0, "InitParams: R must be > 0");
+}
+
+SolverErrT::SolverErrT(const SolveOut& o)
+    : Error(SS_ERR_NOCONVERGE, "redblack_sor: no convergence after " + std::to_string(o.iterations) +
+                                   " iterations (residual " + std::to_string(o.residual) + ")"),
+      iterations(o.iterations),
+      residual(o.residual) {}
+
+// ------------------------------------------------------------------ balls
+// Bounds exactly as seedinit.cpp:22-31 / preprocess.cpp:63-68 (on global coordinates).
+static Ball make_ball(const ss_grid& g, const ss_center& c, double r, int l0) {
+    Ball b{};
+    b.l = c.frame + 1 - l0;
+    b.i0 = std::max(1, int(std::ceil(c.x - r)) + 1);
+    b.i1 = std::min(g.n1, int(std::floor(c.x + r)) + 1);
+    b.j0 = std::max(1, int(std::ceil(c.y - r)) + 1);
+    b.j1 = std::min(g.n2, int(std::floor(c.y + r)) + 1);
+    b.k0 = std::max(1, int(std::ceil(c.z - r)) + 1);
+    b.k1 = std::min(g.n3, int(std::floor(c.z + r)) + 1);
+    b.x = c.x;
+    b.y = c.y;
+    b.z = c.z;
+    b.r = r;
+    b.r_sq = r * r;
+    return b;
+}
+
+static bool boxes_meet(const Ball& a, const Ball& b) {
+    return a.l == b.l && a.i0 <= b.i1 && b.i0 <= a.i1 && a.j0 <= b.j1 && b.j0 <= a.j1 && a.k0 <= b.k1 &&
+           b.k0 <= a.k1;
+}
+
+// Waves: a ball's wave is one past the latest wave of any EARLIER ball whose
+// index box meets its own (same frame), so sequential table order is kept
+// wherever it matters and disjoint balls run concurrently.
+void build_balls(BallSet& bs, const ss_grid& gl, int l0, const ss_center* c, int n, double radius,
+                 bool fixed_radius) {
+    std::vector<Ball> table;
+    std::vector<int> rows;
+    for (int m = 0; m < n; ++m) {
+        if (c[m].frame + 1 - l0 < 1 || c[m].frame + 1 - l0 > gl.n4) continue;  // other slab
+        table.push_back(make_ball(gl, c[m], fixed_radius || radius > 0.0 ? radius : c[m].radius, l0));
+        rows.push_back(m);
+    }
+    const int nb = (int)table.size();
+    std::vector<int> wave(nb, 0);
+    int nw = 0;
+    for (int b = 0; b < nb; ++b) {
+        int w = 0;
+        for (int a = 0; a < b; ++a)
+            if (wave[a] + 1 > w && boxes_meet(table[a], table[b])) w = wave[a] + 1;
+        wave[b] = w;
+        nw = std::max(nw, w + 1);
+    }
+    bs.host.clear();
+    bs.row.clear();
+    bs.wave_off.assign(1, 0);
+    for (int w = 0; w < nw; ++w) {
+        for (int b = 0; b < nb; ++b)
+            if (wave[b] == w) {
+                bs.host.push_back(table[b]);
+                bs.row.push_back(rows[b]);
+            }
+        bs.wave_off.push_back((int)bs.host.size());
+    }
+    bs.dev.alloc(std::max<size_t>(1, bs.host.size()));
+    if (!bs.host.empty())
+        SSB_CUDA(cudaMemcpy(bs.dev.p, bs.host.data(), bs.host.size() * sizeof(Ball), cudaMemcpyHostToDevice));
+}
+
+// ------------------------------------------------------------------ slab
+Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int world, cudaStream_t s)
+    : index(idx), stream(s) {
+    gl = global;
+    gl.n4 = n4_local;
+    L = Layout::make(gl, l0, global.n4);
+    for (auto& f : S) f.alloc(L);
+    coef[0].alloc(L.cs * 8);
+    coef[1].alloc(L.cs * 8);
+    SorArgs t{};
+    pass_tiles(L, t);
+    part[0].alloc((size_t)t.tiles * kPassBY);
+    part[1].alloc((size_t)t.tiles * kPassBY);
+    slice_res.alloc(chunk);
+    norm_loc.alloc(chunk);
+    if (world > 1) {
+        all_slices.alloc((size_t)world * chunk);
+        norm_all.alloc((size_t)world * chunk);
+        SSB_CUDA(cudaMemsetAsync(all_slices.p, 0, all_slices.n * sizeof(double), stream));
+        SSB_CUDA(cudaMemsetAsync(norm_all.p, 0, norm_all.n * sizeof(double), stream));
+    }
+    gloc.alloc(8);
+    gall.alloc((size_t)world * 8);
+    SSB_CUDA(cudaMemsetAsync(slice_res.p, 0, slice_res.n * sizeof(double), stream));
+    SSB_CUDA(cudaMemsetAsync(norm_loc.p, 0, norm_loc.n * sizeof(double), stream));
+    st.alloc(1);
+    scratch.alloc(2 * kReduceBlocks);
+    scal.alloc(8);
+    flags.alloc(4);
+    // zero everything once: ghosts and halos of all buffers are defined from the start
+    for (auto& f : S) launch_fill(stream, L, f.pf(), 0.0);
+    SSB_CUDA(cudaMemsetAsync(coef[0].p, 0, coef[0].n * sizeof(float), stream));
+    SSB_CUDA(cudaMemsetAsync(coef[1].p, 0, coef[1].n * sizeof(float), stream));
+}
+
+double* Slab::stage_p() {
+    stage.alloc(L.P);
+    return stage.p;
+}
+double* Slab::stage8_p() {
+    stage8.alloc(L.P * 8);
+    return stage8.p;
+}
+
+void Slab::upload(const double* host, PField dst, PField t0, PField t1) {
+    double* d = stage_p();
+    SSB_CUDA(cudaMemcpyAsync(d, host, L.P * sizeof(double), cudaMemcpyDefault, stream));
+    launch_pack(stream, L, d, dst, t0, t1);
+}
+
+void Slab::upload_state(const double* host, int role) {
+    upload(host, S[role].pf(), S[(role + 1) % 3].pf(), S[(role + 2) % 3].pf());
+}
+
+void Slab::download(PField src, double* host) {
+    double* d = stage_p();
+    launch_unpack(stream, L, src, d);
+    SSB_CUDA(cudaMemcpyAsync(host, d, L.P * sizeof(double), cudaMemcpyDefault, stream));
+}
+
+void Slab::sync_ghosts_from(int role) {
+    for (int r = 0; r < 3; ++r)
+        if (r != role) launch_copy_ghosts(stream, L, S[r].pf(), S[role].pf());
+}
+
+void Slab::assemble(PField u, bool with_G, double tau, double eps, double* off_out, double* diag_out,
+                    double* abar_out) {
+    AsmArgs a{};
+    a.L = L;
+    a.u[0] = u.c[0];
+    a.u[1] = u.c[1];
+    a.G[0] = with_G ? G[0].p : nullptr;
+    a.G[1] = with_G ? G[1].p : nullptr;
+    a.coef[0] = coef[0].p;
+    a.coef[1] = coef[1].p;
+    const double h[4] = {gl.h1, gl.h2, gl.h3, gl.h4};
+    for (int q = 0; q < 4; ++q) {
+        a.t_h2[q] = tau / (h[q] * h[q]);  // solver.cpp:36-38
+        a.h[q] = h[q];
+    }
+    a.eps = eps;
+    a.bad = flags.p;
+    a.off_out = off_out;
+    a.diag_out = diag_out;
+    a.abar_out = abar_out;
+    SSB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int), stream));
+    launch_assemble(stream, a);
+}
+
+void Slab::face_coefficients(PField I0s, PField ITs, double K, double delta, double vartheta,
+                             double* G_out) {
+    G[0].alloc(L.cs * 8);
+    G[1].alloc(L.cs * 8);
+    EdgeArgs e{};
+    e.L = L;
+    e.I0[0] = I0s.c[0];
+    e.I0[1] = I0s.c[1];
+    e.IT[0] = ITs.c[0];
+    e.IT[1] = ITs.c[1];
+    e.G[0] = G[0].p;
+    e.G[1] = G[1].p;
+    e.G_out = G_out;
+    e.K = K;
+    e.delta = delta;
+    e.vartheta = vartheta;
+    e.h[0] = gl.h1;
+    e.h[1] = gl.h2;
+    e.h[2] = gl.h3;
+    e.h[3] = gl.h4;
+    launch_face_coefficients(stream, e);
+    have_G = true;
+}
+
+void Slab::rescale(int role) {
+    for (int w = 0; w < rescale_balls.waves(); ++w) {
+        const int o = rescale_balls.wave_off[w], n = rescale_balls.wave_off[w + 1] - o;
+        launch_rescale(stream, L, S[role].pf(), rescale_balls.dev.p + o, n);
+    }
+}
+
+void Slab::threshold_minmax(PField img, const BallSet& bs, double* ab) {
+    SSB_CUDA(cudaMemsetAsync(flags.p + 1, 0x7f, sizeof(int), stream));
+    launch_ball_minmax(stream, L, img, bs.dev.p, bs.count(), ab, flags.p + 1);
+}
+
+void Slab::threshold_write(PField img, PField out, const BallSet& bs, const double* ab, double lambda) {
+    for (int w = 0; w < bs.waves(); ++w) {
+        const int o = bs.wave_off[w], m = bs.wave_off[w + 1] - o;
+        launch_threshold_write(stream, L, img, out, bs.dev.p + o, m, ab + 2 * o, lambda);
+    }
+}
+
+void Slab::initial(PField u, const ss_center* c, int n, double v, double R, int profile) {
+    BallSet bs;
+    build_balls(bs, gl, L.l0, c, n, R, true);
+    launch_fill(stream, L, u, 0.0);
+    for (int w = 0; w < bs.waves(); ++w) {
+        const int o = bs.wave_off[w], m = bs.wave_off[w + 1] - o;
+        launch_initial(stream, L, u, bs.dev.p + o, m, v, R, profile);
+    }
+    SSB_CUDA(cudaStreamSynchronize(stream));  // bs is freed on return
+}
+
+SorArgs Slab::sor_args(const PField B[3], const PField& rhs, bool heat, double omega, const double hc[4],
+                       int world) const {
+    SorArgs a{};
+    a.L = L;
+    for (int b = 0; b < 3; ++b)
+        for (int c = 0; c < 2; ++c) a.U[b][c] = B[b].c[c];
+    a.rhs[0] = rhs.c[0];
+    a.rhs[1] = rhs.c[1];
+    a.coef[0] = coef[0].p;
+    a.coef[1] = coef[1].p;
+    a.part[0] = part[0].p;
+    a.part[1] = part[1].p;
+    a.slice_res = slice_res.p;
+    a.all_slices = world == 1 ? slice_res.p : all_slices.p;
+    a.inline_decide = world == 1 ? 1 : 0;
+    a.st = st.p;
+    a.omega = omega;
+    a.keep = 1.0 - omega;
+    for (int q = 0; q < 4; ++q) a.hc[q] = heat ? hc[q] : 0.0;
+    pass_tiles(L, a);
+    a.use_cond = 0;
+    return a;
+}
+
+// ------------------------------------------------------------------ local transport
+void LocalTransport::exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours) {
+    for (size_t s = 0; s + 1 < slabs.size(); ++s) {
+        Slab& a = *slabs[s];
+        const long long P1 = a.L.plane();
+        const int n4 = a.L.n4;
+        for (int c = 0; c < 2; ++c) {
+            if (!(colours & (1 << c))) continue;
+            // a's last owned plane -> b's halo plane 0; b's first owned plane -> a's halo plane n4+1
+            SSB_CUDA(cudaMemcpyAsync(F[s + 1].c[c], F[s].c[c] + n4 * P1, P1 * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, a.stream));
+            SSB_CUDA(cudaMemcpyAsync(F[s].c[c] + (n4 + 1) * P1, F[s + 1].c[c] + P1, P1 * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, a.stream));
+        }
+    }
+}
+
+void LocalTransport::allgather(std::vector<Slab*>& slabs, const std::vector<double*>& local,
+                               const std::vector<double*>& all, int chunk) {
+    for (size_t d = 0; d < slabs.size(); ++d)
+        for (size_t s = 0; s < slabs.size(); ++s)
+            SSB_CUDA(cudaMemcpyAsync(all[d] + s * chunk, local[s], chunk * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, slabs[d]->stream));
+}
+
+// ------------------------------------------------------------------ domain
+struct Domain::GraphEntry {
+    const void* key_ptr[8];
+    int heat;
+    double omega, hc[4];
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    ~GraphEntry() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+    }
+};
+
+void Domain::init_common() {
+    SSB_CUDA(cudaSetDevice(device));
+    SSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    SSB_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+    SSB_CUDA(cudaMallocHost(&st_host, sizeof(SorState)));
+    SSB_CUDA(cudaMallocHost(&flag_host, 8 * sizeof(int)));
+    SSB_CUDA(cudaMallocHost(&scal_host, 64 * sizeof(double)));
+    for (auto& e : ev) SSB_CUDA(cudaEventCreate(&e));
+}
+
+Domain::Domain(const ss_grid& grid, int dev, int n_slabs) : g(grid), world(n_slabs), device(dev) {
+    require(n_slabs >= 1, "Partition: worker count must be >= 1");
+    chunk = (g.n4 + n_slabs - 1) / n_slabs;  // parallel.cpp:9-19
+    const int last = g.n4 - (n_slabs - 1) * chunk;
+    require(last >= 1, "Partition: " + std::to_string(n_slabs) + " workers leave the last one with " +
+                           std::to_string(last) + " slices of " + std::to_string(g.n4));
+    init_common();
+    for (int s = 0; s < n_slabs; ++s) {
+        const int n4l = s == n_slabs - 1 ? last : chunk;
+        slabs.emplace_back(new Slab(g, s * chunk, n4l, s, chunk, world, stream));
+        sp.push_back(slabs.back().get());
+    }
+    if (world == 1)
+        tr.reset(new NullTransport);
+    else
+        tr.reset(new LocalTransport);
+    sync();
+}
+
+Domain::Domain(const ss_grid& grid, int dev, int rank, int w, const unsigned char* uid)
+    : g(grid), world(w), device(dev), distributed(true) {
+    require(w >= 1 && rank >= 0 && rank < w, "invalid rank / world size");
+    chunk = (g.n4 + w - 1) / w;
+    const int last = g.n4 - (w - 1) * chunk;
+    require(last >= 1, "Partition: " + std::to_string(w) + " workers leave the last one with " +
+                           std::to_string(last) + " slices of " + std::to_string(g.n4));
+    init_common();
+    const int n4l = rank == w - 1 ? last : chunk;
+    slabs.emplace_back(new Slab(g, rank * chunk, n4l, rank, chunk, world, stream));
+    sp.push_back(slabs.back().get());
+    tr = make_nccl_transport(uid, rank, w);
+    sync();
+}
+
+Domain::~Domain() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    graphs.clear();
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    for (auto e : ev)
+        if (e) cudaEventDestroy(e);
+    tr.reset();
+    sp.clear();
+    slabs.clear();
+    if (st_host) cudaFreeHost(st_host);
+    if (flag_host) cudaFreeHost(flag_host);
+    if (scal_host) cudaFreeHost(scal_host);
+    if (stream) cudaStreamDestroy(stream);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+}
+
+void Domain::sync() { SSB_CUDA(cudaStreamSynchronize(stream)); }
+
+long long Domain::host_plane() const { return (long long)(g.n1 + 2) * (g.n2 + 2) * (g.n3 + 2); }
+
+// host arrays are global (local group / single) or the rank's slab (distributed)
+const double* Domain::host_slab(const double* base, const Slab& s) const {
+    return distributed ? base : base + (long long)s.L.l0 * host_plane();
+}
+double* Domain::host_slab(double* base, const Slab& s) const {
+    return distributed ? base : base + (long long)s.L.l0 * host_plane();
+}
+
+std::vector<PField> Domain::role_fields(int role) const {
+    std::vector<PField> F;
+    for (Slab* s : sp) F.push_back(s->S[role].pf());
+    return F;
+}
+
+std::vector<Domain::Triple> Domain::role_triples(const int roles[3]) const {
+    std::vector<Triple> B;
+    for (Slab* s : sp) B.push_back({s->S[roles[0]].pf(), s->S[roles[1]].pf(), s->S[roles[2]].pf()});
+    return B;
+}
+
+void Domain::exchange(const std::vector<PField>& F, int colours) { tr->exchange(sp, F, colours); }
+void Domain::exchange_role(int role, int colours) { exchange(role_fields(role), colours); }
+
+std::vector<double> Domain::gather_values(const std::vector<std::vector<double>>& per_slab, int k) {
+    if (world == 1) return per_slab[0];
+    std::vector<double*> loc, all;
+    for (size_t s = 0; s < sp.size(); ++s) {
+        SSB_CUDA(cudaMemcpyAsync(sp[s]->gloc.p, per_slab[s].data(), k * sizeof(double), cudaMemcpyHostToDevice,
+                                 stream));
+        loc.push_back(sp[s]->gloc.p);
+        all.push_back(sp[s]->gall.p);
+    }
+    tr->allgather(sp, loc, all, k);
+    std::vector<double> out((size_t)world * k);
+    SSB_CUDA(cudaMemcpyAsync(out.data(), sp[0]->gall.p, out.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                             stream));
+    sync();
+    return out;
+}
+
+cudaEvent_t Domain::pool_event(size_t idx) {
+    while (ev_pool.size() <= idx) {
+        cudaEvent_t e;
+        SSB_CUDA(cudaEventCreate(&e));
+        ev_pool.push_back(e);
+    }
+    return ev_pool[idx];
+}
+
+cudaGraphExec_t Domain::graph_for(const SorArgs& base, bool heat) {
+    const void* key[8];
+    for (int b = 0; b < 3; ++b)
+        for (int c = 0; c < 2; ++c) key[2 * b + c] = base.U[b][c];
+    key[6] = base.rhs[0];
+    key[7] = base.rhs[1];
+    for (auto& e : graphs) {
+        bool same = e->heat == (int)heat && e->omega == base.omega;
+        for (int q = 0; q < 8 && same; ++q) same = e->key_ptr[q] == key[q];
+        for (int q = 0; q < 4 && same; ++q) same = e->hc[q] == base.hc[q];
+        if (same) return e->exec;
+    }
+    std::unique_ptr<GraphEntry> e(new GraphEntry);
+    std::memcpy(e->key_ptr, key, sizeof key);
+    e->heat = heat;
+    e->omega = base.omega;
+    std::memcpy(e->hc, base.hc, sizeof e->hc);
+    SSB_CUDA(cudaGraphCreate(&e->graph, 0));
+    cudaGraphConditionalHandle h;
+    SSB_CUDA(cudaGraphConditionalHandleCreate(&h, e->graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    SSB_CUDA(cudaGraphAddNode(&node, e->graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    SorArgs a = base;
+    a.use_cond = 1;
+    a.cond = h;
+    const unsigned long long saved = g_launches.load();
+    SSB_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    launch_sor_body(cap_stream, a, heat, nullptr);
+    cudaGraph_t captured = nullptr;
+    SSB_CUDA(cudaStreamEndCapture(cap_stream, &captured));
+    g_launches.store(saved);
+    SSB_CUDA(cudaGraphInstantiate(&e->exec, e->graph, 0));
+    graphs.push_back(std::move(e));
+    if (graphs.size() > 8) graphs.erase(graphs.begin());
+    return graphs.back()->exec;
+}
+
+void Domain::body_single(const SorArgs& a, bool heat, cudaEvent_t* ev4) {
+    launch_sor_body(stream, a, heat, ev4);
+}
+
+// Multi-slab iteration n (solver.cpp:181-193): red on every slab, exchange the
+// new red boundary planes, per-slice residuals + all-gather + decision, black,
+// exchange the new black boundary planes.
+void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>& B, bool heat, int n,
+                        cudaEvent_t* ev4) {
+    const int bout = (n & 1) ? 1 : 2;
+    std::vector<PField> F;
+    for (const Triple& t : B) F.push_back(t[bout]);
+    if (ev4) SSB_CUDA(cudaEventRecord(ev4[0], stream));
+    for (const SorArgs& x : a) launch_sor_pass(stream, x, 0, heat);
+    if (ev4) SSB_CUDA(cudaEventRecord(ev4[1], stream));
+    tr->exchange(sp, F, 1);
+    for (const SorArgs& x : a) launch_sor_finalize(stream, x);
+    std::vector<double*> loc, all;
+    for (Slab* s : sp) {
+        loc.push_back(s->slice_res.p);
+        all.push_back(s->all_slices.p);
+    }
+    tr->allgather(sp, loc, all, chunk);
+    for (const SorArgs& x : a) launch_sor_decide(stream, x);
+    if (ev4) SSB_CUDA(cudaEventRecord(ev4[2], stream));
+    for (const SorArgs& x : a) launch_sor_pass(stream, x, 1, heat);
+    if (ev4) SSB_CUDA(cudaEventRecord(ev4[3], stream));
+    tr->exchange(sp, F, 2);
+}
+
+SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& rhs, bool heat, double omega,
+                       const double hc[4], double tol_abs, bool use_norm, double rel, int max_iter, bool fixed,
+                       int* result) {
+    std::vector<SorArgs> a;
+    for (size_t s = 0; s < sp.size(); ++s) {
+        Slab& x = *sp[s];
+        const double* ns = use_norm ? (world == 1 ? x.norm_loc.p : x.norm_all.p) : nullptr;
+        launch_sor_init(stream, x.st.p, tol_abs, ns, g.n4, rel, max_iter, fixed ? 1 : 0);
+        a.push_back(x.sor_args(B[s].data(), rhs[s], heat, omega, hc, world));
+    }
+    const int limit = max_iter + 1;  // red(max_iter+1) evaluates the last residual
+    if (single() && loop_mode == 1 && !profiling) {
+        cudaGraphExec_t ex = graph_for(a[0], heat);
+        SSB_CUDA(cudaGraphLaunch(ex, stream));
+        SSB_CUDA(cudaMemcpyAsync(st_host, sp[0]->st.p, sizeof(SorState), cudaMemcpyDeviceToHost, stream));
+        sync();
+        count_launch(3ull * (unsigned long long)std::min(limit, st_host->iterations + 1));
+    } else {
+        // host-driven: chunks of loop bodies with one chunk of look-ahead; every
+        // rank runs the same schedule (the decision is identical everywhere)
+        int launched = 0, nb_chunk = 4;
+        int slot = 0, pending = -1;
+        size_t ev_used = 0;
+        std::vector<size_t> body_ev;
+        while (launched < limit) {
+            const int nb = std::min(nb_chunk, limit - launched);
+            for (int b = 0; b < nb; ++b) {
+                const int n = launched + b + 1;
+                cudaEvent_t evs[4];
+                cudaEvent_t* e4 = nullptr;
+                if (profiling) {
+                    for (int q = 0; q < 4; ++q) evs[q] = pool_event(ev_used + q);
+                    body_ev.push_back(ev_used);
+                    ev_used += 4;
+                    e4 = evs;
+                }
+                if (single())
+                    body_single(a[0], heat, e4);
+                else
+                    body_multi(a, B, heat, n, e4);
+            }
+            launched += nb;
+            SSB_CUDA(cudaMemcpyAsync(flag_host + slot, &sp[0]->st.p->done, sizeof(int), cudaMemcpyDeviceToHost,
+                                     stream));
+            SSB_CUDA(cudaEventRecord(ev[slot], stream));
+            if (profiling) {
+                SSB_CUDA(cudaEventSynchronize(ev[slot]));
+                if (flag_host[slot]) break;
+            } else if (pending >= 0) {
+                SSB_CUDA(cudaEventSynchronize(ev[pending]));
+                if (flag_host[pending]) break;
+            }
+            pending = slot;
+            slot ^= 1;
+            nb_chunk = std::min(nb_chunk * 2, 64);
+        }
+        SSB_CUDA(cudaMemcpyAsync(st_host, sp[0]->st.p, sizeof(SorState), cudaMemcpyDeviceToHost, stream));
+        sync();
+        if (profiling) {
+            const int it = st_host->iterations;
+            for (size_t b = 0; b < body_ev.size(); ++b) {
+                float ms = 0.f;
+                const size_t base = body_ev[b];
+                if ((int)b <= it) {  // red(b+1) did real work (b+1 <= it+1)
+                    SSB_CUDA(cudaEventElapsedTime(&ms, ev_pool[base], ev_pool[base + 1]));
+                    prof.red_ms += ms;
+                    prof.red_n++;
+                }
+                if ((int)b < it) {  // black(b+1) did real work
+                    SSB_CUDA(cudaEventElapsedTime(&ms, ev_pool[base + 2], ev_pool[base + 3]));
+                    prof.black_ms += ms;
+                    prof.black_n++;
+                }
+            }
+        }
+    }
+    SolveOut o;
+    o.iterations = st_host->iterations;
+    o.residual = st_host->residual;
+    o.tol = st_host->tol;
+    o.converged = st_host->converged != 0;
+    prof.sweeps += o.iterations;
+    *result = o.iterations == 0 ? 0 : ((o.iterations & 1) ? 1 : 2);
+    return o;
+}
+
+void Domain::mirror_all(const std::vector<PField>& F) {
+    // axes 0..2 on every local plane (halo planes hold exact copies of the
+    // neighbours' planes, so mirroring them locally reproduces the neighbours'
+    // result), then axis 3 at the global ends only (grid.cpp:138-156)
+    for (size_t s = 0; s < sp.size(); ++s) launch_mirror_ghosts(stream, sp[s]->L, F[s], 0, 4);
+}
+
+static void heat_constants(const ss_grid& g, double dt, double hc[4]) {
+    const double h[4] = {g.h1, g.h2, g.h3, g.h4};
+    for (int a = 0; a < 4; ++a) hc[a] = (double)(float)(-(dt / (h[a] * h[a])));  // solver.cpp:89-90,107
+}
+
+int Domain::heat_smooth(const std::vector<Triple>& B, double sigma, int steps, double omega, double tol,
+                        int max_iter) {
+    std::vector<PField> F0;
+    for (const Triple& t : B) F0.push_back(t[0]);
+    if (sigma == 0.0) {
+        mirror_all(F0);
+        return 0;
+    }
+    const double dt = 0.5 * sigma * sigma / steps;
+    double hc[4];
+    heat_constants(g, dt, hc);
+    for (size_t s = 0; s < sp.size(); ++s) {  // the SOR buffers' ghosts/halos = the input's
+        launch_copy_ghosts(stream, sp[s]->L, B[s][1], B[s][0]);
+        launch_copy_ghosts(stream, sp[s]->L, B[s][2], B[s][0]);
+    }
+    int idx[3] = {0, 1, 2};
+    for (int st = 0; st < steps; ++st) {
+        std::vector<Triple> T;
+        std::vector<PField> rhs;
+        for (const Triple& t : B) {
+            T.push_back({t[idx[0]], t[idx[1]], t[idx[2]]});
+            rhs.push_back(t[idx[0]]);
+        }
+        int r = 0;
+        const SolveOut o = solve(T, rhs, true, omega, hc, tol, false, 0.0, max_iter, false, &r);
+        if (!o.converged) throw SolverErrT(o);
+        const int nidx[3] = {idx[r], idx[(r + 1) % 3], idx[(r + 2) % 3]};
+        std::memcpy(idx, nidx, sizeof idx);
+    }
+    std::vector<PField> R;
+    for (const Triple& t : B) R.push_back(t[idx[0]]);
+    mirror_all(R);
+    return idx[0];
+}
+
+void Domain::set_u(const double* host) {
+    for (Slab* s : sp) s->upload_state(host_slab(host, *s), cur);
+}
+
+void Domain::get_u(double* host) {
+    // owned planes (and global ghost planes) of every slab; halo planes are the
+    // neighbours' and are left alone
+    const long long hp = host_plane();
+    for (Slab* s : sp) {
+        double* d = s->stage_p();
+        launch_unpack(stream, s->L, s->S[cur].pf(), d);
+        const int p0 = s->L.glo ? 0 : 1;
+        const int p1 = s->L.ghi ? s->L.n4 + 1 : s->L.n4;
+        SSB_CUDA(cudaMemcpyAsync(host_slab(host, *s) + p0 * hp, d + p0 * hp, (p1 - p0 + 1) * hp * sizeof(double),
+                                 cudaMemcpyDefault, stream));
+    }
+    sync();
+}
+
+void Domain::get_mask(double level, uint8_t* mask) {
+    const size_t fr = (size_t)g.n1 * g.n2 * g.n3;
+    for (Slab* s : sp) {
+        Dev<uint8_t> m;
+        m.alloc(fr * s->L.n4);
+        launch_mask(stream, s->L, s->S[cur].pf(), level, m.p);
+        SSB_CUDA(cudaMemcpyAsync(mask + (distributed ? 0 : fr * s->L.l0), m.p, fr * s->L.n4, cudaMemcpyDefault,
+                                 stream));
+        sync();
+    }
+}
+
+void Domain::prepare(const double* image, const ss_center* c, int n, const ss_seg_params& p, const double* u0) {
+    validate_seg_params(p);
+    validate_centers(g, c, n);
+    require(image != nullptr, "null image");
+    prepared = false;
+    prm = p;
+    for (Slab* s : sp) build_balls(s->rescale_balls, s->gl, s->L.l0, c, n, p.rescale_radius, false);
+
+    // u0 (solver.cpp:416-417): caller's u0 or build_initial, then local_rescale
+    cur = 0;
+    for (Slab* s : sp) {
+        if (u0) {
+            s->upload_state(host_slab(u0, *s), 0);
+        } else {
+            s->initial(s->S[0].pf(), c, n, p.init_v, p.init_R, p.init_profile);
+            s->sync_ghosts_from(0);
+        }
+        s->rescale(0);
+    }
+
+    // local_threshold, heat_smooth x2, face_coefficients (solver.cpp:419-422)
+    std::vector<std::unique_ptr<DevField>> img, th, t1, t2;
+    for (Slab* s : sp) {
+        img.emplace_back(new DevField);
+        th.emplace_back(new DevField);
+        t1.emplace_back(new DevField);
+        t2.emplace_back(new DevField);
+        img.back()->alloc(s->L);
+        th.back()->alloc(s->L);
+        t1.back()->alloc(s->L);
+        t2.back()->alloc(s->L);
+        s->upload(host_slab(image, *s), img.back()->pf());
+    }
+    {
+        std::vector<std::unique_ptr<BallSet>> bsets;
+        std::vector<std::unique_ptr<Dev<double>>> abs;
+        std::vector<std::vector<double>> bad(sp.size(), std::vector<double>(1, (double)INT_MAX));
+        for (size_t s = 0; s < sp.size(); ++s) {
+            Slab& x = *sp[s];
+            bsets.emplace_back(new BallSet);
+            build_balls(*bsets.back(), x.gl, x.L.l0, c, n, 0.0, false);
+            abs.emplace_back(new Dev<double>);
+            abs.back()->alloc(2 * (size_t)std::max(1, bsets.back()->count()));
+            launch_fill(stream, x.L, th[s]->pf(), p.background);
+            if (bsets.back()->count()) x.threshold_minmax(img[s]->pf(), *bsets.back(), abs.back()->p);
+        }
+        sync();
+        for (size_t s = 0; s < sp.size(); ++s) {  // "ball covers no doxels" (preprocess.cpp:89-91)
+            const BallSet& bs = *bsets[s];
+            if (!bs.count()) continue;
+            std::vector<double> h(2 * bs.count());
+            SSB_CUDA(cudaMemcpy(h.data(), abs[s]->p, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            for (int b = 0; b < bs.count(); ++b)
+                if (h[2 * b] > h[2 * b + 1]) bad[s][0] = std::min(bad[s][0], (double)bs.row[b]);
+        }
+        const std::vector<double> allbad = gather_values(bad, 1);
+        const double first = *std::min_element(allbad.begin(), allbad.end());
+        if (first < (double)INT_MAX)
+            throw Error(SS_ERR_VALIDATION,
+                        "local_threshold: ball in centers row " + std::to_string((long long)first + 1) +
+                            " covers no doxels");
+        for (size_t s = 0; s < sp.size(); ++s)
+            if (bsets[s]->count()) sp[s]->threshold_write(img[s]->pf(), th[s]->pf(), *bsets[s], abs[s]->p, p.lambda);
+        sync();
+    }
+    std::vector<PField> thf;
+    for (auto& f : th) thf.push_back(f->pf());
+    exchange(thf, 3);  // halos of the thresholded image (the heat solve reads them)
+
+    std::vector<Triple> b1, b2;
+    for (size_t s = 0; s < sp.size(); ++s) b1.push_back({img[s]->pf(), t1[s]->pf(), t2[s]->pf()});
+    const int r1 = heat_smooth(b1, p.sigma, p.smooth_steps, p.smooth_omega, p.smooth_tol, p.smooth_max_iter);
+    for (size_t s = 0; s < sp.size(); ++s) b2.push_back({th[s]->pf(), b1[s][(r1 + 1) % 3], b1[s][(r1 + 2) % 3]});
+    const int r2 = heat_smooth(b2, p.sigma, p.smooth_steps, p.smooth_omega, p.smooth_tol, p.smooth_max_iter);
+    for (size_t s = 0; s < sp.size(); ++s)
+        sp[s]->face_coefficients(b1[s][r1], b2[s][r2], p.K, p.delta, p.vartheta, nullptr);
+    sync();
+
+    // apply_dirichlet(u, 0) (solver.cpp:425) on every state buffer; halo planes
+    // are refreshed by the exchange at the start of every step
+    for (Slab* s : sp)
+        for (auto& f : s->S) launch_set_ghosts(stream, s->L, f.pf(), 0.0);
+    sync();
+    prepared = true;
+}
+
+void Domain::step(ss_step_diag* diag) {
+    if (!prepared) throw Error(SS_ERR_STATE, "session not prepared");
+    const int roles[3] = {cur, (cur + 1) % 3, (cur + 2) % 3};
+    exchange_role(cur, 3);  // u^{n-1} halos for the face gradients and the first red pass
+    if (profiling) SSB_CUDA(cudaEventRecord(ev[2], stream));
+    for (Slab* s : sp) s->assemble(s->S[cur].pf(), s->have_G, prm.tau, prm.epsilon, nullptr, nullptr, nullptr);
+    if (profiling) SSB_CUDA(cudaEventRecord(ev[3], stream));
+    const bool rel = prm.sor_rel_tol > 0.0;
+    if (rel) {
+        std::vector<double*> loc, all;
+        for (Slab* s : sp) {
+            launch_norm_slices(stream, s->L, s->S[cur].pf(), s->norm_loc.p);
+            loc.push_back(s->norm_loc.p);
+            all.push_back(s->norm_all.p);
+        }
+        if (world > 1) tr->allgather(sp, loc, all, chunk);
+    }
+    // non-finite coefficients anywhere => NumericalError everywhere (solver.cpp:71-75)
+    std::vector<int> fh(sp.size(), 0);
+    for (size_t s = 0; s < sp.size(); ++s)
+        SSB_CUDA(cudaMemcpyAsync(&fh[s], sp[s]->flags.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    sync();
+    std::vector<std::vector<double>> bad(sp.size(), std::vector<double>(1, 0.0));
+    for (size_t s = 0; s < sp.size(); ++s) bad[s][0] = fh[s] ? 1.0 : 0.0;
+    const std::vector<double> anybad = gather_values(bad, 1);
+    if (*std::max_element(anybad.begin(), anybad.end()) > 0.0)
+        throw Error(SS_ERR_NONFINITE, "assemble_step: non-finite coefficient (bad input field?)");
+    if (profiling) {
+        float ms = 0.f;
+        SSB_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[3]));
+        prof.assemble_ms += ms;
+        prof.assemble_n++;
+    }
+    const std::vector<Triple> B = role_triples(roles);
+    std::vector<PField> rhs;
+    for (const Triple& t : B) rhs.push_back(t[0]);  // rhs = guess = u^{n-1} (solver.cpp:430)
+    int rr = 0;
+    const SolveOut o = solve(B, rhs, false, prm.omega, nullptr, prm.sor_tol, rel, prm.sor_rel_tol,
+                             prm.sor_max_iter, false, &rr);
+    if (!o.converged) throw SolverErrT(o);
+    cur = roles[rr];
+    if (prm.rescale_each_step) {
+        if (profiling) SSB_CUDA(cudaEventRecord(ev[2], stream));
+        for (Slab* s : sp) s->rescale(cur);
+        if (profiling) SSB_CUDA(cudaEventRecord(ev[3], stream));
+    }
+    std::vector<double> mh(2 * sp.size(), 0.0);
+    if (diag)
+        for (size_t s = 0; s < sp.size(); ++s) {
+            launch_minmax(stream, sp[s]->L, sp[s]->S[cur].pf(), sp[s]->scratch.p, sp[s]->scal.p + 1);
+            SSB_CUDA(cudaMemcpyAsync(&mh[2 * s], sp[s]->scal.p + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                                     stream));
+        }
+    sync();
+    if (profiling && prm.rescale_each_step) {
+        float ms = 0.f;
+        SSB_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[3]));
+        prof.rescale_ms += ms;
+        prof.rescale_n++;
+    }
+    if (diag) {
+        std::vector<std::vector<double>> mm(sp.size());
+        for (size_t s = 0; s < sp.size(); ++s) mm[s] = {mh[2 * s], mh[2 * s + 1]};
+        const std::vector<double> all = gather_values(mm, 2);
+        double lo = INFINITY, hi = -INFINITY;
+        for (int r = 0; r < world; ++r) {
+            lo = std::min(lo, all[2 * r]);
+            hi = std::max(hi, all[2 * r + 1]);
+        }
+        diag->iterations = o.iterations;
+        diag->residual = o.residual;
+        diag->tol = o.tol;
+        diag->umin = lo;
+        diag->umax = hi;
+    }
+}
+
+double Domain::fixed_sweeps(int n_sweeps) {
+    if (!prepared) throw Error(SS_ERR_STATE, "session not prepared");
+    const int roles[3] = {cur, (cur + 1) % 3, (cur + 2) % 3};
+    exchange_role(cur, 3);
+    for (Slab* s : sp) s->assemble(s->S[cur].pf(), s->have_G, prm.tau, prm.epsilon, nullptr, nullptr, nullptr);
+    const std::vector<Triple> B = role_triples(roles);
+    std::vector<PField> rhs;
+    for (const Triple& t : B) rhs.push_back(t[0]);
+    int rr = 0;
+    const SolveOut o = solve(B, rhs, false, prm.omega, nullptr, 1.0, false, 0.0, n_sweeps, true, &rr);
+    cur = roles[rr];
+    return o.residual;
+}
+
+}  // namespace ssb

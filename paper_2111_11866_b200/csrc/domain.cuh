@@ -1,0 +1,238 @@
+// domain.cuh -- host-side runtime: slabs, transports and the device-resident
+// segment() domain behind the C ABI.
+//
+// A Domain is the grid (or, under NCCL, one rank's share of it) split along the
+// time axis l into slabs (Partition::create semantics, parallel.cpp:9-19).  Each
+// Slab owns its device buffers and a local Layout whose colour parity uses the
+// GLOBAL l; planes 0 and n4+1 of a slab are either global ghosts or halos that a
+// Transport fills with the neighbours' boundary planes (solver.cpp:253-265).
+//   NullTransport   one slab = the whole grid (single GPU; the default)
+//   LocalTransport  several slabs on one device and one stream (tests the
+//                   decomposition bit for bit on a single GPU)
+//   NcclTransport   one slab per process/GPU, ncclSend/Recv of colour-packed
+//                   half-planes and ncclAllGather of per-slice residuals
+#pragma once
+
+#include <array>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace ssb {
+
+template <class T>
+struct Dev {
+    T* p = nullptr;
+    size_t n = 0;
+    Dev() = default;
+    Dev(const Dev&) = delete;
+    Dev& operator=(const Dev&) = delete;
+    ~Dev() { reset(); }
+    void alloc(size_t count) {
+        if (count == n && p) return;
+        reset();
+        if (count == 0) return;
+        SSB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct DevField {
+    Dev<double> c[2];
+    void alloc(const Layout& L) {
+        c[0].alloc(L.cs);
+        c[1].alloc(L.cs);
+    }
+    PField pf() const {
+        PField f;
+        f.c[0] = c[0].p;
+        f.c[1] = c[1].p;
+        return f;
+    }
+};
+
+// Balls grouped into waves preserving table order among overlapping balls.
+struct BallSet {
+    std::vector<Ball> host;     // wave-sorted
+    std::vector<int> row;       // wave-sorted index -> centres-table row
+    std::vector<int> wave_off;  // waves + 1 offsets into host
+    Dev<Ball> dev;
+    int count() const { return (int)host.size(); }
+    int waves() const { return (int)wave_off.size() - 1; }
+};
+// rows whose frame lies in the slab [l0+1, l0+n4_local] only; ball.l is local
+void build_balls(BallSet& bs, const ss_grid& g_local, int l0, const ss_center* c, int n,
+                 double radius, bool fixed_radius);
+
+void require(bool ok, const std::string& msg);
+void validate_grid(const ss_grid* g);
+void validate_solver(double tau, double eps, double omega, double tol, int max_iter, int n_steps);
+void validate_smoothing(double sigma, int steps, double tol, int max_iter, double omega);
+void validate_edge(double K, double delta, double vartheta);
+void validate_centers(const ss_grid& g, const ss_center* c, int n);
+void validate_seg_params(const ss_seg_params& p);
+
+struct SolveOut {
+    int iterations = 0;
+    double residual = 0.0, tol = 0.0;
+    bool converged = false;
+};
+
+struct SolverErrT : Error {
+    int iterations;
+    double residual;
+    explicit SolverErrT(const SolveOut& o);
+};
+
+// ------------------------------------------------------------------ slab
+struct Slab {
+    ss_grid gl{};   // local grid (n4 = owned slices)
+    Layout L{};
+    int index = 0;  // position of the slab along l (= rank for NCCL)
+    cudaStream_t stream = nullptr;  // borrowed from the Domain
+
+    DevField S[3];       // rotating state buffers
+    DevField rhs_sep;    // explicit rhs (per-call redblack_sor)
+    Dev<float> coef[2];
+    Dev<double> G[2];
+    bool have_G = false;
+    Dev<double> part[2];
+    Dev<double> slice_res;   // chunk entries (zero padded)
+    Dev<double> all_slices;  // world * chunk (gathered), unused when world == 1
+    Dev<double> norm_loc, norm_all;
+    Dev<double> gloc, gall;  // small host-driven gathers (k <= 8 values per slab)
+    Dev<SorState> st;
+    Dev<double> scratch, scal;
+    Dev<int> flags;
+    Dev<double> stage, stage8;
+    BallSet rescale_balls;
+
+    Slab(const ss_grid& global, int l0, int n4_local, int index, int chunk, int world,
+         cudaStream_t s);
+    double* stage_p();
+    double* stage8_p();
+    void upload(const double* host_padded, PField dst, PField twin0 = PField(), PField twin1 = PField());
+    void upload_state(const double* host_padded, int role);
+    void download(PField src, double* host_padded);
+    void sync_ghosts_from(int role);
+    void assemble(PField u, bool with_G, double tau, double eps, double* off_out, double* diag_out,
+                  double* abar_out);
+    void face_coefficients(PField I0s, PField ITs, double K, double delta, double vartheta,
+                           double* G_out);
+    void rescale(int role);
+    void threshold_minmax(PField img, const BallSet& bs, double* ab);
+    void threshold_write(PField img, PField out, const BallSet& bs, const double* ab, double lambda);
+    void initial(PField u, const ss_center* c, int n, double v, double R, int profile);
+    SorArgs sor_args(const PField B[3], const PField& rhs, bool heat, double omega,
+                     const double hc[4], int world) const;
+};
+
+// ------------------------------------------------------------------ transports
+struct Transport {
+    virtual ~Transport() = default;
+    // owned boundary planes of F[s] (colour mask: 1 red, 2 black) into the
+    // l-neighbours' halo planes
+    virtual void exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours) = 0;
+    // every slab's local[s] (chunk doubles) -> all[s'][rank * chunk] for all s'
+    virtual void allgather(std::vector<Slab*>& slabs, const std::vector<double*>& local,
+                           const std::vector<double*>& all, int chunk) = 0;
+};
+
+struct NullTransport : Transport {
+    void exchange(std::vector<Slab*>&, const std::vector<PField>&, int) override {}
+    void allgather(std::vector<Slab*>&, const std::vector<double*>&, const std::vector<double*>&,
+                   int) override {}
+};
+
+struct LocalTransport : Transport {
+    void exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours) override;
+    void allgather(std::vector<Slab*>& slabs, const std::vector<double*>& local,
+                   const std::vector<double*>& all, int chunk) override;
+};
+
+std::unique_ptr<Transport> make_nccl_transport(const unsigned char* uid, int rank, int world);
+void nccl_unique_id(unsigned char out[128]);
+
+// ------------------------------------------------------------------ domain
+struct Domain {
+    ss_grid g{};        // global grid
+    int world = 1;      // total slabs (ranks for NCCL)
+    int chunk = 0;      // ceil(n4 / world)
+    int device = 0;
+    bool distributed = false;  // NCCL: slabs.size() == 1 < world
+    cudaStream_t stream = nullptr, cap_stream = nullptr;
+    std::vector<std::unique_ptr<Slab>> slabs;
+    std::vector<Slab*> sp;  // raw pointers, rank order
+    std::unique_ptr<Transport> tr;
+    int cur = 0;
+
+    bool prepared = false;
+    ss_seg_params prm{};
+
+    int loop_mode = 1;
+    bool profiling = false;
+    ss_profile prof{};
+    SorState* st_host = nullptr;
+    int* flag_host = nullptr;
+    double* scal_host = nullptr;
+    struct GraphEntry;
+    std::vector<std::unique_ptr<GraphEntry>> graphs;
+    std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+    // world == 1 (single GPU) or a local group of n_slabs on one device
+    Domain(const ss_grid& grid, int device, int n_slabs);
+    // one rank of an NCCL job
+    Domain(const ss_grid& grid, int device, int rank, int world, const unsigned char* uid);
+    ~Domain();
+
+    void sync();
+    int slabs_local() const { return (int)sp.size(); }
+    bool single() const { return sp.size() == 1 && world == 1; }
+    long long host_plane() const;  // padded doubles per l-plane of a host array
+    const double* host_slab(const double* base, const Slab& s) const;
+    double* host_slab(double* base, const Slab& s) const;
+
+    std::vector<PField> role_fields(int role) const;
+    void exchange_role(int role, int colours);
+    void exchange(const std::vector<PField>& F, int colours);
+    // k doubles from every local slab -> world*k doubles in rank order, identical on all ranks
+    std::vector<double> gather_values(const std::vector<std::vector<double>>& per_slab, int k);
+
+    using Triple = std::array<PField, 3>;
+    std::vector<Triple> role_triples(const int roles[3]) const;
+    // red-black SOR on every slab: guess B[s][0] (never written), rhs[s]; the
+    // result lands in B[s][*result].  Non-convergence is reported, not thrown.
+    SolveOut solve(const std::vector<Triple>& B, const std::vector<PField>& rhs, bool heat,
+                   double omega, const double hc[4], double tol_abs, bool use_norm, double rel,
+                   int max_iter, bool fixed, int* result);
+    // heat_smooth over per-slab buffer triples; returns the index of the result
+    int heat_smooth(const std::vector<Triple>& B, double sigma, int steps, double omega, double tol,
+                    int max_iter);
+    void mirror_all(const std::vector<PField>& F);
+
+    void set_u(const double* host);
+    void get_u(double* host);
+    void get_mask(double level, uint8_t* mask);
+    void prepare(const double* image, const ss_center* c, int n, const ss_seg_params& p,
+                 const double* u0);
+    void step(ss_step_diag* diag);
+    double fixed_sweeps(int n_sweeps);
+
+private:
+    void init_common();
+    cudaEvent_t pool_event(size_t idx);
+    cudaGraphExec_t graph_for(const SorArgs& a, bool heat);
+    void body_single(const SorArgs& a, bool heat, cudaEvent_t* ev4);
+    void body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>& B, bool heat, int n,
+                    cudaEvent_t* ev4);
+};
+
+}  // namespace ssb

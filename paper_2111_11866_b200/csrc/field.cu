@@ -36,7 +36,7 @@ __device__ __forceinline__ Pos decode_interior(const Layout& L, long long e) {
 }
 
 __device__ __forceinline__ double* at(const Layout& L, PField f, int i, int j, int k, int l) {
-    return f.c[Layout::colour(i, j, k, l)] + L.packed(i, j, k, l);
+    return f.c[L.colour(i, j, k, l)] + L.packed(i, j, k, l);
 }
 
 __global__ void pack_kernel(const Layout L, const double* __restrict__ src, PField dst, PField t0,
@@ -44,7 +44,7 @@ __global__ void pack_kernel(const Layout L, const double* __restrict__ src, PFie
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (e >= L.P) return;
     const Pos p = decode_padded(L, e);
-    const int c = Layout::colour(p.i, p.j, p.k, p.l);
+    const int c = L.colour(p.i, p.j, p.k, p.l);
     const long long q = p.row * L.W + (p.i >> 1);
     const double v = src[e];
     dst.c[c][q] = v;
@@ -58,7 +58,7 @@ __global__ void unpack_kernel(const Layout L, PField src, double* __restrict__ d
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (e >= L.P) return;
     const Pos p = decode_padded(L, e);
-    dst[e] = src.c[Layout::colour(p.i, p.j, p.k, p.l)][p.row * L.W + (p.i >> 1)];
+    dst[e] = src.c[L.colour(p.i, p.j, p.k, p.l)][p.row * L.W + (p.i >> 1)];
 }
 
 __global__ void fill_kernel(const Layout L, PField f, double v, int ghosts_only) {
@@ -68,7 +68,7 @@ __global__ void fill_kernel(const Layout L, PField f, double v, int ghosts_only)
     const bool ghost = p.i == 0 || p.i > L.n1 || p.j == 0 || p.j > L.n2 || p.k == 0 ||
                        p.k > L.n3 || p.l == 0 || p.l > L.n4;
     if (ghosts_only && !ghost) return;
-    f.c[Layout::colour(p.i, p.j, p.k, p.l)][p.row * L.W + (p.i >> 1)] = v;
+    f.c[L.colour(p.i, p.j, p.k, p.l)][p.row * L.W + (p.i >> 1)] = v;
 }
 
 // grid.cpp:138-156, one launch per axis (axis order 0..3 carries edges/corners)
@@ -79,6 +79,8 @@ __global__ void mirror_kernel(const Layout L, PField f, int axis) {
     int c[4] = {p.i, p.j, p.k, p.l};
     const int hi[4] = {L.n1 + 1, L.n2 + 1, L.n3 + 1, L.n4 + 1};
     if (c[axis] != 0 && c[axis] != hi[axis]) return;
+    // slab halo planes are the neighbours' data, not ghosts
+    if (axis == 3 && ((c[3] == 0 && !L.glo) || (c[3] == hi[3] && !L.ghi))) return;
     const int dst[4] = {c[0], c[1], c[2], c[3]};
     c[axis] += c[axis] == 0 ? 1 : -1;
     *at(L, f, dst[0], dst[1], dst[2], dst[3]) = *at(L, f, c[0], c[1], c[2], c[3]);
@@ -97,7 +99,7 @@ __global__ void copy_ghosts_kernel(const Layout L, PField dst, PField src) {
     const bool ghost = p.i == 0 || p.i > L.n1 || p.j == 0 || p.j > L.n2 || p.k == 0 ||
                        p.k > L.n3 || p.l == 0 || p.l > L.n4;
     if (!ghost) return;
-    const int c = Layout::colour(p.i, p.j, p.k, p.l);
+    const int c = L.colour(p.i, p.j, p.k, p.l);
     const long long q = p.row * L.W + (p.i >> 1);
     dst.c[c][q] = src.c[c][q];
 }
@@ -157,6 +159,23 @@ __global__ void __launch_bounds__(256) norm_part_kernel(const Layout L, PField f
     }
     s = bsum(s);
     if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// one block per owned slice l (1-based local), fixed-order block reduction
+__global__ void __launch_bounds__(256) norm_slices_kernel(const Layout L, PField f, double* out) {
+    const int l = blockIdx.x + 1;
+    const long long N = (long long)L.n1 * L.n2 * L.n3;
+    double s = 0.0;
+    for (long long e = threadIdx.x; e < N; e += blockDim.x) {
+        const int i = (int)(e % L.n1) + 1;
+        const long long r = e / L.n1;
+        const int j = (int)(r % L.n2) + 1;
+        const int k = (int)(r / L.n2) + 1;
+        const double v = *at(L, f, i, j, k, l);
+        s += v * v;
+    }
+    s = bsum(s);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
 __global__ void __launch_bounds__(256) sum_final_kernel(const double* part, int n, double* out) {
@@ -237,8 +256,8 @@ void launch_set_ghosts(cudaStream_t s, const Layout& L, PField f, double v) {
     SSB_LAUNCHED();
 }
 
-void launch_mirror_ghosts(cudaStream_t s, const Layout& L, PField f) {
-    for (int axis = 0; axis < 4; ++axis) {
+void launch_mirror_ghosts(cudaStream_t s, const Layout& L, PField f, int a0, int a1) {
+    for (int axis = a0; axis < a1; ++axis) {
         mirror_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, f, axis);
         SSB_LAUNCHED();
     }
@@ -255,6 +274,11 @@ void launch_norm_sq(cudaStream_t s, const Layout& L, PField f, double* scratch, 
     norm_part_kernel<<<kReduceBlocks, 256, 0, s>>>(L, f, scratch);
     SSB_LAUNCHED();
     sum_final_kernel<<<1, 256, 0, s>>>(scratch, kReduceBlocks, out);
+    SSB_LAUNCHED();
+}
+
+void launch_norm_slices(cudaStream_t s, const Layout& L, PField f, double* out) {
+    norm_slices_kernel<<<L.n4, 256, 0, s>>>(L, f, out);
     SSB_LAUNCHED();
 }
 

@@ -30,7 +30,9 @@ struct SorArgs {
     const double* rhs[2];   // colour-packed rhs
     const float* coef[2];   // colour-packed fp32 off-diagonals, 8 per doxel (kFaceOffsets order)
     double* part[2];        // per-block squared-residual partials of the red / black pass
-    double* slice_res;      // per-slice residual (solver.cpp:195-199 slice_residual_sq_)
+    double* slice_res;      // per-slice residual of the owned slices (solver.cpp:195-199)
+    const double* all_slices;  // residuals of all n4g slices in global order (== slice_res on 1 slab)
+    int inline_decide;      // single slab: finalize also decides
     SorState* st;
     double omega, keep;
     double hc[4];           // heat stencil constants float(-dt/h_a^2) (solver.cpp:100-110)
@@ -57,9 +59,14 @@ constexpr int kPassBatch = SSB_PASS_BATCH;  // doxels whose loads a thread issue
 
 void pass_tiles(const Layout& L, SorArgs& a);
 dim3 pass_grid(const Layout& L);
-void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_sq,
-                     double rel, int max_iter, int fixed);
+void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_slices,
+                     int n_slices, double rel, int max_iter, int fixed);
+// single-slab loop body: red, finalize (inline decision), black
 void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* ev /*4 or null*/);
+// pieces for the multi-slab body (halo exchange / all-gather between them)
+void launch_sor_pass(cudaStream_t s, const SorArgs& a, int colour, bool heat);
+void launch_sor_finalize(cudaStream_t s, const SorArgs& a);
+void launch_sor_decide(cudaStream_t s, const SorArgs& a);
 
 // ---------------------------------------------------------------- assembly
 struct AsmArgs {
@@ -109,10 +116,13 @@ void launch_fill(cudaStream_t s, const Layout& L, PField f, double v);
 void launch_set_ghosts(cudaStream_t s, const Layout& L, PField f, double v);
 // ghost doxels of src copied into dst
 void launch_copy_ghosts(cudaStream_t s, const Layout& L, PField dst, PField src);
-void launch_mirror_ghosts(cudaStream_t s, const Layout& L, PField f);
+// grid.cpp:138-156 axes [a0, a1); axis 3 only at global boundaries
+void launch_mirror_ghosts(cudaStream_t s, const Layout& L, PField f, int a0 = 0, int a1 = 4);
 void launch_copy_field(cudaStream_t s, const Layout& L, PField dst, PField src);
 // deterministic interior reductions; out[0] = sum of squares or (min,max)
 void launch_norm_sq(cudaStream_t s, const Layout& L, PField f, double* scratch, double* out);
+// per owned slice: sum of squares over the slice's interior (fixed order)
+void launch_norm_slices(cudaStream_t s, const Layout& L, PField f, double* out);
 void launch_minmax(cudaStream_t s, const Layout& L, PField f, double* scratch, double* out2);
 void launch_mask(cudaStream_t s, const Layout& L, PField f, double level, uint8_t* mask);
 constexpr int kReduceBlocks = 592;  // 4 x 148 SMs; fixed => deterministic order

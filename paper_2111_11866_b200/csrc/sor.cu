@@ -68,8 +68,8 @@ __device__ __forceinline__ void load_doxel(const SorArgs& a, const float* __rest
         d.c[3] = j < L.n2 ? (float)a.hc[1] : 0.f;
         d.c[4] = k > 1 ? (float)a.hc[2] : 0.f;
         d.c[5] = k < L.n3 ? (float)a.hc[2] : 0.f;
-        d.c[6] = l > 1 ? (float)a.hc[3] : 0.f;
-        d.c[7] = l < L.n4 ? (float)a.hc[3] : 0.f;
+        d.c[6] = l + L.l0 > 1 ? (float)a.hc[3] : 0.f;  // global l boundaries
+        d.c[7] = l + L.l0 < L.n4g ? (float)a.hc[3] : 0.f;
     } else {
         const float4* cp = reinterpret_cast<const float4*>(cf + p * 8);
         const float4 lo = __ldcs(cp);
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(con
 #pragma unroll
                 for (int b = 0; b < kPassBatch; ++b) {  // all loads of the batch first
                     const int k = k0 + kb + b;
-                    const int i = 1 + ((1 + j + k + l + C) & 1) + 2 * q;
+                    const int i = 1 + ((1 + j + k + l + L.lpar + C) & 1) + 2 * q;
                     ok[b] = k <= L.n3 && i <= L.n1;
                     if (ok[b]) load_doxel<C, HEAT>(a, cf, rh, uc, uo, i, j, k, l, d[b]);
                 }
@@ -181,7 +181,33 @@ __global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(con
     }
 }
 
-// grid = n4 blocks (one per local l-slice), 256 threads
+// Decision of iteration n-1 from the per-slice residuals of ALL slices in
+// global l order (solver.cpp:195-205): identical on every rank.
+__device__ void decide(const SorArgs& a, SorState* st, int n) {
+    if (n >= 2) {
+        double total = 0.0;
+        for (int l = 0; l < a.L.n4g; ++l) total += __ldcg(a.all_slices + l);
+        const double res = sqrt(total);
+        const int it = n - 1;
+        st->residual = res;
+        st->iterations = it;
+        if (!st->fixed && res <= st->tol) {
+            st->done = 1;
+            st->converged = 1;
+        } else if (it >= st->max_iter) {
+            st->done = 1;
+            st->converged = st->fixed;
+        }
+    }
+    st->n_black = n;
+    st->n_red = n + 1;
+    if (a.use_cond) cudaGraphSetConditional(a.cond, st->done ? 0u : 1u);
+}
+
+// grid = local n4 blocks (one per owned slice), 256 threads: slice_res[l] =
+// black partials of black(n-1) + red partials of red(n), each summed in fixed
+// order.  With inline_decide (single slab) the last block also takes the
+// decision; otherwise the slices are all-gathered first (sor_decide).
 __global__ void __launch_bounds__(256) sor_finalize(const SorArgs a) {
     SorState* st = a.st;
     if (*(volatile int*)&st->done) return;
@@ -200,6 +226,7 @@ __global__ void __launch_bounds__(256) sor_finalize(const SorArgs a) {
         b = block_sum(b);
         if (threadIdx.x == 0) a.slice_res[l] = b + r;  // slice_black + red (solver.cpp:359)
     }
+    if (!a.inline_decide) return;
     __shared__ int last;
     __threadfence();
     __syncthreads();
@@ -208,28 +235,18 @@ __global__ void __launch_bounds__(256) sor_finalize(const SorArgs a) {
     if (!last || threadIdx.x != 0) return;
     __threadfence();
     st->counter = 0;
-    if (n >= 2) {
-        double total = 0.0;
-        for (int l = 0; l < (int)gridDim.x; ++l) total += __ldcg(a.slice_res + l);
-        const double res = sqrt(total);
-        const int it = n - 1;
-        st->residual = res;
-        st->iterations = it;
-        if (!st->fixed && res <= st->tol) {
-            st->done = 1;
-            st->converged = 1;
-        } else if (it >= st->max_iter) {
-            st->done = 1;
-            st->converged = st->fixed;
-        }
-    }
-    st->n_black = n;
-    st->n_red = n + 1;
-    if (a.use_cond) cudaGraphSetConditional(a.cond, st->done ? 0u : 1u);
+    decide(a, st, n);
 }
 
-__global__ void sor_init(SorState* st, double tol, const double* norm_sq, double rel, int max_iter,
-                         int fixed) {
+__global__ void sor_decide(const SorArgs a) {
+    SorState* st = a.st;
+    if (*(volatile int*)&st->done) return;
+    decide(a, st, *(volatile int*)&st->n_red);
+}
+
+// tol = rel * sqrt(sum over all slices in global l order) when norm_slices is given
+__global__ void sor_init(SorState* st, double tol, const double* norm_slices, int n_slices, double rel,
+                         int max_iter, int fixed) {
     st->n_red = 1;
     st->n_black = 0;
     st->done = 0;
@@ -239,7 +256,13 @@ __global__ void sor_init(SorState* st, double tol, const double* norm_sq, double
     st->fixed = fixed;
     st->counter = 0;
     st->residual = 0.0;
-    st->tol = norm_sq ? rel * sqrt(*norm_sq) : tol;
+    if (norm_slices) {
+        double s = 0.0;
+        for (int l = 0; l < n_slices; ++l) s += norm_slices[l];
+        st->tol = rel * sqrt(s);
+    } else {
+        st->tol = tol;
+    }
 }
 
 }  // namespace
@@ -271,9 +294,36 @@ static int resident_blocks() {
     return blocks;
 }
 
-void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_sq, double rel,
-                     int max_iter, int fixed) {
-    sor_init<<<1, 1, 0, s>>>(st, tol, norm_sq, rel, max_iter, fixed);
+void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_slices,
+                     int n_slices, double rel, int max_iter, int fixed) {
+    sor_init<<<1, 1, 0, s>>>(st, tol, norm_slices, n_slices, rel, max_iter, fixed);
+    SSB_LAUNCHED();
+}
+
+void launch_sor_pass(cudaStream_t s, const SorArgs& a, int colour, bool heat) {
+    const unsigned grid = (unsigned)std::min<long long>(a.tiles, resident_blocks());
+    const dim3 block(kPassBX, kPassBY);
+    if (colour == 0) {
+        if (heat)
+            sor_pass<0, true><<<grid, block, 0, s>>>(a);
+        else
+            sor_pass<0, false><<<grid, block, 0, s>>>(a);
+    } else {
+        if (heat)
+            sor_pass<1, true><<<grid, block, 0, s>>>(a);
+        else
+            sor_pass<1, false><<<grid, block, 0, s>>>(a);
+    }
+    SSB_LAUNCHED();
+}
+
+void launch_sor_finalize(cudaStream_t s, const SorArgs& a) {
+    sor_finalize<<<a.L.n4, 256, 0, s>>>(a);
+    SSB_LAUNCHED();
+}
+
+void launch_sor_decide(cudaStream_t s, const SorArgs& a) {
+    sor_decide<<<1, 1, 0, s>>>(a);
     SSB_LAUNCHED();
 }
 

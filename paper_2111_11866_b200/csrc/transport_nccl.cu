@@ -1,0 +1,121 @@
+// transport_nccl.cu -- the multi-GPU transport: one slab per rank/GPU.
+//
+// Per colour pass the just-updated colour of the first and last owned planes
+// (one contiguous colour-packed block each, Layout::plane() doubles) goes to
+// the l-neighbours with grouped ncclSend/ncclRecv on the session stream
+// (the paper's Isend/Irecv of overlap slices; the
+// reference's pull_halos, solver.cpp:253-265).  Per-slice residual partials are
+// all-gathered and summed in global l order by every rank, so the stopping
+// decision -- and hence every iterate -- is independent of the GPU count.
+//
+// NCCL is loaded with dlopen("libnccl.so.2") on first use (torch's bundled
+// copy when torch has loaded it, else the system library); nothing links
+// against it, so single-GPU use never needs it.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "domain.cuh"
+
+namespace ssb {
+
+namespace {
+
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& api() {
+    static NcclApi a;
+    static std::once_flag once;
+    static std::string err;
+    std::call_once(once, [] {
+        a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!a.h) {
+            err = dlerror() ? dlerror() : "dlopen failed";
+            return;
+        }
+#define SSB_SYM(name, field) a.field = reinterpret_cast<decltype(a.field)>(dlsym(a.h, name))
+        SSB_SYM("ncclGetUniqueId", GetUniqueId);
+        SSB_SYM("ncclCommInitRank", CommInitRank);
+        SSB_SYM("ncclCommDestroy", CommDestroy);
+        SSB_SYM("ncclGroupStart", GroupStart);
+        SSB_SYM("ncclGroupEnd", GroupEnd);
+        SSB_SYM("ncclSend", Send);
+        SSB_SYM("ncclRecv", Recv);
+        SSB_SYM("ncclAllGather", AllGather);
+        SSB_SYM("ncclGetErrorString", GetErrorString);
+#undef SSB_SYM
+    });
+    if (!a.h || !a.AllGather || !a.Send || !a.CommInitRank)
+        throw Error(SS_ERR_NCCL, "NCCL unavailable: " + (err.empty() ? std::string("missing symbols") : err));
+    return a;
+}
+
+void check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw Error(SS_ERR_NCCL, std::string(what) + ": " + (api().GetErrorString ? api().GetErrorString(r) : "?"));
+}
+
+struct NcclTransport : Transport {
+    ncclComm_t comm = nullptr;
+    int rank, world;
+    NcclTransport(const unsigned char* uid, int r, int w) : rank(r), world(w) {
+        ncclUniqueId id;
+        std::memcpy(id.internal, uid, NCCL_UNIQUE_ID_BYTES);
+        check(api().CommInitRank(&comm, w, id, r), "ncclCommInitRank");
+    }
+    ~NcclTransport() override {
+        if (comm) api().CommDestroy(comm);
+    }
+    void exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours) override {
+        Slab& s = *slabs[0];
+        const size_t P1 = (size_t)s.L.plane();
+        const int n4 = s.L.n4;
+        NcclApi& a = api();
+        check(a.GroupStart(), "ncclGroupStart");
+        for (int c = 0; c < 2; ++c) {
+            if (!(colours & (1 << c))) continue;
+            double* f = F[0].c[c];
+            if (rank > 0) {
+                check(a.Send(f + P1, P1, ncclDouble, rank - 1, comm, s.stream), "ncclSend");
+                check(a.Recv(f, P1, ncclDouble, rank - 1, comm, s.stream), "ncclRecv");
+            }
+            if (rank + 1 < world) {
+                check(a.Send(f + (size_t)n4 * P1, P1, ncclDouble, rank + 1, comm, s.stream), "ncclSend");
+                check(a.Recv(f + (size_t)(n4 + 1) * P1, P1, ncclDouble, rank + 1, comm, s.stream), "ncclRecv");
+            }
+        }
+        check(a.GroupEnd(), "ncclGroupEnd");
+    }
+    void allgather(std::vector<Slab*>& slabs, const std::vector<double*>& local, const std::vector<double*>& all,
+                   int chunk) override {
+        check(api().AllGather(local[0], all[0], (size_t)chunk, ncclDouble, comm, slabs[0]->stream),
+              "ncclAllGather");
+    }
+};
+
+}  // namespace
+
+std::unique_ptr<Transport> make_nccl_transport(const unsigned char* uid, int rank, int world) {
+    return std::unique_ptr<Transport>(new NcclTransport(uid, rank, world));
+}
+
+void nccl_unique_id(unsigned char out[128]) {
+    ncclUniqueId id;
+    check(api().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+}
+
+}  // namespace ssb

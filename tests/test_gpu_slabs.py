@@ -1,0 +1,72 @@
+"""The t-slab decomposition on one GPU: a grid split into n slabs
+that exchange halo planes and all-gather per-slice residuals must give the
+single-slab result bit for bit (same iterates, same iteration counts) -- the
+property the multi-GPU NCCL path relies on."""
+import os
+
+import numpy as np
+import pytest
+
+import _cases as cs
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def run(ss, g, image, rows, params, n_slabs, steps, u0=None, mode=0):
+    with ss.Session(g, n_slabs=n_slabs) as s:
+        s.set_loop_mode(mode)
+        s.prepare(image, rows, params, u0)
+        diags = [s.step() for _ in range(steps)]
+        return s.get_u(), [d["iterations"] for d in diags], diags, s.get_mask(0.5)
+
+
+@pytest.mark.parametrize("n_slabs", [2, 3, 6])
+def test_slabs_match_single_golden(gpu, n_slabs):
+    d = dict(np.load(os.path.join(GOLD, "segment.npz")))
+    dims = tuple(int(x) for x in d["dims"])
+    h = float(d["h"])
+    g = gpu.Grid.make(dims, h)
+    p = gpu.seg_params(tau=h, epsilon=1e-3, omega=1.4, n_steps=3, sigma=np.sqrt(2) * h, K=200.0,
+                       delta=0.5, vartheta=0.5, rescale_radius=3.0, sor_rel_tol=1e-8)
+    u, its, diags, mask = run(gpu, g, d["image"], d["rows"], p, n_slabs, 3)
+    assert its == list(d["iters_rel"])
+    assert np.array_equal(u.view(np.uint64), d["u_rel"].view(np.uint64))
+    assert np.array_equal(mask, (d["u_rel"][g.interior] >= 0.5).astype(np.uint8))
+    np.testing.assert_allclose([x["tol"] for x in diags], d["tol_rel"], rtol=1e-13)
+
+
+@pytest.mark.parametrize("dims,n_slabs", [((9, 7, 6, 7), 3), ((10, 8, 5, 9), 2), ((8, 6, 6, 5), 5)])
+def test_slabs_odd_offsets(gpu, oracle, dims, n_slabs):
+    """Slab offsets with odd l0 exercise the global colour parity; compared with the oracle."""
+    from oracle import oracle_py as op
+    h = 1.0 / dims[0]
+    g = gpu.Grid.make(dims, h)
+    img = cs.f32_image(dims, 5)
+    rows = [(f, (dims[0] - 1) / 2, (dims[1] - 1) / 2, (dims[2] - 1) / 2, 1.5) for f in range(dims[3])]
+    rows += [(dims[3] // 2, 1.0, 1.0, 1.0, 2.0)]
+    kw = dict(tau=h, epsilon=1e-3, omega=1.4, n_steps=2, sigma=np.sqrt(2) * h, K=300.0, delta=0.5,
+              vartheta=0.5, rescale_radius=3.0, sor_rel_tol=1e-8, smooth_steps=2)
+    u, its, _, _ = run(gpu, g, img, rows, gpu.seg_params(**kw), n_slabs, 2)
+    st, uo, info = op.oracle().segment(op.Grid.make(dims, h), img, rows, op.seg_params(**kw))
+    assert st == 0
+    assert its == [x["iterations"] for x in info["diags"]]
+    assert np.array_equal(u.view(np.uint64), uo.view(np.uint64))
+
+
+def test_slabs_fixed_sweeps(gpu):
+    dims = (12, 10, 8, 8)
+    h = 1.0 / 12
+    g = gpu.Grid.make(dims, h)
+    img = cs.f32_image(dims, 9)
+    rows = [(f, 5.5, 4.5, 3.5, 1.5) for f in range(dims[3])]
+    p = gpu.seg_params(tau=h, epsilon=1e-3, omega=1.4, n_steps=1, sigma=np.sqrt(2) * h, K=100.0,
+                       delta=0.5, vartheta=0.5, rescale_radius=3.0)
+    outs = []
+    for n in (1, 4):
+        with gpu.Session(g, n_slabs=n) as s:
+            s.prepare(img, rows, p)
+            r = s.fixed_sweeps(20)
+            outs.append((r, s.get_u()))
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][1].view(np.uint64), outs[1][1].view(np.uint64))
