@@ -178,22 +178,35 @@ def main():
     args.warmup = max(3, args.warmup)
 
     import workloads
-    wl = workloads.CONFIGS[args.config]()
+    rank, world, local = env_rank()
     if args.impl == "reference":
-        return run_reference(args, wl)
+        # the reference CPU solver on one 64^4 replica of the workload (its host cores do not
+        # scale with the GPU count; the metric is a throughput, comparable across N)
+        return run_reference(args, workloads.CONFIGS[args.config]())
 
     import torch
     import paper_2111_11866_b200 as ss
+    from paper_2111_11866_b200 import dist as ssd
 
-    rank, world, local = env_rank()
     torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
+    uid = None
+    force_dist = os.environ.get("SUBSURF_FORCE_DIST") == "1"  # exercise the NCCL path at N=1
+    if world > 1 or force_dist:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.config != "config1":
+            raise SystemExit("multi-GPU bench supports config1 (weak scaling along t)")
+        # weak scaling: config 1 replicated along t, one 64^4 replica per GPU; each rank
+        # builds only its slab (owned planes + one halo/ghost plane per side)
+        lb, cnt = ssd.partition(64 * world, world)[rank]
+        wl = workloads.config1(replicas=world, planes=(lb - 1, lb + cnt))
+        uid = ssd.broadcast_uid(ss.nccl_unique_id() if rank == 0 else None)
+    else:
+        wl = workloads.CONFIGS[args.config]()
 
     g = ss.Grid.make(wl.dims, wl.h)
     p = ss.seg_params(**{**wl.params, "n_steps": args.warmup + args.steps})
-    sess = ss.Session(g, device=local)
+    sess = ss.Session(g, device=local, dist=(rank, world, uid) if (world > 1 or force_dist) else None)
     sess.set_loop_mode(args.loop_mode)
     stream = torch.cuda.ExternalStream(sess.stream, device=torch.device("cuda", local))
 
@@ -225,10 +238,10 @@ def main():
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = world * wl.n_interior * sweeps / (ms_max * 1e-3)
+    value = wl.n_interior * sweeps / (ms_max * 1e-3)  # whole grid (all ranks) per second
 
     # ---------------- e2e: same steps through the public API with host buffers
-    P = g.padded_size()
+    P = int(np.prod(sess.host_shape))  # this rank's host array (whole grid or its slab)
     host_in = torch.empty(P, dtype=torch.float64, pin_memory=True)
     host_out = torch.empty(P, dtype=torch.float64, pin_memory=True)
     sess.prepare(wl.image, wl.rows, p, wl.u0)
@@ -252,7 +265,7 @@ def main():
     t = torch.tensor([ms_e2e], device="cuda")
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = world * wl.n_interior * sweeps_e2e / (float(t.item()) * 1e-3)
+    e2e_value = wl.n_interior * sweeps_e2e / (float(t.item()) * 1e-3)
 
     # ---------------- roofline of the dominant kernel (SOR colour pass), event-timed
     sess.prepare(wl.image, wl.rows, p, wl.u0)
@@ -265,7 +278,8 @@ def main():
     pr = sess.profile()
     sess.set_profiling(False)
     pass_ms = (pr["red_ms"] + pr["black_ms"]) / max(1, pr["red_n"] + pr["black_n"])
-    bytes_per_pass = SURVEY_BYTES_PER_SWEEP * wl.n_interior / 2.0
+    n_local = wl.n_interior // world  # doxels of this rank's slab (weak scaling: equal slabs)
+    bytes_per_pass = SURVEY_BYTES_PER_SWEEP * n_local / 2.0
     achieved = bytes_per_pass / (pass_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
     traffic = None
@@ -283,10 +297,11 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl.name, "dims": list(wl.dims), "sor_rel_tol": 1e-8,
-                       "omega": wl.params["omega"], "parallelism": "replicas" if world > 1 else "1 GPU",
+                       "omega": wl.params["omega"],
+                       "parallelism": f"t-slabs x{world} (NCCL halo exchange per colour pass)" if world > 1 else "1 GPU",
                        "sweeps_timed": int(sweeps), "l2": "inputs larger than L2 (state+rhs+coef+G ~2.5 GB)"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * P,
-                    "d2h_bytes_per_step": 8 * P},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * P * world,
+                    "d2h_bytes_per_step": 8 * P * world},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -70,3 +70,22 @@ def test_slabs_fixed_sweeps(gpu):
             outs.append((r, s.get_u()))
     assert outs[0][0] == outs[1][0]
     assert np.array_equal(outs[0][1].view(np.uint64), outs[1][1].view(np.uint64))
+
+
+def test_nccl_session_world1(gpu):
+    """The NCCL transport end to end at world size 1 (dlopen, comm init, all-gather
+    of slice residuals, slab-shaped host arrays): identical to the plain session."""
+    d = dict(np.load(os.path.join(GOLD, "segment.npz")))
+    dims = tuple(int(x) for x in d["dims"])
+    h = float(d["h"])
+    g = gpu.Grid.make(dims, h)
+    p = gpu.seg_params(tau=h, epsilon=1e-3, omega=1.4, n_steps=3, sigma=np.sqrt(2) * h, K=200.0,
+                       delta=0.5, vartheta=0.5, rescale_radius=3.0, sor_rel_tol=1e-8)
+    uid = gpu.nccl_unique_id()
+    with gpu.Session(g, dist=(0, 1, uid)) as s:
+        assert s.distributed and s.host_shape == g.shape and s.l_begin == 1 and s.l_count == dims[3]
+        s.prepare(d["image"], d["rows"], p)
+        its = [s.step()["iterations"] for _ in range(3)]
+        u = s.get_u()
+    assert its == list(d["iters_rel"])
+    assert np.array_equal(u.view(np.uint64), d["u_rel"].view(np.uint64))

@@ -93,34 +93,78 @@ def config0() -> Workload:
                     notes=dict(noise=0.05, threshold_radius=1, rescale_radius=12))
 
 
-def config1() -> Workload:
-    """64^4, two moving Gaussian blobs (peak 1, radius 0.12), bg 0.1, N(0, 0.08^2),
-    5% salt-and-pepper in blob 1's 0.10-0.12 shell; seeds at each blob's t=0 centre."""
-    dims, h = (64, 64, 64, 64), 1.0 / 64
-    rng = np.random.default_rng(1001)
-    x, y, z, t = _coords(dims, h)
-    T = t  # t in (0, 1)
-    c1 = [0.3 + (0.5 - 0.3) * T, 0.3 + (0.4 - 0.3) * T, 0.5 + 0 * T]
-    c2 = [0.7 + (0.6 - 0.7) * T, 0.7 + (0.6 - 0.7) * T, 0.5 + 0 * T]
-    d1 = np.sqrt((x - c1[0]) ** 2 + (y - c1[1]) ** 2 + (z - c1[2]) ** 2)
-    d2 = np.sqrt((x - c2[0]) ** 2 + (y - c2[1]) ** 2 + (z - c2[2]) ** 2)
-    bg = 0.1
-    g1 = np.where(d1 <= 0.12, (1 - bg) * np.exp(-0.5 * (d1 / 0.06) ** 2), 0.0)
-    g2 = np.where(d2 <= 0.12, (1 - bg) * np.exp(-0.5 * (d2 / 0.06) ** 2), 0.0)
-    img = bg + np.maximum(g1, g2) + rng.normal(0.0, 0.08, size=d1.shape)
-    shell = (d1 >= 0.10) & (d1 <= 0.12)
-    sp = shell & (rng.random(d1.shape) < 0.05)
-    img = np.where(sp, rng.integers(0, 2, size=d1.shape).astype(np.float64), img)
-    image = _padded(dims, img.astype(np.float32).astype(np.float64))
+def _config1_frames(frames, h, n_total):
+    """Interior image planes of config 1 for the given 0-based global frames.
+
+    Weak scaling repeats the 64-frame config along t (frame f uses the config-1
+    time of frame f mod 64); the noise of every frame comes from its own seeded
+    generator, so any rank can build exactly its slab."""
+    n = 64
+    x = ((np.arange(n) + 0.5) * h)[None, None, :]
+    y = ((np.arange(n) + 0.5) * h)[None, :, None]
+    z = ((np.arange(n) + 0.5) * h)[:, None, None]
+    out = np.empty((len(frames), n, n, n))
+    for q, f in enumerate(frames):
+        rng = np.random.default_rng([1001, int(f)])
+        T = ((f % 64) + 0.5) * h
+        c1 = (0.3 + 0.2 * T, 0.3 + 0.1 * T, 0.5)
+        c2 = (0.7 - 0.1 * T, 0.7 - 0.1 * T, 0.5)
+        d1 = np.sqrt((x - c1[0]) ** 2 + (y - c1[1]) ** 2 + (z - c1[2]) ** 2)
+        d2 = np.sqrt((x - c2[0]) ** 2 + (y - c2[1]) ** 2 + (z - c2[2]) ** 2)
+        bg = 0.1
+        g1 = np.where(d1 <= 0.12, (1 - bg) * np.exp(-0.5 * (d1 / 0.06) ** 2), 0.0)
+        g2 = np.where(d2 <= 0.12, (1 - bg) * np.exp(-0.5 * (d2 / 0.06) ** 2), 0.0)
+        img = bg + np.maximum(g1, g2) + rng.normal(0.0, 0.08, size=d1.shape)
+        shell = (d1 >= 0.10) & (d1 <= 0.12)
+        sp = shell & (rng.random(d1.shape) < 0.05)
+        img = np.where(sp, rng.integers(0, 2, size=d1.shape).astype(np.float64), img)
+        out[q] = img.astype(np.float32).astype(np.float64)
+    return out
+
+
+def config1(replicas: int = 1, planes=None) -> Workload:
+    """64^4 (x replicas along t), two moving Gaussian blobs (peak 1, radius 0.12),
+    bg 0.1, N(0, 0.08^2), 5% salt-and-pepper in blob 1's 0.10-0.12 shell; seeds at
+    each blob's t=0 centre (of every 64-frame replica).
+
+    planes=(p0, p1): build only padded planes p0..p1 (inclusive) of the global
+    padded arrays -- a rank's slab plus halos -- instead of the whole grid."""
+    n4 = 64 * replicas
+    dims, h = (64, 64, 64, n4), 1.0 / 64
+    p0, p1 = (0, n4 + 1) if planes is None else planes
+    frames = [p - 1 for p in range(p0, p1 + 1)]
+    inner = [f for f in frames if 0 <= f < n4]
+    image = np.zeros((p1 - p0 + 1, 66, 66, 66))
+    u0 = np.zeros_like(image)
+    if inner:
+        q0 = inner[0] - (p0 - 1)
+        image[q0:q0 + len(inner), 1:-1, 1:-1, 1:-1] = _config1_frames(inner, h, n4)
     t0 = 0.5 * h
-    s1 = (0.3 + 0.2 * t0, 0.3 + 0.1 * t0, 0.5, t0)
-    s2 = (0.7 - 0.1 * t0, 0.7 - 0.1 * t0, 0.5, t0)
-    rows = [(0, s1[0] / h - 0.5, s1[1] / h - 0.5, s1[2] / h - 0.5, 1.0),
-            (0, s2[0] / h - 0.5, s2[1] / h - 0.5, s2[2] / h - 0.5, 1.0)]
-    u0 = _u0_seeds(dims, h, [s1, s2])
-    return Workload("config1: 64^4 two moving blobs", dims, h, image, u0, rows,
-                    _base_params(h, 20, rescale_radius=10.0), 20,
-                    notes=dict(noise=0.08, salt_pepper=0.05, threshold_radius=1, rescale_radius=10))
+    s1 = (0.3 + 0.2 * t0, 0.3 + 0.1 * t0, 0.5)
+    s2 = (0.7 - 0.1 * t0, 0.7 - 0.1 * t0, 0.5)
+    x = ((np.arange(64) + 0.5) * h)[None, None, :]
+    y = ((np.arange(64) + 0.5) * h)[None, :, None]
+    z = ((np.arange(64) + 0.5) * h)[:, None, None]
+    rows = []
+    for r in range(replicas):
+        rows.append((64 * r, s1[0] / h - 0.5, s1[1] / h - 0.5, s1[2] / h - 0.5, 1.0))
+        rows.append((64 * r, s2[0] / h - 0.5, s2[1] / h - 0.5, s2[2] / h - 0.5, 1.0))
+    for q, f in enumerate(frames):
+        if not 0 <= f < n4:
+            continue
+        t = (f + 0.5) * h
+        v = None
+        for r in range(replicas):  # u0 = max over seeds of 1/(|x - s|_4 / h + 1)
+            tr = 64 * r * h + t0
+            for s in (s1, s2):
+                d = np.sqrt((x - s[0]) ** 2 + (y - s[1]) ** 2 + (z - s[2]) ** 2 + (t - tr) ** 2)
+                val = 1.0 / (d / h + 1.0)
+                v = val if v is None else np.maximum(v, val)
+        u0[q, 1:-1, 1:-1, 1:-1] = v
+    name = "config1: 64^4 two moving blobs" + (f" x{replicas} along t (weak scaling)" if replicas > 1 else "")
+    return Workload(name, dims, h, image, u0, rows, _base_params(h, 20, rescale_radius=10.0), 20,
+                    notes=dict(noise=0.08, salt_pepper=0.05, threshold_radius=1, rescale_radius=10,
+                               replicas=replicas, planes=(p0, p1)))
 
 
 def small(dims=(16, 12, 10, 8), seed=7) -> Workload:
