@@ -64,7 +64,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
                  "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -191,7 +191,8 @@ def main():
     torch.cuda.set_device(local)
     uid = None
     force_dist = os.environ.get("SUBSURF_FORCE_DIST") == "1"  # exercise the NCCL path at N=1
-    if world > 1 or force_dist:
+    dist_init = world > 1 or force_dist
+    if dist_init:
         import torch.distributed as tdist
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         if args.config != "config1":
@@ -317,7 +318,7 @@ def main():
                 line["cpu_baseline"] = {"error": str(e)}
         print(json.dumps(line))
     sess.close()
-    if world > 1:
+    if dist_init:
         torch.distributed.destroy_process_group()
     return 0
 
