@@ -195,6 +195,7 @@ def library() -> C.CDLL:
     sig("ss_session_fixed_sweeps", [C.c_void_p, C.c_int, _D])
     sig("ss_session_set_loop_mode", [C.c_void_p, C.c_int])
     sig("ss_session_set_profiling", [C.c_void_p, C.c_int])
+    sig("ss_session_set_kernel", [C.c_void_p, C.c_int])
     sig("ss_session_profile", [C.c_void_p, C.POINTER(Profile)])
     _lib = L
     return L
@@ -487,6 +488,10 @@ class Session:
 
     def set_loop_mode(self, mode: int) -> None:
         _check(library().ss_session_set_loop_mode(self._h, mode))
+
+    def set_kernel(self, kernel: str) -> None:
+        """'tma' (default): TMA-fed SOR pass; 'ldg': plain load pass (A/B comparison)."""
+        _check(library().ss_session_set_kernel(self._h, {"ldg": 0, "tma": 1}[kernel]))
 
     def set_profiling(self, on: bool) -> None:
         _check(library().ss_session_set_profiling(self._h, 1 if on else 0))

@@ -5,6 +5,9 @@
 // Every expression keeps the reference's evaluation order and the file is
 // compiled with -fmad=false, so the fp32 off-diagonals are bit-identical to the
 // reference's (IEEE sqrt/div are correctly rounded on the GPU as on x86).
+#include <algorithm>
+#include <cmath>
+
 #include "kernels.cuh"
 
 namespace ssb {
@@ -32,16 +35,27 @@ __device__ __forceinline__ void unit(int& di, int& dj, int& dk, int& dl, int s) 
     dl = A == 3 ? s : 0;
 }
 
+// x / h_a.  When every spacing is a power of two (h = 1/32, 1/64, ...),
+// x / h == x * (1/h) exactly in IEEE arithmetic (both are exact rescalings by
+// 2^k), so the division is replaced by the multiplication bit for bit.
+template <bool POW2>
+__device__ __forceinline__ double div_h(double x, const double h[4], const double hinv[4], int a) {
+    if constexpr (POW2)
+        return x * hinv[a];
+    else
+        return x / h[a];
+}
+
 // face_gradient (edge.cpp:33-48) for face F of the stencil's doxel
-template <int F>
-__device__ __forceinline__ void face_gradient(const Stencil& S, const double h[4], double p0,
-                                              double g[4]) {
+template <int F, bool POW2>
+__device__ __forceinline__ void face_gradient(const Stencil& S, const double h[4], const double hinv[4],
+                                              double p0, double g[4]) {
     constexpr int A = F >> 1;
     constexpr int SG = (F & 1) ? 1 : -1;
     int ai, aj, ak, al;
     unit<A>(ai, aj, ak, al, SG);
     const double pn = S.at(ai, aj, ak, al);
-    g[A] = (double)SG * (pn - p0) / h[A];
+    g[A] = div_h<POW2>((double)SG * (pn - p0), h, hinv, A);
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
         if (t == A) continue;
@@ -51,38 +65,56 @@ __device__ __forceinline__ void face_gradient(const Stencil& S, const double h[4
             0.25 * (p0 + pn + S.at(ti, tj, tk, tl) + S.at(ai + ti, aj + tj, ak + tk, al + tl));
         const double minus = 0.25 * (p0 + pn + S.at(-ti, -tj, -tk, -tl) +
                                      S.at(ai - ti, aj - tj, ak - tk, al - tl));
-        g[t] = (plus - minus) / h[t];
+        g[t] = div_h<POW2>(plus - minus, h, hinv, t);
     }
 }
 
-template <int F>
-__device__ __forceinline__ double face_g2(const Stencil& S, const double h[4], double p0) {
+template <int F, bool POW2>
+__device__ __forceinline__ double face_g2(const Stencil& S, const double h[4], const double hinv[4], double p0) {
     double g[4];
-    face_gradient<F>(S, h, p0, g);
+    face_gradient<F, POW2>(S, h, hinv, p0, g);
     return g[0] * g[0] + g[1] * g[1] + g[2] * g[2] + g[3] * g[3];  // edge.cpp:53-54
 }
 
-// thread -> interior doxel of colour C (same mapping as the SOR passes)
+// thread -> interior doxel of colour C in tile t of a persistent grid-stride
+// loop over (kPassBX doxels along i) x (kPassBY rows j) x (k, l) tiles
 struct Site {
     int i, j, k, l;
     bool valid;
 };
-__device__ __forceinline__ Site site(const Layout& L, int C) {
+__device__ __forceinline__ Site site(const Layout& L, int C, long long t, int tx, int ty) {
     Site s;
-    const int z = blockIdx.z;
-    s.k = z % L.n3 + 1;
-    s.l = z / L.n3 + 1;
-    s.j = blockIdx.y * kPassBY + threadIdx.y + 1;
-    s.i = 1 + ((1 + s.j + s.k + s.l + L.lpar + C) & 1) + 2 * (int)(blockIdx.x * kPassBX + threadIdx.x);
+    const int bx = (int)(t % tx);
+    long long r = t / tx;
+    const int by = (int)(r % ty);
+    const long long z = r / ty;
+    s.k = (int)(z % L.n3) + 1;
+    s.l = (int)(z / L.n3) + 1;
+    s.j = by * kPassBY + threadIdx.y + 1;
+    s.i = 1 + ((1 + s.j + s.k + s.l + L.lpar + C) & 1) + 2 * (bx * kPassBX + (int)threadIdx.x);
     s.valid = s.j <= L.n2 && s.i <= L.n1;
     return s;
 }
 
-template <int C, bool EXPORT>
+struct TileGrid {
+    int tx, ty;
+    long long tiles;
+};
+__host__ __device__ inline TileGrid tile_grid(const Layout& L) {
+    TileGrid g;
+    g.tx = ((L.n1 + 1) / 2 + kPassBX - 1) / kPassBX;
+    g.ty = (L.n2 + kPassBY - 1) / kPassBY;
+    g.tiles = (long long)g.tx * g.ty * L.n3 * L.n4;
+    return g;
+}
+
+template <int C, bool EXPORT, bool POW2>
 __global__ void __launch_bounds__(kPassBX * kPassBY) assemble_kernel(const AsmArgs a) {
     const Layout& L = a.L;
-    const Site q = site(L, C);
-    if (!q.valid) return;
+    const TileGrid tg = tile_grid(L);
+    for (long long t = blockIdx.x; t < tg.tiles; t += gridDim.x) {
+    const Site q = site(L, C, t, tg.tx, tg.ty);
+    if (!q.valid) continue;
     Stencil S;
     S.f[0] = a.u[0];
     S.f[1] = a.u[1];
@@ -95,14 +127,14 @@ __global__ void __launch_bounds__(kPassBX * kPassBY) assemble_kernel(const AsmAr
     const double p0 = S.at(0, 0, 0, 0);
 
     double g2[8];
-    g2[0] = face_g2<0>(S, a.h, p0);
-    g2[1] = face_g2<1>(S, a.h, p0);
-    g2[2] = face_g2<2>(S, a.h, p0);
-    g2[3] = face_g2<3>(S, a.h, p0);
-    g2[4] = face_g2<4>(S, a.h, p0);
-    g2[5] = face_g2<5>(S, a.h, p0);
-    g2[6] = face_g2<6>(S, a.h, p0);
-    g2[7] = face_g2<7>(S, a.h, p0);
+    g2[0] = face_g2<0, POW2>(S, a.h, a.hinv, p0);
+    g2[1] = face_g2<1, POW2>(S, a.h, a.hinv, p0);
+    g2[2] = face_g2<2, POW2>(S, a.h, a.hinv, p0);
+    g2[3] = face_g2<3, POW2>(S, a.h, a.hinv, p0);
+    g2[4] = face_g2<4, POW2>(S, a.h, a.hinv, p0);
+    g2[5] = face_g2<5, POW2>(S, a.h, a.hinv, p0);
+    g2[6] = face_g2<6, POW2>(S, a.h, a.hinv, p0);
+    g2[7] = face_g2<7, POW2>(S, a.h, a.hinv, p0);
 
     // solver.cpp:48-56
     double af[8];
@@ -151,13 +183,16 @@ __global__ void __launch_bounds__(kPassBX * kPassBY) assemble_kernel(const AsmAr
         a.diag_out[pp] = diag;
         a.abar_out[pp] = abar;
     }
+    }
 }
 
-template <int C, bool EXPORT>
+template <int C, bool EXPORT, bool POW2>
 __global__ void __launch_bounds__(kPassBX * kPassBY) edge_kernel(const EdgeArgs a) {
     const Layout& L = a.L;
-    const Site q = site(L, C);
-    if (!q.valid) return;
+    const TileGrid tg = tile_grid(L);
+    for (long long t = blockIdx.x; t < tg.tiles; t += gridDim.x) {
+    const Site q = site(L, C, t, tg.tx, tg.ty);
+    if (!q.valid) continue;
     Stencil SI, ST;
     SI.f[0] = a.I0[0];
     SI.f[1] = a.I0[1];
@@ -175,8 +210,8 @@ __global__ void __launch_bounds__(kPassBX * kPassBY) edge_kernel(const EdgeArgs 
 #define SSB_EDGE_FACE(F)                                                                   \
     {                                                                                      \
         double gi[4], gt[4];                                                               \
-        face_gradient<F>(SI, a.h, pi0, gi);                                                \
-        face_gradient<F>(ST, a.h, pt0, gt);                                                \
+        face_gradient<F, POW2>(SI, a.h, a.hinv, pi0, gi);                                  \
+        face_gradient<F, POW2>(ST, a.h, a.hinv, pt0, gt);                                  \
         const double ni = sqrt(gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2] + gi[3] * gi[3]); \
         const double nt = sqrt(gt[0] * gt[0] + gt[1] * gt[1] + gt[2] * gt[2] + gt[3] * gt[3]); \
         const double s = a.delta * ni + a.vartheta * nt;                                   \
@@ -199,6 +234,7 @@ __global__ void __launch_bounds__(kPassBX * kPassBY) edge_kernel(const EdgeArgs 
         const long long pp = L.padded(q.i, q.j, q.k, q.l);
 #pragma unroll
         for (int f = 0; f < 8; ++f) a.G_out[pp * 8 + f] = G[f];
+    }
     }
 }
 
@@ -274,33 +310,66 @@ __global__ void heat_export_kernel(const Layout L, const HeatC hc, double* off, 
 
 }  // namespace
 
-void launch_assemble(cudaStream_t s, const AsmArgs& a) {
-    const dim3 grid = pass_grid(a.L), block(kPassBX, kPassBY);
+static unsigned persistent_grid(const void* fn, long long tiles) {
+    int dev = 0, sms = 0, per = 0;
+    SSB_CUDA(cudaGetDevice(&dev));
+    SSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kPassBX * kPassBY, 0));
+    return (unsigned)std::min<long long>(tiles, (long long)sms * std::max(1, per));
+}
+
+static bool pow2(double h) {
+    int e = 0;
+    return std::frexp(h, &e) == 0.5;  // mantissa exactly 1 => power of two
+}
+
+template <int C, bool EXPORT, bool POW2>
+static void asm_launch(cudaStream_t s, const AsmArgs& a) {
+    static unsigned grid = 0;
+    const TileGrid tg = tile_grid(a.L);
+    if (!grid) grid = persistent_grid((const void*)assemble_kernel<C, EXPORT, POW2>, 1LL << 40);
+    assemble_kernel<C, EXPORT, POW2><<<(unsigned)std::min<long long>(tg.tiles, grid), dim3(kPassBX, kPassBY), 0, s>>>(a);
+    SSB_LAUNCHED();
+}
+
+template <int C, bool EXPORT, bool POW2>
+static void edge_launch(cudaStream_t s, const EdgeArgs& a) {
+    static unsigned grid = 0;
+    const TileGrid tg = tile_grid(a.L);
+    if (!grid) grid = persistent_grid((const void*)edge_kernel<C, EXPORT, POW2>, 1LL << 40);
+    edge_kernel<C, EXPORT, POW2><<<(unsigned)std::min<long long>(tg.tiles, grid), dim3(kPassBX, kPassBY), 0, s>>>(a);
+    SSB_LAUNCHED();
+}
+
+void launch_assemble(cudaStream_t s, const AsmArgs& a0) {
+    AsmArgs a = a0;
+    bool p2 = true;
+    for (int q = 0; q < 4; ++q) {
+        p2 = p2 && pow2(a.h[q]);
+        a.hinv[q] = 1.0 / a.h[q];
+    }
     if (a.off_out) {
-        assemble_kernel<0, true><<<grid, block, 0, s>>>(a);
-        SSB_LAUNCHED();
-        assemble_kernel<1, true><<<grid, block, 0, s>>>(a);
-        SSB_LAUNCHED();
+        if (p2) { asm_launch<0, true, true>(s, a); asm_launch<1, true, true>(s, a); }
+        else { asm_launch<0, true, false>(s, a); asm_launch<1, true, false>(s, a); }
     } else {
-        assemble_kernel<0, false><<<grid, block, 0, s>>>(a);
-        SSB_LAUNCHED();
-        assemble_kernel<1, false><<<grid, block, 0, s>>>(a);
-        SSB_LAUNCHED();
+        if (p2) { asm_launch<0, false, true>(s, a); asm_launch<1, false, true>(s, a); }
+        else { asm_launch<0, false, false>(s, a); asm_launch<1, false, false>(s, a); }
     }
 }
 
-void launch_face_coefficients(cudaStream_t s, const EdgeArgs& a) {
-    const dim3 grid = pass_grid(a.L), block(kPassBX, kPassBY);
+void launch_face_coefficients(cudaStream_t s, const EdgeArgs& a0) {
+    EdgeArgs a = a0;
+    bool p2 = true;
+    for (int q = 0; q < 4; ++q) {
+        p2 = p2 && pow2(a.h[q]);
+        a.hinv[q] = 1.0 / a.h[q];
+    }
     if (a.G_out) {
-        edge_kernel<0, true><<<grid, block, 0, s>>>(a);
-        SSB_LAUNCHED();
-        edge_kernel<1, true><<<grid, block, 0, s>>>(a);
-        SSB_LAUNCHED();
+        if (p2) { edge_launch<0, true, true>(s, a); edge_launch<1, true, true>(s, a); }
+        else { edge_launch<0, true, false>(s, a); edge_launch<1, true, false>(s, a); }
     } else {
-        edge_kernel<0, false><<<grid, block, 0, s>>>(a);
-        SSB_LAUNCHED();
-        edge_kernel<1, false><<<grid, block, 0, s>>>(a);
-        SSB_LAUNCHED();
+        if (p2) { edge_launch<0, false, true>(s, a); edge_launch<1, false, true>(s, a); }
+        else { edge_launch<0, false, false>(s, a); edge_launch<1, false, false>(s, a); }
     }
 }
 

@@ -6,7 +6,8 @@
 // (red = 0 = even, solver.cpp:244/291/341, 1-based padded GLOBAL indices).
 // Each colour is a dense array of rows; row r = (l*kMax + k)*jMax + j holds the
 // doxels of that colour at packed position m = i >> 1 (W = (n1+3)/2 slots per
-// row).  For any doxel the j/k/l neighbours sit at the same m in the other
+// row, rounded up to even so rows are 16-byte aligned for bulk copies).  For any
+// doxel the j/k/l neighbours sit at the same m in the other
 // colour's array one row stride away, and the i-1 / i+1 neighbours at
 // m' = (i-1)>>1 and (i+1)>>1.  A colour half-sweep therefore reads and writes
 // whole 32-byte sectors only (no half-used sectors as with the interleaved
@@ -47,7 +48,7 @@ struct Layout {
         L.glo = l0 == 0;
         L.ghi = l0 + g.n4 == L.n4g;
         L.iMax = g.n1 + 2; L.jMax = g.n2 + 2; L.kMax = g.n3 + 2; L.lMax = g.n4 + 2;
-        L.W = (L.iMax + 1) / 2;
+        L.W = (((L.iMax + 1) / 2) + 1) & ~1;  // even: every packed row starts 16-byte aligned (TMA)
         L.rows = (long long)L.jMax * L.kMax * L.lMax;
         L.cs = L.rows * L.W;
         L.sj = L.W;

@@ -143,8 +143,9 @@ Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int 
     coef[1].alloc(L.cs * 8);
     SorArgs t{};
     pass_tiles(L, t);
-    part[0].alloc((size_t)t.tiles * kPassBY);
-    part[1].alloc((size_t)t.tiles * kPassBY);
+    const size_t nparts = std::max((size_t)t.tiles * kPassBY, tma_partials(L));
+    part[0].alloc(nparts);
+    part[1].alloc(nparts);
     slice_res.alloc(chunk);
     norm_loc.alloc(chunk);
     if (world > 1) {
@@ -276,7 +277,7 @@ void Slab::initial(PField u, const ss_center* c, int n, double v, double R, int 
 }
 
 SorArgs Slab::sor_args(const PField B[3], const PField& rhs, bool heat, double omega, const double hc[4],
-                       int world) const {
+                       int world, bool tma) const {
     SorArgs a{};
     a.L = L;
     for (int b = 0; b < 3; ++b)
@@ -294,7 +295,11 @@ SorArgs Slab::sor_args(const PField B[3], const PField& rhs, bool heat, double o
     a.omega = omega;
     a.keep = 1.0 - omega;
     for (int q = 0; q < 4; ++q) a.hc[q] = heat ? hc[q] : 0.0;
-    pass_tiles(L, a);
+    a.tma = tma && tma_pass_supported(L) ? 1 : 0;
+    if (a.tma)
+        tma_pass_tiles(L, a);
+    else
+        pass_tiles(L, a);
     a.use_cond = 0;
     return a;
 }
@@ -458,14 +463,14 @@ cudaGraphExec_t Domain::graph_for(const SorArgs& base, bool heat) {
     key[6] = base.rhs[0];
     key[7] = base.rhs[1];
     for (auto& e : graphs) {
-        bool same = e->heat == (int)heat && e->omega == base.omega;
+        bool same = e->heat == (int)heat + 2 * base.tma && e->omega == base.omega;
         for (int q = 0; q < 8 && same; ++q) same = e->key_ptr[q] == key[q];
         for (int q = 0; q < 4 && same; ++q) same = e->hc[q] == base.hc[q];
         if (same) return e->exec;
     }
     std::unique_ptr<GraphEntry> e(new GraphEntry);
     std::memcpy(e->key_ptr, key, sizeof key);
-    e->heat = heat;
+    e->heat = (int)heat + 2 * base.tma;
     e->omega = base.omega;
     std::memcpy(e->hc, base.hc, sizeof e->hc);
     SSB_CUDA(cudaGraphCreate(&e->graph, 0));
@@ -533,7 +538,7 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
         Slab& x = *sp[s];
         const double* ns = use_norm ? (world == 1 ? x.norm_loc.p : x.norm_all.p) : nullptr;
         launch_sor_init(stream, x.st.p, tol_abs, ns, g.n4, rel, max_iter, fixed ? 1 : 0);
-        a.push_back(x.sor_args(B[s].data(), rhs[s], heat, omega, hc, world));
+        a.push_back(x.sor_args(B[s].data(), rhs[s], heat, omega, hc, world, tma));
     }
     const int limit = max_iter + 1;  // red(max_iter+1) evaluates the last residual
     if (single() && loop_mode == 1 && !profiling) {

@@ -131,7 +131,7 @@ struct Slab {
     void threshold_write(PField img, PField out, const BallSet& bs, const double* ab, double lambda);
     void initial(PField u, const ss_center* c, int n, double v, double R, int profile);
     SorArgs sor_args(const PField B[3], const PField& rhs, bool heat, double omega,
-                     const double hc[4], int world) const;
+                     const double hc[4], int world, bool tma) const;
 };
 
 // ------------------------------------------------------------------ transports
@@ -177,6 +177,7 @@ struct Domain {
     ss_seg_params prm{};
 
     int loop_mode = 1;
+    bool tma = true;  // TMA-fed SOR pass (default) vs the LDG pass
     bool profiling = false;
     ss_profile prof{};
     SorState* st_host = nullptr;

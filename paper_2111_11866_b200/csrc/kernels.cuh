@@ -39,6 +39,7 @@ struct SorArgs {
     int bps;                // residual partials (tiles) per l-slice of one pass
     int tx, ty, tk;         // tile grid of one slice (pass_tiles)
     long long tiles;
+    int tma;                // 1: TMA-fed pass kernel (sor_tma.cu), 0: LDG pass (sor.cu)
     int use_cond;
     cudaGraphConditionalHandle cond;
 };
@@ -58,6 +59,11 @@ constexpr int kPassKC = SSB_PASS_KC;        // planes (k) per tile
 constexpr int kPassBatch = SSB_PASS_BATCH;  // doxels whose loads a thread issues together
 
 void pass_tiles(const Layout& L, SorArgs& a);
+// TMA-fed pass (sor_tma.cu)
+bool tma_pass_supported(const Layout& L);
+void tma_pass_tiles(const Layout& L, SorArgs& a);
+size_t tma_partials(const Layout& L);
+void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat);
 dim3 pass_grid(const Layout& L);
 void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_slices,
                      int n_slices, double rel, int max_iter, int fixed);
@@ -77,6 +83,7 @@ struct AsmArgs {
     double t_h2[4];         // tau / h_a^2 (solver.cpp:36-38)
     double eps;
     double h[4];
+    double hinv[4];         // 1/h (used only when every h is a power of two)
     int* bad;               // set when a diag is non-finite (solver.cpp:71-75)
     // export (per-call API): padded outputs, may be null
     double* off_out;        // 8 per padded doxel
@@ -93,6 +100,7 @@ struct EdgeArgs {
     double* G_out;          // padded export (8 per doxel), may be null
     double K, delta, vartheta;
     double h[4];
+    double hinv[4];
 };
 void launch_face_coefficients(cudaStream_t s, const EdgeArgs& a);
 

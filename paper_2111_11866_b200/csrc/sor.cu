@@ -19,7 +19,7 @@
 // -fmad=false: iterates are bit-identical to the oracle.
 #include <algorithm>
 
-#include "kernels.cuh"
+#include "sor_math.cuh"
 
 namespace ssb {
 
@@ -41,14 +41,6 @@ __device__ __forceinline__ double block_sum(double v) {
     }
     return v;  // valid in thread 0
 }
-
-// Operands of one doxel update; loads are split from the arithmetic so a
-// thread can put the loads of several doxels in flight before the first store.
-struct DoxelIn {
-    float c[8];  // heat: exact float values of float(-dt/h^2), so nothing is lost
-    double rhs, u0, nb[8];
-    long long p;
-};
 
 template <int C, bool HEAT>
 __device__ __forceinline__ void load_doxel(const SorArgs& a, const float* __restrict__ cf,
@@ -87,44 +79,6 @@ __device__ __forceinline__ void load_doxel(const SorArgs& a, const float* __rest
     d.nb[5] = __ldg(uo + p + L.sk);
     d.nb[6] = __ldg(uo + p - L.sl);
     d.nb[7] = __ldg(uo + p + L.sl);
-}
-
-// The update of solver.cpp:292-313; returns the squared residual contribution
-// (black: in-sweep, :309-312; red: of the incoming state, :347-356).
-template <int C>
-__device__ __forceinline__ double compute_doxel(const SorArgs& a, const DoxelIn& d,
-                                                double* __restrict__ ucw) {
-    const double c0 = (double)d.c[0], c1 = (double)d.c[1], c2 = (double)d.c[2];
-    const double c3 = (double)d.c[3], c4 = (double)d.c[4], c5 = (double)d.c[5];
-    const double c6 = (double)d.c[6], c7 = (double)d.c[7];
-    const double dg = 1.0 - (c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7);
-    double acc = d.rhs;
-    acc -= c0 * d.nb[0];
-    acc -= c1 * d.nb[1];
-    acc -= c2 * d.nb[2];
-    acc -= c3 * d.nb[3];
-    acc -= c4 * d.nb[4];
-    acc -= c5 * d.nb[5];
-    acc -= c6 * d.nb[6];
-    acc -= c7 * d.nb[7];
-    const double ubar = acc / dg;
-    const double unew = a.omega * ubar + a.keep * d.u0;
-    ucw[d.p] = unew;
-    if constexpr (C == 1) {
-        const double res = dg * (unew - ubar);
-        return res * res;
-    } else {
-        double res = dg * d.u0 - d.rhs;
-        res += c0 * d.nb[0];
-        res += c1 * d.nb[1];
-        res += c2 * d.nb[2];
-        res += c3 * d.nb[3];
-        res += c4 * d.nb[4];
-        res += c5 * d.nb[5];
-        res += c6 * d.nb[6];
-        res += c7 * d.nb[7];
-        return res * res;
-    }
 }
 
 // Persistent colour pass: a resident grid walks the tiles (kPassBX doxels of one
@@ -301,6 +255,10 @@ void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* nor
 }
 
 void launch_sor_pass(cudaStream_t s, const SorArgs& a, int colour, bool heat) {
+    if (a.tma) {
+        launch_sor_pass_tma(s, a, colour, heat);
+        return;
+    }
     const unsigned grid = (unsigned)std::min<long long>(a.tiles, resident_blocks());
     const dim3 block(kPassBX, kPassBY);
     if (colour == 0) {
@@ -328,23 +286,13 @@ void launch_sor_decide(cudaStream_t s, const SorArgs& a) {
 }
 
 void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* ev) {
-    const unsigned grid = (unsigned)std::min<long long>(a.tiles, resident_blocks());
-    const dim3 block(kPassBX, kPassBY);
     if (ev) SSB_CUDA(cudaEventRecord(ev[0], s));
-    if (heat)
-        sor_pass<0, true><<<grid, block, 0, s>>>(a);
-    else
-        sor_pass<0, false><<<grid, block, 0, s>>>(a);
-    SSB_LAUNCHED();
+    launch_sor_pass(s, a, 0, heat);
     if (ev) SSB_CUDA(cudaEventRecord(ev[1], s));
     sor_finalize<<<a.L.n4, 256, 0, s>>>(a);
     SSB_LAUNCHED();
     if (ev) SSB_CUDA(cudaEventRecord(ev[2], s));
-    if (heat)
-        sor_pass<1, true><<<grid, block, 0, s>>>(a);
-    else
-        sor_pass<1, false><<<grid, block, 0, s>>>(a);
-    SSB_LAUNCHED();
+    launch_sor_pass(s, a, 1, heat);
     if (ev) SSB_CUDA(cudaEventRecord(ev[3], s));
 }
 

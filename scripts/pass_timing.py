@@ -14,6 +14,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "config1"
 wl = workloads.CONFIGS[cfg]()
 g = ss.Grid.make(wl.dims, wl.h)
 s = ss.Session(g)
+s.set_kernel(os.environ.get("SUBSURF_KERNEL", "tma"))
 p = ss.seg_params(**{**wl.params, "n_steps": 10})
 s.prepare(wl.image, wl.rows, p, wl.u0)
 for _ in range(3):
@@ -28,6 +29,7 @@ s.set_profiling(True)
 s.step_nodiag()
 pr = s.profile()
 out = dict(lib=os.path.basename(os.environ.get("SUBSURF_B200_LIB", "default")), cfg=cfg,
+           kernel=os.environ.get("SUBSURF_KERNEL", "tma"),
            red_us=1e3 * pr["red_ms"] / max(1, pr["red_n"]), black_us=1e3 * pr["black_ms"] / max(1, pr["black_n"]),
            sweep_us_wall=1e6 * dt / sweeps, assemble_us=1e3 * pr["assemble_ms"] / max(1, pr["assemble_n"]),
            value=wl.n_interior * sweeps / dt)

@@ -89,3 +89,22 @@ def test_nccl_session_world1(gpu):
         u = s.get_u()
     assert its == list(d["iters_rel"])
     assert np.array_equal(u.view(np.uint64), d["u_rel"].view(np.uint64))
+
+
+@pytest.mark.parametrize("kernel", ["ldg", "tma"])
+def test_pass_kernels_agree(gpu, kernel):
+    """Both SOR colour-pass kernels give the golden segment() result bit for bit."""
+    d = dict(np.load(os.path.join(GOLD, "segment.npz")))
+    dims = tuple(int(x) for x in d["dims"])
+    h = float(d["h"])
+    g = gpu.Grid.make(dims, h)
+    p = gpu.seg_params(tau=h, epsilon=1e-3, omega=1.4, n_steps=3, sigma=np.sqrt(2) * h, K=200.0,
+                       delta=0.5, vartheta=0.5, rescale_radius=3.0, sor_rel_tol=1e-8)
+    for n_slabs in (1, 3):
+        with gpu.Session(g, n_slabs=n_slabs) as s:
+            s.set_kernel(kernel)
+            s.prepare(d["image"], d["rows"], p)
+            its = [s.step()["iterations"] for _ in range(3)]
+            u = s.get_u()
+        assert its == list(d["iters_rel"])
+        assert np.array_equal(u.view(np.uint64), d["u_rel"].view(np.uint64))
