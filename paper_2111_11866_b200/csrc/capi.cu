@@ -168,7 +168,7 @@ ss_status ss_redblack_sor(const ss_grid* g, const double* offdiag, const double*
         s.rhs_sep.alloc(s.L);
         s.upload(rhs, s.rhs_sep.pf());
         s.upload_state(u, 0);
-        const int roles[3] = {0, 1, 2};
+        const int roles[kStateBuffers] = {0, 1, 2, 3};
         int rr = 0;
         const SolveOut o = d.solve(d.role_triples(roles), {s.rhs_sep.pf()}, false, omega, nullptr, sor_tol, false,
                                    0.0, sor_max_iter, false, &rr);
@@ -208,12 +208,13 @@ ss_status ss_heat_smooth(const ss_grid* g, const double* image, double sigma, in
         validate_smoothing(sigma, steps, sor_tol, sor_max_iter, omega);
         Domain& d = cached(*g);
         Slab& s = *d.sp[0];
-        DevField a, b, c;
+        DevField a, b, c, e;
         a.alloc(s.L);
         b.alloc(s.L);
         c.alloc(s.L);
+        e.alloc(s.L);
         s.upload(image, a.pf());
-        const std::vector<Domain::Triple> B = {{a.pf(), b.pf(), c.pf()}};
+        const std::vector<Domain::Triple> B = {{a.pf(), b.pf(), c.pf(), e.pf()}};
         const int r = d.heat_smooth(B, sigma, steps, omega, sor_tol, sor_max_iter);
         s.download(B[0][r], out);
         d.sync();

@@ -144,8 +144,10 @@ Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int 
     SorArgs t{};
     pass_tiles(L, t);
     const size_t nparts = std::max((size_t)t.tiles * kPassBY, tma_partials(L));
-    part[0].alloc(nparts);
-    part[1].alloc(nparts);
+    for (auto& pp : part) {
+        pp[0].alloc(nparts);
+        pp[1].alloc(nparts);
+    }
     slice_res.alloc(chunk);
     norm_loc.alloc(chunk);
     if (world > 1) {
@@ -177,14 +179,15 @@ double* Slab::stage8_p() {
     return stage8.p;
 }
 
-void Slab::upload(const double* host, PField dst, PField t0, PField t1) {
+void Slab::upload(const double* host, PField dst, PField t0, PField t1, PField t2) {
     double* d = stage_p();
     SSB_CUDA(cudaMemcpyAsync(d, host, L.P * sizeof(double), cudaMemcpyDefault, stream));
-    launch_pack(stream, L, d, dst, t0, t1);
+    launch_pack(stream, L, d, dst, t0, t1, t2);
 }
 
 void Slab::upload_state(const double* host, int role) {
-    upload(host, S[role].pf(), S[(role + 1) % 3].pf(), S[(role + 2) % 3].pf());
+    upload(host, S[role].pf(), S[(role + 1) % kStateBuffers].pf(), S[(role + 2) % kStateBuffers].pf(),
+           S[(role + 3) % kStateBuffers].pf());
 }
 
 void Slab::download(PField src, double* host) {
@@ -194,7 +197,7 @@ void Slab::download(PField src, double* host) {
 }
 
 void Slab::sync_ghosts_from(int role) {
-    for (int r = 0; r < 3; ++r)
+    for (int r = 0; r < kStateBuffers; ++r)
         if (r != role) launch_copy_ghosts(stream, L, S[r].pf(), S[role].pf());
 }
 
@@ -276,18 +279,20 @@ void Slab::initial(PField u, const ss_center* c, int n, double v, double R, int 
     SSB_CUDA(cudaStreamSynchronize(stream));  // bs is freed on return
 }
 
-SorArgs Slab::sor_args(const PField B[3], const PField& rhs, bool heat, double omega, const double hc[4],
+SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool heat, double omega, const double hc[4],
                        int world, bool tma) const {
     SorArgs a{};
     a.L = L;
-    for (int b = 0; b < 3; ++b)
+    for (int b = 0; b < kStateBuffers; ++b)
         for (int c = 0; c < 2; ++c) a.U[b][c] = B[b].c[c];
     a.rhs[0] = rhs.c[0];
     a.rhs[1] = rhs.c[1];
     a.coef[0] = coef[0].p;
     a.coef[1] = coef[1].p;
-    a.part[0] = part[0].p;
-    a.part[1] = part[1].p;
+    for (int q = 0; q < 4; ++q) {
+        a.part[q][0] = part[q][0].p;
+        a.part[q][1] = part[q][1].p;
+    }
     a.slice_res = slice_res.p;
     a.all_slices = world == 1 ? slice_res.p : all_slices.p;
     a.inline_decide = world == 1 ? 1 : 0;
@@ -331,7 +336,7 @@ void LocalTransport::allgather(std::vector<Slab*>& slabs, const std::vector<doub
 
 // ------------------------------------------------------------------ domain
 struct Domain::GraphEntry {
-    const void* key_ptr[8];
+    const void* key_ptr[2 * kStateBuffers + 2];
     int heat;
     double omega, hc[4];
     cudaGraph_t graph = nullptr;
@@ -421,9 +426,13 @@ std::vector<PField> Domain::role_fields(int role) const {
     return F;
 }
 
-std::vector<Domain::Triple> Domain::role_triples(const int roles[3]) const {
+std::vector<Domain::Triple> Domain::role_triples(const int roles[kStateBuffers]) const {
     std::vector<Triple> B;
-    for (Slab* s : sp) B.push_back({s->S[roles[0]].pf(), s->S[roles[1]].pf(), s->S[roles[2]].pf()});
+    for (Slab* s : sp) {
+        Triple t;
+        for (int q = 0; q < kStateBuffers; ++q) t[q] = s->S[roles[q]].pf();
+        B.push_back(t);
+    }
     return B;
 }
 
@@ -457,14 +466,15 @@ cudaEvent_t Domain::pool_event(size_t idx) {
 }
 
 cudaGraphExec_t Domain::graph_for(const SorArgs& base, bool heat) {
-    const void* key[8];
-    for (int b = 0; b < 3; ++b)
+    constexpr int NK = 2 * kStateBuffers + 2;
+    const void* key[NK];
+    for (int b = 0; b < kStateBuffers; ++b)
         for (int c = 0; c < 2; ++c) key[2 * b + c] = base.U[b][c];
-    key[6] = base.rhs[0];
-    key[7] = base.rhs[1];
+    key[NK - 2] = base.rhs[0];
+    key[NK - 1] = base.rhs[1];
     for (auto& e : graphs) {
         bool same = e->heat == (int)heat + 2 * base.tma && e->omega == base.omega;
-        for (int q = 0; q < 8 && same; ++q) same = e->key_ptr[q] == key[q];
+        for (int q = 0; q < NK && same; ++q) same = e->key_ptr[q] == key[q];
         for (int q = 0; q < 4 && same; ++q) same = e->hc[q] == base.hc[q];
         if (same) return e->exec;
     }
@@ -509,7 +519,7 @@ void Domain::body_single(const SorArgs& a, bool heat, cudaEvent_t* ev4) {
 // exchange the new black boundary planes.
 void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>& B, bool heat, int n,
                         cudaEvent_t* ev4) {
-    const int bout = (n & 1) ? 1 : 2;
+    const int bout = out_buf(n);
     std::vector<PField> F;
     for (const Triple& t : B) F.push_back(t[bout]);
     if (ev4) SSB_CUDA(cudaEventRecord(ev4[0], stream));
@@ -612,7 +622,7 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
     o.tol = st_host->tol;
     o.converged = st_host->converged != 0;
     prof.sweeps += o.iterations;
-    *result = o.iterations == 0 ? 0 : ((o.iterations & 1) ? 1 : 2);
+    *result = o.iterations == 0 ? 0 : out_buf(o.iterations);
     return o;
 }
 
@@ -639,22 +649,24 @@ int Domain::heat_smooth(const std::vector<Triple>& B, double sigma, int steps, d
     const double dt = 0.5 * sigma * sigma / steps;
     double hc[4];
     heat_constants(g, dt, hc);
-    for (size_t s = 0; s < sp.size(); ++s) {  // the SOR buffers' ghosts/halos = the input's
-        launch_copy_ghosts(stream, sp[s]->L, B[s][1], B[s][0]);
-        launch_copy_ghosts(stream, sp[s]->L, B[s][2], B[s][0]);
-    }
-    int idx[3] = {0, 1, 2};
+    for (size_t s = 0; s < sp.size(); ++s)  // the SOR buffers' ghosts/halos = the input's
+        for (int q = 1; q < kStateBuffers; ++q) launch_copy_ghosts(stream, sp[s]->L, B[s][q], B[s][0]);
+    int idx[kStateBuffers];
+    for (int q = 0; q < kStateBuffers; ++q) idx[q] = q;
     for (int st = 0; st < steps; ++st) {
         std::vector<Triple> T;
         std::vector<PField> rhs;
         for (const Triple& t : B) {
-            T.push_back({t[idx[0]], t[idx[1]], t[idx[2]]});
+            Triple x;
+            for (int q = 0; q < kStateBuffers; ++q) x[q] = t[idx[q]];
+            T.push_back(x);
             rhs.push_back(t[idx[0]]);
         }
         int r = 0;
         const SolveOut o = solve(T, rhs, true, omega, hc, tol, false, 0.0, max_iter, false, &r);
         if (!o.converged) throw SolverErrT(o);
-        const int nidx[3] = {idx[r], idx[(r + 1) % 3], idx[(r + 2) % 3]};
+        int nidx[kStateBuffers];
+        for (int q = 0; q < kStateBuffers; ++q) nidx[q] = idx[(r + q) % kStateBuffers];
         std::memcpy(idx, nidx, sizeof idx);
     }
     std::vector<PField> R;
@@ -715,16 +727,18 @@ void Domain::prepare(const double* image, const ss_center* c, int n, const ss_se
     }
 
     // local_threshold, heat_smooth x2, face_coefficients (solver.cpp:419-422)
-    std::vector<std::unique_ptr<DevField>> img, th, t1, t2;
+    std::vector<std::unique_ptr<DevField>> img, th, t1, t2, t3;
     for (Slab* s : sp) {
         img.emplace_back(new DevField);
         th.emplace_back(new DevField);
         t1.emplace_back(new DevField);
         t2.emplace_back(new DevField);
+        t3.emplace_back(new DevField);
         img.back()->alloc(s->L);
         th.back()->alloc(s->L);
         t1.back()->alloc(s->L);
         t2.back()->alloc(s->L);
+        t3.back()->alloc(s->L);
         s->upload(host_slab(image, *s), img.back()->pf());
     }
     {
@@ -764,9 +778,11 @@ void Domain::prepare(const double* image, const ss_center* c, int n, const ss_se
     exchange(thf, 3);  // halos of the thresholded image (the heat solve reads them)
 
     std::vector<Triple> b1, b2;
-    for (size_t s = 0; s < sp.size(); ++s) b1.push_back({img[s]->pf(), t1[s]->pf(), t2[s]->pf()});
+    for (size_t s = 0; s < sp.size(); ++s) b1.push_back({img[s]->pf(), t1[s]->pf(), t2[s]->pf(), t3[s]->pf()});
     const int r1 = heat_smooth(b1, p.sigma, p.smooth_steps, p.smooth_omega, p.smooth_tol, p.smooth_max_iter);
-    for (size_t s = 0; s < sp.size(); ++s) b2.push_back({th[s]->pf(), b1[s][(r1 + 1) % 3], b1[s][(r1 + 2) % 3]});
+    for (size_t s = 0; s < sp.size(); ++s)
+        b2.push_back({th[s]->pf(), b1[s][(r1 + 1) % kStateBuffers], b1[s][(r1 + 2) % kStateBuffers],
+                      b1[s][(r1 + 3) % kStateBuffers]});
     const int r2 = heat_smooth(b2, p.sigma, p.smooth_steps, p.smooth_omega, p.smooth_tol, p.smooth_max_iter);
     for (size_t s = 0; s < sp.size(); ++s)
         sp[s]->face_coefficients(b1[s][r1], b2[s][r2], p.K, p.delta, p.vartheta, nullptr);
@@ -782,7 +798,8 @@ void Domain::prepare(const double* image, const ss_center* c, int n, const ss_se
 
 void Domain::step(ss_step_diag* diag) {
     if (!prepared) throw Error(SS_ERR_STATE, "session not prepared");
-    const int roles[3] = {cur, (cur + 1) % 3, (cur + 2) % 3};
+    int roles[kStateBuffers];
+    for (int q = 0; q < kStateBuffers; ++q) roles[q] = (cur + q) % kStateBuffers;
     exchange_role(cur, 3);  // u^{n-1} halos for the face gradients and the first red pass
     if (profiling) SSB_CUDA(cudaEventRecord(ev[2], stream));
     for (Slab* s : sp) s->assemble(s->S[cur].pf(), s->have_G, prm.tau, prm.epsilon, nullptr, nullptr, nullptr);
@@ -859,7 +876,8 @@ void Domain::step(ss_step_diag* diag) {
 
 double Domain::fixed_sweeps(int n_sweeps) {
     if (!prepared) throw Error(SS_ERR_STATE, "session not prepared");
-    const int roles[3] = {cur, (cur + 1) % 3, (cur + 2) % 3};
+    int roles[kStateBuffers];
+    for (int q = 0; q < kStateBuffers; ++q) roles[q] = (cur + q) % kStateBuffers;
     exchange_role(cur, 3);
     for (Slab* s : sp) s->assemble(s->S[cur].pf(), s->have_G, prm.tau, prm.epsilon, nullptr, nullptr, nullptr);
     const std::vector<Triple> B = role_triples(roles);

@@ -98,12 +98,12 @@ struct Slab {
     int index = 0;  // position of the slab along l (= rank for NCCL)
     cudaStream_t stream = nullptr;  // borrowed from the Domain
 
-    DevField S[3];       // rotating state buffers
+    DevField S[kStateBuffers];  // rotating state buffers (guess + 3 outputs)
     DevField rhs_sep;    // explicit rhs (per-call redblack_sor)
     Dev<float> coef[2];
     Dev<double> G[2];
     bool have_G = false;
-    Dev<double> part[2];
+    Dev<double> part[4][2];
     Dev<double> slice_res;   // chunk entries (zero padded)
     Dev<double> all_slices;  // world * chunk (gathered), unused when world == 1
     Dev<double> norm_loc, norm_all;
@@ -118,7 +118,8 @@ struct Slab {
          cudaStream_t s);
     double* stage_p();
     double* stage8_p();
-    void upload(const double* host_padded, PField dst, PField twin0 = PField(), PField twin1 = PField());
+    void upload(const double* host_padded, PField dst, PField twin0 = PField(), PField twin1 = PField(),
+                PField twin2 = PField());
     void upload_state(const double* host_padded, int role);
     void download(PField src, double* host_padded);
     void sync_ghosts_from(int role);
@@ -130,7 +131,7 @@ struct Slab {
     void threshold_minmax(PField img, const BallSet& bs, double* ab);
     void threshold_write(PField img, PField out, const BallSet& bs, const double* ab, double lambda);
     void initial(PField u, const ss_center* c, int n, double v, double R, int profile);
-    SorArgs sor_args(const PField B[3], const PField& rhs, bool heat, double omega,
+    SorArgs sor_args(const PField B[kStateBuffers], const PField& rhs, bool heat, double omega,
                      const double hc[4], int world, bool tma) const;
 };
 
@@ -207,8 +208,8 @@ struct Domain {
     // k doubles from every local slab -> world*k doubles in rank order, identical on all ranks
     std::vector<double> gather_values(const std::vector<std::vector<double>>& per_slab, int k);
 
-    using Triple = std::array<PField, 3>;
-    std::vector<Triple> role_triples(const int roles[3]) const;
+    using Triple = std::array<PField, kStateBuffers>;  // guess + the 3 rotating outputs
+    std::vector<Triple> role_triples(const int roles[kStateBuffers]) const;
     // red-black SOR on every slab: guess B[s][0] (never written), rhs[s]; the
     // result lands in B[s][*result].  Non-convergence is reported, not thrown.
     SolveOut solve(const std::vector<Triple>& B, const std::vector<PField>& rhs, bool heat,

@@ -40,7 +40,7 @@ __device__ __forceinline__ double* at(const Layout& L, PField f, int i, int j, i
 }
 
 __global__ void pack_kernel(const Layout L, const double* __restrict__ src, PField dst, PField t0,
-                            PField t1) {
+                            PField t1, PField t2) {
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (e >= L.P) return;
     const Pos p = decode_padded(L, e);
@@ -52,6 +52,7 @@ __global__ void pack_kernel(const Layout L, const double* __restrict__ src, PFie
                        p.k > L.n3 || p.l == 0 || p.l > L.n4;
     if (ghost && t0.c[c]) t0.c[c][q] = v;
     if (ghost && t1.c[c]) t1.c[c][q] = v;
+    if (ghost && t2.c[c]) t2.c[c][q] = v;
 }
 
 __global__ void unpack_kernel(const Layout L, PField src, double* __restrict__ dst) {
@@ -226,8 +227,8 @@ __global__ void mask_kernel(const Layout L, PField f, double level, uint8_t* mas
 }  // namespace
 
 void launch_pack(cudaStream_t s, const Layout& L, const double* src, PField dst, PField t0,
-                 PField t1) {
-    pack_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, src, dst, t0, t1);
+                 PField t1, PField t2) {
+    pack_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, src, dst, t0, t1, t2);
     SSB_LAUNCHED();
 }
 

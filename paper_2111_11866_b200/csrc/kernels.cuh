@@ -20,16 +20,21 @@ struct SorState {
     double tol, residual;
 };
 
+constexpr int kStateBuffers = 4;  // guess + 3 rotating outputs
+__host__ __device__ __forceinline__ int out_buf(int n) { return 1 + (n - 1) % 3; }
+__host__ __device__ __forceinline__ int in_buf(int n) { return n == 1 ? 0 : out_buf(n - 1); }
+
 struct SorArgs {
     Layout L;
     // [buffer][colour].  Buffer 0 holds the initial guess and is never written;
-    // iteration n writes buffer out(n) = n odd ? 1 : 2 and reads in(n) = n == 1 ? 0
-    // : out(n-1), so the rhs may alias buffer 0 and the iterate of the stopping
-    // iteration survives the (lagged-residual) red pass that follows it.
-    double* U[3][2];
+    // iteration n writes buffer out(n) = 1 + (n-1) % 3 and reads in(n) = n == 1 ? 0
+    // : out(n-1), so the rhs may alias buffer 0 and the iterate of a decided
+    // iteration survives the up to two iterations computed after it (the
+    // lagged residual of the two-pass loop, the two-iteration wavefront).
+    double* U[kStateBuffers][2];
     const double* rhs[2];   // colour-packed rhs
     const float* coef[2];   // colour-packed fp32 off-diagonals, 8 per doxel (kFaceOffsets order)
-    double* part[2];        // per-block squared-residual partials of the red / black pass
+    double* part[4][2];     // squared-residual partials, [iteration n & 3][red / black pass]
     double* slice_res;      // per-slice residual of the owned slices (solver.cpp:195-199)
     const double* all_slices;  // residuals of all n4g slices in global order (== slice_res on 1 slab)
     int inline_decide;      // single slab: finalize also decides
@@ -115,9 +120,9 @@ void launch_heat_export(cudaStream_t s, const Layout& L, double dt_h2[4], double
                         double* diag, double* abar);
 
 // ---------------------------------------------------------------- fields
-// src (padded) -> dst; ghost doxels are also written into twin0/twin1 (null members skipped)
+// src (padded) -> dst; ghost doxels are also written into the twins (null members skipped)
 void launch_pack(cudaStream_t s, const Layout& L, const double* src, PField dst, PField twin0,
-                 PField twin1);
+                 PField twin1, PField twin2);
 void launch_fill_raw(cudaStream_t s, double* p, long long n, double v);
 void launch_unpack(cudaStream_t s, const Layout& L, PField src, double* dst);
 void launch_fill(cudaStream_t s, const Layout& L, PField f, double v);

@@ -92,8 +92,8 @@ __global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(con
     const SorState* st = a.st;
     if (*(volatile const int*)&st->done) return;
     const int n = C == 0 ? *(volatile const int*)&st->n_red : *(volatile const int*)&st->n_black;
-    const int bout = (n & 1) ? 1 : 2;
-    const int bin = n == 1 ? 0 : (((n - 1) & 1) ? 1 : 2);
+    const int bout = out_buf(n);
+    const int bin = in_buf(n);
     const Layout& L = a.L;
     const double* __restrict__ uc = a.U[bin][C];
     const double* __restrict__ uo = C == 0 ? a.U[bin][1] : a.U[bout][0];
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(con
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
-        if (threadIdx.x == 0) a.part[C][t * kPassBY + threadIdx.y] = r2;
+        if (threadIdx.x == 0) a.part[n & 3][C][t * kPassBY + threadIdx.y] = r2;
     }
 }
 
@@ -168,8 +168,8 @@ __global__ void __launch_bounds__(256) sor_finalize(const SorArgs a) {
     const int n = *(volatile int*)&st->n_red;
     if (n >= 2) {
         const int l = blockIdx.x;
-        const double* pr = a.part[0] + (long long)l * a.bps;
-        const double* pb = a.part[1] + (long long)l * a.bps;
+        const double* pr = a.part[n & 3][0] + (long long)l * a.bps;        // red(n)
+        const double* pb = a.part[(n - 1) & 3][1] + (long long)l * a.bps;  // black(n-1)
         double r = 0.0, b = 0.0;
         for (int q = threadIdx.x; q < a.bps; q += blockDim.x) {
             r += pr[q];

@@ -105,8 +105,8 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
     const SorState* st = a.st;
     if (*(volatile const int*)&st->done) return;
     const int n = C == 0 ? *(volatile const int*)&st->n_red : *(volatile const int*)&st->n_black;
-    const int bout = (n & 1) ? 1 : 2;
-    const int bin = n == 1 ? 0 : (((n - 1) & 1) ? 1 : 2);
+    const int bout = out_buf(n);
+    const int bin = in_buf(n);
     const Layout& L = a.L;
     const double* __restrict__ uc = a.U[bin][C];
     const double* __restrict__ uo = C == 0 ? a.U[bin][1] : a.U[bout][0];
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
         ph0 = sc + 1 == kStages ? pc ^ 1 : pc;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
-        if (lane == 0) a.part[C][t * kWarps + warp] = r2;
+        if (lane == 0) a.part[n & 3][C][t * kWarps + warp] = r2;
     }
 }
 
