@@ -165,7 +165,8 @@ SS_API ss_status ss_session_get_mask(ss_session* s, double level, uint8_t* mask)
 SS_API ss_status ss_session_fixed_sweeps(ss_session* s, int n_sweeps, double* residual);
 /* 0 = host-driven chunked loop, 1 = CUDA-graph conditional loop (default) */
 SS_API ss_status ss_session_set_loop_mode(ss_session* s, int mode);
-/* SOR colour-pass kernel: 1 = TMA-fed (default), 0 = plain LDG (for A/B comparison) */
+/* SOR kernel: 1 = TMA-fed two-pass (default), 0 = plain LDG two-pass, 2 = two-iteration
+ * TMA wavefront through L2 (experimental; measured slower on B200) */
 SS_API ss_status ss_session_set_kernel(ss_session* s, int kernel);
 /* per-pass CUDA-event timing of the SOR kernels (forces the host-driven loop) */
 SS_API ss_status ss_session_set_profiling(ss_session* s, int enable);

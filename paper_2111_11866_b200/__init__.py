@@ -490,8 +490,9 @@ class Session:
         _check(library().ss_session_set_loop_mode(self._h, mode))
 
     def set_kernel(self, kernel: str) -> None:
-        """'tma' (default): TMA-fed SOR pass; 'ldg': plain load pass (A/B comparison)."""
-        _check(library().ss_session_set_kernel(self._h, {"ldg": 0, "tma": 1}[kernel]))
+        """'tma' (default): TMA-fed two-pass; 'ldg': plain load two-pass; 'wave':
+        two-iteration TMA wavefront through L2 (experimental, measured slower)."""
+        _check(library().ss_session_set_kernel(self._h, {"ldg": 0, "tma": 1, "wave": 2}[kernel]))
 
     def set_profiling(self, on: bool) -> None:
         _check(library().ss_session_set_profiling(self._h, 1 if on else 0))

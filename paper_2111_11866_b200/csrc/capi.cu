@@ -467,8 +467,8 @@ ss_status ss_session_set_loop_mode(ss_session* s, int mode) {
 ss_status ss_session_set_kernel(ss_session* s, int kernel) {
     return guard([&] {
         require(s != nullptr, "null session");
-        require(kernel == 0 || kernel == 1, "kernel must be 0 (LDG) or 1 (TMA)");
-        s->d->tma = kernel == 1;
+        require(kernel >= 0 && kernel <= 2, "kernel must be 0 (LDG), 1 (TMA) or 2 (TMA wavefront)");
+        s->d->kernel = kernel;
     });
 }
 

@@ -158,6 +158,10 @@ Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int 
     }
     gloc.alloc(8);
     gall.alloc((size_t)world * 8);
+    if (world == 1 && wave_supported(L)) {
+        wflags.alloc(wave_flags(L));
+        SSB_CUDA(cudaMemsetAsync(wflags.p, 0, wflags.n * sizeof(int), stream));
+    }
     SSB_CUDA(cudaMemsetAsync(slice_res.p, 0, slice_res.n * sizeof(double), stream));
     SSB_CUDA(cudaMemsetAsync(norm_loc.p, 0, norm_loc.n * sizeof(double), stream));
     st.alloc(1);
@@ -280,7 +284,7 @@ void Slab::initial(PField u, const ss_center* c, int n, double v, double R, int 
 }
 
 SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool heat, double omega, const double hc[4],
-                       int world, bool tma) const {
+                       int world, int kernel) const {
     SorArgs a{};
     a.L = L;
     for (int b = 0; b < kStateBuffers; ++b)
@@ -300,7 +304,9 @@ SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool he
     a.omega = omega;
     a.keep = 1.0 - omega;
     for (int q = 0; q < 4; ++q) a.hc[q] = heat ? hc[q] : 0.0;
-    a.tma = tma && tma_pass_supported(L) ? 1 : 0;
+    a.tma = kernel >= 1 && tma_pass_supported(L) ? 1 : 0;
+    a.wave = kernel == 2 && world == 1 && wflags.p != nullptr ? 1 : 0;
+    a.flags = wflags.p;
     if (a.tma)
         tma_pass_tiles(L, a);
     else
@@ -473,14 +479,14 @@ cudaGraphExec_t Domain::graph_for(const SorArgs& base, bool heat) {
     key[NK - 2] = base.rhs[0];
     key[NK - 1] = base.rhs[1];
     for (auto& e : graphs) {
-        bool same = e->heat == (int)heat + 2 * base.tma && e->omega == base.omega;
+        bool same = e->heat == (int)heat + 2 * base.tma + 4 * base.wave && e->omega == base.omega;
         for (int q = 0; q < NK && same; ++q) same = e->key_ptr[q] == key[q];
         for (int q = 0; q < 4 && same; ++q) same = e->hc[q] == base.hc[q];
         if (same) return e->exec;
     }
     std::unique_ptr<GraphEntry> e(new GraphEntry);
     std::memcpy(e->key_ptr, key, sizeof key);
-    e->heat = (int)heat + 2 * base.tma;
+    e->heat = (int)heat + 2 * base.tma + 4 * base.wave;
     e->omega = base.omega;
     std::memcpy(e->hc, base.hc, sizeof e->hc);
     SSB_CUDA(cudaGraphCreate(&e->graph, 0));
@@ -544,19 +550,25 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
                        const double hc[4], double tol_abs, bool use_norm, double rel, int max_iter, bool fixed,
                        int* result) {
     std::vector<SorArgs> a;
+    solve_count = (solve_count + 1) & 0x3fff;
+    const int epoch_base = (solve_count + 1) << 16;  // differs from the previous solve's
     for (size_t s = 0; s < sp.size(); ++s) {
         Slab& x = *sp[s];
         const double* ns = use_norm ? (world == 1 ? x.norm_loc.p : x.norm_all.p) : nullptr;
-        launch_sor_init(stream, x.st.p, tol_abs, ns, g.n4, rel, max_iter, fixed ? 1 : 0);
-        a.push_back(x.sor_args(B[s].data(), rhs[s], heat, omega, hc, world, tma));
+        launch_sor_init(stream, x.st.p, tol_abs, ns, g.n4, rel, max_iter, fixed ? 1 : 0, epoch_base);
+        a.push_back(x.sor_args(B[s].data(), rhs[s], heat, omega, hc, world, kernel));
     }
-    const int limit = max_iter + 1;  // red(max_iter+1) evaluates the last residual
+    const bool wave = a[0].wave != 0;
+    // loop bodies: red(max_iter+1) evaluates the last residual; a wavefront body
+    // covers two iterations
+    const int limit = wave ? (max_iter + 2) / 2 : max_iter + 1;
     if (single() && loop_mode == 1 && !profiling) {
         cudaGraphExec_t ex = graph_for(a[0], heat);
         SSB_CUDA(cudaGraphLaunch(ex, stream));
         SSB_CUDA(cudaMemcpyAsync(st_host, sp[0]->st.p, sizeof(SorState), cudaMemcpyDeviceToHost, stream));
         sync();
-        count_launch(3ull * (unsigned long long)std::min(limit, st_host->iterations + 1));
+        const int bodies = wave ? st_host->iterations / 2 + 1 : st_host->iterations + 1;
+        count_launch(3ull * (unsigned long long)std::min(limit, bodies));
     } else {
         // host-driven: chunks of loop bodies with one chunk of look-ahead; every
         // rank runs the same schedule (the decision is identical everywhere)
@@ -598,7 +610,15 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
         }
         SSB_CUDA(cudaMemcpyAsync(st_host, sp[0]->st.p, sizeof(SorState), cudaMemcpyDeviceToHost, stream));
         sync();
-        if (profiling) {
+        if (profiling && wave) {  // wave kernel time per body, 4 colour passes each
+            const int bodies = st_host->iterations / 2 + 1;
+            for (size_t b = 0; b < body_ev.size() && (int)b < bodies; ++b) {
+                float ms = 0.f;
+                SSB_CUDA(cudaEventElapsedTime(&ms, ev_pool[body_ev[b]], ev_pool[body_ev[b] + 1]));
+                prof.red_ms += ms;
+                prof.red_n += 4;
+            }
+        } else if (profiling) {
             const int it = st_host->iterations;
             for (size_t b = 0; b < body_ev.size(); ++b) {
                 float ms = 0.f;

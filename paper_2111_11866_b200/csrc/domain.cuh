@@ -108,6 +108,7 @@ struct Slab {
     Dev<double> all_slices;  // world * chunk (gathered), unused when world == 1
     Dev<double> norm_loc, norm_all;
     Dev<double> gloc, gall;  // small host-driven gathers (k <= 8 values per slab)
+    Dev<int> wflags;         // wavefront item completion flags
     Dev<SorState> st;
     Dev<double> scratch, scal;
     Dev<int> flags;
@@ -132,7 +133,7 @@ struct Slab {
     void threshold_write(PField img, PField out, const BallSet& bs, const double* ab, double lambda);
     void initial(PField u, const ss_center* c, int n, double v, double R, int profile);
     SorArgs sor_args(const PField B[kStateBuffers], const PField& rhs, bool heat, double omega,
-                     const double hc[4], int world, bool tma) const;
+                     const double hc[4], int world, int kernel) const;
 };
 
 // ------------------------------------------------------------------ transports
@@ -178,7 +179,9 @@ struct Domain {
     ss_seg_params prm{};
 
     int loop_mode = 1;
-    bool tma = true;  // TMA-fed SOR pass (default) vs the LDG pass
+    int kernel = 1;   // SOR: 1 = TMA two-pass (default), 0 = LDG two-pass,
+                      // 2 = TMA two-iteration wavefront (experimental, slower; sor_tma.cu)
+    int solve_count = 0;
     bool profiling = false;
     ss_profile prof{};
     SorState* st_host = nullptr;

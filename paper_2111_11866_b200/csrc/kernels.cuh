@@ -16,7 +16,8 @@ struct SorState {
     int done, converged;
     int iterations, max_iter;
     int fixed, pad;
-    unsigned int counter, pad2;
+    unsigned int counter;
+    int epoch_base;  // distinct per solve: completion flags of the wavefront kernel compare to epoch_base + n
     double tol, residual;
 };
 
@@ -45,6 +46,8 @@ struct SorArgs {
     int tx, ty, tk;         // tile grid of one slice (pass_tiles)
     long long tiles;
     int tma;                // 1: TMA-fed pass kernel (sor_tma.cu), 0: LDG pass (sor.cu)
+    int wave;               // 1: two-iteration wavefront kernel per loop body
+    int* flags;             // wavefront item completion flags (epochs)
     int use_cond;
     cudaGraphConditionalHandle cond;
 };
@@ -69,9 +72,12 @@ bool tma_pass_supported(const Layout& L);
 void tma_pass_tiles(const Layout& L, SorArgs& a);
 size_t tma_partials(const Layout& L);
 void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat);
+bool wave_supported(const Layout& L);
+size_t wave_flags(const Layout& L);
+void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat);
 dim3 pass_grid(const Layout& L);
 void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_slices,
-                     int n_slices, double rel, int max_iter, int fixed);
+                     int n_slices, double rel, int max_iter, int fixed, int epoch_base);
 // single-slab loop body: red, finalize (inline decision), black
 void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* ev /*4 or null*/);
 // pieces for the multi-slab body (halo exchange / all-gather between them)

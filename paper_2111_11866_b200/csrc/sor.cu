@@ -200,7 +200,8 @@ __global__ void sor_decide(const SorArgs a) {
 
 // tol = rel * sqrt(sum over all slices in global l order) when norm_slices is given
 __global__ void sor_init(SorState* st, double tol, const double* norm_slices, int n_slices, double rel,
-                         int max_iter, int fixed) {
+                         int max_iter, int fixed, int epoch_base) {
+    st->epoch_base = epoch_base;
     st->n_red = 1;
     st->n_black = 0;
     st->done = 0;
@@ -249,8 +250,8 @@ static int resident_blocks() {
 }
 
 void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_slices,
-                     int n_slices, double rel, int max_iter, int fixed) {
-    sor_init<<<1, 1, 0, s>>>(st, tol, norm_slices, n_slices, rel, max_iter, fixed);
+                     int n_slices, double rel, int max_iter, int fixed, int epoch_base) {
+    sor_init<<<1, 1, 0, s>>>(st, tol, norm_slices, n_slices, rel, max_iter, fixed, epoch_base);
     SSB_LAUNCHED();
 }
 
@@ -286,6 +287,20 @@ void launch_sor_decide(cudaStream_t s, const SorArgs& a) {
 }
 
 void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* ev) {
+    if (a.wave) {  // iterations n and n+1 in one wavefront launch, then both decisions
+        if (ev) SSB_CUDA(cudaEventRecord(ev[0], s));
+        launch_sor_wave(s, a, heat);
+        if (ev) SSB_CUDA(cudaEventRecord(ev[1], s));
+        sor_finalize<<<a.L.n4, 256, 0, s>>>(a);
+        SSB_LAUNCHED();
+        sor_finalize<<<a.L.n4, 256, 0, s>>>(a);
+        SSB_LAUNCHED();
+        if (ev) {
+            SSB_CUDA(cudaEventRecord(ev[2], s));
+            SSB_CUDA(cudaEventRecord(ev[3], s));
+        }
+        return;
+    }
     if (ev) SSB_CUDA(cudaEventRecord(ev[0], s));
     launch_sor_pass(s, a, 0, heat);
     if (ev) SSB_CUDA(cudaEventRecord(ev[1], s));

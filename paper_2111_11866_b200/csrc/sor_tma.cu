@@ -33,6 +33,9 @@ constexpr int kWarps = 8;         // consumer warps
 constexpr int kThreads = (kWarps + 1) * 32;
 constexpr int kStages = 5;
 constexpr int kPlanesPerItem = 8;
+#ifndef SSB_WAVE_SKEW
+#define SSB_WAVE_SKEW 0  // 0: 2 * nkc sub-slices (measured: nkc+1 starves, 16..48 equal)
+#endif
 
 __device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -98,6 +101,157 @@ __host__ __device__ inline Geo make_geo(const Layout& L) {
     return g;
 }
 
+// Work item geometry (item = row group jg x plane chunk kc of slice l)
+struct Item {
+    int l, j0, rows, k0, k1;
+};
+__device__ __forceinline__ Item make_item(const Layout& L, const Geo& G, int l, int jg, int kc) {
+    Item it;
+    it.l = l;
+    it.j0 = jg * G.R + 1;
+    it.rows = min(G.R, L.n2 - it.j0 + 1);
+    it.k0 = kc * kPlanesPerItem + 1;
+    it.k1 = min(it.k0 + kPlanesPerItem - 1, L.n3);
+    return it;
+}
+
+struct Ring {  // producer-side position of the next stage
+    uint32_t slot = 0, phase = 0, used = 0;
+};
+
+// Producer: issue the k1-k0+3 stages of one item (planes k0-1 .. k1+1).
+template <bool HEAT>
+__device__ __forceinline__ void produce_item(const Layout& L, const Geo& G, unsigned char* smem, uint64_t* full,
+                                             uint64_t* empty, Ring& rg, const Item& it, const float* coef,
+                                             const double* rhs, const double* uc, const double* uo) {
+    const long long W = L.W;
+    const long long plane_rows = (long long)L.jMax * L.kMax;
+    const uint32_t rb = G.row_bytes;
+    for (int p = it.k0 - 1; p <= it.k1 + 1; ++p) {
+        if (rg.used >= kStages) mbar_wait(&empty[rg.slot], rg.phase ^ 1);
+        unsigned char* s = smem + rg.slot * G.stage_bytes;
+        const bool interior = p >= it.k0 && p <= it.k1;
+        uint32_t bytes = (it.rows + 2) * rb;
+        if (interior) bytes += (HEAT ? 4u : 8u) * it.rows * rb;
+        uint64_t* bar = &full[rg.slot];
+        mbar_expect_tx(bar, bytes);
+        const long long row0 = ((long long)it.l * L.kMax + p) * L.jMax + it.j0;  // row (j0, p, l)
+        bulk_g2s(s + G.off_uk, uo + (row0 - 1) * W, (it.rows + 2) * rb, bar);
+        if (interior) {
+            if (!HEAT) bulk_g2s(s + G.off_coef, coef + row0 * W * 8, 4 * it.rows * rb, bar);
+            bulk_g2s(s + G.off_rhs, rhs + row0 * W, it.rows * rb, bar);
+            bulk_g2s(s + G.off_uc, uc + row0 * W, it.rows * rb, bar);
+            bulk_g2s(s + G.off_ulm, uo + (row0 - plane_rows) * W, it.rows * rb, bar);
+            bulk_g2s(s + G.off_ulp, uo + (row0 + plane_rows) * W, it.rows * rb, bar);
+        }
+        ++rg.used;
+        if (++rg.slot == kStages) {
+            rg.slot = 0;
+            rg.phase ^= 1;
+        }
+    }
+}
+
+// Consumers (8 warps): update colour C on the item's planes from the staged
+// rows; returns this warp's sum of squared residuals.  (s0, ph0) is the ring
+// position of the item's first stage and is advanced past the item.
+template <int C, bool HEAT>
+__device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L, const Geo& G,
+                                               unsigned char* smem, uint64_t* full, uint64_t* empty,
+                                               uint32_t& s0, uint32_t& ph0, const Item& it,
+                                               double* __restrict__ ucw, int warp, int lane) {
+    const long long W = L.W;
+    const int rloc = warp / G.wpr, seg = warp % G.wpr;
+    const int nq = (L.n1 + 1) / 2;
+    const int l = it.l;
+    const int j = it.j0 + rloc;
+    double r2 = 0.0;
+    // (slot, phase) of stages q-1 (plane p-1), q (p), q+1 (p+1)
+    uint32_t sm = s0, pm = ph0;
+    uint32_t sc = sm + 1 == kStages ? 0 : sm + 1, pc = sm + 1 == kStages ? pm ^ 1 : pm;
+    mbar_wait(&full[sm], pm);
+    mbar_wait(&full[sc], pc);
+    for (int p = it.k0; p <= it.k1; ++p) {
+        const uint32_t sp = sc + 1 == kStages ? 0 : sc + 1, pp = sc + 1 == kStages ? pc ^ 1 : pc;
+        mbar_wait(&full[sp], pp);
+        if (rloc < it.rows) {
+            const unsigned char* scb = smem + sc * G.stage_bytes;
+            const double* ukm = reinterpret_cast<const double*>(smem + sm * G.stage_bytes + G.off_uk);
+            const double* ukc = reinterpret_cast<const double*>(scb + G.off_uk);
+            const double* ukp = reinterpret_cast<const double*>(smem + sp * G.stage_bytes + G.off_uk);
+            const float* cf = reinterpret_cast<const float*>(scb + G.off_coef) + (long long)rloc * W * 8;
+            const double* rh = reinterpret_cast<const double*>(scb + G.off_rhs) + rloc * W;
+            const double* u0r = reinterpret_cast<const double*>(scb + G.off_uc) + rloc * W;
+            const double* ulm = reinterpret_cast<const double*>(scb + G.off_ulm) + rloc * W;
+            const double* ulp = reinterpret_cast<const double*>(scb + G.off_ulp) + rloc * W;
+            const double* ukc_r = ukc + (rloc + 1) * W;  // this row in the (rows+2)-row block
+            const long long grow = (((long long)l * L.kMax + p) * L.jMax + j) * W;
+            const int i0 = 1 + ((1 + j + p + l + L.lpar + C) & 1);
+            for (int qq = seg * 32 + lane; qq < nq; qq += 32 * G.wpr) {
+                const int i = i0 + 2 * qq;
+                if (i > L.n1) break;
+                const int m = i >> 1;
+                DoxelIn d;
+                if constexpr (HEAT) {
+                    d.c[0] = i > 1 ? (float)a.hc[0] : 0.f;
+                    d.c[1] = i < L.n1 ? (float)a.hc[0] : 0.f;
+                    d.c[2] = j > 1 ? (float)a.hc[1] : 0.f;
+                    d.c[3] = j < L.n2 ? (float)a.hc[1] : 0.f;
+                    d.c[4] = p > 1 ? (float)a.hc[2] : 0.f;
+                    d.c[5] = p < L.n3 ? (float)a.hc[2] : 0.f;
+                    d.c[6] = l + L.l0 > 1 ? (float)a.hc[3] : 0.f;
+                    d.c[7] = l + L.l0 < L.n4g ? (float)a.hc[3] : 0.f;
+                } else {
+                    const float4 lo = *reinterpret_cast<const float4*>(cf + m * 8);
+                    const float4 hi = *reinterpret_cast<const float4*>(cf + m * 8 + 4);
+                    d.c[0] = lo.x; d.c[1] = lo.y; d.c[2] = lo.z; d.c[3] = lo.w;
+                    d.c[4] = hi.x; d.c[5] = hi.y; d.c[6] = hi.z; d.c[7] = hi.w;
+                }
+                d.rhs = rh[m];
+                d.u0 = u0r[m];
+                d.nb[0] = ukc_r[(i - 1) >> 1];
+                d.nb[1] = ukc_r[(i + 1) >> 1];
+                d.nb[2] = ukc[rloc * W + m];
+                d.nb[3] = ukc[(rloc + 2) * W + m];
+                d.nb[4] = ukm[(rloc + 1) * W + m];
+                d.nb[5] = ukp[(rloc + 1) * W + m];
+                d.nb[6] = ulm[m];
+                d.nb[7] = ulp[m];
+                d.p = grow + m;
+                r2 += compute_doxel<C>(a, d, ucw);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[sm]);  // plane p-1's stage is done
+        sm = sc;
+        pm = pc;
+        sc = sp;
+        pc = pp;
+    }
+    // the last two stages of the item (planes k1, k1+1)
+    __syncwarp();
+    if (lane == 0) {
+        mbar_arrive(&empty[sm]);
+        mbar_arrive(&empty[sc]);
+    }
+    s0 = sc + 1 == kStages ? 0 : sc + 1;
+    ph0 = sc + 1 == kStages ? pc ^ 1 : pc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
+    return r2;
+}
+
+__device__ __forceinline__ void init_barriers(uint64_t* full, uint64_t* empty) {
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+}
+
 template <int C, bool HEAT>
 __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -108,151 +262,150 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
     const int bout = out_buf(n);
     const int bin = in_buf(n);
     const Layout& L = a.L;
-    const double* __restrict__ uc = a.U[bin][C];
-    const double* __restrict__ uo = C == 0 ? a.U[bin][1] : a.U[bout][0];
-    double* __restrict__ ucw = a.U[bout][C];
+    const double* uc = a.U[bin][C];
+    const double* uo = C == 0 ? a.U[bin][1] : a.U[bout][0];
+    double* ucw = a.U[bout][C];
     const Geo G = make_geo(L);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    init_barriers(full, empty);
 
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kWarps);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    const long long W = L.W;
-    const long long plane_rows = (long long)L.jMax * L.kMax;  // rows per l-plane
-    if (warp == kWarps) {
-        // ---------------- producer: one thread issues every bulk copy
+    if (warp == kWarps) {  // producer: one thread issues every bulk copy
         if (lane != 0) return;
-        uint32_t slot = 0, phase = 0, used = 0;  // ring position of the next stage
+        Ring rg;
         for (long long t = blockIdx.x; t < G.items; t += gridDim.x) {
             const int jg = (int)(t % G.njg);
-            long long r = t / G.njg;
-            const int kc = (int)(r % G.nkc);
-            const int l = (int)(r / G.nkc) + 1;
-            const int j0 = jg * G.R + 1;
-            const int rows = min(G.R, L.n2 - j0 + 1);
-            const int k0 = kc * kPlanesPerItem + 1;
-            const int k1 = min(k0 + kPlanesPerItem - 1, L.n3);
-            for (int p = k0 - 1; p <= k1 + 1; ++p) {
-                if (used >= kStages) mbar_wait(&empty[slot], phase ^ 1);
-                unsigned char* s = smem + slot * G.stage_bytes;
-                const bool interior = p >= k0 && p <= k1;
-                const uint32_t rb = G.row_bytes;
-                uint32_t bytes = (rows + 2) * rb;
-                if (interior) bytes += (HEAT ? 4u : 8u) * rows * rb;
-                mbar_expect_tx(&full[slot], bytes);
-                const long long row0 = ((long long)l * L.kMax + p) * L.jMax + j0;  // row (j0, p, l)
-                bulk_g2s(s + G.off_uk, uo + (row0 - 1) * W, (rows + 2) * rb, &full[slot]);
-                if (interior) {
-                    if (!HEAT) bulk_g2s(s + G.off_coef, a.coef[C] + row0 * W * 8, 4 * rows * rb, &full[slot]);
-                    bulk_g2s(s + G.off_rhs, a.rhs[C] + row0 * W, rows * rb, &full[slot]);
-                    bulk_g2s(s + G.off_uc, uc + row0 * W, rows * rb, &full[slot]);
-                    bulk_g2s(s + G.off_ulm, uo + (row0 - plane_rows) * W, rows * rb, &full[slot]);
-                    bulk_g2s(s + G.off_ulp, uo + (row0 + plane_rows) * W, rows * rb, &full[slot]);
-                }
-                ++used;
-                if (++slot == kStages) {
-                    slot = 0;
-                    phase ^= 1;
-                }
-            }
+            const long long r = t / G.njg;
+            const Item it = make_item(L, G, (int)(r / G.nkc) + 1, jg, (int)(r % G.nkc));
+            produce_item<HEAT>(L, G, smem, full, empty, rg, it, a.coef[C], a.rhs[C], uc, uo);
         }
         return;
     }
-
-    // ---------------- consumers
-    const int rloc = warp / G.wpr, seg = warp % G.wpr;
-    const int nq = (L.n1 + 1) / 2;
-    uint32_t s0 = 0, ph0 = 0;  // ring slot / phase of the item's first stage (plane k0-1)
+    uint32_t s0 = 0, ph0 = 0;
     for (long long t = blockIdx.x; t < G.items; t += gridDim.x) {
         const int jg = (int)(t % G.njg);
-        long long r = t / G.njg;
-        const int kc = (int)(r % G.nkc);
-        const int l = (int)(r / G.nkc) + 1;
-        const int j0 = jg * G.R + 1;
-        const int rows = min(G.R, L.n2 - j0 + 1);
-        const int k0 = kc * kPlanesPerItem + 1;
-        const int k1 = min(k0 + kPlanesPerItem - 1, L.n3);
-        double r2 = 0.0;
-        const int j = j0 + rloc;
-        // (slot, phase) of stages q-1 (plane p-1), q (p), q+1 (p+1)
-        uint32_t sm = s0, pm = ph0;
-        uint32_t sc = sm + 1 == kStages ? 0 : sm + 1, pc = sm + 1 == kStages ? pm ^ 1 : pm;
-        mbar_wait(&full[sm], pm);
-        mbar_wait(&full[sc], pc);
-        for (int p = k0; p <= k1; ++p) {
-            const uint32_t sp = sc + 1 == kStages ? 0 : sc + 1, pp = sc + 1 == kStages ? pc ^ 1 : pc;
-            mbar_wait(&full[sp], pp);
-            if (rloc < rows) {
-                const unsigned char* scb = smem + sc * G.stage_bytes;
-                const double* ukm = reinterpret_cast<const double*>(smem + sm * G.stage_bytes + G.off_uk);
-                const double* ukc = reinterpret_cast<const double*>(scb + G.off_uk);
-                const double* ukp = reinterpret_cast<const double*>(smem + sp * G.stage_bytes + G.off_uk);
-                const float* cf = reinterpret_cast<const float*>(scb + G.off_coef) + (long long)rloc * W * 8;
-                const double* rh = reinterpret_cast<const double*>(scb + G.off_rhs) + rloc * W;
-                const double* u0r = reinterpret_cast<const double*>(scb + G.off_uc) + rloc * W;
-                const double* ulm = reinterpret_cast<const double*>(scb + G.off_ulm) + rloc * W;
-                const double* ulp = reinterpret_cast<const double*>(scb + G.off_ulp) + rloc * W;
-                const double* ukc_r = ukc + (rloc + 1) * W;  // this row in the (rows+2)-row block
-                const long long grow = (((long long)l * L.kMax + p) * L.jMax + j) * W;
-                const int i0 = 1 + ((1 + j + p + l + L.lpar + C) & 1);
-                for (int qq = seg * 32 + lane; qq < nq; qq += 32 * G.wpr) {
-                    const int i = i0 + 2 * qq;
-                    if (i > L.n1) break;
-                    const int m = i >> 1;
-                    DoxelIn d;
-                    if constexpr (HEAT) {
-                        d.c[0] = i > 1 ? (float)a.hc[0] : 0.f;
-                        d.c[1] = i < L.n1 ? (float)a.hc[0] : 0.f;
-                        d.c[2] = j > 1 ? (float)a.hc[1] : 0.f;
-                        d.c[3] = j < L.n2 ? (float)a.hc[1] : 0.f;
-                        d.c[4] = p > 1 ? (float)a.hc[2] : 0.f;
-                        d.c[5] = p < L.n3 ? (float)a.hc[2] : 0.f;
-                        d.c[6] = l + L.l0 > 1 ? (float)a.hc[3] : 0.f;
-                        d.c[7] = l + L.l0 < L.n4g ? (float)a.hc[3] : 0.f;
-                    } else {
-                        const float4 lo = *reinterpret_cast<const float4*>(cf + m * 8);
-                        const float4 hi = *reinterpret_cast<const float4*>(cf + m * 8 + 4);
-                        d.c[0] = lo.x; d.c[1] = lo.y; d.c[2] = lo.z; d.c[3] = lo.w;
-                        d.c[4] = hi.x; d.c[5] = hi.y; d.c[6] = hi.z; d.c[7] = hi.w;
-                    }
-                    d.rhs = rh[m];
-                    d.u0 = u0r[m];
-                    d.nb[0] = ukc_r[(i - 1) >> 1];
-                    d.nb[1] = ukc_r[(i + 1) >> 1];
-                    d.nb[2] = ukc[rloc * W + m];
-                    d.nb[3] = ukc[(rloc + 2) * W + m];
-                    d.nb[4] = ukm[(rloc + 1) * W + m];
-                    d.nb[5] = ukp[(rloc + 1) * W + m];
-                    d.nb[6] = ulm[m];
-                    d.nb[7] = ulp[m];
-                    d.p = grow + m;
-                    r2 += compute_doxel<C>(a, d, ucw);
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[sm]);  // plane p-1's stage is done
-            sm = sc;
-            pm = pc;
-            sc = sp;
-            pc = pp;
-        }
-        // the last two stages of the item (planes k1, k1+1)
-        __syncwarp();
-        if (lane == 0) {
-            mbar_arrive(&empty[sm]);
-            mbar_arrive(&empty[sc]);
-        }
-        s0 = sc + 1 == kStages ? 0 : sc + 1;
-        ph0 = sc + 1 == kStages ? pc ^ 1 : pc;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
+        const long long r = t / G.njg;
+        const Item it = make_item(L, G, (int)(r / G.nkc) + 1, jg, (int)(r % G.nkc));
+        const double r2 = consume_item<C, HEAT>(a, L, G, smem, full, empty, s0, ph0, it, ucw, warp, lane);
         if (lane == 0) a.part[n & 3][C][t * kWarps + warp] = r2;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Two-iteration wavefront (temporal blocking through L2).
+//
+// One launch computes iterations n and n+1 as a wavefront over sub-slices
+// s = (l-1)*nkc + kc (a slice split into its plane chunks): step sigma runs
+// red(n, s=sigma), black(n, sigma-S), red(n+1, sigma-2S), black(n+1, sigma-3S)
+// with skew S = 2*nkc sub-slices, each split into the row-group items above.
+// A phase depends on the previous phase at most one slice + one chunk ahead,
+// i.e. on items of earlier steps only.
+// MEASURED (config 1, B200): 122 us per colour pass vs 111 us for the two-pass
+// kernel -- DRAM reads per two sweeps only fall from 2.07 to 1.76 GB: with
+// enough skew for ~300 CTAs to find independent work, a slice's rows are
+// evicted from L2 before the second iteration reuses them.  Kept as an
+// option (kernel 2), not the default.  An item waits (producer, spinning on
+// per-item completion flags in global memory) for the items of the previous
+// phase that produced the rows it reads: the same chunk at l-1, l, l+1 and
+// the in-plane neighbour chunks (jg +- 1, kc +- 1) at l.  Items are taken in
+// sequence order by a resident persistent grid, so the earliest unfinished
+// item never waits on an unfinished one (no deadlock).  With the slices of
+// ~4 wavefront steps resident in L2 (config 1: ~67 MB of 126 MB), the
+// coefficient, rhs and state rows of a slice are read from DRAM about once
+// per TWO sweeps.  Iterates are unchanged: every update reads exactly the
+// values it reads in the two-pass order (the outputs rotate over 3 buffers, so
+// nothing a later phase writes is read by an earlier one), and residual
+// partials go to the same per-iteration slots, decided afterwards by two
+// finalize launches.
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <bool HEAT>
+__global__ void __launch_bounds__(kThreads, 2) sor_wave_tma(const SorArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    const SorState* st = a.st;
+    if (*(volatile const int*)&st->done) return;
+    const int n = *(volatile const int*)&st->n_red;
+    const int epoch = *(volatile const int*)&st->epoch_base + n;
+    const Layout& L = a.L;
+    const Geo G = make_geo(L);
+    const int CH = G.njg * G.nkc;  // items per slice and phase
+    // wavefront over sub-slices s = (l-1)*nkc + kc: phase d of step sigma works on
+    // s = sigma - skew*d; each step has 4 phases x njg row groups
+    const int skew = SSB_WAVE_SKEW > 0 ? SSB_WAVE_SKEW : 2 * G.nkc;
+    const long long NS = (long long)L.n4 * G.nkc;
+    const long long NT = (NS + 3LL * skew) * 4 * G.njg;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    init_barriers(full, empty);
+
+    auto decode = [&](long long t, int& d, int& l, int& c) {
+        const int jg = (int)(t % G.njg);
+        const long long r = t / G.njg;
+        d = (int)(r & 3);
+        const long long s = (r >> 2) - (long long)skew * d;  // sub-slice of this phase
+        if (s < 0 || s >= NS) {
+            l = 0;
+            c = 0;
+            return;
+        }
+        l = (int)(s / G.nkc) + 1;
+        c = (int)(s % G.nkc) * G.njg + jg;
+    };
+
+    if (warp == kWarps) {  // producer
+        if (lane != 0) return;
+        Ring rg;
+        for (long long t = blockIdx.x; t < NT; t += gridDim.x) {
+            int d, l, c;
+            decode(t, d, l, c);
+            if (l < 1 || l > L.n4) continue;
+            const int m = n + (d >> 1), C = d & 1;
+            const int jg = c % G.njg, kc = c / G.njg;
+            if (d > 0) {  // wait for the producing phase d-1 around this item
+                const int* f = a.flags + (long long)(d - 1) * L.n4 * CH;
+                auto wait = [&](int ll, int cc) {
+                    const int* q = f + (long long)(ll - 1) * CH + cc;
+                    while (ld_acquire(q) != epoch) __nanosleep(64);
+                };
+                wait(l, c);
+                if (l > 1) wait(l - 1, c);
+                if (l < L.n4) wait(l + 1, c);
+                if (jg > 0) wait(l, c - 1);
+                if (jg + 1 < G.njg) wait(l, c + 1);
+                if (kc > 0) wait(l, c - G.njg);
+                if (kc + 1 < G.nkc) wait(l, c + G.njg);
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+            }
+            const int bin = in_buf(m), bout = out_buf(m);
+            const double* uc = a.U[bin][C];
+            const double* uo = C == 0 ? a.U[bin][1] : a.U[bout][0];
+            const Item it = make_item(L, G, l, jg, kc);
+            produce_item<HEAT>(L, G, smem, full, empty, rg, it, a.coef[C], a.rhs[C], uc, uo);
+        }
+        return;
+    }
+    uint32_t s0 = 0, ph0 = 0;
+    for (long long t = blockIdx.x; t < NT; t += gridDim.x) {
+        int d, l, c;
+        decode(t, d, l, c);
+        if (l < 1 || l > L.n4) continue;
+        const int m = n + (d >> 1), C = d & 1;
+        const int jg = c % G.njg, kc = c / G.njg;
+        const Item it = make_item(L, G, l, jg, kc);
+        double* ucw = a.U[out_buf(m)][C];
+        const double r2 = C == 0 ? consume_item<0, HEAT>(a, L, G, smem, full, empty, s0, ph0, it, ucw, warp, lane)
+                                 : consume_item<1, HEAT>(a, L, G, smem, full, empty, s0, ph0, it, ucw, warp, lane);
+        if (lane == 0) a.part[m & 3][C][((long long)(l - 1) * CH + c) * kWarps + warp] = r2;
+        // publish: every consumer's stores, then one flag store (release)
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+        if (threadIdx.x == 0) {
+            int* q = a.flags + ((long long)d * L.n4 + (l - 1)) * CH + c;
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(q), "r"(epoch) : "memory");
+        }
     }
 }
 
@@ -266,7 +419,19 @@ void configure() {
     }
 }
 
-int tma_blocks(size_t smem_bytes) {
+template <bool HEAT>
+void configure_wave() {
+    static bool done = false;
+    if (!done) {
+        SSB_CUDA(cudaFuncSetAttribute(sor_wave_tma<HEAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      96 * 1024 + 64 * 1024));
+        done = true;
+    }
+}
+
+// resident CTAs for this kernel and shared-memory size (the wavefront kernel
+// relies on every CTA being resident: items wait only on earlier items)
+int tma_blocks(const void* fn, size_t smem_bytes) {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -274,7 +439,7 @@ int tma_blocks(size_t smem_bytes) {
         SSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
     int per = 0;
-    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sor_pass_tma<0, false>, kThreads, smem_bytes));
+    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, smem_bytes));
     return sms * std::max(1, per);
 }
 
@@ -296,6 +461,41 @@ void tma_pass_tiles(const Layout& L, SorArgs& a) {
 
 size_t tma_partials(const Layout& L) { return (size_t)make_geo(L).items * kWarps; }
 
+size_t wave_flags(const Layout& L) {
+    const Geo G = make_geo(L);
+    return (size_t)4 * L.n4 * G.njg * G.nkc;
+}
+
+bool wave_supported(const Layout& L) {
+    // the slices of ~4 wavefront steps (coefficients 32 B + rhs + 3 states ~ 64 B per
+    // doxel) must stay in L2 for the temporal blocking to pay; one slab only
+    const double slice = (double)L.n1 * L.n2 * L.n3 * 64.0;
+    return tma_pass_supported(L) && L.glo && L.ghi && 4.0 * slice <= 80.0 * 1024 * 1024;
+}
+
+void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat) {
+    const Geo G = make_geo(a.L);
+    const size_t smem = (size_t)G.stage_bytes * kStages;
+    configure_wave<false>();
+    configure_wave<true>();
+    configure<0, false>();
+    static size_t last_smem = 0;
+    static int blocks = 0;
+    if (smem != last_smem) {
+        blocks = std::min(tma_blocks((const void*)sor_wave_tma<false>, smem),
+                          tma_blocks((const void*)sor_wave_tma<true>, smem));
+        last_smem = smem;
+    }
+    const int skew = SSB_WAVE_SKEW > 0 ? SSB_WAVE_SKEW : 2 * G.nkc;
+    const long long NT = ((long long)a.L.n4 * G.nkc + 3LL * skew) * 4 * G.njg;
+    const unsigned grid = (unsigned)std::min<long long>(NT, blocks);
+    if (heat)
+        sor_wave_tma<true><<<grid, kThreads, smem, s>>>(a);
+    else
+        sor_wave_tma<false><<<grid, kThreads, smem, s>>>(a);
+    SSB_LAUNCHED();
+}
+
 void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat) {
     const Geo G = make_geo(a.L);
     const size_t smem = (size_t)G.stage_bytes * kStages;
@@ -306,7 +506,7 @@ void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat
     static size_t last_smem = 0;
     static int blocks = 0;
     if (smem != last_smem) {
-        blocks = tma_blocks(smem);
+        blocks = tma_blocks((const void*)sor_pass_tma<0, false>, smem);
         last_smem = smem;
     }
     const unsigned grid = (unsigned)std::min<long long>(G.items, blocks);

@@ -275,10 +275,15 @@ def test_fixed_sweeps_and_launch_count(gpu):
     h = float(d["h"])
     with gpu.Session(g) as s:
         s.prepare(d["image"], d["rows"], _seg_params(gpu, h, sor_rel_tol=1e-8))
+        s.set_kernel("tma")
         n0 = gpu.launch_count()
         r = s.fixed_sweeps(50)
         assert np.isfinite(r)
         assert gpu.launch_count() - n0 >= 150  # 50 x (red, finalize, black)
+        s.set_kernel("wave")
+        n0 = gpu.launch_count()
+        s.fixed_sweeps(50)
+        assert gpu.launch_count() - n0 >= 75  # 25 x (wavefront, finalize, finalize)
 
 
 def test_grid_helpers(gpu, oracle):

@@ -91,7 +91,7 @@ def test_nccl_session_world1(gpu):
     assert np.array_equal(u.view(np.uint64), d["u_rel"].view(np.uint64))
 
 
-@pytest.mark.parametrize("kernel", ["ldg", "tma"])
+@pytest.mark.parametrize("kernel", ["ldg", "tma", "wave"])
 def test_pass_kernels_agree(gpu, kernel):
     """Both SOR colour-pass kernels give the golden segment() result bit for bit."""
     d = dict(np.load(os.path.join(GOLD, "segment.npz")))
