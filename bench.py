@@ -165,6 +165,68 @@ def run_reference(args, wl):
     return 0
 
 
+def make_workload(workloads, ssd, config, rank, world):
+    """config0: 32^4 (1 GPU); config1: 64^4, weak-scaled along t for N > 1 (one 64^4
+    replica per GPU); config2: 256x256x64x32 (strong scaling over N); config3:
+    512x512x128x64 (strong, N >= 2); config4: 256x256x128x(16 N) weak, fixed 50 sweeps."""
+    if config == "config0":
+        if world > 1:
+            raise SystemExit("config0 is a single-GPU config")
+        return workloads.config0()
+    if config == "config1":
+        if world == 1:
+            return workloads.config1()
+        lb, cnt = ssd.partition(64 * world, world)[rank]
+        return workloads.config1(replicas=world, planes=(lb - 1, lb + cnt))
+    n4 = {"config2": 32, "config3": 64, "config4": 16 * world}[config]
+    lb, cnt = ssd.partition(n4, world)[rank]
+    planes = (lb - 1, lb + cnt) if world > 1 else None
+    if config == "config4":
+        return workloads.config4(gpus=world, planes=planes)
+    return workloads.CONFIGS[config](planes=planes)
+
+
+def run_reference_sample(args, config):
+    """Reference arm for the big configs: the reference's redblack_sor on one 16-frame
+    t-slab of the config's grid (configs 3/4 do not fit host RAM
+    whole), 5 sweeps per step, G == 1 coefficients assembled at u0."""
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import workloads
+    from oracle import oracle_py as op
+    if not op.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return 0
+    wl = workloads.CONFIGS[config](planes=(0, 17)) if config != "config4" else workloads.config4(1, planes=(0, 17))
+    n1, n2, n3, _ = wl.dims
+    dims = (n1, n2, n3, 16)
+    R = op.ref()
+    g = op.Grid.make(dims, wl.h)
+    workers = min(R.lib.ref_hardware_threads(), 16)
+    u0 = np.ascontiguousarray(wl.u0)
+    st, off, _, _ = R.assemble_step(g, u0, None, wl.params["tau"], wl.params["epsilon"], workers)
+    sweeps, secs = 0, 0.0
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        st, u, it, res = R.redblack_sor(g, off, u0, u0, wl.params["omega"], 1e-300, 5, workers)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            sweeps += it
+            secs += dt
+    n = n1 * n2 * n3 * 16
+    value = n * sweeps / secs
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": wl.name, "sample_dims": list(dims)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
+                         "sample": f"5 red-black sweeps per step of redblack_sor on a 16-frame t-slab {dims}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -180,9 +242,11 @@ def main():
     import workloads
     rank, world, local = env_rank()
     if args.impl == "reference":
-        # the reference CPU solver on one 64^4 replica of the workload (its host cores do not
+        # the reference CPU solver on the N=1 workload of the config (its host cores do not
         # scale with the GPU count; the metric is a throughput, comparable across N)
-        return run_reference(args, workloads.CONFIGS[args.config]())
+        if args.config in ("config0", "config1"):
+            return run_reference(args, workloads.CONFIGS[args.config]())
+        return run_reference_sample(args, args.config)
 
     import torch
     import paper_2111_11866_b200 as ss
@@ -195,15 +259,13 @@ def main():
     if dist_init:
         import torch.distributed as tdist
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        if args.config != "config1":
-            raise SystemExit("multi-GPU bench supports config1 (weak scaling along t)")
-        # weak scaling: config 1 replicated along t, one 64^4 replica per GPU; each rank
-        # builds only its slab (owned planes + one halo/ghost plane per side)
-        lb, cnt = ssd.partition(64 * world, world)[rank]
-        wl = workloads.config1(replicas=world, planes=(lb - 1, lb + cnt))
+        # each rank builds only its slab (owned planes + one halo/ghost plane per side)
+        wl = make_workload(workloads, ssd, args.config, rank, world)
         uid = ssd.broadcast_uid(ss.nccl_unique_id() if rank == 0 else None)
     else:
-        wl = workloads.CONFIGS[args.config]()
+        wl = make_workload(workloads, ssd, args.config, 0, 1)
+    fixed = wl.notes.get("fixed_sweeps")
+    scaling = "strong" if (world > 1 and args.config in ("config2", "config3")) else "weak"
 
     g = ss.Grid.make(wl.dims, wl.h)
     p = ss.seg_params(**{**wl.params, "n_steps": args.warmup + args.steps})
@@ -216,10 +278,16 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    def do_step():
+        if fixed:
+            sess.fixed_sweeps(fixed)  # config 4: assemble + exactly 50 sweeps
+        else:
+            sess.step_nodiag()
+
     # ---------------- value: device-resident steps
     sess.prepare(wl.image, wl.rows, p, wl.u0)
     for _ in range(args.warmup):
-        sess.step_nodiag()
+        do_step()
     sess.profile()  # reset counters
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -227,7 +295,7 @@ def main():
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            sess.step_nodiag()
+            do_step()
         e1.record(stream)
         e1.synchronize()
     launches = ss.launch_count() - l0
@@ -247,7 +315,7 @@ def main():
     host_out = torch.empty(P, dtype=torch.float64, pin_memory=True)
     sess.prepare(wl.image, wl.rows, p, wl.u0)
     for _ in range(args.warmup):
-        sess.step_nodiag()
+        do_step()
     sess.get_u_ptr(host_in.data_ptr())
     sess.profile()
     barrier()
@@ -255,7 +323,7 @@ def main():
     f0.record(stream)
     for _ in range(args.steps):
         sess.set_u_ptr(host_in.data_ptr())     # H2D of the step's input u^{n-1}
-        sess.step_nodiag()
+        do_step()
         sess.get_u_ptr(host_out.data_ptr())    # D2H of the step's result u^n
         host_in, host_out = host_out, host_in
     f1.record(stream)
@@ -271,11 +339,11 @@ def main():
     # ---------------- roofline of the dominant kernel (SOR colour pass), event-timed
     sess.prepare(wl.image, wl.rows, p, wl.u0)
     for _ in range(args.warmup):
-        sess.step_nodiag()
+        do_step()
     sess.set_profiling(True)
     sess.profile()
     for _ in range(2):
-        sess.step_nodiag()
+        do_step()
     pr = sess.profile()
     sess.set_profiling(False)
     pass_ms = (pr["red_ms"] + pr["black_ms"]) / max(1, pr["red_n"] + pr["black_n"])
@@ -296,11 +364,14 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl.name, "dims": list(wl.dims), "sor_rel_tol": 1e-8,
                        "omega": wl.params["omega"],
                        "parallelism": f"t-slabs x{world} (NCCL halo exchange per colour pass)" if world > 1 else "1 GPU",
-                       "sweeps_timed": int(sweeps), "l2": "inputs larger than L2 (state+rhs+coef+G ~2.5 GB)"},
+                       "sor": f"fixed {fixed} sweeps/step" if fixed else "to relative residual 1e-8",
+                       "sweeps_timed": int(sweeps),
+                       "l2": f"inputs larger than L2: state+coef+G = {wl.n_interior // world * 200 / 1e9:.1f} GB per GPU vs 0.126 GB L2"
+                       if wl.n_interior // world * 200 > 1e9 else "working set partly L2-resident (small config)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * P * world,
                     "d2h_bytes_per_step": 8 * P * world},
             "gpu_launches": int(launches),

@@ -167,6 +167,114 @@ def config1(replicas: int = 1, planes=None) -> Workload:
                                replicas=replicas, planes=(p0, p1)))
 
 
+def _nuclei_tracks(n_nuclei, dims, n_frames, seed):
+    """Seeded nucleus trajectories (config 2/3): start position, semi-axes U[4,8]
+    voxels, intensity U[0.4,1], a N(0, 1.5^2)-per-frame random walk; 10% divide
+    once into two daughters 6 voxels apart that walk on independently.
+    Returns [(birth_frame, death_frame, positions[f] (x,y,z), axes, intensity)]."""
+    n1, n2, n3 = dims
+    rng = np.random.default_rng(seed)
+    tracks = []
+    for _ in range(n_nuclei):
+        axes = rng.uniform(4.0, 8.0, size=3)
+        inten = rng.uniform(0.4, 1.0)
+        p = np.array([rng.uniform(8, n1 - 9), rng.uniform(8, n2 - 9), rng.uniform(6, n3 - 7)])
+        divide_at = int(rng.integers(1, n_frames)) if rng.random() < 0.10 and n_frames > 1 else -1
+        pos = np.zeros((n_frames, 3))
+        for f in range(n_frames):
+            pos[f] = p
+            p = p + rng.normal(0.0, 1.5, size=3)
+            p = np.clip(p, [2, 2, 2], [n1 - 3, n2 - 3, n3 - 3])
+        if divide_at < 0:
+            tracks.append((0, n_frames, pos, axes, inten))
+            continue
+        tracks.append((0, divide_at, pos, axes, inten))
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        for sgn in (-1.0, 1.0):
+            q = pos[divide_at] + sgn * 3.0 * d
+            dpos = pos.copy()
+            for f in range(divide_at, n_frames):
+                dpos[f] = q
+                q = np.clip(q + rng.normal(0.0, 1.5, size=3), [2, 2, 2], [n1 - 3, n2 - 3, n3 - 3])
+            tracks.append((divide_at, n_frames, dpos, axes * 0.8, inten))
+    return tracks
+
+
+def _nuclei_frame(dims, f, tracks, seed):
+    """One frame (z, y, x) of the nuclei volume: background N(0.05, 0.03^2) blurred
+    with a 2-voxel Gaussian, plus the ellipsoids alive in frame f (max-combined)."""
+    from scipy.ndimage import gaussian_filter
+    n1, n2, n3 = dims
+    rng = np.random.default_rng([seed, int(f)])
+    img = gaussian_filter(rng.normal(0.05, 0.03, size=(n3, n2, n1)).astype(np.float32), 2.0).astype(np.float64)
+    for b, e, pos, axes, inten in tracks:
+        if not b <= f < e:
+            continue
+        c = pos[f]
+        lo = np.maximum(np.floor(c - axes).astype(int), 0)
+        hi = np.minimum(np.ceil(c + axes).astype(int) + 1, [n1, n2, n3])
+        x = np.arange(lo[0], hi[0])[None, None, :]
+        y = np.arange(lo[1], hi[1])[None, :, None]
+        z = np.arange(lo[2], hi[2])[:, None, None]
+        inside = ((x - c[0]) / axes[0]) ** 2 + ((y - c[1]) / axes[1]) ** 2 + ((z - c[2]) / axes[2]) ** 2 <= 1.0
+        sub = img[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]]
+        np.maximum(sub, np.where(inside, inten, 0.0), out=sub)
+    return img.astype(np.float32).astype(np.float64)
+
+
+def _nuclei_workload(name, dims, n_nuclei, seed, n_steps, planes, h=1.0 / 32, **over):
+    n1, n2, n3, n4 = dims
+    tracks = _nuclei_tracks(n_nuclei, (n1, n2, n3), n4, seed)
+    p0, p1 = (0, n4 + 1) if planes is None else planes
+    image = np.zeros((p1 - p0 + 1, n3 + 2, n2 + 2, n1 + 2))
+    u0 = np.zeros_like(image)
+    # one seed per nucleus at its first-frame centre; ball = the nucleus + 2 voxels
+    rows = [(b, pos[b][0], pos[b][1], pos[b][2], float(axes.max()) + 2.0)
+            for b, e, pos, axes, inten in tracks if b == 0]
+    x = ((np.arange(n1) + 0.5) * h)[None, None, :]
+    y = ((np.arange(n2) + 0.5) * h)[None, :, None]
+    z = ((np.arange(n3) + 0.5) * h)[:, None, None]
+    for q, p in enumerate(range(p0, p1 + 1)):
+        f = p - 1
+        if not 0 <= f < n4:
+            continue
+        image[q, 1:-1, 1:-1, 1:-1] = _nuclei_frame((n1, n2, n3), f, tracks, seed)
+        if f == 0:  # u0: peak profile 1/(d/h + 1) around every seed of frame 0 (max-combined)
+            v = np.zeros((n3, n2, n1))
+            for r in rows:
+                c = (np.array(r[1:4]) + 0.5) * h
+                lo = np.maximum(np.floor(np.array(r[1:4]) - 12).astype(int), 0)
+                hi = np.minimum(np.ceil(np.array(r[1:4]) + 13).astype(int), [n1, n2, n3])
+                d = np.sqrt((x[..., lo[0]:hi[0]] - c[0]) ** 2 + (y[:, lo[1]:hi[1]] - c[1]) ** 2
+                            + (z[lo[2]:hi[2]] - c[2]) ** 2)
+                sub = v[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]]
+                np.maximum(sub, 1.0 / (d / h + 1.0), out=sub)
+            u0[q, 1:-1, 1:-1, 1:-1] = v
+    params = _base_params(h, n_steps, K=5000.0, lambda_=0.7, rescale_radius=0.0, **over)
+    return Workload(name, dims, h, image, u0, rows, params, n_steps,
+                    notes=dict(nuclei=n_nuclei, h=h, threshold="0.3 -> lambda 0.7", planes=(p0, p1)))
+
+
+def config2(planes=None) -> Workload:
+    """256x256x64 x 32 frames, ~150 nuclei, K=5000, threshold 0.3, 30 steps (h = 1/32)."""
+    return _nuclei_workload("config2: 256x256x64x32 nuclei", (256, 256, 64, 32), 150, 1002, 30, planes)
+
+
+def config3(planes=None) -> Workload:
+    """512x512x128 x 64 frames, ~2000 nuclei, 10 steps, omega 1.4 (>= 2 GPUs)."""
+    return _nuclei_workload("config3: 512x512x128x64 nuclei", (512, 512, 128, 64), 2000, 1003, 10, planes)
+
+
+def config4(gpus: int = 1, planes=None) -> Workload:
+    """Weak scaling: 256x256x128 x (16 * gpus) frames, config-2 data and solver
+    settings, fixed 50 SOR sweeps per time step (no early stop)."""
+    wl = _nuclei_workload(f"config4: 256x256x128x{16 * gpus} nuclei (fixed 50 sweeps/step)",
+                          (256, 256, 128, 16 * gpus), 150 * gpus, 1004, 2, planes)
+    wl.notes["fixed_sweeps"] = 50
+    return wl
+
+
 def small(dims=(16, 12, 10, 8), seed=7) -> Workload:
     """Tiny smoke / test case with config-0 parameters."""
     n1, n2, n3, n4 = dims
@@ -182,4 +290,5 @@ def small(dims=(16, 12, 10, 8), seed=7) -> Workload:
     return Workload(f"small {dims}", dims, h, image, u0, rows, _base_params(h, 3, rescale_radius=4.0), 3)
 
 
-CONFIGS = {"config0": config0, "config1": config1}
+CONFIGS = {"config0": config0, "config1": config1, "config2": config2, "config3": config3,
+           "config4": config4}
