@@ -305,6 +305,8 @@ SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool he
     a.keep = 1.0 - omega;
     for (int q = 0; q < 4; ++q) a.hc[q] = heat ? hc[q] : 0.0;
     a.tma = kernel >= 1 && tma_pass_supported(L) ? 1 : 0;
+    a.l_lo = 1;
+    a.l_hi = L.n4;
     a.wave = kernel == 2 && world == 1 && wflags.p != nullptr ? 1 : 0;
     a.flags = wflags.p;
     if (a.tma)
@@ -316,7 +318,8 @@ SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool he
 }
 
 // ------------------------------------------------------------------ local transport
-void LocalTransport::exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours) {
+void LocalTransport::exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours,
+                              cudaStream_t st) {
     for (size_t s = 0; s + 1 < slabs.size(); ++s) {
         Slab& a = *slabs[s];
         const long long P1 = a.L.plane();
@@ -325,9 +328,9 @@ void LocalTransport::exchange(std::vector<Slab*>& slabs, const std::vector<PFiel
             if (!(colours & (1 << c))) continue;
             // a's last owned plane -> b's halo plane 0; b's first owned plane -> a's halo plane n4+1
             SSB_CUDA(cudaMemcpyAsync(F[s + 1].c[c], F[s].c[c] + n4 * P1, P1 * sizeof(double),
-                                     cudaMemcpyDeviceToDevice, a.stream));
+                                     cudaMemcpyDeviceToDevice, st));
             SSB_CUDA(cudaMemcpyAsync(F[s].c[c] + (n4 + 1) * P1, F[s + 1].c[c] + P1, P1 * sizeof(double),
-                                     cudaMemcpyDeviceToDevice, a.stream));
+                                     cudaMemcpyDeviceToDevice, st));
         }
     }
 }
@@ -357,6 +360,9 @@ void Domain::init_common() {
     SSB_CUDA(cudaSetDevice(device));
     SSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     SSB_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+    SSB_CUDA(cudaStreamCreateWithFlags(&comm, cudaStreamNonBlocking));
+    SSB_CUDA(cudaEventCreateWithFlags(&ev_bnd, cudaEventDisableTiming));
+    SSB_CUDA(cudaEventCreateWithFlags(&ev_xchg, cudaEventDisableTiming));
     SSB_CUDA(cudaMallocHost(&st_host, sizeof(SorState)));
     SSB_CUDA(cudaMallocHost(&flag_host, 8 * sizeof(int)));
     SSB_CUDA(cudaMallocHost(&scal_host, 64 * sizeof(double)));
@@ -410,8 +416,12 @@ Domain::~Domain() {
     if (st_host) cudaFreeHost(st_host);
     if (flag_host) cudaFreeHost(flag_host);
     if (scal_host) cudaFreeHost(scal_host);
+    if (comm) cudaStreamSynchronize(comm);
+    if (ev_bnd) cudaEventDestroy(ev_bnd);
+    if (ev_xchg) cudaEventDestroy(ev_xchg);
     if (stream) cudaStreamDestroy(stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (comm) cudaStreamDestroy(comm);
 }
 
 void Domain::sync() { SSB_CUDA(cudaStreamSynchronize(stream)); }
@@ -442,7 +452,17 @@ std::vector<Domain::Triple> Domain::role_triples(const int roles[kStateBuffers])
     return B;
 }
 
-void Domain::exchange(const std::vector<PField>& F, int colours) { tr->exchange(sp, F, colours); }
+// every exchange runs on the comm stream, fenced by events against the main
+// stream (one stream per communicator keeps the NCCL issue order identical on
+// every rank)
+void Domain::exchange(const std::vector<PField>& F, int colours) {
+    if (world == 1) return;
+    SSB_CUDA(cudaEventRecord(ev_bnd, stream));
+    SSB_CUDA(cudaStreamWaitEvent(comm, ev_bnd, 0));
+    tr->exchange(sp, F, colours, comm);
+    SSB_CUDA(cudaEventRecord(ev_xchg, comm));
+    SSB_CUDA(cudaStreamWaitEvent(stream, ev_xchg, 0));
+}
 void Domain::exchange_role(int role, int colours) { exchange(role_fields(role), colours); }
 
 std::vector<double> Domain::gather_values(const std::vector<std::vector<double>>& per_slab, int k) {
@@ -528,10 +548,24 @@ void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>
     const int bout = out_buf(n);
     std::vector<PField> F;
     for (const Triple& t : B) F.push_back(t[bout]);
+    // boundary slices first, their exchange on the comm stream overlapped with
+    // the interior slices (the paper overlaps Isend/Irecv the same way)
+    auto pass = [&](int colour) {
+        for (const SorArgs& x : a) {
+            const int n4 = x.L.n4;
+            launch_sor_pass_range(stream, x, colour, heat, 1, 1);
+            if (n4 > 1) launch_sor_pass_range(stream, x, colour, heat, n4, n4);
+        }
+        SSB_CUDA(cudaEventRecord(ev_bnd, stream));
+        SSB_CUDA(cudaStreamWaitEvent(comm, ev_bnd, 0));
+        tr->exchange(sp, F, colour == 0 ? 1 : 2, comm);
+        SSB_CUDA(cudaEventRecord(ev_xchg, comm));
+        for (const SorArgs& x : a) launch_sor_pass_range(stream, x, colour, heat, 2, x.L.n4 - 1);
+        SSB_CUDA(cudaStreamWaitEvent(stream, ev_xchg, 0));
+    };
     if (ev4) SSB_CUDA(cudaEventRecord(ev4[0], stream));
-    for (const SorArgs& x : a) launch_sor_pass(stream, x, 0, heat);
+    pass(0);
     if (ev4) SSB_CUDA(cudaEventRecord(ev4[1], stream));
-    tr->exchange(sp, F, 1);
     for (const SorArgs& x : a) launch_sor_finalize(stream, x);
     std::vector<double*> loc, all;
     for (Slab* s : sp) {
@@ -541,9 +575,8 @@ void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>
     tr->allgather(sp, loc, all, chunk);
     for (const SorArgs& x : a) launch_sor_decide(stream, x);
     if (ev4) SSB_CUDA(cudaEventRecord(ev4[2], stream));
-    for (const SorArgs& x : a) launch_sor_pass(stream, x, 1, heat);
+    pass(1);
     if (ev4) SSB_CUDA(cudaEventRecord(ev4[3], stream));
-    tr->exchange(sp, F, 2);
 }
 
 SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& rhs, bool heat, double omega,

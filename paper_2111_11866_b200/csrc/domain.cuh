@@ -140,21 +140,23 @@ struct Slab {
 struct Transport {
     virtual ~Transport() = default;
     // owned boundary planes of F[s] (colour mask: 1 red, 2 black) into the
-    // l-neighbours' halo planes
-    virtual void exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours) = 0;
+    // l-neighbours' halo planes, issued on stream s
+    virtual void exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours,
+                          cudaStream_t s) = 0;
     // every slab's local[s] (chunk doubles) -> all[s'][rank * chunk] for all s'
     virtual void allgather(std::vector<Slab*>& slabs, const std::vector<double*>& local,
                            const std::vector<double*>& all, int chunk) = 0;
 };
 
 struct NullTransport : Transport {
-    void exchange(std::vector<Slab*>&, const std::vector<PField>&, int) override {}
+    void exchange(std::vector<Slab*>&, const std::vector<PField>&, int, cudaStream_t) override {}
     void allgather(std::vector<Slab*>&, const std::vector<double*>&, const std::vector<double*>&,
                    int) override {}
 };
 
 struct LocalTransport : Transport {
-    void exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours) override;
+    void exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours,
+                  cudaStream_t s) override;
     void allgather(std::vector<Slab*>& slabs, const std::vector<double*>& local,
                    const std::vector<double*>& all, int chunk) override;
 };
@@ -170,6 +172,8 @@ struct Domain {
     int device = 0;
     bool distributed = false;  // NCCL: slabs.size() == 1 < world
     cudaStream_t stream = nullptr, cap_stream = nullptr;
+    cudaStream_t comm = nullptr;  // halo exchanges (overlapped with interior slices)
+    cudaEvent_t ev_bnd = nullptr, ev_xchg = nullptr;
     std::vector<std::unique_ptr<Slab>> slabs;
     std::vector<Slab*> sp;  // raw pointers, rank order
     std::unique_ptr<Transport> tr;

@@ -46,6 +46,7 @@ struct SorArgs {
     int tx, ty, tk;         // tile grid of one slice (pass_tiles)
     long long tiles;
     int tma;                // 1: TMA-fed pass kernel (sor_tma.cu), 0: LDG pass (sor.cu)
+    int l_lo, l_hi;         // slices (local, 1-based) a pass launch covers (default 1 .. n4)
     int wave;               // 1: two-iteration wavefront kernel per loop body
     int* flags;             // wavefront item completion flags (epochs)
     int use_cond;
@@ -82,6 +83,8 @@ void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* nor
 void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* ev /*4 or null*/);
 // pieces for the multi-slab body (halo exchange / all-gather between them)
 void launch_sor_pass(cudaStream_t s, const SorArgs& a, int colour, bool heat);
+// the same pass restricted to slices [lo, hi] (boundary-first halo overlap)
+void launch_sor_pass_range(cudaStream_t s, const SorArgs& a, int colour, bool heat, int lo, int hi);
 void launch_sor_finalize(cudaStream_t s, const SorArgs& a);
 void launch_sor_decide(cudaStream_t s, const SorArgs& a);
 

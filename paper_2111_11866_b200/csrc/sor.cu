@@ -101,7 +101,9 @@ __global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(con
 
     const float* __restrict__ cf = a.coef[C];
     const double* __restrict__ rh = a.rhs[C];
-    for (long long t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+    const long long per_slice = a.tiles / L.n4;
+    const long long t_end = (long long)a.l_hi * per_slice;
+    for (long long t = (long long)(a.l_lo - 1) * per_slice + blockIdx.x; t < t_end; t += gridDim.x) {
         const int bx = (int)(t % a.tx);
         long long r = t / a.tx;
         const int by = (int)(r % a.ty);
@@ -260,7 +262,8 @@ void launch_sor_pass(cudaStream_t s, const SorArgs& a, int colour, bool heat) {
         launch_sor_pass_tma(s, a, colour, heat);
         return;
     }
-    const unsigned grid = (unsigned)std::min<long long>(a.tiles, resident_blocks());
+    const long long items = a.tiles / a.L.n4 * (a.l_hi - a.l_lo + 1);
+    const unsigned grid = (unsigned)std::min<long long>(items, resident_blocks());
     const dim3 block(kPassBX, kPassBY);
     if (colour == 0) {
         if (heat)
@@ -274,6 +277,14 @@ void launch_sor_pass(cudaStream_t s, const SorArgs& a, int colour, bool heat) {
             sor_pass<1, false><<<grid, block, 0, s>>>(a);
     }
     SSB_LAUNCHED();
+}
+
+void launch_sor_pass_range(cudaStream_t s, const SorArgs& a, int colour, bool heat, int lo, int hi) {
+    if (lo > hi) return;
+    SorArgs b = a;
+    b.l_lo = lo;
+    b.l_hi = hi;
+    launch_sor_pass(s, b, colour, heat);
 }
 
 void launch_sor_finalize(cudaStream_t s, const SorArgs& a) {

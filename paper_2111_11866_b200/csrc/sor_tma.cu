@@ -267,12 +267,14 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
     double* ucw = a.U[bout][C];
     const Geo G = make_geo(L);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long per_slice = (long long)G.njg * G.nkc;
+    const long long t_begin = (long long)(a.l_lo - 1) * per_slice, t_end = (long long)a.l_hi * per_slice;
     init_barriers(full, empty);
 
     if (warp == kWarps) {  // producer: one thread issues every bulk copy
         if (lane != 0) return;
         Ring rg;
-        for (long long t = blockIdx.x; t < G.items; t += gridDim.x) {
+        for (long long t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
             const int jg = (int)(t % G.njg);
             const long long r = t / G.njg;
             const Item it = make_item(L, G, (int)(r / G.nkc) + 1, jg, (int)(r % G.nkc));
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
         return;
     }
     uint32_t s0 = 0, ph0 = 0;
-    for (long long t = blockIdx.x; t < G.items; t += gridDim.x) {
+    for (long long t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
         const int jg = (int)(t % G.njg);
         const long long r = t / G.njg;
         const Item it = make_item(L, G, (int)(r / G.nkc) + 1, jg, (int)(r % G.nkc));
@@ -509,7 +511,8 @@ void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat
         blocks = tma_blocks((const void*)sor_pass_tma<0, false>, smem);
         last_smem = smem;
     }
-    const unsigned grid = (unsigned)std::min<long long>(G.items, blocks);
+    const long long items = (long long)G.njg * G.nkc * (a.l_hi - a.l_lo + 1);
+    const unsigned grid = (unsigned)std::min<long long>(items, blocks);
     if (colour == 0) {
         if (heat)
             sor_pass_tma<0, true><<<grid, kThreads, smem, s>>>(a);

@@ -28,6 +28,7 @@ struct NcclApi {
     ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -50,6 +51,7 @@ NcclApi& api() {
         SSB_SYM("ncclGetUniqueId", GetUniqueId);
         SSB_SYM("ncclCommInitRank", CommInitRank);
         SSB_SYM("ncclCommDestroy", CommDestroy);
+        SSB_SYM("ncclCommSplit", CommSplit);
         SSB_SYM("ncclGroupStart", GroupStart);
         SSB_SYM("ncclGroupEnd", GroupEnd);
         SSB_SYM("ncclSend", Send);
@@ -58,7 +60,7 @@ NcclApi& api() {
         SSB_SYM("ncclGetErrorString", GetErrorString);
 #undef SSB_SYM
     });
-    if (!a.h || !a.AllGather || !a.Send || !a.CommInitRank)
+    if (!a.h || !a.AllGather || !a.Send || !a.CommInitRank || !a.CommSplit)
         throw Error(SS_ERR_NCCL, "NCCL unavailable: " + (err.empty() ? std::string("missing symbols") : err));
     return a;
 }
@@ -68,18 +70,24 @@ void check(ncclResult_t r, const char* what) {
         throw Error(SS_ERR_NCCL, std::string(what) + ": " + (api().GetErrorString ? api().GetErrorString(r) : "?"));
 }
 
+// Two communicators: `halo` for the send/recv exchanges (always issued on the
+// Domain's comm stream) and `comm` for the residual all-gathers (main stream),
+// so each communicator's operations are issued from one stream in the same
+// order on every rank.
 struct NcclTransport : Transport {
-    ncclComm_t comm = nullptr;
+    ncclComm_t comm = nullptr, halo = nullptr;
     int rank, world;
     NcclTransport(const unsigned char* uid, int r, int w) : rank(r), world(w) {
         ncclUniqueId id;
         std::memcpy(id.internal, uid, NCCL_UNIQUE_ID_BYTES);
         check(api().CommInitRank(&comm, w, id, r), "ncclCommInitRank");
+        check(api().CommSplit(comm, 0, r, &halo, nullptr), "ncclCommSplit");
     }
     ~NcclTransport() override {
+        if (halo) api().CommDestroy(halo);
         if (comm) api().CommDestroy(comm);
     }
-    void exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours) override {
+    void exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours, cudaStream_t st) override {
         Slab& s = *slabs[0];
         const size_t P1 = (size_t)s.L.plane();
         const int n4 = s.L.n4;
@@ -89,12 +97,12 @@ struct NcclTransport : Transport {
             if (!(colours & (1 << c))) continue;
             double* f = F[0].c[c];
             if (rank > 0) {
-                check(a.Send(f + P1, P1, ncclDouble, rank - 1, comm, s.stream), "ncclSend");
-                check(a.Recv(f, P1, ncclDouble, rank - 1, comm, s.stream), "ncclRecv");
+                check(a.Send(f + P1, P1, ncclDouble, rank - 1, halo, st), "ncclSend");
+                check(a.Recv(f, P1, ncclDouble, rank - 1, halo, st), "ncclRecv");
             }
             if (rank + 1 < world) {
-                check(a.Send(f + (size_t)n4 * P1, P1, ncclDouble, rank + 1, comm, s.stream), "ncclSend");
-                check(a.Recv(f + (size_t)(n4 + 1) * P1, P1, ncclDouble, rank + 1, comm, s.stream), "ncclRecv");
+                check(a.Send(f + (size_t)n4 * P1, P1, ncclDouble, rank + 1, halo, st), "ncclSend");
+                check(a.Recv(f + (size_t)(n4 + 1) * P1, P1, ncclDouble, rank + 1, halo, st), "ncclRecv");
             }
         }
         check(a.GroupEnd(), "ncclGroupEnd");
