@@ -163,6 +163,11 @@ SS_API ss_status ss_session_get_mask(ss_session* s, double level, uint8_t* mask)
 /* fixed-sweep mode (BASELINE config 4): assemble at the current u, then exactly
  * n_sweeps red+black sweeps with no stopping test; *residual = last residual. */
 SS_API ss_status ss_session_fixed_sweeps(ss_session* s, int n_sweeps, double* residual);
+/* run_levelset_row (eoc.cpp:83-137): the EOC verification row n (10/20/40/80/160) on a
+ * session created for the grid n^4 with h = 2.5/n; *err = space-time L2 error,
+ * *sweeps = total SOR sweeps (may be NULL).  EocConfig defaults: omega 1.5, tol 1e-8. */
+SS_API ss_status ss_session_eoc_row(ss_session* s, int n, double omega, double sor_tol, int sor_max_iter,
+                                    double* err, long long* sweeps);
 /* 0 = host-driven chunked loop, 1 = CUDA-graph conditional loop (default) */
 SS_API ss_status ss_session_set_loop_mode(ss_session* s, int mode);
 /* SOR kernel: 1 = TMA-fed two-pass (default), 0 = plain LDG two-pass, 2 = two-iteration

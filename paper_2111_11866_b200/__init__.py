@@ -194,6 +194,8 @@ def library() -> C.CDLL:
     sig("ss_session_get_mask", [C.c_void_p, C.c_double, C.POINTER(C.c_uint8)])
     sig("ss_session_fixed_sweeps", [C.c_void_p, C.c_int, _D])
     sig("ss_session_set_loop_mode", [C.c_void_p, C.c_int])
+    sig("ss_session_eoc_row", [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, _D,
+                               C.POINTER(C.c_longlong)])
     sig("ss_session_set_profiling", [C.c_void_p, C.c_int])
     sig("ss_session_set_kernel", [C.c_void_p, C.c_int])
     sig("ss_session_profile", [C.c_void_p, C.POINTER(Profile)])
@@ -380,6 +382,17 @@ def segment(image, centers, params: SegParams, g: Grid, u0=None):
     _check(library().ss_segment(C.byref(g), _dp(a), arr, n, C.byref(params), _dp(u0a), _dp(out), diags))
     return out, [dict(iterations=d.iterations, residual=d.residual, tol=d.tol, umin=d.umin,
                       umax=d.umax) for d in diags]
+
+
+def eoc_row(n: int, omega: float = 1.5, sor_tol: float = 1e-8, sor_max_iter: int = 10000,
+            n_slabs: int = 1, device: int = 0):
+    """run_levelset_row (eoc.cpp:83-137) on the GPU: returns (L2 error, total SOR sweeps)."""
+    g = Grid.make((n,) * 4, 2.5 / n)
+    with Session(g, device=device, n_slabs=n_slabs) as s:
+        err = C.c_double(0.0)
+        sw = C.c_longlong(0)
+        _check(library().ss_session_eoc_row(s._h, n, omega, sor_tol, sor_max_iter, C.byref(err), C.byref(sw)))
+        return err.value, sw.value
 
 
 # ----------------------------------------------------------------------------- device session

@@ -456,6 +456,17 @@ ss_status ss_session_fixed_sweeps(ss_session* s, int n_sweeps, double* residual)
     });
 }
 
+ss_status ss_session_eoc_row(ss_session* s, int n, double omega, double sor_tol, int sor_max_iter, double* err,
+                             long long* sweeps) {
+    return guard([&] {
+        require(s && err, "null session / output");
+        validate_solver(1.0, 1.0, omega, sor_tol, sor_max_iter, 1);
+        SSB_CUDA(cudaSetDevice(s->d->device));
+        s->d->prepared = false;
+        *err = s->d->eoc_row(n, omega, sor_tol, sor_max_iter, sweeps);
+    });
+}
+
 ss_status ss_session_set_loop_mode(ss_session* s, int mode) {
     return guard([&] {
         require(s != nullptr, "null session");

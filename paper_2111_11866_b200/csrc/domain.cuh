@@ -234,6 +234,8 @@ struct Domain {
                  const double* u0);
     void step(ss_step_diag* diag);
     double fixed_sweeps(int n_sweeps);
+    // EOC verification row (eoc.cpp:83-137) on an n^4 session; returns the space-time L2 error
+    double eoc_row(int n, double omega, double sor_tol, int max_iter, long long* total_sweeps);
 
 private:
     void init_common();
