@@ -29,8 +29,13 @@ namespace ssb {
 
 namespace {
 
-constexpr int kWarps = 8;         // consumer warps
-constexpr int kThreads = (kWarps + 1) * 32;
+constexpr int kWarps = 8;  // "virtual" consumer warps: one row (segment) each, one residual partial each
+#ifndef SSB_RPW
+#define SSB_RPW 1
+#endif
+constexpr int kRPW = SSB_RPW;                   // virtual warps computed (interleaved) per physical warp
+constexpr int kConsumers = kWarps / kRPW;       // physical consumer warps
+constexpr int kThreads = (kConsumers + 1) * 32;
 constexpr int kStages = 5;
 constexpr int kPlanesPerItem = 8;
 #ifndef SSB_WAVE_SKEW
@@ -152,20 +157,29 @@ __device__ __forceinline__ void produce_item(const Layout& L, const Geo& G, unsi
     }
 }
 
-// Consumers (8 warps): update colour C on the item's planes from the staged
-// rows; returns this warp's sum of squared residuals.  (s0, ph0) is the ring
-// position of the item's first stage and is advanced past the item.
+// Consumers: update colour C on the item's planes from the staged rows.  Each
+// physical warp computes kRPW virtual warps (rows / row segments) with their
+// loads and dependency chains interleaved (ILP), and returns each virtual
+// warp's sum of squared residuals in r2[].  (s0, ph0) is the ring position of
+// the item's first stage and is advanced past the item.
 template <int C, bool HEAT>
-__device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L, const Geo& G,
-                                               unsigned char* smem, uint64_t* full, uint64_t* empty,
-                                               uint32_t& s0, uint32_t& ph0, const Item& it,
-                                               double* __restrict__ ucw, int warp, int lane) {
+__device__ __forceinline__ void consume_item(const SorArgs& a, const Layout& L, const Geo& G,
+                                             unsigned char* smem, uint64_t* full, uint64_t* empty,
+                                             uint32_t& s0, uint32_t& ph0, const Item& it,
+                                             double* __restrict__ ucw, int warp, int lane,
+                                             double r2[kRPW]) {
     const long long W = L.W;
-    const int rloc = warp / G.wpr, seg = warp % G.wpr;
     const int nq = (L.n1 + 1) / 2;
     const int l = it.l;
-    const int j = it.j0 + rloc;
-    double r2 = 0.0;
+    int rloc[kRPW], seg[kRPW], jv[kRPW];
+#pragma unroll
+    for (int v = 0; v < kRPW; ++v) {
+        const int vw = warp * kRPW + v;
+        rloc[v] = vw / G.wpr;
+        seg[v] = vw % G.wpr;
+        jv[v] = it.j0 + rloc[v];
+        r2[v] = 0.0;
+    }
     // (slot, phase) of stages q-1 (plane p-1), q (p), q+1 (p+1)
     uint32_t sm = s0, pm = ph0;
     uint32_t sc = sm + 1 == kStages ? 0 : sm + 1, pc = sm + 1 == kStages ? pm ^ 1 : pm;
@@ -174,52 +188,68 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
     for (int p = it.k0; p <= it.k1; ++p) {
         const uint32_t sp = sc + 1 == kStages ? 0 : sc + 1, pp = sc + 1 == kStages ? pc ^ 1 : pc;
         mbar_wait(&full[sp], pp);
-        if (rloc < it.rows) {
-            const unsigned char* scb = smem + sc * G.stage_bytes;
-            const double* ukm = reinterpret_cast<const double*>(smem + sm * G.stage_bytes + G.off_uk);
-            const double* ukc = reinterpret_cast<const double*>(scb + G.off_uk);
-            const double* ukp = reinterpret_cast<const double*>(smem + sp * G.stage_bytes + G.off_uk);
-            const float* cf = reinterpret_cast<const float*>(scb + G.off_coef) + (long long)rloc * W * 8;
-            const double* rh = reinterpret_cast<const double*>(scb + G.off_rhs) + rloc * W;
-            const double* u0r = reinterpret_cast<const double*>(scb + G.off_uc) + rloc * W;
-            const double* ulm = reinterpret_cast<const double*>(scb + G.off_ulm) + rloc * W;
-            const double* ulp = reinterpret_cast<const double*>(scb + G.off_ulp) + rloc * W;
-            const double* ukc_r = ukc + (rloc + 1) * W;  // this row in the (rows+2)-row block
-            const long long grow = (((long long)l * L.kMax + p) * L.jMax + j) * W;
-            const int i0 = 1 + ((1 + j + p + l + L.lpar + C) & 1);
-            for (int qq = seg * 32 + lane; qq < nq; qq += 32 * G.wpr) {
-                const int i = i0 + 2 * qq;
-                if (i > L.n1) break;
+        const unsigned char* scb = smem + sc * G.stage_bytes;
+        const double* ukm = reinterpret_cast<const double*>(smem + sm * G.stage_bytes + G.off_uk);
+        const double* ukc = reinterpret_cast<const double*>(scb + G.off_uk);
+        const double* ukp = reinterpret_cast<const double*>(smem + sp * G.stage_bytes + G.off_uk);
+        const float* cf = reinterpret_cast<const float*>(scb + G.off_coef);
+        const double* rh = reinterpret_cast<const double*>(scb + G.off_rhs);
+        const double* u0r = reinterpret_cast<const double*>(scb + G.off_uc);
+        const double* ulm = reinterpret_cast<const double*>(scb + G.off_ulm);
+        const double* ulp = reinterpret_cast<const double*>(scb + G.off_ulp);
+        for (int q0 = lane; q0 < nq; q0 += 32 * G.wpr) {
+            DoxelIn d[kRPW];
+            bool ok[kRPW];
+#pragma unroll
+            for (int v = 0; v < kRPW; ++v) {  // all loads first
+                const int j = jv[v], r = rloc[v];
+                const int i = 1 + ((1 + j + p + l + L.lpar + C) & 1) + 2 * (q0 + 32 * seg[v]);
+                ok[v] = r < it.rows && q0 + 32 * seg[v] < nq && i <= L.n1;
+                if (!ok[v]) continue;
                 const int m = i >> 1;
-                DoxelIn d;
                 if constexpr (HEAT) {
-                    d.c[0] = i > 1 ? (float)a.hc[0] : 0.f;
-                    d.c[1] = i < L.n1 ? (float)a.hc[0] : 0.f;
-                    d.c[2] = j > 1 ? (float)a.hc[1] : 0.f;
-                    d.c[3] = j < L.n2 ? (float)a.hc[1] : 0.f;
-                    d.c[4] = p > 1 ? (float)a.hc[2] : 0.f;
-                    d.c[5] = p < L.n3 ? (float)a.hc[2] : 0.f;
-                    d.c[6] = l + L.l0 > 1 ? (float)a.hc[3] : 0.f;
-                    d.c[7] = l + L.l0 < L.n4g ? (float)a.hc[3] : 0.f;
+                    d[v].c[0] = i > 1 ? (float)a.hc[0] : 0.f;
+                    d[v].c[1] = i < L.n1 ? (float)a.hc[0] : 0.f;
+                    d[v].c[2] = j > 1 ? (float)a.hc[1] : 0.f;
+                    d[v].c[3] = j < L.n2 ? (float)a.hc[1] : 0.f;
+                    d[v].c[4] = p > 1 ? (float)a.hc[2] : 0.f;
+                    d[v].c[5] = p < L.n3 ? (float)a.hc[2] : 0.f;
+                    d[v].c[6] = l + L.l0 > 1 ? (float)a.hc[3] : 0.f;
+                    d[v].c[7] = l + L.l0 < L.n4g ? (float)a.hc[3] : 0.f;
                 } else {
-                    const float4 lo = *reinterpret_cast<const float4*>(cf + m * 8);
-                    const float4 hi = *reinterpret_cast<const float4*>(cf + m * 8 + 4);
-                    d.c[0] = lo.x; d.c[1] = lo.y; d.c[2] = lo.z; d.c[3] = lo.w;
-                    d.c[4] = hi.x; d.c[5] = hi.y; d.c[6] = hi.z; d.c[7] = hi.w;
+                    const float* c8 = cf + ((long long)r * W + m) * 8;
+                    const float4 lo = *reinterpret_cast<const float4*>(c8);
+                    const float4 hi = *reinterpret_cast<const float4*>(c8 + 4);
+                    d[v].c[0] = lo.x; d[v].c[1] = lo.y; d[v].c[2] = lo.z; d[v].c[3] = lo.w;
+                    d[v].c[4] = hi.x; d[v].c[5] = hi.y; d[v].c[6] = hi.z; d[v].c[7] = hi.w;
                 }
-                d.rhs = rh[m];
-                d.u0 = u0r[m];
-                d.nb[0] = ukc_r[(i - 1) >> 1];
-                d.nb[1] = ukc_r[(i + 1) >> 1];
-                d.nb[2] = ukc[rloc * W + m];
-                d.nb[3] = ukc[(rloc + 2) * W + m];
-                d.nb[4] = ukm[(rloc + 1) * W + m];
-                d.nb[5] = ukp[(rloc + 1) * W + m];
-                d.nb[6] = ulm[m];
-                d.nb[7] = ulp[m];
-                d.p = grow + m;
-                r2 += compute_doxel<C>(a, d, ucw);
+                const double* ur = ukc + (r + 1) * W;  // this row in the (rows+2)-row block
+                d[v].rhs = rh[r * W + m];
+                d[v].u0 = u0r[r * W + m];
+                d[v].nb[0] = ur[(i - 1) >> 1];
+                d[v].nb[1] = ur[(i + 1) >> 1];
+                d[v].nb[2] = ukc[r * W + m];
+                d[v].nb[3] = ukc[(r + 2) * W + m];
+                d[v].nb[4] = ukm[(r + 1) * W + m];
+                d[v].nb[5] = ukp[(r + 1) * W + m];
+                d[v].nb[6] = ulm[r * W + m];
+                d[v].nb[7] = ulp[r * W + m];
+                d[v].p = (((long long)l * L.kMax + p) * L.jMax + j) * W + m;
             }
+#ifndef SSB_NOCOMPUTE
+#pragma unroll
+            for (int v = 0; v < kRPW; ++v)
+                if (ok[v]) r2[v] += compute_doxel<C>(a, d[v], ucw);
+#else  // data-movement floor experiment: touch the operands, store u0
+#pragma unroll
+            for (int v = 0; v < kRPW; ++v)
+                if (ok[v]) {
+                    double s = d[v].rhs + d[v].u0 + (double)d[v].c[0] + (double)d[v].c[7];
+                    for (int f = 0; f < 8; ++f) s += d[v].nb[f];
+                    ucw[d[v].p] = s;
+                    r2[v] += s * 1e-300;
+                }
+#endif
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[sm]);  // plane p-1's stage is done
@@ -237,15 +267,16 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
     s0 = sc + 1 == kStages ? 0 : sc + 1;
     ph0 = sc + 1 == kStages ? pc ^ 1 : pc;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
-    return r2;
+    for (int v = 0; v < kRPW; ++v)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r2[v] += __shfl_down_sync(0xffffffffu, r2[v], o);
 }
 
 __device__ __forceinline__ void init_barriers(uint64_t* full, uint64_t* empty) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kWarps);
+            mbar_init(&empty[s], kConsumers);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -271,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
     const long long t_begin = (long long)(a.l_lo - 1) * per_slice, t_end = (long long)a.l_hi * per_slice;
     init_barriers(full, empty);
 
-    if (warp == kWarps) {  // producer: one thread issues every bulk copy
+    if (warp == kConsumers) {  // producer: one thread issues every bulk copy
         if (lane != 0) return;
         Ring rg;
         for (long long t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
@@ -287,8 +318,11 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
         const int jg = (int)(t % G.njg);
         const long long r = t / G.njg;
         const Item it = make_item(L, G, (int)(r / G.nkc) + 1, jg, (int)(r % G.nkc));
-        const double r2 = consume_item<C, HEAT>(a, L, G, smem, full, empty, s0, ph0, it, ucw, warp, lane);
-        if (lane == 0) a.part[n & 3][C][t * kWarps + warp] = r2;
+        double r2[kRPW];
+        consume_item<C, HEAT>(a, L, G, smem, full, empty, s0, ph0, it, ucw, warp, lane, r2);
+        if (lane == 0)
+#pragma unroll
+            for (int v = 0; v < kRPW; ++v) a.part[n & 3][C][t * kWarps + warp * kRPW + v] = r2[v];
     }
 }
 
@@ -357,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 2) sor_wave_tma(const SorArgs a) {
         c = (int)(s % G.nkc) * G.njg + jg;
     };
 
-    if (warp == kWarps) {  // producer
+    if (warp == kConsumers) {  // producer
         if (lane != 0) return;
         Ring rg;
         for (long long t = blockIdx.x; t < NT; t += gridDim.x) {
@@ -398,12 +432,18 @@ __global__ void __launch_bounds__(kThreads, 2) sor_wave_tma(const SorArgs a) {
         const int jg = c % G.njg, kc = c / G.njg;
         const Item it = make_item(L, G, l, jg, kc);
         double* ucw = a.U[out_buf(m)][C];
-        const double r2 = C == 0 ? consume_item<0, HEAT>(a, L, G, smem, full, empty, s0, ph0, it, ucw, warp, lane)
-                                 : consume_item<1, HEAT>(a, L, G, smem, full, empty, s0, ph0, it, ucw, warp, lane);
-        if (lane == 0) a.part[m & 3][C][((long long)(l - 1) * CH + c) * kWarps + warp] = r2;
+        double r2[kRPW];
+        if (C == 0)
+            consume_item<0, HEAT>(a, L, G, smem, full, empty, s0, ph0, it, ucw, warp, lane, r2);
+        else
+            consume_item<1, HEAT>(a, L, G, smem, full, empty, s0, ph0, it, ucw, warp, lane, r2);
+        if (lane == 0)
+#pragma unroll
+            for (int v = 0; v < kRPW; ++v)
+                a.part[m & 3][C][((long long)(l - 1) * CH + c) * kWarps + warp * kRPW + v] = r2[v];
         // publish: every consumer's stores, then one flag store (release)
         __threadfence();
-        asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
         if (threadIdx.x == 0) {
             int* q = a.flags + ((long long)d * L.n4 + (l - 1)) * CH + c;
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(q), "r"(epoch) : "memory");
