@@ -309,6 +309,9 @@ SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool he
     a.l_hi = L.n4;
     a.wave = kernel == 2 && world == 1 && wflags.p != nullptr ? 1 : 0;
     a.flags = wflags.p;
+    a.snake = pass_snake();
+    a.l2hint = pass_l2hint();
+    a.order = pass_order();
     if (a.tma)
         tma_pass_tiles(L, a);
     else

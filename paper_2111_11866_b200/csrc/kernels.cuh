@@ -49,6 +49,10 @@ struct SorArgs {
     int l_lo, l_hi;         // slices (local, 1-based) a pass launch covers (default 1 .. n4)
     int wave;               // 1: two-iteration wavefront kernel per loop body
     int* flags;             // wavefront item completion flags (epochs)
+    int snake;              // TMA pass: black passes walk the items in reverse (L2 reuse at the turn)
+    int order;              // TMA pass item order: 0 slice-major, 1 slice-fastest
+    int l2hint;             // TMA pass L2 policies: bit0 coef/rhs evict_first, bit1 u loads evict_last,
+                            // bit2 u stores evict_last
     int use_cond;
     cudaGraphConditionalHandle cond;
 };
@@ -73,6 +77,9 @@ bool tma_pass_supported(const Layout& L);
 void tma_pass_tiles(const Layout& L, SorArgs& a);
 size_t tma_partials(const Layout& L);
 void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat);
+int pass_snake();   // SorArgs::snake default (env SSB_SNAKE)
+int pass_l2hint();  // SorArgs::l2hint default (env SSB_L2HINT)
+int pass_order();   // SorArgs::order default (env SSB_ORDER)
 bool wave_supported(const Layout& L);
 size_t wave_flags(const Layout& L);
 void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat);

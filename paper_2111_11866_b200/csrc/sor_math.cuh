@@ -15,15 +15,20 @@ struct DoxelIn {
     long long p;
 };
 
+// store of the new value; with an L2 cache policy (TMA pass) or plain (LDG pass)
+__device__ __forceinline__ void store_u(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 // The update of solver.cpp:292-313; returns the squared residual contribution
 // (black: in-sweep, :309-312; red: of the incoming state, :347-356).
 // Every rounding is the reference's: the products c_f * u_f are formed once and
 // feed both the update (acc -= p_f) and the red residual (res += p_f) -- the
 // reference evaluates the same products in both places -- so the three
 // dependency chains (diag sum, acc, residual) can overlap.
-template <int C>
+template <int C, bool HINT = false>
 __device__ __forceinline__ double compute_doxel(const SorArgs& a, const DoxelIn& d,
-                                                double* __restrict__ ucw) {
+                                                double* __restrict__ ucw, uint64_t pol = 0) {
     const double c0 = (double)d.c[0], c1 = (double)d.c[1], c2 = (double)d.c[2];
     const double c3 = (double)d.c[3], c4 = (double)d.c[4], c5 = (double)d.c[5];
     const double c6 = (double)d.c[6], c7 = (double)d.c[7];
@@ -50,12 +55,19 @@ __device__ __forceinline__ double compute_doxel(const SorArgs& a, const DoxelIn&
         res += p6;
         res += p7;
         const double ubar = acc / dg;
-        ucw[d.p] = a.omega * ubar + a.keep * d.u0;
+        const double unew = a.omega * ubar + a.keep * d.u0;
+        if constexpr (HINT)
+            store_u(ucw + d.p, unew, pol);
+        else
+            ucw[d.p] = unew;
         return res * res;
     } else {
         const double ubar = acc / dg;
         const double unew = a.omega * ubar + a.keep * d.u0;
-        ucw[d.p] = unew;
+        if constexpr (HINT)
+            store_u(ucw + d.p, unew, pol);
+        else
+            ucw[d.p] = unew;
         const double res = dg * (unew - ubar);
         return res * res;
     }

@@ -1,27 +1,33 @@
 // sor_tma.cu -- TMA-fed red-black SOR colour pass (the hot kernel).
 //
 // The LDG pass (sor.cu) is latency-bound: every thread waits on eleven global
-// loads per doxel.  Here one producer thread per CTA streams, with
+// loads per doxel.  Here two producer threads per CTA stream, with
 // cp.async.bulk (TMA) and mbarrier completion, everything a work item needs
-// into a ring of shared-memory stages, and eight consumer warps compute from
-// shared memory only; up to kStages-3 planes are in flight per CTA.
+// into two rings of shared-memory stages, and eight consumer warps compute from
+// shared memory only.
 //
 // Work item = R consecutive rows j0..j0+R-1 (all W packed slots of a row) x a
-// chunk of planes k0..k1 of one slice l.  Stage q of an item holds, for plane
-// p = k0-1+q:
-//     UK   rows j0-1..j0+R of the other colour at (p, l)       (always)
-//     COEF R rows of fp32 coefficients of colour C at (p, l)  (interior planes)
+// chunk of planes k0..k1 of one slice l.  Per plane p the item needs
+//     UK   rows j0-1..j0+R of the other colour at (p, l)       (planes k0-1..k1+1)
+//     COEF R rows of fp32 coefficients of colour C at (p, l)  (planes k0..k1)
 //     RHS  R rows of rhs, UC R rows of colour C's own values
 //     ULM / ULP  R rows of the other colour at (p, l-1) / (p, l+1)
-// so the consumer of plane p reads UK of stages q-1, q, q+1 (the k-1, k, k+1
-// neighbours: a rolling window -- each other-colour row is fetched once per
-// item, not three times) and everything else from stage q.  Rows of a plane
-// are consecutive in the packed layout, so every stream of a stage is ONE
+// The consumer of plane p reads UK of planes p-1, p, p+1 (a rolling window:
+// each other-colour row is fetched once per item) and the rest of plane p
+// only, so UK stages live in their own ring (held for three planes) and the
+// main stages (COEF..ULP, released after one plane) in another: the main ring
+// keeps kMainStages-1 planes in flight per CTA.  Rows of a plane are
+// consecutive in the packed layout, so every stream of a stage is ONE
 // contiguous bulk copy (W is even: rows are 16-byte aligned).
 //
-// Residual partials: one per (item, warp), items ordered l-major, so the
-// per-slice sums do not depend on the grid size (same contract as sor.cu).
+// Item order: slice-fastest (order 1), so items of slices l-1, l, l+1 at the
+// same (jg, kc) run together and the ULM/ULP rows hit L2 even when one slice
+// is larger than L2; black passes walk the items backwards (snake), starting
+// where the red pass ended.  Residual partials: one per (item, warp) at the
+// item's canonical slice-major id, so per-slice sums do not depend on the
+// traversal or the grid size (same contract as sor.cu).
 #include <algorithm>
+#include <cstdlib>
 
 #include "sor_math.cuh"
 
@@ -30,14 +36,20 @@ namespace ssb {
 namespace {
 
 constexpr int kWarps = 8;  // "virtual" consumer warps: one row (segment) each, one residual partial each
-#ifndef SSB_RPW
-#define SSB_RPW 1
+constexpr int kConsumers = kWarps;
+constexpr int kThreads = (kConsumers + 2) * 32;  // + a producer warp per ring
+#ifndef SSB_MAIN_STAGES
+#define SSB_MAIN_STAGES 5
 #endif
-constexpr int kRPW = SSB_RPW;                   // virtual warps computed (interleaved) per physical warp
-constexpr int kConsumers = kWarps / kRPW;       // physical consumer warps
-constexpr int kThreads = (kConsumers + 1) * 32;
-constexpr int kStages = 5;
+#ifndef SSB_UK_STAGES
+#define SSB_UK_STAGES 5
+#endif
+constexpr int kMainStages = SSB_MAIN_STAGES;  // per-plane operands (consumed by one plane)
+constexpr int kUKStages = SSB_UK_STAGES;      // other-colour planes (held for three planes)
 constexpr int kPlanesPerItem = 8;
+constexpr int kDefaultSnake = 1;
+constexpr int kDefaultL2Hint = 0;
+constexpr int kDefaultOrder = 1;
 #ifndef SSB_WAVE_SKEW
 #define SSB_WAVE_SKEW 0  // 0: 2 * nkc sub-slices (measured: nkc+1 starves, 16..48 equal)
 #endif
@@ -64,11 +76,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sptr(dst)),
-        "l"(src), "r"(bytes), "r"(sptr(bar))
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            sptr(dst)),
+        "l"(src), "r"(bytes), "r"(sptr(bar)), "l"(pol)
         : "memory");
+}
+
+// L2 eviction policies (createpolicy): streamed-once operands vs state rows
+struct Policies {
+    uint64_t stream, uload, ustore;
+};
+__device__ __forceinline__ Policies make_policies(int hint) {
+    uint64_t first, last, normal;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(first));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(last));
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(normal));
+    Policies p;
+    p.stream = hint & 1 ? first : normal;
+    p.uload = hint & 2 ? last : normal;
+    p.ustore = hint & 4 ? last : normal;
+    return p;
 }
 
 struct Geo {  // per-launch tiling (identical on host and device)
@@ -78,8 +107,11 @@ struct Geo {  // per-launch tiling (identical on host and device)
     int nkc;  // plane chunks per slice
     long long items;
     uint32_t row_bytes;   // one packed row of doubles
-    uint32_t stage_bytes;
-    uint32_t off_coef, off_rhs, off_uc, off_ulm, off_ulp, off_uk;
+    uint32_t main_bytes;  // one main stage: COEF RHS UC ULM ULP of a plane
+    uint32_t uk_bytes;    // one UK stage: R+2 other-colour rows of a plane
+    uint32_t off_coef, off_rhs, off_uc, off_ulm, off_ulp;
+    uint32_t off_ukring;  // the UK ring follows the main ring
+    uint32_t smem;
 };
 
 __host__ __device__ inline Geo make_geo(const Layout& L) {
@@ -101,8 +133,10 @@ __host__ __device__ inline Geo make_geo(const Layout& L) {
     g.off_uc = g.off_rhs + R * rb;
     g.off_ulm = g.off_uc + R * rb;
     g.off_ulp = g.off_ulm + R * rb;
-    g.off_uk = g.off_ulp + R * rb;
-    g.stage_bytes = g.off_uk + (R + 2u) * rb;
+    g.main_bytes = g.off_ulp + R * rb;
+    g.uk_bytes = (R + 2u) * rb;
+    g.off_ukring = kMainStages * g.main_bytes;
+    g.smem = g.off_ukring + kUKStages * g.uk_bytes;
     return g;
 }
 
@@ -120,163 +154,226 @@ __device__ __forceinline__ Item make_item(const Layout& L, const Geo& G, int l, 
     return it;
 }
 
-struct Ring {  // producer-side position of the next stage
+// Launch-local item t (0 .. items of slices l_lo..l_hi) -> its Item and canonical
+// id ((l-1)*nkc + kc)*njg + jg, which indexes the residual partials (so per-slice
+// sums are independent of the traversal).  order 0: slice-major; order 1: slice
+// fastest, so the items of slices l-1, l, l+1 at the same (jg, kc) run
+// concurrently and share their other-colour rows through L2 (a slice of a large
+// grid is bigger than L2).
+__device__ __forceinline__ long long decode_item(const Layout& L, const Geo& G, int order, int l_lo, int nl,
+                                                 long long t, Item& it) {
+    int l, jg, kc;
+    if (order == 0) {
+        const long long c = (long long)(l_lo - 1) * G.njg * G.nkc + t;
+        jg = (int)(c % G.njg);
+        const long long r = c / G.njg;
+        kc = (int)(r % G.nkc);
+        l = (int)(r / G.nkc) + 1;
+    } else {
+        l = l_lo + (int)(t % nl);
+        const long long r = t / nl;
+        jg = (int)(r % G.njg);
+        kc = (int)(r / G.njg);
+    }
+    it = make_item(L, G, l, jg, kc);
+    return ((long long)(l - 1) * G.nkc + kc) * G.njg + jg;
+}
+
+template <int N>
+struct Ring {  // producer-side position of the next stage of an N-stage ring
     uint32_t slot = 0, phase = 0, used = 0;
+    __device__ __forceinline__ void acquire(uint64_t* empty) {
+        if (used >= N) mbar_wait(&empty[slot], phase ^ 1);
+    }
+    __device__ __forceinline__ void advance() {
+        ++used;
+        if (++slot == N) {
+            slot = 0;
+            phase ^= 1;
+        }
+    }
 };
 
-// Producer: issue the k1-k0+3 stages of one item (planes k0-1 .. k1+1).
-template <bool HEAT>
-__device__ __forceinline__ void produce_item(const Layout& L, const Geo& G, unsigned char* smem, uint64_t* full,
-                                             uint64_t* empty, Ring& rg, const Item& it, const float* coef,
-                                             const double* rhs, const double* uc, const double* uo) {
-    const long long W = L.W;
-    const long long plane_rows = (long long)L.jMax * L.kMax;
-    const uint32_t rb = G.row_bytes;
-    for (int p = it.k0 - 1; p <= it.k1 + 1; ++p) {
-        if (rg.used >= kStages) mbar_wait(&empty[rg.slot], rg.phase ^ 1);
-        unsigned char* s = smem + rg.slot * G.stage_bytes;
-        const bool interior = p >= it.k0 && p <= it.k1;
-        uint32_t bytes = (it.rows + 2) * rb;
-        if (interior) bytes += (HEAT ? 4u : 8u) * it.rows * rb;
-        uint64_t* bar = &full[rg.slot];
-        mbar_expect_tx(bar, bytes);
-        const long long row0 = ((long long)it.l * L.kMax + p) * L.jMax + it.j0;  // row (j0, p, l)
-        bulk_g2s(s + G.off_uk, uo + (row0 - 1) * W, (it.rows + 2) * rb, bar);
-        if (interior) {
-            if (!HEAT) bulk_g2s(s + G.off_coef, coef + row0 * W * 8, 4 * it.rows * rb, bar);
-            bulk_g2s(s + G.off_rhs, rhs + row0 * W, it.rows * rb, bar);
-            bulk_g2s(s + G.off_uc, uc + row0 * W, it.rows * rb, bar);
-            bulk_g2s(s + G.off_ulm, uo + (row0 - plane_rows) * W, it.rows * rb, bar);
-            bulk_g2s(s + G.off_ulp, uo + (row0 + plane_rows) * W, it.rows * rb, bar);
-        }
-        ++rg.used;
-        if (++rg.slot == kStages) {
-            rg.slot = 0;
-            rg.phase ^= 1;
-        }
+// consumer-side ring position
+template <int N>
+__device__ __forceinline__ void next_stage(uint32_t& slot, uint32_t& phase) {
+    if (++slot == N) {
+        slot = 0;
+        phase ^= 1;
     }
 }
 
-// Consumers: update colour C on the item's planes from the staged rows.  Each
-// physical warp computes kRPW virtual warps (rows / row segments) with their
-// loads and dependency chains interleaved (ILP), and returns each virtual
-// warp's sum of squared residuals in r2[].  (s0, ph0) is the ring position of
-// the item's first stage and is advanced past the item.
-template <int C, bool HEAT>
-__device__ __forceinline__ void consume_item(const SorArgs& a, const Layout& L, const Geo& G,
-                                             unsigned char* smem, uint64_t* full, uint64_t* empty,
-                                             uint32_t& s0, uint32_t& ph0, const Item& it,
-                                             double* __restrict__ ucw, int warp, int lane,
-                                             double r2[kRPW]) {
+// Main producer: one stage per interior plane k0..k1 of the item.
+template <bool HEAT>
+__device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsigned char* smem, uint64_t* full,
+                                             uint64_t* empty, Ring<kMainStages>& rg, const Item& it,
+                                             const float* coef, const double* rhs, const double* uc,
+                                             const double* uo, const Policies& pol) {
     const long long W = L.W;
-    const int nq = (L.n1 + 1) / 2;
-    const int l = it.l;
-    int rloc[kRPW], seg[kRPW], jv[kRPW];
-#pragma unroll
-    for (int v = 0; v < kRPW; ++v) {
-        const int vw = warp * kRPW + v;
-        rloc[v] = vw / G.wpr;
-        seg[v] = vw % G.wpr;
-        jv[v] = it.j0 + rloc[v];
-        r2[v] = 0.0;
-    }
-    // (slot, phase) of stages q-1 (plane p-1), q (p), q+1 (p+1)
-    uint32_t sm = s0, pm = ph0;
-    uint32_t sc = sm + 1 == kStages ? 0 : sm + 1, pc = sm + 1 == kStages ? pm ^ 1 : pm;
-    mbar_wait(&full[sm], pm);
-    mbar_wait(&full[sc], pc);
+    const long long plane_rows = (long long)L.jMax * L.kMax;
+    const uint32_t rb = G.row_bytes;
     for (int p = it.k0; p <= it.k1; ++p) {
-        const uint32_t sp = sc + 1 == kStages ? 0 : sc + 1, pp = sc + 1 == kStages ? pc ^ 1 : pc;
-        mbar_wait(&full[sp], pp);
-        const unsigned char* scb = smem + sc * G.stage_bytes;
-        const double* ukm = reinterpret_cast<const double*>(smem + sm * G.stage_bytes + G.off_uk);
-        const double* ukc = reinterpret_cast<const double*>(scb + G.off_uk);
-        const double* ukp = reinterpret_cast<const double*>(smem + sp * G.stage_bytes + G.off_uk);
-        const float* cf = reinterpret_cast<const float*>(scb + G.off_coef);
-        const double* rh = reinterpret_cast<const double*>(scb + G.off_rhs);
-        const double* u0r = reinterpret_cast<const double*>(scb + G.off_uc);
-        const double* ulm = reinterpret_cast<const double*>(scb + G.off_ulm);
-        const double* ulp = reinterpret_cast<const double*>(scb + G.off_ulp);
-        for (int q0 = lane; q0 < nq; q0 += 32 * G.wpr) {
-            DoxelIn d[kRPW];
-            bool ok[kRPW];
-#pragma unroll
-            for (int v = 0; v < kRPW; ++v) {  // all loads first
-                const int j = jv[v], r = rloc[v];
-                const int i = 1 + ((1 + j + p + l + L.lpar + C) & 1) + 2 * (q0 + 32 * seg[v]);
-                ok[v] = r < it.rows && q0 + 32 * seg[v] < nq && i <= L.n1;
-                if (!ok[v]) continue;
-                const int m = i >> 1;
+        rg.acquire(empty);
+        unsigned char* s = smem + rg.slot * G.main_bytes;
+        uint64_t* bar = &full[rg.slot];
+        mbar_expect_tx(bar, (HEAT ? 4u : 8u) * it.rows * rb);
+        const long long row0 = ((long long)it.l * L.kMax + p) * L.jMax + it.j0;  // row (j0, p, l)
+        if (!HEAT) bulk_g2s(s + G.off_coef, coef + row0 * W * 8, 4 * it.rows * rb, bar, pol.stream);
+        bulk_g2s(s + G.off_rhs, rhs + row0 * W, it.rows * rb, bar, pol.stream);
+        bulk_g2s(s + G.off_uc, uc + row0 * W, it.rows * rb, bar, pol.uload);
+        bulk_g2s(s + G.off_ulm, uo + (row0 - plane_rows) * W, it.rows * rb, bar, pol.uload);
+        bulk_g2s(s + G.off_ulp, uo + (row0 + plane_rows) * W, it.rows * rb, bar, pol.uload);
+        rg.advance();
+    }
+}
+
+// UK producer: the other colour's rows j0-1..j0+rows of planes k0-1 .. k1+1.
+__device__ __forceinline__ void produce_uk(const Layout& L, const Geo& G, unsigned char* smem, uint64_t* full,
+                                           uint64_t* empty, Ring<kUKStages>& rg, const Item& it, const double* uo,
+                                           const Policies& pol) {
+    const long long W = L.W;
+    const uint32_t rb = G.row_bytes;
+    for (int p = it.k0 - 1; p <= it.k1 + 1; ++p) {
+        rg.acquire(empty);
+        unsigned char* s = smem + G.off_ukring + rg.slot * G.uk_bytes;
+        uint64_t* bar = &full[rg.slot];
+        mbar_expect_tx(bar, (it.rows + 2) * rb);
+        const long long row0 = ((long long)it.l * L.kMax + p) * L.jMax + it.j0;
+        bulk_g2s(s, uo + (row0 - 1) * W, (it.rows + 2) * rb, bar, pol.uload);
+        rg.advance();
+    }
+}
+
+// Consumers: update colour C on the item's planes from the staged rows.  Warp w
+// owns row w / wpr of the item and the slot segment w % wpr; with parity
+// par = (1 + j + k + l + C) & 1 its doxels of plane k sit at i = 1 + par + 2q,
+// i.e. packed slot m = q + par, with the i-1 / i+1 neighbours at slots q and q+1
+// of the other colour's row -- so every address is a loop-invariant base plus
+// q, and only par flips from plane to plane.  Returns the warp's sum of squared
+// residuals.  (ms, mph) / (s0, ph0) are the main / UK ring positions of the
+// item's first stages and are advanced past the item.
+template <int C, bool HEAT>
+__device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L, const Geo& G,
+                                               unsigned char* smem, uint64_t* fullM, uint64_t* emptyM,
+                                               uint64_t* fullK, uint64_t* emptyK, uint32_t& ms,
+                                               uint32_t& mph, uint32_t& s0, uint32_t& ph0, const Item& it,
+                                               double* __restrict__ ucw, int warp, int lane,
+                                               uint64_t pol_store) {
+    const int W = L.W;
+    const int r = warp / G.wpr;
+    const int j = it.j0 + r;
+    const bool row_ok = r < it.rows;
+    const int q_begin = lane + 32 * (warp % G.wpr), q_step = 32 * G.wpr;
+    // last slot q with i = 1 + par + 2q <= n1, per parity
+    const int q_end0 = (L.n1 - 1) >> 1, q_end1 = (L.n1 - 2) >> 1;
+    int par = (1 + j + it.k0 + it.l + L.lpar + C) & 1;
+    // shared-memory element offsets of row r: R-row blocks / the (R+2)-row UK block
+    const int o_row = r * W, o_uk = (r + 1) * W;
+    double* wrow = ucw + L.row(j, it.k0, it.l) * (long long)W;  // this row at plane k0
+    const long long wstep = (long long)L.jMax * W;
+    const unsigned char* ukr = smem + G.off_ukring;
+    double r2 = 0.0;
+    // UK (slot, phase) of planes p-1, p, p+1; main stage (ms, mph) of plane p
+    uint32_t sm = s0, pm = ph0;
+    uint32_t sc = sm, pc = pm;
+    next_stage<kUKStages>(sc, pc);
+    mbar_wait(&fullK[sm], pm);
+    mbar_wait(&fullK[sc], pc);
+    for (int p = it.k0; p <= it.k1; ++p) {
+        uint32_t sp = sc, pp = pc;
+        next_stage<kUKStages>(sp, pp);
+        mbar_wait(&fullK[sp], pp);
+        mbar_wait(&fullM[ms], mph);
+        const unsigned char* mb = smem + ms * G.main_bytes;
+        const double* ukm = reinterpret_cast<const double*>(ukr + sm * G.uk_bytes) + o_uk;
+        const double* ukc = reinterpret_cast<const double*>(ukr + sc * G.uk_bytes) + o_uk;
+        const double* ukp = reinterpret_cast<const double*>(ukr + sp * G.uk_bytes) + o_uk;
+        const float* cf = reinterpret_cast<const float*>(mb + G.off_coef) + 8 * o_row;
+        const double* rh = reinterpret_cast<const double*>(mb + G.off_rhs) + o_row;
+        const double* u0r = reinterpret_cast<const double*>(mb + G.off_uc) + o_row;
+        const double* ulm = reinterpret_cast<const double*>(mb + G.off_ulm) + o_row;
+        const double* ulp = reinterpret_cast<const double*>(mb + G.off_ulp) + o_row;
+        const int q_end = par ? q_end1 : q_end0;
+        if (row_ok)
+            for (int q = q_begin; q <= q_end; q += q_step) {
+                const int m = q + par;
+                DoxelIn d;
                 if constexpr (HEAT) {
-                    d[v].c[0] = i > 1 ? (float)a.hc[0] : 0.f;
-                    d[v].c[1] = i < L.n1 ? (float)a.hc[0] : 0.f;
-                    d[v].c[2] = j > 1 ? (float)a.hc[1] : 0.f;
-                    d[v].c[3] = j < L.n2 ? (float)a.hc[1] : 0.f;
-                    d[v].c[4] = p > 1 ? (float)a.hc[2] : 0.f;
-                    d[v].c[5] = p < L.n3 ? (float)a.hc[2] : 0.f;
-                    d[v].c[6] = l + L.l0 > 1 ? (float)a.hc[3] : 0.f;
-                    d[v].c[7] = l + L.l0 < L.n4g ? (float)a.hc[3] : 0.f;
+                    const int i = 1 + par + 2 * q;
+                    d.c[0] = i > 1 ? (float)a.hc[0] : 0.f;
+                    d.c[1] = i < L.n1 ? (float)a.hc[0] : 0.f;
+                    d.c[2] = j > 1 ? (float)a.hc[1] : 0.f;
+                    d.c[3] = j < L.n2 ? (float)a.hc[1] : 0.f;
+                    d.c[4] = p > 1 ? (float)a.hc[2] : 0.f;
+                    d.c[5] = p < L.n3 ? (float)a.hc[2] : 0.f;
+                    d.c[6] = it.l + L.l0 > 1 ? (float)a.hc[3] : 0.f;
+                    d.c[7] = it.l + L.l0 < L.n4g ? (float)a.hc[3] : 0.f;
                 } else {
-                    const float* c8 = cf + ((long long)r * W + m) * 8;
-                    const float4 lo = *reinterpret_cast<const float4*>(c8);
-                    const float4 hi = *reinterpret_cast<const float4*>(c8 + 4);
-                    d[v].c[0] = lo.x; d[v].c[1] = lo.y; d[v].c[2] = lo.z; d[v].c[3] = lo.w;
-                    d[v].c[4] = hi.x; d[v].c[5] = hi.y; d[v].c[6] = hi.z; d[v].c[7] = hi.w;
+                    const float4 lo = *reinterpret_cast<const float4*>(cf + 8 * m);
+                    const float4 hi = *reinterpret_cast<const float4*>(cf + 8 * m + 4);
+                    d.c[0] = lo.x; d.c[1] = lo.y; d.c[2] = lo.z; d.c[3] = lo.w;
+                    d.c[4] = hi.x; d.c[5] = hi.y; d.c[6] = hi.z; d.c[7] = hi.w;
                 }
-                const double* ur = ukc + (r + 1) * W;  // this row in the (rows+2)-row block
-                d[v].rhs = rh[r * W + m];
-                d[v].u0 = u0r[r * W + m];
-                d[v].nb[0] = ur[(i - 1) >> 1];
-                d[v].nb[1] = ur[(i + 1) >> 1];
-                d[v].nb[2] = ukc[r * W + m];
-                d[v].nb[3] = ukc[(r + 2) * W + m];
-                d[v].nb[4] = ukm[(r + 1) * W + m];
-                d[v].nb[5] = ukp[(r + 1) * W + m];
-                d[v].nb[6] = ulm[r * W + m];
-                d[v].nb[7] = ulp[r * W + m];
-                d[v].p = (((long long)l * L.kMax + p) * L.jMax + j) * W + m;
-            }
+                d.rhs = rh[m];
+                d.u0 = u0r[m];
+                d.nb[0] = ukc[q];
+                d.nb[1] = ukc[q + 1];
+                d.nb[2] = ukc[m - W];
+                d.nb[3] = ukc[m + W];
+                d.nb[4] = ukm[m];
+                d.nb[5] = ukp[m];
+                d.nb[6] = ulm[m];
+                d.nb[7] = ulp[m];
+                d.p = m;
 #ifndef SSB_NOCOMPUTE
-#pragma unroll
-            for (int v = 0; v < kRPW; ++v)
-                if (ok[v]) r2[v] += compute_doxel<C>(a, d[v], ucw);
+                r2 += compute_doxel<C, true>(a, d, wrow, pol_store);
 #else  // data-movement floor experiment: touch the operands, store u0
-#pragma unroll
-            for (int v = 0; v < kRPW; ++v)
-                if (ok[v]) {
-                    double s = d[v].rhs + d[v].u0 + (double)d[v].c[0] + (double)d[v].c[7];
-                    for (int f = 0; f < 8; ++f) s += d[v].nb[f];
-                    ucw[d[v].p] = s;
-                    r2[v] += s * 1e-300;
-                }
+                double t = d.rhs + d.u0 + (double)d.c[0] + (double)d.c[7];
+                for (int f = 0; f < 8; ++f) t += d.nb[f];
+                wrow[m] = t;
+                r2 += t * 1e-300;
 #endif
-        }
+            }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[sm]);  // plane p-1's stage is done
+        if (lane == 0) {
+            mbar_arrive(&emptyM[ms]);  // plane p's operands are done
+            mbar_arrive(&emptyK[sm]);  // and plane p-1's other-colour rows
+        }
+        next_stage<kMainStages>(ms, mph);
         sm = sc;
         pm = pc;
         sc = sp;
         pc = pp;
+        par ^= 1;
+        wrow += wstep;
     }
-    // the last two stages of the item (planes k1, k1+1)
+    // the last two UK stages of the item (planes k1, k1+1)
     __syncwarp();
     if (lane == 0) {
-        mbar_arrive(&empty[sm]);
-        mbar_arrive(&empty[sc]);
+        mbar_arrive(&emptyK[sm]);
+        mbar_arrive(&emptyK[sc]);
     }
-    s0 = sc + 1 == kStages ? 0 : sc + 1;
-    ph0 = sc + 1 == kStages ? pc ^ 1 : pc;
+    next_stage<kUKStages>(sc, pc);
+    s0 = sc;
+    ph0 = pc;
 #pragma unroll
-    for (int v = 0; v < kRPW; ++v)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) r2[v] += __shfl_down_sync(0xffffffffu, r2[v], o);
+    for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
+    return r2;
 }
 
-__device__ __forceinline__ void init_barriers(uint64_t* full, uint64_t* empty) {
+struct Bars {
+    uint64_t fullM[kMainStages], emptyM[kMainStages], fullK[kUKStages], emptyK[kUKStages];
+};
+
+__device__ __forceinline__ void init_barriers(Bars& b) {
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumers);
+        for (int s = 0; s < kMainStages; ++s) {
+            mbar_init(&b.fullM[s], 1);
+            mbar_init(&b.emptyM[s], kConsumers);
+        }
+        for (int s = 0; s < kUKStages; ++s) {
+            mbar_init(&b.fullK[s], 1);
+            mbar_init(&b.emptyK[s], kConsumers);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -286,7 +383,7 @@ __device__ __forceinline__ void init_barriers(uint64_t* full, uint64_t* empty) {
 template <int C, bool HEAT>
 __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    __shared__ __align__(8) Bars bars;
     const SorState* st = a.st;
     if (*(volatile const int*)&st->done) return;
     const int n = C == 0 ? *(volatile const int*)&st->n_red : *(volatile const int*)&st->n_black;
@@ -298,31 +395,35 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
     double* ucw = a.U[bout][C];
     const Geo G = make_geo(L);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long per_slice = (long long)G.njg * G.nkc;
-    const long long t_begin = (long long)(a.l_lo - 1) * per_slice, t_end = (long long)a.l_hi * per_slice;
-    init_barriers(full, empty);
+    const int nl = a.l_hi - a.l_lo + 1;
+    const long long n_items = (long long)G.njg * G.nkc * nl;
+    // snake order: black passes walk the items backwards, so each pass starts on
+    // the rows the previous pass touched last (still in L2)
+    const bool rev = C == 1 && a.snake;
+    const Policies pol = make_policies(a.l2hint);
+    init_barriers(bars);
 
-    if (warp == kConsumers) {  // producer: one thread issues every bulk copy
+    if (warp >= kConsumers) {  // producers: one thread per ring issues its bulk copies
         if (lane != 0) return;
-        Ring rg;
-        for (long long t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
-            const int jg = (int)(t % G.njg);
-            const long long r = t / G.njg;
-            const Item it = make_item(L, G, (int)(r / G.nkc) + 1, jg, (int)(r % G.nkc));
-            produce_item<HEAT>(L, G, smem, full, empty, rg, it, a.coef[C], a.rhs[C], uc, uo);
+        Ring<kMainStages> rm;
+        Ring<kUKStages> rk;
+        for (long long tt = blockIdx.x; tt < n_items; tt += gridDim.x) {
+            Item it;
+            decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - tt : tt, it);
+            if (warp == kConsumers)
+                produce_main<HEAT>(L, G, smem, bars.fullM, bars.emptyM, rm, it, a.coef[C], a.rhs[C], uc, uo, pol);
+            else
+                produce_uk(L, G, smem, bars.fullK, bars.emptyK, rk, it, uo, pol);
         }
         return;
     }
-    uint32_t s0 = 0, ph0 = 0;
-    for (long long t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
-        const int jg = (int)(t % G.njg);
-        const long long r = t / G.njg;
-        const Item it = make_item(L, G, (int)(r / G.nkc) + 1, jg, (int)(r % G.nkc));
-        double r2[kRPW];
-        consume_item<C, HEAT>(a, L, G, smem, full, empty, s0, ph0, it, ucw, warp, lane, r2);
-        if (lane == 0)
-#pragma unroll
-            for (int v = 0; v < kRPW; ++v) a.part[n & 3][C][t * kWarps + warp * kRPW + v] = r2[v];
+    uint32_t ms = 0, mph = 0, s0 = 0, ph0 = 0;
+    for (long long tt = blockIdx.x; tt < n_items; tt += gridDim.x) {
+        Item it;
+        const long long t = decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - tt : tt, it);
+        const double r2 = consume_item<C, HEAT>(a, L, G, smem, bars.fullM, bars.emptyM, bars.fullK, bars.emptyK,
+                                                ms, mph, s0, ph0, it, ucw, warp, lane, pol.ustore);
+        if (lane == 0) a.part[n & 3][C][t * kWarps + warp] = r2;
     }
 }
 
@@ -361,7 +462,7 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 template <bool HEAT>
 __global__ void __launch_bounds__(kThreads, 2) sor_wave_tma(const SorArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    __shared__ __align__(8) Bars bars;
     const SorState* st = a.st;
     if (*(volatile const int*)&st->done) return;
     const int n = *(volatile const int*)&st->n_red;
@@ -375,7 +476,8 @@ __global__ void __launch_bounds__(kThreads, 2) sor_wave_tma(const SorArgs a) {
     const long long NS = (long long)L.n4 * G.nkc;
     const long long NT = (NS + 3LL * skew) * 4 * G.njg;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    init_barriers(full, empty);
+    const Policies pol = make_policies(0);
+    init_barriers(bars);
 
     auto decode = [&](long long t, int& d, int& l, int& c) {
         const int jg = (int)(t % G.njg);
@@ -391,9 +493,10 @@ __global__ void __launch_bounds__(kThreads, 2) sor_wave_tma(const SorArgs a) {
         c = (int)(s % G.nkc) * G.njg + jg;
     };
 
-    if (warp == kConsumers) {  // producer
+    if (warp >= kConsumers) {  // producers (each waits for the flags itself)
         if (lane != 0) return;
-        Ring rg;
+        Ring<kMainStages> rm;
+        Ring<kUKStages> rk;
         for (long long t = blockIdx.x; t < NT; t += gridDim.x) {
             int d, l, c;
             decode(t, d, l, c);
@@ -419,11 +522,14 @@ __global__ void __launch_bounds__(kThreads, 2) sor_wave_tma(const SorArgs a) {
             const double* uc = a.U[bin][C];
             const double* uo = C == 0 ? a.U[bin][1] : a.U[bout][0];
             const Item it = make_item(L, G, l, jg, kc);
-            produce_item<HEAT>(L, G, smem, full, empty, rg, it, a.coef[C], a.rhs[C], uc, uo);
+            if (warp == kConsumers)
+                produce_main<HEAT>(L, G, smem, bars.fullM, bars.emptyM, rm, it, a.coef[C], a.rhs[C], uc, uo, pol);
+            else
+                produce_uk(L, G, smem, bars.fullK, bars.emptyK, rk, it, uo, pol);
         }
         return;
     }
-    uint32_t s0 = 0, ph0 = 0;
+    uint32_t ms = 0, mph = 0, s0 = 0, ph0 = 0;
     for (long long t = blockIdx.x; t < NT; t += gridDim.x) {
         int d, l, c;
         decode(t, d, l, c);
@@ -432,15 +538,12 @@ __global__ void __launch_bounds__(kThreads, 2) sor_wave_tma(const SorArgs a) {
         const int jg = c % G.njg, kc = c / G.njg;
         const Item it = make_item(L, G, l, jg, kc);
         double* ucw = a.U[out_buf(m)][C];
-        double r2[kRPW];
-        if (C == 0)
-            consume_item<0, HEAT>(a, L, G, smem, full, empty, s0, ph0, it, ucw, warp, lane, r2);
-        else
-            consume_item<1, HEAT>(a, L, G, smem, full, empty, s0, ph0, it, ucw, warp, lane, r2);
-        if (lane == 0)
-#pragma unroll
-            for (int v = 0; v < kRPW; ++v)
-                a.part[m & 3][C][((long long)(l - 1) * CH + c) * kWarps + warp * kRPW + v] = r2[v];
+        const double r2 =
+            C == 0 ? consume_item<0, HEAT>(a, L, G, smem, bars.fullM, bars.emptyM, bars.fullK, bars.emptyK, ms, mph,
+                                           s0, ph0, it, ucw, warp, lane, pol.ustore)
+                   : consume_item<1, HEAT>(a, L, G, smem, bars.fullM, bars.emptyM, bars.fullK, bars.emptyK, ms, mph,
+                                           s0, ph0, it, ucw, warp, lane, pol.ustore);
+        if (lane == 0) a.part[m & 3][C][((long long)(l - 1) * CH + c) * kWarps + warp] = r2;
         // publish: every consumer's stores, then one flag store (release)
         __threadfence();
         asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
@@ -487,9 +590,32 @@ int tma_blocks(const void* fn, size_t smem_bytes) {
 
 }  // namespace
 
+// pass-order / L2-policy switches (env SSB_SNAKE, SSB_L2HINT; measured defaults)
+int pass_snake() {
+    static const int v = [] {
+        const char* e = std::getenv("SSB_SNAKE");
+        return e ? std::atoi(e) : kDefaultSnake;
+    }();
+    return v;
+}
+int pass_order() {
+    static const int v = [] {
+        const char* e = std::getenv("SSB_ORDER");
+        return e ? std::atoi(e) : kDefaultOrder;
+    }();
+    return v;
+}
+int pass_l2hint() {
+    static const int v = [] {
+        const char* e = std::getenv("SSB_L2HINT");
+        return e ? std::atoi(e) : kDefaultL2Hint;
+    }();
+    return v;
+}
+
 bool tma_pass_supported(const Layout& L) {
     const Geo G = make_geo(L);
-    return (size_t)G.stage_bytes * kStages <= 160 * 1024;
+    return (size_t)G.smem <= 160 * 1024;
 }
 
 void tma_pass_tiles(const Layout& L, SorArgs& a) {
@@ -517,7 +643,7 @@ bool wave_supported(const Layout& L) {
 
 void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat) {
     const Geo G = make_geo(a.L);
-    const size_t smem = (size_t)G.stage_bytes * kStages;
+    const size_t smem = (size_t)G.smem;
     configure_wave<false>();
     configure_wave<true>();
     configure<0, false>();
@@ -540,7 +666,7 @@ void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat) {
 
 void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat) {
     const Geo G = make_geo(a.L);
-    const size_t smem = (size_t)G.stage_bytes * kStages;
+    const size_t smem = (size_t)G.smem;
     configure<0, false>();
     configure<1, false>();
     configure<0, true>();
