@@ -4,6 +4,7 @@
 #include "domain.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -149,6 +150,8 @@ Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int 
         pp[1].alloc(nparts);
     }
     slice_res.alloc(chunk);
+    slice_cnt.alloc(chunk);
+    SSB_CUDA(cudaMemsetAsync(slice_cnt.p, 0, slice_cnt.n * sizeof(unsigned), stream));
     norm_loc.alloc(chunk);
     if (world > 1) {
         all_slices.alloc((size_t)world * chunk);
@@ -312,6 +315,8 @@ SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool he
     a.snake = pass_snake();
     a.l2hint = pass_l2hint();
     a.order = pass_order();
+    a.fuse_final = a.tma && world == 1 && !a.wave && pass_fuse_final() && tma_fuse_ok(L) ? 1 : 0;
+    a.slice_cnt = slice_cnt.p;
     if (a.tma)
         tma_pass_tiles(L, a);
     else
@@ -494,6 +499,15 @@ cudaEvent_t Domain::pool_event(size_t idx) {
     return ev_pool[idx];
 }
 
+// loop bodies per conditional-node iteration (env SSB_UNROLL)
+int graph_unroll() {
+    static const int v = [] {
+        const char* e = std::getenv("SSB_UNROLL");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    return v;
+}
+
 cudaGraphExec_t Domain::graph_for(const SorArgs& base, bool heat) {
     constexpr int NK = 2 * kStateBuffers + 2;
     const void* key[NK];
@@ -529,7 +543,8 @@ cudaGraphExec_t Domain::graph_for(const SorArgs& base, bool heat) {
     const unsigned long long saved = g_launches.load();
     SSB_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeThreadLocal));
-    launch_sor_body(cap_stream, a, heat, nullptr);
+    // the body holds graph_unroll() iterations: a decided loop makes the rest no-ops
+    for (int u = 0; u < graph_unroll(); ++u) launch_sor_body(cap_stream, a, heat, nullptr);
     cudaGraph_t captured = nullptr;
     SSB_CUDA(cudaStreamEndCapture(cap_stream, &captured));
     g_launches.store(saved);
@@ -604,7 +619,8 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
         SSB_CUDA(cudaMemcpyAsync(st_host, sp[0]->st.p, sizeof(SorState), cudaMemcpyDeviceToHost, stream));
         sync();
         const int bodies = wave ? st_host->iterations / 2 + 1 : st_host->iterations + 1;
-        count_launch(3ull * (unsigned long long)std::min(limit, bodies));
+        const int U = graph_unroll();
+        count_launch(3ull * U * (unsigned long long)((std::min(limit, bodies) + U - 1) / U));
     } else {
         // host-driven: chunks of loop bodies with one chunk of look-ahead; every
         // rank runs the same schedule (the decision is identical everywhere)

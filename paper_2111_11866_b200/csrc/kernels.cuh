@@ -39,6 +39,8 @@ struct SorArgs {
     double* slice_res;      // per-slice residual of the owned slices (solver.cpp:195-199)
     const double* all_slices;  // residuals of all n4g slices in global order (== slice_res on 1 slab)
     int inline_decide;      // single slab: finalize also decides
+    int fuse_final;         // TMA single slab: the red pass sums slices and decides in its tail
+    unsigned* slice_cnt;    // per owned slice: red-pass items completed (fuse_final)
     SorState* st;
     double omega, keep;
     double hc[4];           // heat stencil constants float(-dt/h_a^2) (solver.cpp:100-110)
@@ -76,10 +78,12 @@ void pass_tiles(const Layout& L, SorArgs& a);
 bool tma_pass_supported(const Layout& L);
 void tma_pass_tiles(const Layout& L, SorArgs& a);
 size_t tma_partials(const Layout& L);
+bool tma_fuse_ok(const Layout& L);  // the red pass can take the finalize into its tail
 void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat);
 int pass_snake();   // SorArgs::snake default (env SSB_SNAKE)
 int pass_l2hint();  // SorArgs::l2hint default (env SSB_L2HINT)
 int pass_order();   // SorArgs::order default (env SSB_ORDER)
+int pass_fuse_final();  // SorArgs::fuse_final allowed (env SSB_FUSE_FINAL)
 bool wave_supported(const Layout& L);
 size_t wave_flags(const Layout& L);
 void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat);

@@ -19,28 +19,13 @@
 // -fmad=false: iterates are bit-identical to the oracle.
 #include <algorithm>
 
+#include "sor_final.cuh"
 #include "sor_math.cuh"
 
 namespace ssb {
 
 namespace {
 
-__device__ __forceinline__ double block_sum(double v) {
-    // fixed-shape tree => deterministic
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    __shared__ double ws[32];
-    const int tid = threadIdx.x + threadIdx.y * blockDim.x;
-    const int nw = (blockDim.x * blockDim.y + 31) >> 5;
-    if ((tid & 31) == 0) ws[tid >> 5] = v;
-    __syncthreads();
-    if (tid < 32) {
-        v = tid < nw ? ws[tid] : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    }
-    return v;  // valid in thread 0
-}
 
 template <int C, bool HEAT>
 __device__ __forceinline__ void load_doxel(const SorArgs& a, const float* __restrict__ cf,
@@ -137,50 +122,18 @@ __global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(con
     }
 }
 
-// Decision of iteration n-1 from the per-slice residuals of ALL slices in
-// global l order (solver.cpp:195-205): identical on every rank.
-__device__ void decide(const SorArgs& a, SorState* st, int n) {
-    if (n >= 2) {
-        double total = 0.0;
-        for (int l = 0; l < a.L.n4g; ++l) total += __ldcg(a.all_slices + l);
-        const double res = sqrt(total);
-        const int it = n - 1;
-        st->residual = res;
-        st->iterations = it;
-        if (!st->fixed && res <= st->tol) {
-            st->done = 1;
-            st->converged = 1;
-        } else if (it >= st->max_iter) {
-            st->done = 1;
-            st->converged = st->fixed;
-        }
-    }
-    st->n_black = n;
-    st->n_red = n + 1;
-    if (a.use_cond) cudaGraphSetConditional(a.cond, st->done ? 0u : 1u);
-}
-
-// grid = local n4 blocks (one per owned slice), 256 threads: slice_res[l] =
-// black partials of black(n-1) + red partials of red(n), each summed in fixed
-// order.  With inline_decide (single slab) the last block also takes the
-// decision; otherwise the slices are all-gathered first (sor_decide).
+// grid = local n4 blocks (one per owned slice), 256 threads: slice_res[l] via
+// slice_residual (sor_final.cuh).  With inline_decide (single slab) the last
+// block also takes the decision; otherwise the slices are all-gathered first
+// (sor_decide).  The TMA red pass does the same in its tail (fuse_final).
 __global__ void __launch_bounds__(256) sor_finalize(const SorArgs a) {
+    __shared__ double ws[32];
     SorState* st = a.st;
     if (*(volatile int*)&st->done) return;
     const int n = *(volatile int*)&st->n_red;
     if (n >= 2) {
-        const int l = blockIdx.x;
-        const double* pr = a.part[n & 3][0] + (long long)l * a.bps;        // red(n)
-        const double* pb = a.part[(n - 1) & 3][1] + (long long)l * a.bps;  // black(n-1)
-        double r = 0.0, b = 0.0;
-        for (int q = threadIdx.x; q < a.bps; q += blockDim.x) {
-            r += pr[q];
-            b += pb[q];
-        }
-        r = block_sum(r);
-        __syncthreads();
-        b = block_sum(b);
-        if (threadIdx.x == 0) a.slice_res[l] = b + r;  // slice_black + red (solver.cpp:359)
+        const double v = slice_residual(a, n, blockIdx.x, ws, threadIdx.x);
+        if (threadIdx.x == 0) a.slice_res[blockIdx.x] = v;
     }
     if (!a.inline_decide) return;
     __shared__ int last;
@@ -191,13 +144,13 @@ __global__ void __launch_bounds__(256) sor_finalize(const SorArgs a) {
     if (!last || threadIdx.x != 0) return;
     __threadfence();
     st->counter = 0;
-    decide(a, st, n);
+    sor_decide_state(a, st, n);
 }
 
 __global__ void sor_decide(const SorArgs a) {
     SorState* st = a.st;
     if (*(volatile int*)&st->done) return;
-    decide(a, st, *(volatile int*)&st->n_red);
+    sor_decide_state(a, st, *(volatile int*)&st->n_red);
 }
 
 // tol = rel * sqrt(sum over all slices in global l order) when norm_slices is given
@@ -315,8 +268,10 @@ void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* e
     if (ev) SSB_CUDA(cudaEventRecord(ev[0], s));
     launch_sor_pass(s, a, 0, heat);
     if (ev) SSB_CUDA(cudaEventRecord(ev[1], s));
-    sor_finalize<<<a.L.n4, 256, 0, s>>>(a);
-    SSB_LAUNCHED();
+    if (!a.fuse_final) {  // else the red pass took the decision in its tail
+        sor_finalize<<<a.L.n4, 256, 0, s>>>(a);
+        SSB_LAUNCHED();
+    }
     if (ev) SSB_CUDA(cudaEventRecord(ev[2], s));
     launch_sor_pass(s, a, 1, heat);
     if (ev) SSB_CUDA(cudaEventRecord(ev[3], s));

@@ -1,0 +1,120 @@
+// sor_final.cuh -- the end-of-red-pass bookkeeping of one SOR iteration
+// (solver.cpp:195-205), shared by the stand-alone finalize kernel (sor.cu) and
+// the TMA red pass that performs it in its tail (sor_tma.cu).
+//
+// slice_res[l] = (sum of the black(n-1) partials of slice l) + (sum of the
+// red(n) partials of slice l), each summed by 256 threads in one fixed order;
+// the decision sums the slices in global l order.  Both callers use exactly
+// these functions, so iterates and iteration counts do not depend on which
+// path ran.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace ssb {
+
+// 256 threads (tid 0..255) synchronised with named barrier 1: fixed-shape tree
+__device__ __forceinline__ double group256_sum(double v, double* ws, int tid) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((tid & 31) == 0) ws[tid >> 5] = v;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (tid < 32) {
+        v = tid < 8 ? ws[tid] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    }
+    return v;  // valid in tid 0
+}
+
+// residual of slice l (local, 0-based) of state n-1; valid in tid 0
+__device__ __forceinline__ double slice_residual(const SorArgs& a, int n, int l, double* ws, int tid) {
+    const double* pr = a.part[n & 3][0] + (long long)l * a.bps;        // red(n)
+    const double* pb = a.part[(n - 1) & 3][1] + (long long)l * a.bps;  // black(n-1)
+    double r = 0.0, b = 0.0;
+    for (int q = tid; q < a.bps; q += 256) {
+        r += __ldcg(pr + q);
+        b += __ldcg(pb + q);
+    }
+    r = group256_sum(r, ws, tid);
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    b = group256_sum(b, ws, tid);
+    return b + r;  // slice_black + red (solver.cpp:359)
+}
+
+// Decision of iteration n-1 from the per-slice residuals of ALL slices in
+// global l order (solver.cpp:195-205): identical on every rank.
+__device__ __forceinline__ void sor_decide_state(const SorArgs& a, SorState* st, int n) {
+    if (n >= 2) {
+        double total = 0.0;  // sequential in l; loads issued 8 at a time
+        for (int l0 = 0; l0 < a.L.n4g; l0 += 8) {
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = l0 + q < a.L.n4g ? __ldcg(a.all_slices + l0 + q) : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (l0 + q < a.L.n4g) total += v[q];
+        }
+        const double res = sqrt(total);
+        const int it = n - 1;
+        st->residual = res;
+        st->iterations = it;
+        if (!st->fixed && res <= st->tol) {
+            st->done = 1;
+            st->converged = 1;
+        } else if (it >= st->max_iter) {
+            st->done = 1;
+            st->converged = st->fixed;
+        }
+    }
+    st->n_black = n;
+    st->n_red = n + 1;
+    if (a.use_cond) cudaGraphSetConditional(a.cond, st->done ? 0u : 1u);
+}
+
+// Red pass tail, run once by the 256 consumer threads of each CTA after all of
+// its work items (t = blockIdx.x + k * gridDim.x) have written their partials: one atomic per item on its
+// slice's counter; the CTA that completes a slice sums it, the CTA that
+// completes the last slice decides.
+// slice_of(t) = the launch-local item's slice; done_slices holds kMaxDoneSlices
+// entries (the host enables the fusion only when no CTA has more items).
+constexpr int kMaxDoneSlices = 256;
+template <typename SliceOf>
+__device__ __forceinline__ void red_pass_done(const SorArgs& a, int n, int items_per_slice, long long n_items,
+                                              SliceOf slice_of, double* ws, int* done_slices, int* n_done,
+                                              int tid) {
+    if (tid == 0) *n_done = 0;
+    asm volatile("bar.sync 1, 256;" ::: "memory");  // every partial of this CTA is written
+    const long long mine = n_items > blockIdx.x ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    __threadfence();
+    for (long long k = tid; k < mine; k += 256) {
+        const long long t = blockIdx.x + k * gridDim.x;
+        const int l = slice_of(t);
+        if (atomicAdd(a.slice_cnt + (l - 1), 1u) == (unsigned)items_per_slice - 1)
+            done_slices[atomicAdd(n_done, 1)] = l;
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const int nd = *n_done;
+    if (nd == 0) return;
+    __threadfence();
+    for (int q = 0; q < nd; ++q) {
+        const int l = done_slices[q];
+        if (n >= 2) {
+            const double v = slice_residual(a, n, l - 1, ws, tid);
+            if (tid == 0) a.slice_res[l - 1] = v;
+        }
+        if (tid == 0) a.slice_cnt[l - 1] = 0;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
+    if (tid == 0) {
+        __threadfence();
+        SorState* st = a.st;
+        if (atomicAdd(&st->counter, (unsigned)nd) + nd == (unsigned)a.L.n4) {
+            __threadfence();
+            st->counter = 0;
+            sor_decide_state(a, st, n);
+        }
+    }
+}
+
+}  // namespace ssb

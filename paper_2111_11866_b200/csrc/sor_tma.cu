@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "sor_final.cuh"
 #include "sor_math.cuh"
 
 namespace ssb {
@@ -384,6 +385,8 @@ template <int C, bool HEAT>
 __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) Bars bars;
+    __shared__ double ws[32];
+    __shared__ int done_slices[kMaxDoneSlices], n_done;
     const SorState* st = a.st;
     if (*(volatile const int*)&st->done) return;
     const int n = C == 0 ? *(volatile const int*)&st->n_red : *(volatile const int*)&st->n_black;
@@ -425,6 +428,16 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
                                                 ms, mph, s0, ph0, it, ucw, warp, lane, pol.ustore);
         if (lane == 0) a.part[n & 3][C][t * kWarps + warp] = r2;
     }
+    if constexpr (C == 0)
+        if (a.fuse_final)
+            red_pass_done(
+                a, n, G.njg * G.nkc, n_items,
+                [&](long long t) {
+                    Item it;
+                    decode_item(L, G, a.order, a.l_lo, nl, t, it);
+                    return it.l;
+                },
+                ws, done_slices, &n_done, threadIdx.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -598,6 +611,13 @@ int pass_snake() {
     }();
     return v;
 }
+int pass_fuse_final() {
+    static const int v = [] {
+        const char* e = std::getenv("SSB_FUSE_FINAL");
+        return e ? std::atoi(e) : 0;  // measured: slower on config 1 (tail), see DESIGN.md
+    }();
+    return v;
+}
 int pass_order() {
     static const int v = [] {
         const char* e = std::getenv("SSB_ORDER");
@@ -625,6 +645,13 @@ void tma_pass_tiles(const Layout& L, SorArgs& a) {
     a.tx = G.njg;
     a.ty = G.nkc;
     a.tk = 1;
+}
+
+bool tma_fuse_ok(const Layout& L) {
+    // the red pass tail records the slices a CTA completes in kMaxDoneSlices entries
+    const Geo G = make_geo(L);
+    const long long blocks = tma_blocks((const void*)sor_pass_tma<0, false>, G.smem);
+    return (G.items + blocks - 1) / blocks <= kMaxDoneSlices;
 }
 
 size_t tma_partials(const Layout& L) { return (size_t)make_geo(L).items * kWarps; }
