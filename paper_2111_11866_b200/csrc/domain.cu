@@ -153,6 +153,7 @@ Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int 
     slice_cnt.alloc(chunk);
     SSB_CUDA(cudaMemsetAsync(slice_cnt.p, 0, slice_cnt.n * sizeof(unsigned), stream));
     norm_loc.alloc(chunk);
+    norm_part.alloc((size_t)chunk * kNormChunks);
     if (world > 1) {
         all_slices.alloc((size_t)world * chunk);
         norm_all.alloc((size_t)world * chunk);
@@ -880,7 +881,7 @@ void Domain::step(ss_step_diag* diag) {
     if (rel) {
         std::vector<double*> loc, all;
         for (Slab* s : sp) {
-            launch_norm_slices(stream, s->L, s->S[cur].pf(), s->norm_loc.p);
+            launch_norm_slices(stream, s->L, s->S[cur].pf(), s->norm_part.p, s->norm_loc.p);
             loc.push_back(s->norm_loc.p);
             all.push_back(s->norm_all.p);
         }

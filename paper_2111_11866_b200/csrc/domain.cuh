@@ -108,6 +108,7 @@ struct Slab {
     Dev<unsigned> slice_cnt; // red-pass items completed per slice (fused finalize)
     Dev<double> all_slices;  // world * chunk (gathered), unused when world == 1
     Dev<double> norm_loc, norm_all;
+    Dev<double> norm_part;   // chunk * kNormChunks partials of launch_norm_slices
     Dev<double> gloc, gall;  // small host-driven gathers (k <= 8 values per slab)
     Dev<int> wflags;         // wavefront item completion flags
     Dev<SorState> st;

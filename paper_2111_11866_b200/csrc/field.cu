@@ -162,21 +162,48 @@ __global__ void __launch_bounds__(256) norm_part_kernel(const Layout L, PField f
     if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// one block per owned slice l (1-based local), fixed-order block reduction
-__global__ void __launch_bounds__(256) norm_slices_kernel(const Layout L, PField f, double* out) {
-    const int l = blockIdx.x + 1;
-    const long long N = (long long)L.n1 * L.n2 * L.n3;
+// Per-slice sum of squares, in two fixed-shape steps: block (c, l) sums the
+// interior slots of rows c, c + kNormChunks, ... of slice l (both colours,
+// one warp per row, coalesced), then one thread per slice adds the kNormChunks
+// partials in order.  The result depends only on the slice's values (not on
+// the slab decomposition).
+__global__ void __launch_bounds__(256) slice_norm_part_kernel(const Layout L, PField f, double* part) {
+    const int l = blockIdx.y + 1;
+    const int rows = L.n2 * L.n3;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int U = 4;  // rows whose loads are in flight together
     double s = 0.0;
-    for (long long e = threadIdx.x; e < N; e += blockDim.x) {
-        const int i = (int)(e % L.n1) + 1;
-        const long long r = e / L.n1;
-        const int j = (int)(r % L.n2) + 1;
-        const int k = (int)(r / L.n2) + 1;
-        const double v = *at(L, f, i, j, k, l);
-        s += v * v;
+    for (int r0 = blockIdx.x + kNormChunks * warp; r0 < rows; r0 += kNormChunks * 8 * U) {
+        for (int m0 = 0; m0 < L.W; m0 += 32) {
+            const int m = m0 + lane;
+            double v[U][2];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int r = r0 + u * kNormChunks * 8;
+                const int j = r % L.n2 + 1, k = r / L.n2 + 1;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    // slot m of colour c holds i = 2m + b
+                    const int i = 2 * m + ((c + j + k + l + L.lpar) & 1);
+                    v[u][c] = r < rows && m < L.W && i >= 1 && i <= L.n1 ? f.c[c][L.row(j, k, l) * L.W + m] : 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) s += v[u][c] * v[u][c];
+        }
     }
     s = bsum(s);
-    if (threadIdx.x == 0) out[blockIdx.x] = s;
+    if (threadIdx.x == 0) part[(long long)blockIdx.y * kNormChunks + blockIdx.x] = s;
+}
+
+__global__ void norm_slices_kernel(const double* part, int n4, double* out) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= n4) return;
+    double s = 0.0;
+    for (int c = 0; c < kNormChunks; ++c) s += part[(long long)l * kNormChunks + c];
+    out[l] = s;
 }
 
 __global__ void __launch_bounds__(256) sum_final_kernel(const double* part, int n, double* out) {
@@ -278,8 +305,10 @@ void launch_norm_sq(cudaStream_t s, const Layout& L, PField f, double* scratch, 
     SSB_LAUNCHED();
 }
 
-void launch_norm_slices(cudaStream_t s, const Layout& L, PField f, double* out) {
-    norm_slices_kernel<<<L.n4, 256, 0, s>>>(L, f, out);
+void launch_norm_slices(cudaStream_t s, const Layout& L, PField f, double* scratch, double* out) {
+    slice_norm_part_kernel<<<dim3(kNormChunks, L.n4), 256, 0, s>>>(L, f, scratch);
+    SSB_LAUNCHED();
+    norm_slices_kernel<<<ceil_div(L.n4, 128), 128, 0, s>>>(scratch, L.n4, out);
     SSB_LAUNCHED();
 }
 

@@ -155,7 +155,9 @@ void launch_copy_field(cudaStream_t s, const Layout& L, PField dst, PField src);
 // deterministic interior reductions; out[0] = sum of squares or (min,max)
 void launch_norm_sq(cudaStream_t s, const Layout& L, PField f, double* scratch, double* out);
 // per owned slice: sum of squares over the slice's interior (fixed order)
-void launch_norm_slices(cudaStream_t s, const Layout& L, PField f, double* out);
+constexpr int kNormChunks = 64;  // row chunks per slice of launch_norm_slices
+// scratch: n4 * kNormChunks doubles
+void launch_norm_slices(cudaStream_t s, const Layout& L, PField f, double* scratch, double* out);
 void launch_minmax(cudaStream_t s, const Layout& L, PField f, double* scratch, double* out2);
 void launch_mask(cudaStream_t s, const Layout& L, PField f, double level, uint8_t* mask);
 constexpr int kReduceBlocks = 592;  // 4 x 148 SMs; fixed => deterministic order

@@ -164,7 +164,8 @@ def eoc_row_gpu(ss, n, omega=1.5, tol=1e-8):
 
 
 # ------------------------------------------------------------------ oracle, random cases
-SHAPES = [(6, 5, 4, 5), (7, 3, 5, 4), (1, 4, 3, 5), (9, 1, 1, 3), (33, 6, 5, 4), (64, 3, 2, 3)]
+SHAPES = [(6, 5, 4, 5), (7, 3, 5, 4), (1, 4, 3, 5), (9, 1, 1, 3), (33, 6, 5, 4), (64, 3, 2, 3),
+          (257, 5, 9, 3), (130, 17, 10, 2)]  # wide rows: R < 8 rows per item, several slots per lane
 
 
 @pytest.mark.parametrize("dims", SHAPES)
