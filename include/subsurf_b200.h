@@ -123,6 +123,45 @@ SS_API ss_status ss_interior_minmax(const ss_grid* g, const double* f, double* l
 /* extract_mask (tracking.hpp:55, tracking.cpp:35-52): n4 frames of n1*n2*n3 bytes */
 SS_API ss_status ss_extract_mask(const ss_grid* g, const double* u, double level,
                                  uint8_t* mask);
+/* ---------------- cell tracking (tracking.hpp, tracking.cpp) ----------------
+ * Frames are n4 volumes of n1*n2*n3 voxels, 0-based, x fastest (MaskFrames /
+ * LabelField, tracking.hpp:14-34).  Per-voxel work (labelling, distance
+ * transform, centres, predecessor candidates) runs on the GPU; the per-cell
+ * linking on the host. */
+typedef struct { /* CellRecord (tracking.hpp:36-42) */
+    int frame, label;   /* 0-based frame, label 1..k */
+    int cx, cy, cz;     /* 0-based centre voxel */
+    int max_distance;   /* 26-neighbourhood BFS distance to background at the centre */
+    long long voxel_count;
+} ss_cell_record;
+typedef struct { /* TrajectoryPoint (io.hpp:36-40) */
+    int trajectory_id, frame;
+    double x, y, z;
+} ss_track_point;
+/* label_components (tracking.hpp:59, tracking.cpp:69-127): labels n4*n1*n2*n3,
+ * labels_per_frame n4 */
+SS_API ss_status ss_label_components(const ss_grid* g, const uint8_t* mask, int32_t* labels,
+                                     int* labels_per_frame);
+/* distance_centers (tracking.hpp:64, tracking.cpp:189-215): one record per
+ * (frame, label) in that order; *n_records = sum of labels_per_frame.  Fails with
+ * SS_ERR_VALIDATION (and sets *n_records) when capacity is too small. */
+SS_API ss_status ss_distance_centers(const ss_grid* g, const int32_t* labels,
+                                     const int* labels_per_frame, ss_cell_record* out,
+                                     int capacity, int* n_records);
+/* backtrack_link (tracking.hpp:69-70, tracking.cpp:220-296): partial trajectories
+ * as record indices (into the distance_centers order) with frames increasing;
+ * chain c = record_index[chain_start[c] .. chain_start[c+1]-1], chain_start has
+ * n_records + 1 entries; *n_chains set. */
+SS_API ss_status ss_backtrack_link(const ss_grid* g, const int32_t* labels,
+                                   const int* labels_per_frame, const ss_cell_record* records,
+                                   int n_records, int* record_index, int* chain_start,
+                                   int* n_chains);
+/* track (tracking.hpp:81-82, tracking.cpp:374-401): extract_mask(u, level), the
+ * whole pipeline, trajectory points in output order; *n_points set; fails with
+ * SS_ERR_VALIDATION when capacity is too small. */
+SS_API ss_status ss_track(const ss_grid* g, const double* u, double level, int window,
+                          double radius, ss_track_point* out, int capacity, int* n_points);
+
 /* segment (solver.hpp:91-92, solver.cpp:405-441).  u0 may be NULL
  * (build_initial); diags: n_steps entries or NULL. */
 SS_API ss_status ss_segment(const ss_grid* g, const double* image, const ss_center* c, int n,
@@ -160,6 +199,10 @@ SS_API ss_status ss_session_step(ss_session* s, ss_step_diag* diag);
 SS_API ss_status ss_session_set_u(ss_session* s, const double* host_u);
 SS_API ss_status ss_session_get_u(ss_session* s, double* host_u);
 SS_API ss_status ss_session_get_mask(ss_session* s, double level, uint8_t* mask);
+/* track() on the session's device-resident u (no host round trip of u); single-process
+ * sessions (one slab or an in-process slab group) */
+SS_API ss_status ss_session_track(ss_session* s, double level, int window, double radius,
+                                  ss_track_point* out, int capacity, int* n_points);
 /* fixed-sweep mode (BASELINE config 4): assemble at the current u, then exactly
  * n_sweeps red+black sweeps with no stopping test; *residual = last residual. */
 SS_API ss_status ss_session_fixed_sweeps(ss_session* s, int n_sweeps, double* residual);

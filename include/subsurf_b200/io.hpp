@@ -29,6 +29,9 @@ Field4D read_image4d(const std::string& header_path, const std::string& data_pat
 void write_image4d(const Field4D& field, const std::string& header_path, const std::string& data_path);
 // "frame,x,y,z,radius" rows, optional header line, validated (io.cpp:142-168)
 CentersTable read_centers(const std::string& path, const GridSpec& spec);
+// "trajectory_id,frame,x,y,z" CSV (io.cpp:170-196)
+void write_trajectories(const TrajectoryFile& trajectories, const std::string& path);
+TrajectoryFile read_trajectories(const std::string& path);
 // legacy ASCII STRUCTURED_POINTS of interior frame l (io.cpp:198-223)
 void export_frame_vtk(const Field4D& field, int l, const std::string& path);
 

@@ -232,13 +232,54 @@ struct SegmentationParams {
 Field4D segment(const Field4D& image, const CentersTable& centers, const SegmentationParams& params,
                 std::ostream* diagnostics = nullptr);
 
-// ---------------------------------------------------------------- tracking subset (tracking.hpp:13-55)
+// ---------------------------------------------------------------- tracking (tracking.hpp:13-82)
 struct MaskFrames {
     int n1 = 0, n2 = 0, n3 = 0;
     std::vector<std::vector<std::uint8_t>> frames;
     std::size_t voxel(int x, int y, int z) const { return (std::size_t(z) * n2 + y) * n1 + x; }
     std::size_t frame_size() const { return std::size_t(n1) * n2 * n3; }
 };
-MaskFrames extract_mask(const Field4D& u, double level = 0.5);
+struct LabelField {  // tracking.hpp:23-34
+    int n1 = 0, n2 = 0, n3 = 0;
+    std::vector<std::vector<std::int32_t>> frames;
+    std::vector<int> labels_per_frame;
+    std::size_t voxel(int x, int y, int z) const { return (std::size_t(z) * n2 + y) * n1 + x; }
+    std::size_t frame_size() const { return std::size_t(n1) * n2 * n3; }
+};
+struct CellRecord {  // tracking.hpp:36-42
+    int frame = 0;
+    int label = 0;
+    std::array<int, 3> center{};
+    int max_distance = 0;
+    std::size_t voxel_count = 0;
+};
+struct Trajectory {  // tracking.hpp:44-47
+    int id = 0;
+    std::vector<CellRecord> records;
+};
+struct TrackParams {  // tracking.hpp:49-53
+    double level = 0.5;
+    int window = 3;
+    double radius = 5.0;
+};
+struct TrajectoryPoint {  // io.hpp:36-40
+    int trajectory_id = 0;
+    int frame = 0;
+    double x = 0.0, y = 0.0, z = 0.0;
+};
+struct TrajectoryFile {  // io.hpp:42-44
+    std::vector<TrajectoryPoint> points;
+};
+MaskFrames extract_mask(const Field4D& u, double level = 0.5);  // GPU
+MaskFrames mask_from_labels(const LabelField& labels);          // host
+LabelField label_components(const MaskFrames& mask);            // GPU
+std::vector<CellRecord> distance_centers(const LabelField& labels);  // GPU
+// GPU predecessor candidates + host linking
+std::vector<Trajectory> backtrack_link(const std::vector<CellRecord>& records, const LabelField& labels);
+// host
+std::vector<Trajectory> prolong_and_merge(std::vector<Trajectory> partials, int window, double radius);
+// the whole pipeline: GPU per-voxel work, host per-cell linking
+std::vector<Trajectory> track_cells(const Field4D& u, const TrackParams& params = {});
+TrajectoryFile track(const Field4D& u, const TrackParams& params = {});
 
 }  // namespace subsurf

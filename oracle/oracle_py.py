@@ -131,6 +131,12 @@ class _Lib:
         if with_workers:
             seg_args += [_D, C.POINTER(C.c_longlong), _D]
         self._seg = sig("segment", seg_args)
+        if with_workers:  # tracking: the reference itself (tracking.cpp) is the checker
+            _I = C.POINTER(C.c_int)
+            self._lab = sig("label_components", [_G, C.POINTER(C.c_ubyte), _I, _I])
+            self._dc = sig("distance_centers", [_G, _I, _I, C.POINTER(C.c_longlong), C.c_int, _I])
+            self._bt = sig("backtrack_link", [_G, _I, _I, _I, _I, _I])
+            self._trk = sig("track", [_G, _D, C.c_double, C.c_int, C.c_double, _I, _D, C.c_int, _I])
 
     def _wk(self, workers):
         return [int(workers)] if self.w else []
@@ -201,6 +207,55 @@ class _Lib:
         m = np.empty(g.n1 * g.n2 * g.n3 * g.n4, dtype=np.uint8)
         self._mask(C.byref(g), _p(u), level, m.ctypes.data_as(C.POINTER(C.c_ubyte)))
         return m.reshape(g.n4, g.n3, g.n2, g.n1)
+
+    # ---- tracking (reference only; frames (n4, n3, n2, n1), x fastest) ----
+    def label_components(self, g, mask):
+        mask = np.ascontiguousarray(mask, dtype=np.uint8)
+        lab = np.empty(mask.shape, dtype=np.int32)
+        lpf = np.empty(g.n4, dtype=np.int32)
+        st = self._lab(C.byref(g), mask.ctypes.data_as(C.POINTER(C.c_ubyte)),
+                       lab.ctypes.data_as(C.POINTER(C.c_int)), lpf.ctypes.data_as(C.POINTER(C.c_int)))
+        assert st == 0, st
+        return lab, lpf.tolist()
+
+    def distance_centers(self, g, labels, lpf):
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        lpf = np.asarray(lpf, dtype=np.int32)
+        cap = int(lpf.sum())
+        out = np.zeros((max(cap, 1), 7), dtype=np.int64)
+        n = C.c_int(0)
+        st = self._dc(C.byref(g), labels.ctypes.data_as(C.POINTER(C.c_int)), lpf.ctypes.data_as(C.POINTER(C.c_int)),
+                      out.ctypes.data_as(C.POINTER(C.c_longlong)), cap, C.byref(n))
+        assert st == 0, st
+        return out[:n.value]
+
+    def backtrack_link(self, g, labels, lpf):
+        """chains as lists of (frame, label), the reference's own records"""
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        lpf = np.asarray(lpf, dtype=np.int32)
+        cap = int(lpf.sum())
+        fl = np.zeros((max(cap, 1), 2), dtype=np.int32)
+        cs = np.zeros(cap + 2, dtype=np.int32)
+        nc = C.c_int(0)
+        ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int))
+        st = self._bt(C.byref(g), ip(labels), ip(lpf), ip(fl), ip(cs), C.byref(nc))
+        assert st == 0, st
+        return [[tuple(x) for x in fl[cs[c]:cs[c + 1]].tolist()] for c in range(nc.value)]
+
+    def track(self, g, u, level=0.5, window=3, radius=5.0):
+        """rows (trajectory_id, frame, x, y, z)"""
+        cap = 1 << 16
+        while True:
+            idf = np.zeros((cap, 2), dtype=np.int32)
+            xyz = np.zeros((cap, 3))
+            n = C.c_int(0)
+            st = self._trk(C.byref(g), _p(np.ascontiguousarray(u, dtype=np.float64)), level, window, radius,
+                           idf.ctypes.data_as(C.POINTER(C.c_int)), _p(xyz), cap, C.byref(n))
+            if st == 0:
+                return [(int(a), int(b), float(x), float(y), float(z))
+                        for (a, b), (x, y, z) in zip(idf[:n.value].tolist(), xyz[:n.value].tolist())]
+            assert n.value > cap, st
+            cap = n.value
 
     def eoc_row(self, n, omega=1.5, tol=1e-8, max_iter=10000, workers=1):
         err = C.c_double(0.0)

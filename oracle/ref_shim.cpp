@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <optional>
+#include <stdexcept>
 #include <thread>
 
 #include "subsurf/edge.hpp"
@@ -252,6 +253,100 @@ void ref_extract_mask(const or_grid* g, const double* u, double level, unsigned 
     std::size_t q = 0;
     for (const auto& fr : m.frames)
         for (auto b : fr) mask[q++] = b;
+}
+
+// ---- tracking (tracking.cpp), flat arrays: frames of n1*n2*n3, x fastest
+static LabelField labels_of(const or_grid* g, const int* labels, const int* lpf) {
+    LabelField L;
+    L.n1 = g->n1;
+    L.n2 = g->n2;
+    L.n3 = g->n3;
+    const std::size_t fs = L.frame_size();
+    L.frames.resize(g->n4);
+    L.labels_per_frame.assign(lpf, lpf + g->n4);
+    for (int f = 0; f < g->n4; ++f) L.frames[f].assign(labels + f * fs, labels + (f + 1) * fs);
+    return L;
+}
+
+/* label_components: labels n4*fs, lpf n4 */
+int ref_label_components(const or_grid* g, const unsigned char* mask, int* labels, int* lpf) {
+    return guarded([&] {
+        MaskFrames m;
+        m.n1 = g->n1;
+        m.n2 = g->n2;
+        m.n3 = g->n3;
+        const std::size_t fs = m.frame_size();
+        m.frames.resize(g->n4);
+        for (int f = 0; f < g->n4; ++f) m.frames[f].assign(mask + f * fs, mask + (f + 1) * fs);
+        const LabelField L = label_components(m);
+        for (int f = 0; f < g->n4; ++f) {
+            std::memcpy(labels + f * fs, L.frames[f].data(), fs * sizeof(int));
+            lpf[f] = L.labels_per_frame[f];
+        }
+    });
+}
+
+/* distance_centers: 7 ints per record (frame, label, cx, cy, cz, max_distance, voxel_count) */
+int ref_distance_centers(const or_grid* g, const int* labels, const int* lpf, long long* out, int capacity,
+                         int* n) {
+    return guarded([&] {
+        const std::vector<CellRecord> r = distance_centers(labels_of(g, labels, lpf));
+        *n = int(r.size());
+        if (int(r.size()) > capacity) throw std::runtime_error("capacity");
+        for (std::size_t i = 0; i < r.size(); ++i) {
+            long long* o = out + 7 * i;
+            o[0] = r[i].frame;
+            o[1] = r[i].label;
+            o[2] = r[i].center[0];
+            o[3] = r[i].center[1];
+            o[4] = r[i].center[2];
+            o[5] = r[i].max_distance;
+            o[6] = (long long)r[i].voxel_count;
+        }
+    });
+}
+
+/* backtrack_link on the reference's own records: per chain the (frame, label)
+ * pairs, chains concatenated; chain_start n_chains+1 entries */
+int ref_backtrack_link(const or_grid* g, const int* labels, const int* lpf, int* frame_label, int* chain_start,
+                       int* n_chains) {
+    return guarded([&] {
+        const LabelField L = labels_of(g, labels, lpf);
+        const std::vector<CellRecord> recs = distance_centers(L);
+        const std::vector<Trajectory> t = backtrack_link(recs, L);
+        int k = 0;
+        for (std::size_t c = 0; c < t.size(); ++c) {
+            chain_start[c] = k;
+            for (const CellRecord& r : t[c].records) {
+                frame_label[2 * k] = r.frame;
+                frame_label[2 * k + 1] = r.label;
+                ++k;
+            }
+        }
+        chain_start[t.size()] = k;
+        *n_chains = int(t.size());
+    });
+}
+
+/* track(u): points (id, frame) ints + (x, y, z) doubles */
+int ref_track(const or_grid* g, const double* u, double level, int window, double radius, int* id_frame,
+              double* xyz, int capacity, int* n) {
+    return guarded([&] {
+        TrackParams p;
+        p.level = level;
+        p.window = window;
+        p.radius = radius;
+        const TrajectoryFile tf = track(field_of(g, u), p);
+        *n = int(tf.points.size());
+        if (*n > capacity) throw std::runtime_error("capacity");
+        for (int i = 0; i < *n; ++i) {
+            id_frame[2 * i] = tf.points[i].trajectory_id;
+            id_frame[2 * i + 1] = tf.points[i].frame;
+            xyz[3 * i] = tf.points[i].x;
+            xyz[3 * i + 1] = tf.points[i].y;
+            xyz[3 * i + 2] = tf.points[i].z;
+        }
+    });
 }
 
 int ref_eoc_row(int n, double omega, double sor_tol, int max_iter, int workers, double* err) {

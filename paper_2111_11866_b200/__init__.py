@@ -118,6 +118,16 @@ class StepDiag(C.Structure):
                 ("umin", C.c_double), ("umax", C.c_double)]
 
 
+class CellRecord(C.Structure):  # ss_cell_record (CellRecord, tracking.hpp:36-42)
+    _fields_ = [("frame", C.c_int), ("label", C.c_int), ("cx", C.c_int), ("cy", C.c_int), ("cz", C.c_int),
+                ("max_distance", C.c_int), ("voxel_count", C.c_longlong)]
+
+
+class TrackPoint(C.Structure):  # ss_track_point (TrajectoryPoint, io.hpp:36-40)
+    _fields_ = [("trajectory_id", C.c_int), ("frame", C.c_int), ("x", C.c_double), ("y", C.c_double),
+                ("z", C.c_double)]
+
+
 class Profile(C.Structure):
     _fields_ = [("red_ms", C.c_double), ("black_ms", C.c_double), ("assemble_ms", C.c_double),
                 ("rescale_ms", C.c_double), ("red_n", C.c_longlong), ("black_n", C.c_longlong),
@@ -180,6 +190,13 @@ def library() -> C.CDLL:
     sig("ss_apply_mirror_ghosts", [_GP, _D])
     sig("ss_interior_minmax", [_GP, _D, _D, _D])
     sig("ss_segment", [_GP, _D, _CP, C.c_int, C.POINTER(SegParams), _D, _D, C.POINTER(StepDiag)])
+    _IP = C.POINTER(C.c_int)
+    sig("ss_label_components", [_GP, C.POINTER(C.c_uint8), _IP, _IP])
+    sig("ss_distance_centers", [_GP, _IP, _IP, C.POINTER(CellRecord), C.c_int, _IP])
+    sig("ss_backtrack_link", [_GP, _IP, _IP, C.POINTER(CellRecord), C.c_int, _IP, _IP, _IP])
+    sig("ss_track", [_GP, _D, C.c_double, C.c_int, C.c_double, C.POINTER(TrackPoint), C.c_int, _IP])
+    sig("ss_session_track", [C.c_void_p, C.c_double, C.c_int, C.c_double, C.POINTER(TrackPoint), C.c_int, _IP])
+
     sig("ss_session_create", [_GP, C.c_int, C.POINTER(C.c_void_p)])
     sig("ss_session_create_group", [_GP, C.c_int, C.c_int, C.POINTER(C.c_void_p)])
     sig("ss_nccl_unique_id", [C.POINTER(C.c_uint8)])
@@ -350,6 +367,74 @@ def extract_mask(u, g: Grid, level: float = 0.5) -> np.ndarray:
     return m
 
 
+# ----------------------------------------------------------------------------- tracking
+# frames are (n4, n3, n2, n1) arrays, x fastest (MaskFrames / LabelField, tracking.hpp:14-34)
+def _ip(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+def label_components(mask, g: Grid):
+    """tracking.cpp:69-127 -> (labels int32 (n4, n3, n2, n1), labels_per_frame list)"""
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    if m.shape != (g.n4, g.n3, g.n2, g.n1):
+        raise ValidationError(f"mask shape {m.shape} != {(g.n4, g.n3, g.n2, g.n1)}")
+    lab = np.empty(m.shape, dtype=np.int32)
+    lpf = np.empty(g.n4, dtype=np.int32)
+    _check(library().ss_label_components(C.byref(g), m.ctypes.data_as(C.POINTER(C.c_uint8)), _ip(lab), _ip(lpf)))
+    return lab, lpf.tolist()
+
+
+def distance_centers(labels, labels_per_frame, g: Grid):
+    """tracking.cpp:189-215 -> list of CellRecord (frame, label order)"""
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    lpf = np.ascontiguousarray(labels_per_frame, dtype=np.int32)
+    n = int(lpf.sum())
+    out = (CellRecord * max(n, 1))()
+    got = C.c_int(0)
+    _check(library().ss_distance_centers(C.byref(g), _ip(lab), _ip(lpf), out, n, C.byref(got)))
+    return list(out[:got.value])
+
+
+def backtrack_link(records, labels, labels_per_frame, g: Grid):
+    """tracking.cpp:220-296 -> partial trajectories as lists of record indices"""
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    lpf = np.ascontiguousarray(labels_per_frame, dtype=np.int32)
+    n = len(records)
+    arr = (CellRecord * max(n, 1))(*records)
+    idx = np.zeros(max(n, 1), dtype=np.int32)
+    starts = np.zeros(n + 2, dtype=np.int32)
+    nc = C.c_int(0)
+    _check(library().ss_backtrack_link(C.byref(g), _ip(lab), _ip(lpf), arr, n, _ip(idx), _ip(starts), C.byref(nc)))
+    return [idx[starts[c]:starts[c + 1]].tolist() for c in range(nc.value)]
+
+
+def _points(call):
+    cap = 4096
+    while True:
+        out = (TrackPoint * cap)()
+        n = C.c_int(0)
+        st = call(out, cap, C.byref(n))
+        if st == 0:
+            return [(p.trajectory_id, p.frame, p.x, p.y, p.z) for p in out[:n.value]]
+        if n.value <= cap:
+            _check(st)
+        cap = n.value
+
+
+def track(u, g: Grid, level: float = 0.5, window: int = 3, radius: float = 5.0):
+    """track() (tracking.cpp:374-401): rows (trajectory_id, frame, x, y, z) in output order"""
+    a = _field(g, u, "u")
+    return _points(lambda out, cap, n: library().ss_track(C.byref(g), _dp(a), level, window, radius, out, cap, n))
+
+
+def write_trajectories(points, path: str) -> None:
+    """io.cpp:170-177 format: header + "id,frame,x,y,z" rows (C++ ostream default precision)"""
+    with open(path, "w") as f:
+        f.write("trajectory_id,frame,x,y,z\n")
+        for tid, fr, x, y, z in points:
+            f.write(f"{tid},{fr},{x:g},{y:g},{z:g}\n")
+
+
 def apply_dirichlet(f, g: Grid, value: float) -> np.ndarray:
     """grid.cpp:126-136 (returns a copy)."""
     out = np.array(_field(g, f, "field"), copy=True)
@@ -493,6 +578,10 @@ class Session:
         m = np.empty((self.l_count if self.distributed else g.n4, g.n3, g.n2, g.n1), dtype=np.uint8)
         _check(library().ss_session_get_mask(self._h, level, m.ctypes.data_as(C.POINTER(C.c_uint8))))
         return m
+
+    def track(self, level: float = 0.5, window: int = 3, radius: float = 5.0):
+        """track() on the device-resident u (single-process sessions)"""
+        return _points(lambda out, cap, n: library().ss_session_track(self._h, level, window, radius, out, cap, n))
 
     def fixed_sweeps(self, n: int) -> float:
         r = C.c_double(0.0)

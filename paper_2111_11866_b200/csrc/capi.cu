@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "domain.cuh"
+#include "track.cuh"
 
 namespace ssb {
 
@@ -339,6 +340,115 @@ ss_status ss_extract_mask(const ss_grid* g, const double* u, double level, uint8
     });
 }
 
+// ---------------------------------------------------------------- tracking
+static cudaStream_t track_stream() {
+    static cudaStream_t s = [] {
+        cudaStream_t t;
+        SSB_CUDA(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+        return t;
+    }();
+    return s;
+}
+
+static std::vector<ssb_track::Cell> to_cells(const ss_cell_record* r, int n) {
+    std::vector<ssb_track::Cell> c(n);
+    for (int i = 0; i < n; ++i) {
+        c[i].frame = r[i].frame;
+        c[i].label = r[i].label;
+        c[i].cx = r[i].cx;
+        c[i].cy = r[i].cy;
+        c[i].cz = r[i].cz;
+        c[i].max_distance = r[i].max_distance;
+        c[i].voxel_count = r[i].voxel_count;
+    }
+    return c;
+}
+
+static void put_points(const std::vector<ss_track_point>& pts, ss_track_point* out, int capacity, int* n_points) {
+    *n_points = (int)pts.size();
+    if ((int)pts.size() > capacity || (!out && !pts.empty()))
+        throw Error(SS_ERR_VALIDATION, "track: " + std::to_string(pts.size()) + " points, capacity " +
+                                           std::to_string(capacity));
+    if (!pts.empty()) std::memcpy(out, pts.data(), pts.size() * sizeof(ss_track_point));
+}
+
+ss_status ss_label_components(const ss_grid* g, const uint8_t* mask, int32_t* labels, int* labels_per_frame) {
+    return guard([&] {
+        validate_grid(g);
+        require(mask && labels && labels_per_frame, "null buffer");
+        require_device();
+        Tracker t(g->n1, g->n2, g->n3, g->n4, track_stream());
+        SSB_CUDA(cudaMemcpyAsync(t.mask(), mask, (size_t)t.frame_size() * g->n4, cudaMemcpyHostToDevice,
+                                 track_stream()));
+        t.label();
+        SSB_CUDA(cudaMemcpyAsync(labels, t.labels(), (size_t)t.frame_size() * g->n4 * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, track_stream()));
+        SSB_CUDA(cudaStreamSynchronize(track_stream()));
+        std::copy(t.labels_per_frame().begin(), t.labels_per_frame().end(), labels_per_frame);
+    });
+}
+
+ss_status ss_distance_centers(const ss_grid* g, const int32_t* labels, const int* labels_per_frame,
+                              ss_cell_record* out, int capacity, int* n_records) {
+    return guard([&] {
+        validate_grid(g);
+        require(labels && labels_per_frame && n_records, "null buffer");
+        require_device();
+        Tracker t(g->n1, g->n2, g->n3, g->n4, track_stream());
+        t.set_labels(labels, std::vector<int>(labels_per_frame, labels_per_frame + g->n4));
+        t.centers();
+        const std::vector<ssb_track::Cell>& c = t.cells();
+        *n_records = (int)c.size();
+        if ((int)c.size() > capacity || (!out && !c.empty()))
+            throw Error(SS_ERR_VALIDATION, "distance_centers: " + std::to_string(c.size()) + " records, capacity " +
+                                               std::to_string(capacity));
+        for (size_t i = 0; i < c.size(); ++i)
+            out[i] = ss_cell_record{c[i].frame, c[i].label, c[i].cx, c[i].cy, c[i].cz, c[i].max_distance,
+                                    c[i].voxel_count};
+    });
+}
+
+ss_status ss_backtrack_link(const ss_grid* g, const int32_t* labels, const int* labels_per_frame,
+                            const ss_cell_record* records, int n_records, int* record_index, int* chain_start,
+                            int* n_chains) {
+    return guard([&] {
+        validate_grid(g);
+        require(labels && labels_per_frame && (records || n_records == 0) && record_index && chain_start && n_chains,
+                "null buffer");
+        require_device();
+        Tracker t(g->n1, g->n2, g->n3, g->n4, track_stream());
+        t.set_labels(labels, std::vector<int>(labels_per_frame, labels_per_frame + g->n4));
+        t.set_cells(to_cells(records, n_records));
+        std::vector<int> proj, overlap;
+        t.targets(proj, overlap);
+        const std::vector<ssb_track::Chain> ch =
+            ssb_track::backtrack(t.labels_per_frame(), t.first(), t.cells(), proj, overlap);
+        int k = 0;
+        for (size_t c = 0; c < ch.size(); ++c) {
+            chain_start[c] = k;
+            for (int r : ch[c]) record_index[k++] = r;
+        }
+        chain_start[ch.size()] = k;
+        *n_chains = (int)ch.size();
+    });
+}
+
+ss_status ss_track(const ss_grid* g, const double* u, double level, int window, double radius, ss_track_point* out,
+                   int capacity, int* n_points) {
+    return guard([&] {
+        validate_grid(g);
+        require(u && n_points, "null buffer");
+        Domain& d = cached(*g);
+        Slab& s = *d.sp[0];
+        s.upload_state(u, 0);
+        Tracker t(g->n1, g->n2, g->n3, g->n4, d.stream);
+        launch_mask(d.stream, s.L, s.S[0].pf(), level, t.mask());
+        std::vector<ss_track_point> pts;
+        track_points(t, window, radius, pts);
+        put_points(pts, out, capacity, n_points);
+    });
+}
+
 ss_status ss_segment(const ss_grid* g, const double* image, const ss_center* c, int n, const ss_seg_params* p,
                      const double* u0, double* u_out, ss_step_diag* diags) {
     return guard([&] {
@@ -443,6 +553,22 @@ ss_status ss_session_get_mask(ss_session* s, double level, uint8_t* mask) {
         require(s && mask, "null session / buffer");
         SSB_CUDA(cudaSetDevice(s->d->device));
         s->d->get_mask(level, mask);
+    });
+}
+
+ss_status ss_session_track(ss_session* s, double level, int window, double radius, ss_track_point* out,
+                           int capacity, int* n_points) {
+    return guard([&] {
+        require(s && n_points, "null session / output");
+        Domain& d = *s->d;
+        require(!d.distributed, "track on a distributed session: gather u on one rank first");
+        SSB_CUDA(cudaSetDevice(d.device));
+        Tracker t(d.g.n1, d.g.n2, d.g.n3, d.g.n4, d.stream);
+        const long long fr = t.frame_size();
+        for (Slab* sl : d.sp) launch_mask(d.stream, sl->L, sl->S[d.cur].pf(), level, t.mask() + fr * sl->L.l0);
+        std::vector<ss_track_point> pts;
+        track_points(t, window, radius, pts);
+        put_points(pts, out, capacity, n_points);
     });
 }
 

@@ -4,11 +4,12 @@
 //   subsurf-b200 segment --config FILE [--workers N] [--output PREFIX]
 //   subsurf-b200 eoc [--max-n N] [--workers N] [--device D]
 //   subsurf-b200 threshold-preview --config FILE [--output PREFIX]
+//   subsurf-b200 track --config FILE [--output CSV]
 //
 // Config: `key = value` lines, `#` comments, later keys win (cli.cpp:193-215);
 // the reference's keys and defaults (cli.cpp:73-107).  Extensions: `sor_rel_tol`
 // (> 0: per-step tolerance rel * ||u^{n-1}||_2), `u0_header`/`u0_data` (an initial
-// function instead of build_initial), `device`.  `track` is out of scope.
+// function instead of build_initial), `device`.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -174,6 +175,32 @@ int cmd_threshold_preview(const std::string& config_path, const std::string& out
     return 0;
 }
 
+// cmd_track (cli.cpp:161-188): labelling, distance transform and predecessor
+// candidates on the GPU, per-cell linking on the host
+int cmd_track(const std::string& config_path, const std::string& output_override) {
+    const Config cfg = Config::load(config_path);
+    const Field4D u = read_image4d(cfg.str("input_header"), cfg.str("input_data"));
+    TrackParams params;
+    params.level = cfg.num("level", 0.5);
+    params.window = cfg.integer("window", 3);
+    params.radius = cfg.num("radius", 5.0);
+    const std::string output = output_override.empty() ? cfg.str("output") : output_override;
+    write_trajectories(track(u, params), output);
+    if (cfg.has("vtk_prefix")) {
+        const LabelField labels = label_components(extract_mask(u, params.level));
+        const GridSpec& spec = u.spec();
+        Field4D lf(spec, 0.0);
+        for (int l = 1; l <= spec.n4; ++l)
+            for (int k = 1; k <= spec.n3; ++k)
+                for (int j = 1; j <= spec.n2; ++j)
+                    for (int i = 1; i <= spec.n1; ++i)
+                        lf.at(i, j, k, l) = double(labels.frames[l - 1][labels.voxel(i - 1, j - 1, k - 1)]);
+        for (int l = 1; l <= spec.n4; ++l)
+            export_frame_vtk(lf, l, cfg.str("vtk_prefix") + "_f" + std::to_string(l - 1) + ".vtk");
+    }
+    return 0;
+}
+
 // run_eoc + print_report (eoc.cpp:175-205) on the GPU
 int cmd_eoc(int max_n, int device) {
     static const int sched[5] = {10, 20, 40, 80, 160};
@@ -208,7 +235,8 @@ void usage(std::ostream& o) {
     o << "subsurf-b200: 4D generalized subjective-surface segmentation on B200 (GPU)\n"
          "  segment --config FILE [--workers N] [--output PREFIX]\n"
          "  eoc [--max-n 10|20|40|80|160] [--workers N] [--device D]\n"
-         "  threshold-preview --config FILE [--output PREFIX]\n";
+         "  threshold-preview --config FILE [--output PREFIX]\n"
+         "  track --config FILE [--output CSV]\n";
 }
 
 }  // namespace
@@ -247,16 +275,17 @@ int main(int argc, char** argv) {
         }
     }
     try {
-        if (cmd == "segment" || cmd == "threshold-preview") {
+        if (cmd == "segment" || cmd == "threshold-preview" || cmd == "track") {
             if (config_path.empty()) {
                 std::cerr << "error: --config is required\n";
                 return 2;
             }
+            if (cmd == "track") return cmd_track(config_path, output);
             return cmd == "segment" ? cmd_segment(config_path, workers, output)
                                     : cmd_threshold_preview(config_path, output);
         }
         if (cmd == "eoc") return cmd_eoc(max_n, device);
-        std::cerr << "error: unknown subcommand " << cmd << " (track is out of scope)\n";
+        std::cerr << "error: unknown subcommand " << cmd << "\n";
         usage(std::cerr);
         return 2;
     } catch (const std::exception& e) {

@@ -164,6 +164,35 @@ CentersTable read_centers(const std::string& path, const GridSpec& spec) {
     return t;
 }
 
+void write_trajectories(const TrajectoryFile& t, const std::string& path) {
+    std::ofstream out(path);
+    if (!out) throw IoError("cannot write trajectories: " + path);
+    out << "trajectory_id,frame,x,y,z\n";  // default ostream formatting, like the reference
+    for (const TrajectoryPoint& p : t.points)
+        out << p.trajectory_id << ',' << p.frame << ',' << p.x << ',' << p.y << ',' << p.z << "\n";
+    if (!out) throw IoError("short write on " + path);
+}
+
+TrajectoryFile read_trajectories(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw IoError("cannot open trajectories: " + path);
+    TrajectoryFile t;
+    std::string line;
+    std::size_t lineno = 0;
+    while (std::getline(in, line)) {
+        ++lineno;
+        if (line.empty() || line.compare(0, 13, "trajectory_id") == 0) continue;
+        for (char& c : line)
+            if (c == ',') c = ' ';
+        std::istringstream ss(line);
+        TrajectoryPoint p;
+        if (!(ss >> p.trajectory_id >> p.frame >> p.x >> p.y >> p.z))
+            throw FormatError(path + ":" + std::to_string(lineno) + ": bad trajectory row");
+        t.points.push_back(p);
+    }
+    return t;
+}
+
 void export_frame_vtk(const Field4D& field, int l, const std::string& path) {
     const GridSpec& s = field.spec();
     if (l < 1 || l > s.n4)

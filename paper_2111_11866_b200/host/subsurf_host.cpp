@@ -8,6 +8,7 @@
 #include <ostream>
 
 #include "subsurf_b200.h"
+#include "subsurf_b200/track_link.hpp"
 
 namespace subsurf {
 
@@ -298,6 +299,167 @@ MaskFrames extract_mask(const Field4D& u, double level) {
         m.frames[l].assign(all.begin() + std::size_t(l) * m.frame_size(),
                            all.begin() + std::size_t(l + 1) * m.frame_size());
     return m;
+}
+
+// ---------------------------------------------------------------- tracking
+namespace {
+
+ss_grid frames_grid(int n1, int n2, int n3, std::size_t frames) {
+    return ss_grid{n1, n2, n3, int(frames), 1.0, 1.0, 1.0, 1.0};
+}
+
+std::vector<std::int32_t> flat_labels(const LabelField& L) {
+    std::vector<std::int32_t> all;
+    all.reserve(L.frame_size() * L.frames.size());
+    for (const auto& f : L.frames) {
+        if (f.size() != L.frame_size()) throw ValidationError("label frame size mismatch");
+        all.insert(all.end(), f.begin(), f.end());
+    }
+    return all;
+}
+
+ssb_track::Cell cell_of(const CellRecord& r) {
+    ssb_track::Cell c;
+    c.frame = r.frame;
+    c.label = r.label;
+    c.cx = r.center[0];
+    c.cy = r.center[1];
+    c.cz = r.center[2];
+    c.max_distance = r.max_distance;
+    c.voxel_count = (long long)r.voxel_count;
+    return c;
+}
+
+}  // namespace
+
+MaskFrames mask_from_labels(const LabelField& labels) {  // tracking.cpp:55-67
+    MaskFrames m;
+    m.n1 = labels.n1;
+    m.n2 = labels.n2;
+    m.n3 = labels.n3;
+    m.frames.resize(labels.frames.size());
+    for (std::size_t f = 0; f < labels.frames.size(); ++f) {
+        m.frames[f].resize(labels.frames[f].size());
+        for (std::size_t v = 0; v < labels.frames[f].size(); ++v) m.frames[f][v] = labels.frames[f][v] > 0 ? 1 : 0;
+    }
+    return m;
+}
+
+LabelField label_components(const MaskFrames& mask) {
+    LabelField L;
+    L.n1 = mask.n1;
+    L.n2 = mask.n2;
+    L.n3 = mask.n3;
+    const std::size_t F = mask.frames.size(), fs = mask.frame_size();
+    L.frames.resize(F);
+    L.labels_per_frame.assign(F, 0);
+    if (F == 0 || fs == 0) return L;
+    std::vector<std::uint8_t> all;
+    all.reserve(fs * F);
+    for (const auto& f : mask.frames) {
+        if (f.size() != fs) throw ValidationError("mask frame size mismatch");
+        all.insert(all.end(), f.begin(), f.end());
+    }
+    std::vector<std::int32_t> lab(fs * F);
+    const ss_grid g = frames_grid(mask.n1, mask.n2, mask.n3, F);
+    raise(ss_label_components(&g, all.data(), lab.data(), L.labels_per_frame.data()));
+    for (std::size_t f = 0; f < F; ++f) L.frames[f].assign(lab.begin() + f * fs, lab.begin() + (f + 1) * fs);
+    return L;
+}
+
+std::vector<CellRecord> distance_centers(const LabelField& labels) {
+    const std::size_t F = labels.frames.size();
+    std::vector<CellRecord> out;
+    if (F == 0 || labels.frame_size() == 0) return out;
+    const std::vector<std::int32_t> all = flat_labels(labels);
+    int n = 0;
+    for (int k : labels.labels_per_frame) n += k;
+    std::vector<ss_cell_record> r(std::max(n, 1));
+    const ss_grid g = frames_grid(labels.n1, labels.n2, labels.n3, F);
+    int got = 0;
+    raise(ss_distance_centers(&g, all.data(), labels.labels_per_frame.data(), r.data(), n, &got));
+    out.resize(got);
+    for (int i = 0; i < got; ++i) {
+        out[i].frame = r[i].frame;
+        out[i].label = r[i].label;
+        out[i].center = {r[i].cx, r[i].cy, r[i].cz};
+        out[i].max_distance = r[i].max_distance;
+        out[i].voxel_count = std::size_t(r[i].voxel_count);
+    }
+    return out;
+}
+
+std::vector<Trajectory> backtrack_link(const std::vector<CellRecord>& records, const LabelField& labels) {
+    const std::size_t F = labels.frames.size();
+    std::vector<Trajectory> out;
+    if (F == 0 || labels.frame_size() == 0) return out;
+    const std::vector<std::int32_t> all = flat_labels(labels);
+    std::vector<ss_cell_record> r(records.size());
+    for (std::size_t i = 0; i < records.size(); ++i)
+        r[i] = ss_cell_record{records[i].frame, records[i].label, records[i].center[0], records[i].center[1],
+                              records[i].center[2], records[i].max_distance, (long long)records[i].voxel_count};
+    std::vector<int> idx(std::max<std::size_t>(records.size(), 1)), starts(records.size() + 2);
+    int nc = 0;
+    const ss_grid g = frames_grid(labels.n1, labels.n2, labels.n3, F);
+    raise(ss_backtrack_link(&g, all.data(), labels.labels_per_frame.data(), r.data(), int(records.size()),
+                            idx.data(), starts.data(), &nc));
+    out.resize(nc);
+    for (int c = 0; c < nc; ++c) {
+        out[c].id = c + 1;
+        for (int k = starts[c]; k < starts[c + 1]; ++k) out[c].records.push_back(records[idx[k]]);
+    }
+    return out;
+}
+
+std::vector<Trajectory> prolong_and_merge(std::vector<Trajectory> partials, int window, double radius) {
+    std::vector<ssb_track::Cell> cells;
+    std::vector<CellRecord> recs;
+    std::vector<ssb_track::Chain> parts(partials.size());
+    for (std::size_t p = 0; p < partials.size(); ++p)
+        for (const CellRecord& r : partials[p].records) {
+            parts[p].push_back(int(cells.size()));
+            cells.push_back(cell_of(r));
+            recs.push_back(r);
+        }
+    const std::vector<ssb_track::Chain> merged = ssb_track::merge(cells, parts, window, radius);
+    std::vector<Trajectory> out(merged.size());
+    for (std::size_t t = 0; t < merged.size(); ++t) {
+        out[t].id = int(t) + 1;
+        for (int c : merged[t]) out[t].records.push_back(recs[c]);
+    }
+    return out;
+}
+
+std::vector<Trajectory> track_cells(const Field4D& u, const TrackParams& params) {
+    const LabelField labels = label_components(extract_mask(u, params.level));
+    const std::vector<CellRecord> records = distance_centers(labels);
+    std::vector<Trajectory> merged =
+        prolong_and_merge(backtrack_link(records, labels), params.window, params.radius);
+    std::sort(merged.begin(), merged.end(), [&](const Trajectory& a, const Trajectory& b) {  // tracking.cpp:379-386
+        const CellRecord& ra = a.records.front();
+        const CellRecord& rb = b.records.front();
+        if (ra.frame != rb.frame) return ra.frame < rb.frame;
+        return labels.voxel(ra.center[0], ra.center[1], ra.center[2]) <
+               labels.voxel(rb.center[0], rb.center[1], rb.center[2]);
+    });
+    for (std::size_t t = 0; t < merged.size(); ++t) merged[t].id = int(t) + 1;
+    return merged;
+}
+
+TrajectoryFile track(const Field4D& u, const TrackParams& params) {
+    const ss_grid g = grid_of(u.spec());
+    std::vector<ss_track_point> pts(4096);
+    int n = 0;
+    ss_status st = ss_track(&g, u.data(), params.level, params.window, params.radius, pts.data(), int(pts.size()), &n);
+    if (st != SS_OK && n > int(pts.size())) {
+        pts.resize(n);
+        st = ss_track(&g, u.data(), params.level, params.window, params.radius, pts.data(), n, &n);
+    }
+    raise(st);
+    TrajectoryFile f;
+    f.points.resize(n);
+    for (int i = 0; i < n; ++i) f.points[i] = TrajectoryPoint{pts[i].trajectory_id, pts[i].frame, pts[i].x, pts[i].y, pts[i].z};
+    return f;
 }
 
 }  // namespace subsurf

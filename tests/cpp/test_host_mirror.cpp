@@ -193,6 +193,37 @@ int main() {
         mok = std::memcmp(m.frames[l].data(), om.data() + l * m.frame_size(), m.frame_size()) == 0;
     CHECK(mok, "extract_mask");
 
+    // tracking: the composed C++ pipeline (label_components -> distance_centers ->
+    // backtrack_link -> prolong_and_merge -> order) == the one-call GPU track()
+    {
+        const GridSpec ts(20, 16, 8, 6, 1.0, 1.0, 1.0, 1.0);
+        Field4D tu(ts, 0.0);
+        for (int l = 1; l <= ts.n4; ++l)
+            for (int c = 0; c < 3; ++c) {
+                const double cx = 4.0 + 5.0 * c + 0.7 * l, cy = 5.0 + 2.0 * c + 0.4 * l, cz = 3.5;
+                for (int k = 1; k <= ts.n3; ++k)
+                    for (int j = 1; j <= ts.n2; ++j)
+                        for (int i = 1; i <= ts.n1; ++i) {
+                            const double d = (i - 1 - cx) * (i - 1 - cx) / 4.0 + (j - 1 - cy) * (j - 1 - cy) / 3.0 +
+                                             (k - 1 - cz) * (k - 1 - cz) / 2.0;
+                            if (d < 1.0 && !(c == 1 && l == 3)) tu.at(i, j, k, l) = 1.0 - 0.3 * d;
+                        }
+            }
+        const std::vector<Trajectory> tc = track_cells(tu, TrackParams{});
+        const TrajectoryFile tf = track(tu, TrackParams{});
+        std::size_t q = 0;
+        bool tok = true;
+        for (const Trajectory& t : tc)
+            for (const CellRecord& r : t.records) {
+                tok = tok && q < tf.points.size() && tf.points[q].trajectory_id == t.id && tf.points[q].frame == r.frame &&
+                      tf.points[q].x == r.center[0] && tf.points[q].y == r.center[1] && tf.points[q].z == r.center[2];
+                ++q;
+            }
+        CHECK(tok && q == tf.points.size() && !tc.empty(), "track_cells == track");
+        const MaskFrames tm = mask_from_labels(label_components(extract_mask(tu, 0.5)));
+        CHECK(tm.frames == extract_mask(tu, 0.5).frames, "mask_from_labels(label_components(mask)) == mask");
+    }
+
     std::printf(failures ? "FAILED %d\n" : "ALL OK\n", failures);
     return failures ? 1 : 0;
 }

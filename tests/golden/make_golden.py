@@ -107,6 +107,21 @@ def main():
     assert st == 0
     save("eoc", e10=e10, e20=e20)
 
+    # --- tracking (tracking.cpp): extract_mask -> label_components -> distance_centers
+    #     -> backtrack_link -> prolong_and_merge -> track on a moving-cells scene
+    dims = (24, 20, 10, 8)
+    g = op.Grid.make(dims, 1.0)
+    u = cs.track_scene(dims, 5)
+    m = R.extract_mask(g, u, 0.5)
+    lab, lpf = R.label_components(g, m)
+    rec = R.distance_centers(g, lab, lpf)
+    chains = R.backtrack_link(g, lab, lpf)
+    pts = R.track(g, u, 0.5, 3, 5.0)
+    starts = np.cumsum([0] + [len(c) for c in chains])
+    save("track", dims=np.array(dims), u=u, level=0.5, window=3, radius=5.0, labels=lab, lpf=np.array(lpf),
+         records=rec, chain_fl=np.array([x for c in chains for x in c]), chain_start=starts,
+         points=np.array([p[:2] for p in pts]), points_xyz=np.array([p[2:] for p in pts]))
+
 
 if __name__ == "__main__":
     main()

@@ -109,3 +109,27 @@ def test_cli_threshold_and_eoc(cli, oracle, tmp_path):
     lines = r.stdout.strip().splitlines()
     assert len(lines) == 3 and float(lines[1].split()[3]) == pytest.approx(1.684177e-2, rel=1e-6)
     assert float(lines[2].split()[4]) == pytest.approx(1.851052, rel=1e-5)
+
+
+@pytest.mark.gpu
+def test_cli_track_matches_reference(cli, ref, tmp_path):
+    """`subsurf-b200 track` (cli.cpp:161-188) == the reference's track() on the same f32 field."""
+    from oracle.oracle_py import Grid
+    dims = (24, 20, 10, 8)
+    u = cs.track_scene(dims, 11)
+    u32 = np.zeros_like(u)
+    u32[1:-1, 1:-1, 1:-1, 1:-1] = u[1:-1, 1:-1, 1:-1, 1:-1].astype(np.float32)
+    d = str(tmp_path)
+    json.dump({"dims": list(dims), "spacing": [1.0] * 4, "dtype": "f32le", "order": "i-fastest"},
+              open(os.path.join(d, "u.json"), "w"))
+    u32[1:-1, 1:-1, 1:-1, 1:-1].astype("<f4").tofile(os.path.join(d, "u.raw"))
+    with open(os.path.join(d, "trk.txt"), "w") as f:
+        f.write(f"input_header = {d}/u.json\ninput_data = {d}/u.raw\noutput = {d}/traj.csv\n"
+                f"level = 0.5\nwindow = 3\nradius = 5\nvtk_prefix = {d}/lab\n")
+    r = subprocess.run([cli, "track", "--config", os.path.join(d, "trk.txt")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    rows = open(os.path.join(d, "traj.csv")).read().splitlines()
+    assert rows[0] == "trajectory_id,frame,x,y,z"
+    want = ref.track(Grid.make(dims, 1.0), u32, 0.5, 3, 5.0)
+    assert rows[1:] == [f"{a},{b},{x:g},{y:g},{z:g}" for a, b, x, y, z in want]
+    assert os.path.exists(os.path.join(d, f"lab_f{dims[3] - 1}.vtk"))
