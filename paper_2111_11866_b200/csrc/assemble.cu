@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kPassBX * kPassBY) assemble_kernel(const AsmAr
     }
     const double diag = 1.0 - sum;
     if (!isfinite(diag)) atomicOr(a.bad, 1);
-    float4* cw = reinterpret_cast<float4*>(a.coef[C] + p * 8);
+    float4* cw = reinterpret_cast<float4*>(a.coef[C] + (S.row * L.Wc + ((q.i - 1) >> 1)) * 8);
     cw[0] = make_float4(cf[0], cf[1], cf[2], cf[3]);
     cw[1] = make_float4(cf[4], cf[5], cf[6], cf[7]);
     if constexpr (EXPORT) {
@@ -249,7 +249,7 @@ __global__ void pack_coef_kernel(const Layout L, const double* __restrict__ off,
     const int k = (int)((r / L.jMax) % L.kMax);
     const int l = (int)(r / ((long long)L.jMax * L.kMax));
     if (i < 1 || i > L.n1 || j < 1 || j > L.n2 || k < 1 || k > L.n3 || l < 1 || l > L.n4) return;
-    float* dst = (L.colour(i, j, k, l) ? c1 : c0) + (r * L.W + (i >> 1)) * 8;
+    float* dst = (L.colour(i, j, k, l) ? c1 : c0) + L.coef_slot(i, j, k, l) * 8;
 #pragma unroll
     for (int f = 0; f < 8; ++f) dst[f] = (float)off[e * 8 + f];
 }

@@ -34,6 +34,8 @@ struct Layout {
     int glo, ghi;         // local planes 0 / n4+1 are global ghosts (else: halos)
     int iMax, jMax, kMax, lMax;
     int W;            // packed slots per row
+    int Wc;           // coefficient slots per row: interior doxels of one colour, (n1+1)/2
+                      // (slot s <-> i = 2s + 1 + parity; no ghost slot, rows stay 32-byte aligned)
     long long rows;   // jMax * kMax * lMax
     long long cs;     // elements per colour array = rows * W
     long long sj, sk, sl;  // packed row strides for j, k, l neighbours
@@ -49,6 +51,7 @@ struct Layout {
         L.ghi = l0 + g.n4 == L.n4g;
         L.iMax = g.n1 + 2; L.jMax = g.n2 + 2; L.kMax = g.n3 + 2; L.lMax = g.n4 + 2;
         L.W = (((L.iMax + 1) / 2) + 1) & ~1;  // even: every packed row starts 16-byte aligned (TMA)
+        L.Wc = (g.n1 + 1) / 2;
         L.rows = (long long)L.jMax * L.kMax * L.lMax;
         L.cs = L.rows * L.W;
         L.sj = L.W;
@@ -71,6 +74,10 @@ struct Layout {
         return (i + j + k + l + lpar) & 1;
     }
     long long plane() const { return (long long)jMax * kMax * W; }  // one colour, one l-plane
+    // index of doxel (i, j, k, l) in a colour's coefficient rows (8 floats each)
+    __host__ __device__ __forceinline__ long long coef_slot(int i, int j, int k, int l) const {
+        return row(j, k, l) * Wc + ((i - 1) >> 1);
+    }
 };
 
 // A colour-packed scalar field: two device arrays (red, black).

@@ -140,8 +140,8 @@ Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int 
     gl.n4 = n4_local;
     L = Layout::make(gl, l0, global.n4);
     for (auto& f : S) f.alloc(L);
-    coef[0].alloc(L.cs * 8);
-    coef[1].alloc(L.cs * 8);
+    coef[0].alloc(L.rows * L.Wc * 8);
+    coef[1].alloc(L.rows * L.Wc * 8);
     SorArgs t{};
     pass_tiles(L, t);
     const size_t nparts = std::max((size_t)t.tiles * kPassBY, tma_partials(L));

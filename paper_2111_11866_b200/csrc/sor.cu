@@ -48,7 +48,7 @@ __device__ __forceinline__ void load_doxel(const SorArgs& a, const float* __rest
         d.c[6] = l + L.l0 > 1 ? (float)a.hc[3] : 0.f;  // global l boundaries
         d.c[7] = l + L.l0 < L.n4g ? (float)a.hc[3] : 0.f;
     } else {
-        const float4* cp = reinterpret_cast<const float4*>(cf + p * 8);
+        const float4* cp = reinterpret_cast<const float4*>(cf + (L.row(j, k, l) * L.Wc + ((i - 1) >> 1)) * 8);
         const float4 lo = __ldcs(cp);
         const float4 hi = __ldcs(cp + 1);
         d.c[0] = lo.x; d.c[1] = lo.y; d.c[2] = lo.z; d.c[3] = lo.w;

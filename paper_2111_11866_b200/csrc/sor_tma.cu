@@ -108,6 +108,7 @@ struct Geo {  // per-launch tiling (identical on host and device)
     int nkc;  // plane chunks per slice
     long long items;
     uint32_t row_bytes;   // one packed row of doubles
+    uint32_t coef_row_bytes;  // one row of fp32 coefficients (Wc slots x 8)
     uint32_t main_bytes;  // one main stage: COEF RHS UC ULM ULP of a plane
     uint32_t uk_bytes;    // one UK stage: R+2 other-colour rows of a plane
     uint32_t off_coef, off_rhs, off_uc, off_ulm, off_ulp;
@@ -130,7 +131,8 @@ __host__ __device__ inline Geo make_geo(const Layout& L) {
     g.items = (long long)g.njg * g.nkc * L.n4;
     g.row_bytes = rb;
     g.off_coef = 0;
-    g.off_rhs = g.off_coef + 4u * R * rb;  // fp32 x 8 per slot = 4 x a double row
+    g.coef_row_bytes = (uint32_t)L.Wc * 32u;
+    g.off_rhs = g.off_coef + R * g.coef_row_bytes;
     g.off_uc = g.off_rhs + R * rb;
     g.off_ulm = g.off_uc + R * rb;
     g.off_ulp = g.off_ulm + R * rb;
@@ -217,9 +219,9 @@ __device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsi
         rg.acquire(empty);
         unsigned char* s = smem + rg.slot * G.main_bytes;
         uint64_t* bar = &full[rg.slot];
-        mbar_expect_tx(bar, (HEAT ? 4u : 8u) * it.rows * rb);
+        mbar_expect_tx(bar, (HEAT ? 0u : it.rows * G.coef_row_bytes) + 4u * it.rows * rb);
         const long long row0 = ((long long)it.l * L.kMax + p) * L.jMax + it.j0;  // row (j0, p, l)
-        if (!HEAT) bulk_g2s(s + G.off_coef, coef + row0 * W * 8, 4 * it.rows * rb, bar, pol.stream);
+        if (!HEAT) bulk_g2s(s + G.off_coef, coef + row0 * L.Wc * 8, it.rows * G.coef_row_bytes, bar, pol.stream);
         bulk_g2s(s + G.off_rhs, rhs + row0 * W, it.rows * rb, bar, pol.stream);
         bulk_g2s(s + G.off_uc, uc + row0 * W, it.rows * rb, bar, pol.uload);
         bulk_g2s(s + G.off_ulm, uo + (row0 - plane_rows) * W, it.rows * rb, bar, pol.uload);
@@ -289,7 +291,7 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
         const double* ukm = reinterpret_cast<const double*>(ukr + sm * G.uk_bytes) + o_uk;
         const double* ukc = reinterpret_cast<const double*>(ukr + sc * G.uk_bytes) + o_uk;
         const double* ukp = reinterpret_cast<const double*>(ukr + sp * G.uk_bytes) + o_uk;
-        const float* cf = reinterpret_cast<const float*>(mb + G.off_coef) + 8 * o_row;
+        const float* cf = reinterpret_cast<const float*>(mb + G.off_coef) + 8 * r * L.Wc;
         const double* rh = reinterpret_cast<const double*>(mb + G.off_rhs) + o_row;
         const double* u0r = reinterpret_cast<const double*>(mb + G.off_uc) + o_row;
         const double* ulm = reinterpret_cast<const double*>(mb + G.off_ulm) + o_row;
@@ -310,8 +312,8 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
                     d.c[6] = it.l + L.l0 > 1 ? (float)a.hc[3] : 0.f;
                     d.c[7] = it.l + L.l0 < L.n4g ? (float)a.hc[3] : 0.f;
                 } else {
-                    const float4 lo = *reinterpret_cast<const float4*>(cf + 8 * m);
-                    const float4 hi = *reinterpret_cast<const float4*>(cf + 8 * m + 4);
+                    const float4 lo = *reinterpret_cast<const float4*>(cf + 8 * q);  // slot q <-> i = 1 + par + 2q
+                    const float4 hi = *reinterpret_cast<const float4*>(cf + 8 * q + 4);
                     d.c[0] = lo.x; d.c[1] = lo.y; d.c[2] = lo.z; d.c[3] = lo.w;
                     d.c[4] = hi.x; d.c[5] = hi.y; d.c[6] = hi.z; d.c[7] = hi.w;
                 }
