@@ -592,9 +592,12 @@ class Session:
         _check(library().ss_session_set_loop_mode(self._h, mode))
 
     def set_kernel(self, kernel: str) -> None:
-        """'tma' (default): TMA-fed two-pass; 'ldg': plain load two-pass; 'wave':
-        two-iteration TMA wavefront through L2 (experimental, measured slower)."""
-        _check(library().ss_session_set_kernel(self._h, {"ldg": 0, "tma": 1, "wave": 2}[kernel]))
+        """'auto' (default): 'resident' when the solve's working set fits L2, else 'tma';
+        'tma': TMA-fed two-pass; 'ldg': plain load two-pass; 'resident': the whole solve
+        in one cooperative launch (LDG tiles, grid barriers); 'wave': two-iteration TMA
+        wavefront through L2 (experimental, measured slower)."""
+        _check(library().ss_session_set_kernel(
+            self._h, {"ldg": 0, "tma": 1, "wave": 2, "resident": 3, "auto": 4}[kernel]))
 
     def set_profiling(self, on: bool) -> None:
         _check(library().ss_session_set_profiling(self._h, 1 if on else 0))

@@ -185,8 +185,9 @@ struct Domain {
     ss_seg_params prm{};
 
     int loop_mode = 1;
-    int kernel = 1;   // SOR: 1 = TMA two-pass (default), 0 = LDG two-pass,
-                      // 2 = TMA two-iteration wavefront (experimental, slower; sor_tma.cu)
+    int kernel = 4;   // SOR: 4 = auto (default: resident when the working set fits L2, else TMA),
+                      // 1 = TMA two-pass, 0 = LDG two-pass, 3 = resident (one cooperative launch
+                      // per solve), 2 = TMA wavefront (experimental, slower; sor_tma.cu)
     int solve_count = 0;
     bool profiling = false;
     ss_profile prof{};

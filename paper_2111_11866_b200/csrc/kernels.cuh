@@ -86,6 +86,7 @@ int pass_order();   // SorArgs::order default (env SSB_ORDER)
 int pass_fuse_final();  // SorArgs::fuse_final allowed (env SSB_FUSE_FINAL)
 bool wave_supported(const Layout& L);
 size_t wave_flags(const Layout& L);
+int wave_iters();  // SOR iterations per wavefront launch (SSB_WAVE_PHASES / 2)
 void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat);
 dim3 pass_grid(const Layout& L);
 void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_slices,
@@ -97,6 +98,9 @@ void launch_sor_pass(cudaStream_t s, const SorArgs& a, int colour, bool heat);
 // the same pass restricted to slices [lo, hi] (boundary-first halo overlap)
 void launch_sor_pass_range(cudaStream_t s, const SorArgs& a, int colour, bool heat, int lo, int hi);
 void launch_sor_finalize(cudaStream_t s, const SorArgs& a);
+// whole solve in one cooperative launch (LDG tiles, state in L2); single slab
+bool resident_supported(const Layout& L);
+void launch_sor_resident(cudaStream_t s, const SorArgs& a, bool heat);
 void launch_sor_decide(cudaStream_t s, const SorArgs& a);
 
 // ---------------------------------------------------------------- assembly

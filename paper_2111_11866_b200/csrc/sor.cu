@@ -19,15 +19,29 @@
 // -fmad=false: iterates are bit-identical to the oracle.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "sor_final.cuh"
 #include "sor_math.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ssb {
 
 namespace {
 
 
-template <int C, bool HEAT>
+// CG: the state arrays were written earlier in the SAME launch (resident loop):
+// read them through L2 (ld.global.cg), not the non-coherent read-only path.
+template <bool CG>
+__device__ __forceinline__ double ld_state(const double* p) {
+    if constexpr (CG)
+        return __ldcg(p);
+    else
+        return __ldg(p);
+}
+
+template <int C, bool HEAT, bool CG = false>
 __device__ __forceinline__ void load_doxel(const SorArgs& a, const float* __restrict__ cf,
                                            const double* __restrict__ rh,
                                            const double* __restrict__ uc,
@@ -55,15 +69,15 @@ __device__ __forceinline__ void load_doxel(const SorArgs& a, const float* __rest
         d.c[4] = hi.x; d.c[5] = hi.y; d.c[6] = hi.z; d.c[7] = hi.w;
     }
     d.rhs = __ldcs(rh + p);
-    d.u0 = __ldg(uc + p);
-    d.nb[0] = __ldg(uo + rb + ((i - 1) >> 1));
-    d.nb[1] = __ldg(uo + rb + ((i + 1) >> 1));
-    d.nb[2] = __ldg(uo + p - L.sj);
-    d.nb[3] = __ldg(uo + p + L.sj);
-    d.nb[4] = __ldg(uo + p - L.sk);
-    d.nb[5] = __ldg(uo + p + L.sk);
-    d.nb[6] = __ldg(uo + p - L.sl);
-    d.nb[7] = __ldg(uo + p + L.sl);
+    d.u0 = ld_state<CG>(uc + p);
+    d.nb[0] = ld_state<CG>(uo + rb + ((i - 1) >> 1));
+    d.nb[1] = ld_state<CG>(uo + rb + ((i + 1) >> 1));
+    d.nb[2] = ld_state<CG>(uo + p - L.sj);
+    d.nb[3] = ld_state<CG>(uo + p + L.sj);
+    d.nb[4] = ld_state<CG>(uo + p - L.sk);
+    d.nb[5] = ld_state<CG>(uo + p + L.sk);
+    d.nb[6] = ld_state<CG>(uo + p - L.sl);
+    d.nb[7] = ld_state<CG>(uo + p + L.sl);
 }
 
 // Persistent colour pass: a resident grid walks the tiles (kPassBX doxels of one
@@ -72,11 +86,8 @@ __device__ __forceinline__ void load_doxel(const SorArgs& a, const float* __rest
 // writes one partial; the partials of a slice are contiguous and indexed by
 // (tile, warp), so the per-slice sums do not depend on the grid size, and no
 // block barrier stalls the load pipeline between tiles.
-template <int C, bool HEAT>
-__global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(const SorArgs a) {
-    const SorState* st = a.st;
-    if (*(volatile const int*)&st->done) return;
-    const int n = C == 0 ? *(volatile const int*)&st->n_red : *(volatile const int*)&st->n_black;
+template <int C, bool HEAT, bool CG>
+__device__ __forceinline__ void pass_body(const SorArgs& a, int n) {
     const int bout = out_buf(n);
     const int bin = in_buf(n);
     const Layout& L = a.L;
@@ -109,7 +120,7 @@ __global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(con
                     const int k = k0 + kb + b;
                     const int i = 1 + ((1 + j + k + l + L.lpar + C) & 1) + 2 * q;
                     ok[b] = k <= L.n3 && i <= L.n1;
-                    if (ok[b]) load_doxel<C, HEAT>(a, cf, rh, uc, uo, i, j, k, l, d[b]);
+                    if (ok[b]) load_doxel<C, HEAT, CG>(a, cf, rh, uc, uo, i, j, k, l, d[b]);
                 }
 #pragma unroll
                 for (int b = 0; b < kPassBatch; ++b)
@@ -119,6 +130,78 @@ __global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(con
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
         if (threadIdx.x == 0) a.part[n & 3][C][t * kPassBY + threadIdx.y] = r2;
+    }
+}
+
+template <int C, bool HEAT>
+__global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(const SorArgs a) {
+    const SorState* st = a.st;
+    if (*(volatile const int*)&st->done) return;
+    const int n = C == 0 ? *(volatile const int*)&st->n_red : *(volatile const int*)&st->n_black;
+    pass_body<C, HEAT, false>(a, n);
+}
+
+// Resident solve (grids whose working set fits in L2, e.g. BASELINE config 0):
+// ONE cooperative launch runs the whole loop -- red pass, grid barrier, slice
+// residuals, grid barrier, the decision (taken by every CTA from the same slice
+// values in the same order, so all agree; CTA 0 publishes it), black pass, grid
+// barrier -- instead of three launches per iteration.  Same tiles, partials,
+// per-doxel arithmetic and reductions as the LDG kernels: iterates, residuals and
+// iteration counts are those of kernel 0 bit for bit.  State arrays are read
+// through L2 (they change between passes of the launch).
+template <bool HEAT>
+__global__ void __launch_bounds__(kPassBX * kPassBY, 2) sor_resident(const SorArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double ws[32];
+    __shared__ int stop;
+    SorState* st = a.st;
+    const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+    if (*(volatile int*)&st->done) return;  // uniform: nobody has written st yet
+    int n = *(volatile int*)&st->n_red;
+    const double tol = st->tol;
+    const int fixed = st->fixed, max_iter = st->max_iter;
+    grid.sync();  // everyone has read the state before CTA 0 rewrites it
+    while (true) {
+        pass_body<0, HEAT, true>(a, n);
+        grid.sync();
+        if (n >= 2)
+            for (int l = blockIdx.x; l < a.L.n4; l += gridDim.x) {
+                const double v = slice_residual(a, n, l, ws, tid);
+                if (tid == 0) a.slice_res[l] = v;
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+            }
+        grid.sync();
+        if (tid == 0) {  // sor_decide_state, evaluated by every CTA
+            int done = 0, conv = 0;
+            double res = 0.0;
+            if (n >= 2) {
+                double total = 0.0;
+                for (int l = 0; l < a.L.n4g; ++l) total += __ldcg(a.all_slices + l);
+                res = sqrt(total);
+                if (!fixed && res <= tol) {
+                    done = conv = 1;
+                } else if (n - 1 >= max_iter) {
+                    done = 1;
+                    conv = fixed;
+                }
+            }
+            if (blockIdx.x == 0) {
+                if (n >= 2) {
+                    st->residual = res;
+                    st->iterations = n - 1;
+                }
+                st->done = done;
+                st->converged = conv;
+                st->n_black = n;
+                st->n_red = n + 1;
+            }
+            stop = done;
+        }
+        __syncthreads();
+        if (stop) break;
+        pass_body<1, HEAT, true>(a, n);
+        grid.sync();
+        ++n;
     }
 }
 
@@ -250,15 +333,38 @@ void launch_sor_decide(cudaStream_t s, const SorArgs& a) {
     SSB_LAUNCHED();
 }
 
+bool resident_supported(const Layout& L) {
+    // active working set of one iteration: coefficients + rhs/guess + in + out buffers
+    const double bytes = 2.0 * L.rows * L.Wc * 32.0 + 3.0 * 2.0 * L.cs * 8.0;
+    return bytes <= 96.0 * 1024 * 1024 && L.glo && L.ghi;
+}
+
+void launch_sor_resident(cudaStream_t s, const SorArgs& a, bool heat) {
+    static int blocks = 0;
+    if (!blocks) {
+        int dev = 0, sms = 0, per0 = 0, per1 = 0;
+        SSB_CUDA(cudaGetDevice(&dev));
+        SSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per0, sor_resident<false>, kPassBX * kPassBY, 0));
+        SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, sor_resident<true>, kPassBX * kPassBY, 0));
+        blocks = sms * std::max(1, std::min(per0, per1));
+    }
+    const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(a.tiles, blocks));
+    void* args[] = {const_cast<SorArgs*>(&a)};
+    const void* fn = heat ? (const void*)sor_resident<true> : (const void*)sor_resident<false>;
+    SSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kPassBX, kPassBY), args, 0, s));
+    SSB_LAUNCHED();
+}
+
 void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* ev) {
     if (a.wave) {  // iterations n and n+1 in one wavefront launch, then both decisions
         if (ev) SSB_CUDA(cudaEventRecord(ev[0], s));
         launch_sor_wave(s, a, heat);
         if (ev) SSB_CUDA(cudaEventRecord(ev[1], s));
-        sor_finalize<<<a.L.n4, 256, 0, s>>>(a);
-        SSB_LAUNCHED();
-        sor_finalize<<<a.L.n4, 256, 0, s>>>(a);
-        SSB_LAUNCHED();
+        for (int q = 0; q < wave_iters(); ++q) {
+            sor_finalize<<<a.L.n4, 256, 0, s>>>(a);
+            SSB_LAUNCHED();
+        }
         if (ev) {
             SSB_CUDA(cudaEventRecord(ev[2], s));
             SSB_CUDA(cudaEventRecord(ev[3], s));

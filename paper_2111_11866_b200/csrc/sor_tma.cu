@@ -54,6 +54,10 @@ constexpr int kDefaultOrder = 1;
 #ifndef SSB_WAVE_SKEW
 #define SSB_WAVE_SKEW 0  // 0: 2 * nkc sub-slices (measured: nkc+1 starves, 16..48 equal)
 #endif
+#ifndef SSB_WAVE_PHASES
+#define SSB_WAVE_PHASES 4  // colour phases per wavefront launch: 4 = two iterations, 2 = one sweep
+#endif
+constexpr int kWavePH = SSB_WAVE_PHASES;
 
 __device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -486,19 +490,19 @@ __global__ void __launch_bounds__(kThreads, 2) sor_wave_tma(const SorArgs a) {
     const Geo G = make_geo(L);
     const int CH = G.njg * G.nkc;  // items per slice and phase
     // wavefront over sub-slices s = (l-1)*nkc + kc: phase d of step sigma works on
-    // s = sigma - skew*d; each step has 4 phases x njg row groups
+    // s = sigma - skew*d; each step has kWavePH phases x njg row groups
     const int skew = SSB_WAVE_SKEW > 0 ? SSB_WAVE_SKEW : 2 * G.nkc;
     const long long NS = (long long)L.n4 * G.nkc;
-    const long long NT = (NS + 3LL * skew) * 4 * G.njg;
+    const long long NT = (NS + (kWavePH - 1LL) * skew) * kWavePH * G.njg;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const Policies pol = make_policies(0);
+    const Policies pol = make_policies(a.l2hint);
     init_barriers(bars);
 
     auto decode = [&](long long t, int& d, int& l, int& c) {
         const int jg = (int)(t % G.njg);
         const long long r = t / G.njg;
-        d = (int)(r & 3);
-        const long long s = (r >> 2) - (long long)skew * d;  // sub-slice of this phase
+        d = (int)(r % kWavePH);
+        const long long s = r / kWavePH - (long long)skew * d;  // sub-slice of this phase
         if (s < 0 || s >= NS) {
             l = 0;
             c = 0;
@@ -658,6 +662,8 @@ bool tma_fuse_ok(const Layout& L) {
 
 size_t tma_partials(const Layout& L) { return (size_t)make_geo(L).items * kWarps; }
 
+int wave_iters() { return kWavePH / 2; }
+
 size_t wave_flags(const Layout& L) {
     const Geo G = make_geo(L);
     return (size_t)4 * L.n4 * G.njg * G.nkc;
@@ -684,7 +690,7 @@ void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat) {
         last_smem = smem;
     }
     const int skew = SSB_WAVE_SKEW > 0 ? SSB_WAVE_SKEW : 2 * G.nkc;
-    const long long NT = ((long long)a.L.n4 * G.nkc + 3LL * skew) * 4 * G.njg;
+    const long long NT = ((long long)a.L.n4 * G.nkc + (kWavePH - 1LL) * skew) * kWavePH * G.njg;
     const unsigned grid = (unsigned)std::min<long long>(NT, blocks);
     if (heat)
         sor_wave_tma<true><<<grid, kThreads, smem, s>>>(a);

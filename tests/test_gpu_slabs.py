@@ -91,7 +91,7 @@ def test_nccl_session_world1(gpu):
     assert np.array_equal(u.view(np.uint64), d["u_rel"].view(np.uint64))
 
 
-@pytest.mark.parametrize("kernel", ["ldg", "tma", "wave"])
+@pytest.mark.parametrize("kernel", ["ldg", "tma", "wave", "resident", "auto"])
 def test_pass_kernels_agree(gpu, kernel):
     """Both SOR colour-pass kernels give the golden segment() result bit for bit."""
     d = dict(np.load(os.path.join(GOLD, "segment.npz")))
@@ -108,3 +108,30 @@ def test_pass_kernels_agree(gpu, kernel):
             u = s.get_u()
         assert its == list(d["iters_rel"])
         assert np.array_equal(u.view(np.uint64), d["u_rel"].view(np.uint64))
+
+
+@pytest.mark.parametrize("dims", [(7, 5, 6, 4), (33, 9, 5, 3), (130, 6, 9, 2), (1, 3, 2, 5)])
+def test_kernels_agree_odd_shapes(gpu, oracle, dims):
+    """Every SOR kernel (TMA two-pass, LDG two-pass, resident single launch) against the
+    oracle's segment() on odd shapes: identical iterates and iteration counts."""
+    h = 1.0 / max(dims[:3])
+    g = gpu.Grid.make(dims, h)
+    img = cs.f32_image(dims, sum(dims), noise=0.05)
+    rows = [(f, (dims[0] - 1) / 2, (dims[1] - 1) / 2, (dims[2] - 1) / 2, 1.5) for f in range(dims[3])]
+    kw = dict(tau=h, epsilon=1e-3, omega=1.4, sor_rel_tol=1e-8, n_steps=2, sigma=np.sqrt(2) * h, K=100.0,
+              delta=0.5, vartheta=0.5, rescale_radius=2.0)
+    st, uo, info = oracle.segment(cs.grid(dims, h), img, rows, oracle_params(kw))
+    assert st == 0
+    for kernel in ("tma", "ldg", "resident"):
+        with gpu.Session(g) as s:
+            s.set_kernel(kernel)
+            s.prepare(img, rows, gpu.seg_params(**kw))
+            its = [s.step()["iterations"] for _ in range(2)]
+            u = s.get_u()
+        assert its == [x["iterations"] for x in info["diags"]], kernel
+        assert np.array_equal(u.view(np.uint64), uo.view(np.uint64)), kernel
+
+
+def oracle_params(kw):
+    from oracle.oracle_py import seg_params
+    return seg_params(**kw)
