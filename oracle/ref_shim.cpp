@@ -328,6 +328,39 @@ int ref_backtrack_link(const or_grid* g, const int* labels, const int* lpf, int*
     });
 }
 
+/* prolong_and_merge on partials given as records (frame, x, y, z) concatenated;
+ * sizes[np]; output: merged trajectories as records concatenated + sizes */
+int ref_prolong_and_merge(int np, const int* sizes, const int* fxyz, int window, double radius, int* out_fxyz,
+                          int* out_sizes, int* n_out) {
+    return guarded([&] {
+        std::vector<Trajectory> parts(np);
+        int k = 0;
+        for (int p = 0; p < np; ++p) {
+            parts[p].id = p + 1;
+            for (int r = 0; r < sizes[p]; ++r, ++k) {
+                CellRecord c;
+                c.frame = fxyz[4 * k];
+                c.center = {fxyz[4 * k + 1], fxyz[4 * k + 2], fxyz[4 * k + 3]};
+                c.label = k + 1;
+                parts[p].records.push_back(c);
+            }
+        }
+        const std::vector<Trajectory> m = prolong_and_merge(parts, window, radius);
+        int q = 0;
+        for (std::size_t t = 0; t < m.size(); ++t) {
+            out_sizes[t] = int(m[t].records.size());
+            for (const CellRecord& c : m[t].records) {
+                out_fxyz[4 * q] = c.frame;
+                out_fxyz[4 * q + 1] = c.center[0];
+                out_fxyz[4 * q + 2] = c.center[1];
+                out_fxyz[4 * q + 3] = c.center[2];
+                ++q;
+            }
+        }
+        *n_out = int(m.size());
+    });
+}
+
 /* track(u): points (id, frame) ints + (x, y, z) doubles */
 int ref_track(const or_grid* g, const double* u, double level, int window, double radius, int* id_frame,
               double* xyz, int capacity, int* n) {
