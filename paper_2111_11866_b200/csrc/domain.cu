@@ -144,7 +144,7 @@ Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int 
     coef[1].alloc(L.rows * L.Wc * 8);
     SorArgs t{};
     pass_tiles(L, t);
-    const size_t nparts = std::max((size_t)t.tiles * kPassBY, tma_partials(L));
+    const size_t nparts = std::max({(size_t)t.tiles * kPassBY, tma_partials(L), resident_partials(L)});
     for (auto& pp : part) {
         pp[0].alloc(nparts);
         pp[1].alloc(nparts);

@@ -141,16 +141,79 @@ __global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(con
     pass_body<C, HEAT, false>(a, n);
 }
 
+// Resident pass: the pass's doxel slots of slice l, (k, j, q) with q fastest over
+// nq = (n1+1)/2, are cut into aligned chunks of 32; a warp computes one chunk per
+// lane set (lane = slot), kResidentBatch chunks with all their loads issued
+// first (the state lives in L2: latency, not bandwidth, bounds a pass), and
+// writes one partial per chunk at (slice, chunk) -- so per-slice sums do not
+// depend on the grid size.  All CTAs' warps share one grid-stride over chunks.
+#ifndef SSB_RES_BATCH
+#define SSB_RES_BATCH 1
+#endif
+#ifndef SSB_RES_MINB
+#define SSB_RES_MINB 2
+#endif
+constexpr int kResidentBatch = SSB_RES_BATCH;
+
+__host__ __device__ inline long long resident_chunks(const Layout& L) {
+    return ((long long)L.n2 * L.n3 * ((L.n1 + 1) / 2) + 31) / 32;
+}
+
+template <int C, bool HEAT>
+__device__ __forceinline__ void resident_body(const SorArgs& a, int n) {
+    const int bout = out_buf(n);
+    const int bin = in_buf(n);
+    const Layout& L = a.L;
+    const double* __restrict__ uc = a.U[bin][C];
+    const double* __restrict__ uo = C == 0 ? a.U[bin][1] : a.U[bout][0];
+    double* __restrict__ ucw = a.U[bout][C];
+    const float* __restrict__ cf = a.coef[C];
+    const double* __restrict__ rh = a.rhs[C];
+    const int nq = (L.n1 + 1) / 2;
+    const long long cps = resident_chunks(L);  // chunks per slice
+    const long long total = cps * L.n4;
+    const int lane = threadIdx.x;  // blockDim = (32, 8)
+    const long long w0 = (long long)blockIdx.x * blockDim.y + threadIdx.y;
+    const long long nw = (long long)gridDim.x * blockDim.y;
+    for (long long c0 = w0; c0 < total; c0 += nw * kResidentBatch) {
+        DoxelIn d[kResidentBatch];
+        bool ok[kResidentBatch];
+#pragma unroll
+        for (int b = 0; b < kResidentBatch; ++b) {  // all loads of the batch first
+            const long long c = c0 + b * nw;
+            ok[b] = false;
+            if (c >= total) continue;
+            const int l = (int)(c / cps) + 1;
+            const long long e = (c % cps) * 32 + lane;  // slot within the slice
+            const int q = (int)(e % nq);
+            const long long rr = e / nq;
+            const int j = (int)(rr % L.n2) + 1, k = (int)(rr / L.n2) + 1;
+            const int i = 1 + ((1 + j + k + l + L.lpar + C) & 1) + 2 * q;
+            ok[b] = k <= L.n3 && i <= L.n1;
+            if (ok[b]) load_doxel<C, HEAT, true>(a, cf, rh, uc, uo, i, j, k, l, d[b]);
+        }
+#pragma unroll
+        for (int b = 0; b < kResidentBatch; ++b) {
+            const long long c = c0 + b * nw;
+            if (c >= total) continue;  // warp-uniform
+            double r2 = ok[b] ? compute_doxel<C>(a, d[b], ucw) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
+            if (lane == 0) a.part[n & 3][C][c] = r2;
+        }
+    }
+}
+
 // Resident solve (grids whose working set fits in L2, e.g. BASELINE config 0):
 // ONE cooperative launch runs the whole loop -- red pass, grid barrier, slice
-// residuals, grid barrier, the decision (taken by every CTA from the same slice
-// values in the same order, so all agree; CTA 0 publishes it), black pass, grid
-// barrier -- instead of three launches per iteration.  Same tiles, partials,
-// per-doxel arithmetic and reductions as the LDG kernels: iterates, residuals and
-// iteration counts are those of kernel 0 bit for bit.  State arrays are read
-// through L2 (they change between passes of the launch).
+// residuals and black pass, grid barrier, the decision (taken by every CTA from
+// the same slice values in the same order, so all agree; CTA 0 publishes it) --
+// instead of three launches per iteration.  Same tiles, partials,
+// per-doxel arithmetic and slice reductions as the other kernels (partials per
+// 32-slot chunk, resident_body): iterates bit for bit, iteration counts equal.
+// State arrays are read through L2 (they change between passes of the launch).
 template <bool HEAT>
-__global__ void __launch_bounds__(kPassBX * kPassBY, 2) sor_resident(const SorArgs a) {
+__global__ void __launch_bounds__(kPassBX * kPassBY, SSB_RES_MINB) sor_resident(const SorArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double ws[32];
     __shared__ int stop;
@@ -162,14 +225,19 @@ __global__ void __launch_bounds__(kPassBX * kPassBY, 2) sor_resident(const SorAr
     const int fixed = st->fixed, max_iter = st->max_iter;
     grid.sync();  // everyone has read the state before CTA 0 rewrites it
     while (true) {
-        pass_body<0, HEAT, true>(a, n);
+        resident_body<0, HEAT>(a, n);
         grid.sync();
+        // slice residuals of state n-1, then (without waiting for the decision) the
+        // black pass of iteration n: if iterate n-1 turns out converged, black(n)
+        // only wrote buffer out(n), which nobody reads -- one wasted pass per
+        // solve instead of a grid barrier per iteration
         if (n >= 2)
             for (int l = blockIdx.x; l < a.L.n4; l += gridDim.x) {
                 const double v = slice_residual(a, n, l, ws, tid);
                 if (tid == 0) a.slice_res[l] = v;
                 asm volatile("bar.sync 1, 256;" ::: "memory");
             }
+        resident_body<1, HEAT>(a, n);
         grid.sync();
         if (tid == 0) {  // sor_decide_state, evaluated by every CTA
             int done = 0, conv = 0;
@@ -199,8 +267,6 @@ __global__ void __launch_bounds__(kPassBX * kPassBY, 2) sor_resident(const SorAr
         }
         __syncthreads();
         if (stop) break;
-        pass_body<1, HEAT, true>(a, n);
-        grid.sync();
         ++n;
     }
 }
@@ -339,6 +405,8 @@ bool resident_supported(const Layout& L) {
     return bytes <= 96.0 * 1024 * 1024 && L.glo && L.ghi;
 }
 
+size_t resident_partials(const Layout& L) { return (size_t)resident_chunks(L) * L.n4; }
+
 void launch_sor_resident(cudaStream_t s, const SorArgs& a, bool heat) {
     static int blocks = 0;
     if (!blocks) {
@@ -349,8 +417,10 @@ void launch_sor_resident(cudaStream_t s, const SorArgs& a, bool heat) {
         SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, sor_resident<true>, kPassBX * kPassBY, 0));
         blocks = sms * std::max(1, std::min(per0, per1));
     }
-    const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(a.tiles, blocks));
-    void* args[] = {const_cast<SorArgs*>(&a)};
+    SorArgs b = a;
+    b.bps = (int)resident_chunks(a.L);  // slice partials of resident_body
+    const unsigned grid = (unsigned)std::max(1LL, std::min<long long>((resident_chunks(a.L) * a.L.n4 + 7) / 8, blocks));
+    void* args[] = {&b};
     const void* fn = heat ? (const void*)sor_resident<true> : (const void*)sor_resident<false>;
     SSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kPassBX, kPassBY), args, 0, s));
     SSB_LAUNCHED();

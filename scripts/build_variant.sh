@@ -1,5 +1,6 @@
 #!/bin/bash
-# build_variant.sh NAME "-DFLAG=V ..." : libsubsurf_b200.so with sor_tma.cu rebuilt under
+# build_variant.sh NAME "-DFLAG=V ..." [source.cu] : libsubsurf_b200.so with one source
+# (default sor_tma.cu) rebuilt under
 # extra defines, written to variants/NAME.so (git-ignored; travels with gpurun).
 # Select it with SUBSURF_B200_LIB=variants/NAME.so.
 set -e
@@ -8,8 +9,10 @@ C=$ROOT/paper_2111_11866_b200/csrc
 make -s -C $C >/dev/null
 mkdir -p $ROOT/variants/$1
 ARCH="-gencode arch=compute_100a,code=sm_100a"
+SRC=${3:-sor_tma.cu}
+OBJ=${SRC%.cu}.o
 nvcc $ARCH -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC,-fvisibility=hidden -I$ROOT/include $2 \
-    -c -o $ROOT/variants/$1/sor_tma.o $C/sor_tma.cu
-OBJS=$(ls $C/build/*.o | grep -v sor_tma.o)
-nvcc $ARCH -shared -o $ROOT/variants/$1.so $OBJS $ROOT/variants/$1/sor_tma.o -Xlinker -z,defs -lcudart_static -lrt -lpthread -ldl
+    -c -o $ROOT/variants/$1/$OBJ $C/$SRC
+OBJS=$(ls $C/build/*.o | grep -v "/$OBJ")
+nvcc $ARCH -shared -o $ROOT/variants/$1.so $OBJS $ROOT/variants/$1/$OBJ -Xlinker -z,defs -lcudart_static -lrt -lpthread -ldl
 echo variants/$1.so
