@@ -150,8 +150,6 @@ Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int 
         pp[1].alloc(nparts);
     }
     slice_res.alloc(chunk);
-    slice_cnt.alloc(chunk);
-    SSB_CUDA(cudaMemsetAsync(slice_cnt.p, 0, slice_cnt.n * sizeof(unsigned), stream));
     norm_loc.alloc(chunk);
     norm_part.alloc((size_t)chunk * kNormChunks);
     if (world > 1) {
@@ -317,7 +315,6 @@ SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool he
     a.l2hint = pass_l2hint();
     a.order = pass_order();
     a.fuse_final = a.tma && world == 1 && !a.wave && pass_fuse_final() && tma_fuse_ok(L) ? 1 : 0;
-    a.slice_cnt = slice_cnt.p;
     if (a.tma)
         tma_pass_tiles(L, a);
     else
@@ -655,7 +652,10 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
         sync();
         const int bodies = wave ? st_host->iterations / WI + 1 : st_host->iterations + 1;
         const int U = graph_unroll();
-        count_launch(3ull * U * (unsigned long long)((std::min(limit, bodies) + U - 1) / U));
+        // kernels per loop body: red, finalize, black (finalize folded into black: 2;
+        // wavefront: the wave kernel + one finalize per iteration it covers)
+        const unsigned long long per = wave ? 1ull + WI : (a[0].fuse_final ? 2ull : 3ull);
+        count_launch(per * U * (unsigned long long)((std::min(limit, bodies) + U - 1) / U));
     } else {
         // host-driven: chunks of loop bodies with one chunk of look-ahead; every
         // rank runs the same schedule (the decision is identical everywhere)

@@ -105,7 +105,6 @@ struct Slab {
     bool have_G = false;
     Dev<double> part[4][2];
     Dev<double> slice_res;   // chunk entries (zero padded)
-    Dev<unsigned> slice_cnt; // red-pass items completed per slice (fused finalize)
     Dev<double> all_slices;  // world * chunk (gathered), unused when world == 1
     Dev<double> norm_loc, norm_all;
     Dev<double> norm_part;   // chunk * kNormChunks partials of launch_norm_slices

@@ -39,8 +39,7 @@ struct SorArgs {
     double* slice_res;      // per-slice residual of the owned slices (solver.cpp:195-199)
     const double* all_slices;  // residuals of all n4g slices in global order (== slice_res on 1 slab)
     int inline_decide;      // single slab: finalize also decides
-    int fuse_final;         // TMA single slab: the red pass sums slices and decides in its tail
-    unsigned* slice_cnt;    // per owned slice: red-pass items completed (fuse_final)
+    int fuse_final;         // TMA single slab: the black pass sums slices and decides in its head
     SorState* st;
     double omega, keep;
     double hc[4];           // heat stencil constants float(-dt/h_a^2) (solver.cpp:100-110)

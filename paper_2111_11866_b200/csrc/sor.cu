@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kPassBX * kPassBY, SSB_RES_MINB) sor_resident(
 // grid = local n4 blocks (one per owned slice), 256 threads: slice_res[l] via
 // slice_residual (sor_final.cuh).  With inline_decide (single slab) the last
 // block also takes the decision; otherwise the slices are all-gathered first
-// (sor_decide).  The TMA red pass does the same in its tail (fuse_final).
+// (sor_decide).  The TMA black pass does the same in its head (fuse_final).
 __global__ void __launch_bounds__(256) sor_finalize(const SorArgs a) {
     __shared__ double ws[32];
     SorState* st = a.st;
@@ -444,7 +444,7 @@ void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* e
     if (ev) SSB_CUDA(cudaEventRecord(ev[0], s));
     launch_sor_pass(s, a, 0, heat);
     if (ev) SSB_CUDA(cudaEventRecord(ev[1], s));
-    if (!a.fuse_final) {  // else the red pass took the decision in its tail
+    if (!a.fuse_final) {  // else the black pass takes the decision in its head
         sor_finalize<<<a.L.n4, 256, 0, s>>>(a);
         SSB_LAUNCHED();
     }

@@ -1,6 +1,7 @@
 // sor_final.cuh -- the end-of-red-pass bookkeeping of one SOR iteration
-// (solver.cpp:195-205), shared by the stand-alone finalize kernel (sor.cu) and
-// the TMA red pass that performs it in its tail (sor_tma.cu).
+// (solver.cpp:195-205), shared by the stand-alone finalize kernel (sor.cu), the
+// TMA black pass that performs it in its head (sor_tma.cu) and the resident
+// solve (sor.cu).
 //
 // slice_res[l] = (sum of the black(n-1) partials of slice l) + (sum of the
 // red(n) partials of slice l), each summed by 256 threads in one fixed order;
@@ -72,44 +73,28 @@ __device__ __forceinline__ void sor_decide_state(const SorArgs& a, SorState* st,
     if (a.use_cond) cudaGraphSetConditional(a.cond, st->done ? 0u : 1u);
 }
 
-// Red pass tail, run once by the 256 consumer threads of each CTA after all of
-// its work items (t = blockIdx.x + k * gridDim.x) have written their partials: one atomic per item on its
-// slice's counter; the CTA that completes a slice sums it, the CTA that
-// completes the last slice decides.
-// slice_of(t) = the launch-local item's slice; done_slices holds kMaxDoneSlices
-// entries (the host enables the fusion only when no CTA has more items).
-constexpr int kMaxDoneSlices = 256;
-template <typename SliceOf>
-__device__ __forceinline__ void red_pass_done(const SorArgs& a, int n, int items_per_slice, long long n_items,
-                                              SliceOf slice_of, double* ws, int* done_slices, int* n_done,
-                                              int tid) {
-    if (tid == 0) *n_done = 0;
-    asm volatile("bar.sync 1, 256;" ::: "memory");  // every partial of this CTA is written
-    const long long mine = n_items > blockIdx.x ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    __threadfence();
-    for (long long k = tid; k < mine; k += 256) {
-        const long long t = blockIdx.x + k * gridDim.x;
-        const int l = slice_of(t);
-        if (atomicAdd(a.slice_cnt + (l - 1), 1u) == (unsigned)items_per_slice - 1)
-            done_slices[atomicAdd(n_done, 1)] = l;
-    }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    const int nd = *n_done;
-    if (nd == 0) return;
-    __threadfence();
-    for (int q = 0; q < nd; ++q) {
-        const int l = done_slices[q];
+// Finalize in the head of the black pass (fuse_final): CTAs l < n4 (grid-stride)
+// compute slice l's residual of state n-1 -- red(n) is complete, the black pass
+// runs after it -- and the CTA that completes the last slice decides.  The
+// black pass of iteration n runs whatever the decision (if iterate n-1 has
+// converged it only writes buffer out(n), which nobody reads).  Called by the
+// 256 consumer threads of a CTA.
+__device__ __forceinline__ void black_head_finalize(const SorArgs& a, int n, double* ws, int* last, int tid) {
+    int mine = 0;
+    for (int l = blockIdx.x; l < a.L.n4; l += gridDim.x) {
         if (n >= 2) {
-            const double v = slice_residual(a, n, l - 1, ws, tid);
-            if (tid == 0) a.slice_res[l - 1] = v;
+            const double v = slice_residual(a, n, l, ws, tid);
+            if (tid == 0) a.slice_res[l] = v;
         }
-        if (tid == 0) a.slice_cnt[l - 1] = 0;
+        ++mine;
         asm volatile("bar.sync 1, 256;" ::: "memory");
     }
+    if (!mine) return;
     if (tid == 0) {
         __threadfence();
         SorState* st = a.st;
-        if (atomicAdd(&st->counter, (unsigned)nd) + nd == (unsigned)a.L.n4) {
+        *last = atomicAdd(&st->counter, (unsigned)mine) + mine == (unsigned)a.L.n4;
+        if (*last) {
             __threadfence();
             st->counter = 0;
             sor_decide_state(a, st, n);

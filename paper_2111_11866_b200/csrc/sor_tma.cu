@@ -392,10 +392,15 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) Bars bars;
     __shared__ double ws[32];
-    __shared__ int done_slices[kMaxDoneSlices], n_done;
-    const SorState* st = a.st;
+    __shared__ int last;
+    SorState* st = a.st;
     if (*(volatile const int*)&st->done) return;
     const int n = C == 0 ? *(volatile const int*)&st->n_red : *(volatile const int*)&st->n_black;
+    // fuse_final: no finalize launch between the passes.  The red pass hands its
+    // n to the black pass (n_black: black CTAs read it, nobody else writes it
+    // during the red pass); the black pass's first CTAs take the finalize's
+    // place before their own items (black_head_finalize).
+    if (C == 0 && a.fuse_final && blockIdx.x == 0 && threadIdx.x == 0) st->n_black = n;
     const int bout = out_buf(n);
     const int bin = in_buf(n);
     const Layout& L = a.L;
@@ -426,6 +431,7 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
         }
         return;
     }
+    if (C == 1 && a.fuse_final) black_head_finalize(a, n, ws, &last, threadIdx.x);
     uint32_t ms = 0, mph = 0, s0 = 0, ph0 = 0;
     for (long long tt = blockIdx.x; tt < n_items; tt += gridDim.x) {
         Item it;
@@ -434,16 +440,7 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
                                                 ms, mph, s0, ph0, it, ucw, warp, lane, pol.ustore);
         if (lane == 0) a.part[n & 3][C][t * kWarps + warp] = r2;
     }
-    if constexpr (C == 0)
-        if (a.fuse_final)
-            red_pass_done(
-                a, n, G.njg * G.nkc, n_items,
-                [&](long long t) {
-                    Item it;
-                    decode_item(L, G, a.order, a.l_lo, nl, t, it);
-                    return it.l;
-                },
-                ws, done_slices, &n_done, threadIdx.x);
+
 }
 
 // ---------------------------------------------------------------------------
@@ -620,7 +617,7 @@ int pass_snake() {
 int pass_fuse_final() {
     static const int v = [] {
         const char* e = std::getenv("SSB_FUSE_FINAL");
-        return e ? std::atoi(e) : 0;  // measured: slower on config 1 (tail), see DESIGN.md
+        return e ? std::atoi(e) : 1;
     }();
     return v;
 }
@@ -653,12 +650,7 @@ void tma_pass_tiles(const Layout& L, SorArgs& a) {
     a.tk = 1;
 }
 
-bool tma_fuse_ok(const Layout& L) {
-    // the red pass tail records the slices a CTA completes in kMaxDoneSlices entries
-    const Geo G = make_geo(L);
-    const long long blocks = tma_blocks((const void*)sor_pass_tma<0, false>, G.smem);
-    return (G.items + blocks - 1) / blocks <= kMaxDoneSlices;
-}
+bool tma_fuse_ok(const Layout& L) { return L.glo && L.ghi; }  // single slab
 
 size_t tma_partials(const Layout& L) { return (size_t)make_geo(L).items * kWarps; }
 
