@@ -600,8 +600,8 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
                        int* result) {
     std::vector<SorArgs> a;
     // resident loop: single slab whose working set fits L2 (auto) or on request
-    const bool resident = single() && (kernel == 3 || (kernel == 4 && resident_supported(sp[0]->L)));
-    const int kern = resident ? 0 : (kernel == 4 || kernel == 3 ? 1 : kernel);  // LDG tiles for resident
+    bool resident = single() && (kernel == 3 || (kernel == 4 && resident_supported(sp[0]->L)));
+    int kern = resident ? 0 : (kernel == 4 || kernel == 3 ? 1 : kernel);  // LDG tiles for resident
     solve_count = (solve_count + 1) & 0x3fff;
     const int epoch_base = (solve_count + 1) << 16;  // differs from the previous solve's
     for (size_t s = 0; s < sp.size(); ++s) {
@@ -610,14 +610,20 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
         launch_sor_init(stream, x.st.p, tol_abs, ns, g.n4, rel, max_iter, fixed ? 1 : 0, epoch_base);
         a.push_back(x.sor_args(B[s].data(), rhs[s], heat, omega, hc, world, kern));
     }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (resident) {
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (profiling) {
             e0 = pool_event(0);
             e1 = pool_event(1);
             SSB_CUDA(cudaEventRecord(e0, stream));
         }
-        launch_sor_resident(stream, a[0], heat);
+        if (!launch_sor_resident(stream, a[0], heat)) {  // cannot be co-resident: pass kernels
+            resident = false;
+            kern = 1;
+            a[0] = sp[0]->sor_args(B[0].data(), rhs[0], heat, omega, hc, world, kern);
+        }
+    }
+    if (resident) {
         if (profiling) SSB_CUDA(cudaEventRecord(e1, stream));
         SSB_CUDA(cudaMemcpyAsync(st_host, sp[0]->st.p, sizeof(SorState), cudaMemcpyDeviceToHost, stream));
         sync();

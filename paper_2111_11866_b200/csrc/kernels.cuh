@@ -99,7 +99,8 @@ void launch_sor_pass_range(cudaStream_t s, const SorArgs& a, int colour, bool he
 void launch_sor_finalize(cudaStream_t s, const SorArgs& a);
 // whole solve in one cooperative launch (LDG tiles, state in L2); single slab
 bool resident_supported(const Layout& L);
-void launch_sor_resident(cudaStream_t s, const SorArgs& a, bool heat);
+// false (nothing launched) when the grid cannot be co-resident: use the pass kernels
+bool launch_sor_resident(cudaStream_t s, const SorArgs& a, bool heat);
 size_t resident_partials(const Layout& L);  // partial slots per colour of the resident passes
 void launch_sor_decide(cudaStream_t s, const SorArgs& a);
 

@@ -407,7 +407,7 @@ bool resident_supported(const Layout& L) {
 
 size_t resident_partials(const Layout& L) { return (size_t)resident_chunks(L) * L.n4; }
 
-void launch_sor_resident(cudaStream_t s, const SorArgs& a, bool heat) {
+bool launch_sor_resident(cudaStream_t s, const SorArgs& a, bool heat) {
     static int blocks = 0;
     if (!blocks) {
         int dev = 0, sms = 0, per0 = 0, per1 = 0;
@@ -422,8 +422,14 @@ void launch_sor_resident(cudaStream_t s, const SorArgs& a, bool heat) {
     const unsigned grid = (unsigned)std::max(1LL, std::min<long long>((resident_chunks(a.L) * a.L.n4 + 7) / 8, blocks));
     void* args[] = {&b};
     const void* fn = heat ? (const void*)sor_resident<true> : (const void*)sor_resident<false>;
-    SSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kPassBX, kPassBY), args, 0, s));
+    const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kPassBX, kPassBY), args, 0, s);
+    if (e == cudaErrorCooperativeLaunchTooLarge) {  // fewer SMs available than at startup (MPS, ...)
+        (void)cudaGetLastError();
+        return false;
+    }
+    SSB_CUDA(e);
     SSB_LAUNCHED();
+    return true;
 }
 
 void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* ev) {
