@@ -109,7 +109,10 @@ __host__ __device__ inline TileGrid tile_grid(const Layout& L) {
 }
 
 template <int C, bool EXPORT, bool POW2>
-__global__ void __launch_bounds__(kPassBX * kPassBY) assemble_kernel(const AsmArgs a) {
+#ifndef SSB_ASM_MINB
+#define SSB_ASM_MINB 3  // 3 CTAs/SM: 449 vs 464 us per colour on config 1 (fp64-latency bound)
+#endif
+__global__ void __launch_bounds__(kPassBX * kPassBY, SSB_ASM_MINB) assemble_kernel(const AsmArgs a) {
     const Layout& L = a.L;
     const TileGrid tg = tile_grid(L);
     for (long long t = blockIdx.x; t < tg.tiles; t += gridDim.x) {

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -39,7 +40,14 @@ static void require_device() {
                                      "); this library has no CPU fallback");
 }
 
+// The per-call entry points share one cached Domain: a call holds its lock from
+// cached() to the end of guard(), so concurrent per-call use from several host
+// threads is serialised (sessions are independent objects and are not locked).
+static std::mutex g_cached_mu;
+static thread_local std::unique_lock<std::mutex> t_cached_lock;
+
 static Domain& cached(const ss_grid& g) {
+    if (!t_cached_lock.owns_lock()) t_cached_lock = std::unique_lock<std::mutex>(g_cached_mu);
     require_device();
     if (!g_cached || !same_grid(g_cached->g, g)) {
         g_cached.reset();
@@ -53,6 +61,11 @@ static Domain& cached(const ss_grid& g) {
 
 template <class F>
 static ss_status guard(F&& fn) {
+    struct Release {
+        ~Release() {
+            if (t_cached_lock.owns_lock()) t_cached_lock.unlock();
+        }
+    } release;
     try {
         fn();
         t_err.clear();
