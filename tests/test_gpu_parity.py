@@ -299,3 +299,33 @@ def test_grid_helpers(gpu, oracle):
     assert np.all(d[ghost] == 0.25) and np.array_equal(d[~ghost], f[~ghost])
     lo, hi = gpu.interior_minmax(f, g)
     assert lo == f[g.interior].min() and hi == f[g.interior].max()
+
+
+def test_per_call_api_thread_safe(gpu):
+    """The per-call entry points share one cached device context: concurrent calls from
+    several host threads (ctypes drops the GIL) on different grids give the serial results."""
+    import threading
+    cases = []
+    for dims in [(6, 5, 4, 5), (9, 7, 3, 4)]:
+        g = gpu.Grid.make(dims, 0.25)
+        u = cs.rand_field(dims, sum(dims))
+        G = cs.rand_G(dims, 3 + sum(dims))
+        cases.append((g, u, G, gpu.assemble_step(u, G, 0.1, 1e-3, g)))
+    errors = []
+
+    def work(k):
+        try:
+            for r in range(4):
+                g, u, G, want = cases[(k + r) % 2]
+                got = gpu.assemble_step(u, G, 0.1, 1e-3, g)
+                for f in ("offdiag", "diag", "abar"):
+                    assert np.array_equal(getattr(got, f), getattr(want, f))
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
