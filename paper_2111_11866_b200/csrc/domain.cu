@@ -315,6 +315,7 @@ SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool he
     a.l2hint = pass_l2hint();
     a.order = pass_order();
     a.fuse_final = a.tma && world == 1 && !a.wave && pass_fuse_final() && tma_fuse_ok(L) ? 1 : 0;
+    // halo push pointers are filled in by the Domain (it knows the neighbours)
     if (a.tma)
         tma_pass_tiles(L, a);
     else
@@ -497,6 +498,15 @@ cudaEvent_t Domain::pool_event(size_t idx) {
     return ev_pool[idx];
 }
 
+// halo push for in-process slab groups (env SSB_PUSH, default on)
+bool halo_push() {
+    static const int v = [] {
+        const char* e = std::getenv("SSB_PUSH");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 // loop bodies per conditional-node iteration (env SSB_UNROLL)
 int graph_unroll() {
     static const int v = [] {
@@ -566,7 +576,12 @@ void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>
     for (const Triple& t : B) F.push_back(t[bout]);
     // boundary slices first, their exchange on the comm stream overlapped with
     // the interior slices (the paper overlaps Isend/Irecv the same way)
+    const bool push = a[0].push_lo[0][0] != nullptr || a[0].push_hi[0][0] != nullptr;
     auto pass = [&](int colour) {
+        if (push) {  // the pass kernels write the neighbours' halo planes themselves
+            for (const SorArgs& x : a) launch_sor_pass(stream, x, colour, heat);
+            return;
+        }
         for (const SorArgs& x : a) {
             const int n4 = x.L.n4;
             launch_sor_pass_range(stream, x, colour, heat, 1, 1);
@@ -609,6 +624,20 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
         const double* ns = use_norm ? (world == 1 ? x.norm_loc.p : x.norm_all.p) : nullptr;
         launch_sor_init(stream, x.st.p, tol_abs, ns, g.n4, rel, max_iter, fixed ? 1 : 0, epoch_base);
         a.push_back(x.sor_args(B[s].data(), rhs[s], heat, omega, hc, world, kern));
+    }
+    // in-process slab group with the TMA pass: neighbours' halo planes are written by
+    // the pass kernels themselves (no exchange copies between the passes)
+    if (!distributed && sp.size() > 1 && a[0].tma && !a[0].wave && halo_push()) {
+        const long long P1 = sp[0]->L.plane();
+        for (size_t s = 0; s < sp.size(); ++s) {
+            for (int b = 0; b < kStateBuffers; ++b)
+                for (int c = 0; c < 2; ++c) {
+                    a[s].push_lo[b][c] = s > 0 ? B[s - 1][b].c[c] : nullptr;
+                    a[s].push_hi[b][c] = s + 1 < sp.size() ? B[s + 1][b].c[c] : nullptr;
+                }
+            a[s].push_lo_off = s > 0 ? (long long)sp[s - 1]->L.n4 * P1 : 0;  // my plane 1 -> its plane n4'+1
+            a[s].push_hi_off = -(long long)sp[s]->L.n4 * P1;                 // my plane n4 -> its plane 0
+        }
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (resident) {

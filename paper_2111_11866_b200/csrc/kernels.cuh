@@ -40,6 +40,13 @@ struct SorArgs {
     const double* all_slices;  // residuals of all n4g slices in global order (== slice_res on 1 slab)
     int inline_decide;      // single slab: finalize also decides
     int fuse_final;         // TMA single slab: the black pass sums slices and decides in its head
+    // halo push (slab groups): the TMA pass stores the values it computes on its first /
+    // last owned plane ALSO into the low / high neighbour's halo plane -- the exchange
+    // happens inside the compute kernel.  [buffer][colour] neighbour arrays (null: none)
+    // and the index offset from this slab's packed index to the neighbour's.
+    double* push_lo[kStateBuffers][2];
+    double* push_hi[kStateBuffers][2];
+    long long push_lo_off, push_hi_off;
     SorState* st;
     double omega, keep;
     double hc[4];           // heat stencil constants float(-dt/h_a^2) (solver.cpp:100-110)

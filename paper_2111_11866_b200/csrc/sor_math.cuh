@@ -26,9 +26,10 @@ __device__ __forceinline__ void store_u(double* p, double v, uint64_t pol) {
 // feed both the update (acc -= p_f) and the red residual (res += p_f) -- the
 // reference evaluates the same products in both places -- so the three
 // dependency chains (diag sum, acc, residual) can overlap.
-template <int C, bool HINT = false>
+template <int C, bool HINT = false, bool MIRROR = false>
 __device__ __forceinline__ double compute_doxel(const SorArgs& a, const DoxelIn& d,
-                                                double* __restrict__ ucw, uint64_t pol = 0) {
+                                                double* __restrict__ ucw, uint64_t pol = 0,
+                                                double* mir_lo = nullptr, double* mir_hi = nullptr) {
     const double c0 = (double)d.c[0], c1 = (double)d.c[1], c2 = (double)d.c[2];
     const double c3 = (double)d.c[3], c4 = (double)d.c[4], c5 = (double)d.c[5];
     const double c6 = (double)d.c[6], c7 = (double)d.c[7];
@@ -60,6 +61,10 @@ __device__ __forceinline__ double compute_doxel(const SorArgs& a, const DoxelIn&
             store_u(ucw + d.p, unew, pol);
         else
             ucw[d.p] = unew;
+        if constexpr (MIRROR) {  // halo push (uniform per work item)
+            if (mir_lo) mir_lo[d.p] = unew;
+            if (mir_hi) mir_hi[d.p] = unew;
+        }
         return res * res;
     } else {
         const double ubar = acc / dg;
@@ -68,6 +73,10 @@ __device__ __forceinline__ double compute_doxel(const SorArgs& a, const DoxelIn&
             store_u(ucw + d.p, unew, pol);
         else
             ucw[d.p] = unew;
+        if constexpr (MIRROR) {
+            if (mir_lo) mir_lo[d.p] = unew;
+            if (mir_hi) mir_hi[d.p] = unew;
+        }
         const double res = dg * (unew - ubar);
         return res * res;
     }

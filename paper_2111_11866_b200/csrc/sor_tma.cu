@@ -259,13 +259,14 @@ __device__ __forceinline__ void produce_uk(const Layout& L, const Geo& G, unsign
 // q, and only par flips from plane to plane.  Returns the warp's sum of squared
 // residuals.  (ms, mph) / (s0, ph0) are the main / UK ring positions of the
 // item's first stages and are advanced past the item.
-template <int C, bool HEAT>
+template <int C, bool HEAT, bool PUSH = false>
 __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L, const Geo& G,
                                                unsigned char* smem, uint64_t* fullM, uint64_t* emptyM,
                                                uint64_t* fullK, uint64_t* emptyK, uint32_t& ms,
                                                uint32_t& mph, uint32_t& s0, uint32_t& ph0, const Item& it,
                                                double* __restrict__ ucw, int warp, int lane,
-                                               uint64_t pol_store) {
+                                               uint64_t pol_store, double* push_lo = nullptr,
+                                               double* push_hi = nullptr) {
     const int W = L.W;
     const int r = warp / G.wpr;
     const int j = it.j0 + r;
@@ -277,6 +278,9 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
     // shared-memory element offsets of row r: R-row blocks / the (R+2)-row UK block
     const int o_row = r * W, o_uk = (r + 1) * W;
     double* wrow = ucw + L.row(j, it.k0, it.l) * (long long)W;  // this row at plane k0
+    // halo push: the same row in the neighbours' arrays (first / last owned plane only)
+    double* wlo = PUSH && push_lo ? push_lo + (wrow - ucw) + a.push_lo_off : nullptr;
+    double* whi = PUSH && push_hi ? push_hi + (wrow - ucw) + a.push_hi_off : nullptr;
     const long long wstep = (long long)L.jMax * W;
     const unsigned char* ukr = smem + G.off_ukring;
     double r2 = 0.0;
@@ -333,7 +337,7 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
                 d.nb[7] = ulp[m];
                 d.p = m;
 #ifndef SSB_NOCOMPUTE
-                r2 += compute_doxel<C, true>(a, d, wrow, pol_store);
+                r2 += compute_doxel<C, true, PUSH>(a, d, wrow, pol_store, wlo, whi);
 #else  // data-movement floor experiment: touch the operands, store u0
                 double t = d.rhs + d.u0 + (double)d.c[0] + (double)d.c[7];
                 for (int f = 0; f < 8; ++f) t += d.nb[f];
@@ -353,6 +357,10 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
         pc = pp;
         par ^= 1;
         wrow += wstep;
+        if constexpr (PUSH) {
+            if (wlo) wlo += wstep;
+            if (whi) whi += wstep;
+        }
     }
     // the last two UK stages of the item (planes k1, k1+1)
     __syncwarp();
@@ -387,7 +395,7 @@ __device__ __forceinline__ void init_barriers(Bars& b) {
     __syncthreads();
 }
 
-template <int C, bool HEAT>
+template <int C, bool HEAT, bool PUSH>
 __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) Bars bars;
@@ -436,8 +444,10 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
     for (long long tt = blockIdx.x; tt < n_items; tt += gridDim.x) {
         Item it;
         const long long t = decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - tt : tt, it);
-        const double r2 = consume_item<C, HEAT>(a, L, G, smem, bars.fullM, bars.emptyM, bars.fullK, bars.emptyK,
-                                                ms, mph, s0, ph0, it, ucw, warp, lane, pol.ustore);
+        double* plo = PUSH && it.l == 1 ? a.push_lo[bout][C] : nullptr;
+        double* phi = PUSH && it.l == L.n4 ? a.push_hi[bout][C] : nullptr;
+        const double r2 = consume_item<C, HEAT, PUSH>(a, L, G, smem, bars.fullM, bars.emptyM, bars.fullK, bars.emptyK,
+                                                ms, mph, s0, ph0, it, ucw, warp, lane, pol.ustore, plo, phi);
         if (lane == 0) a.part[n & 3][C][t * kWarps + warp] = r2;
     }
 
@@ -570,11 +580,11 @@ __global__ void __launch_bounds__(kThreads, 2) sor_wave_tma(const SorArgs a) {
     }
 }
 
-template <int C, bool HEAT>
+template <int C, bool HEAT, bool PUSH>
 void configure() {
     static bool done = false;
     if (!done) {
-        SSB_CUDA(cudaFuncSetAttribute(sor_pass_tma<C, HEAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SSB_CUDA(cudaFuncSetAttribute(sor_pass_tma<C, HEAT, PUSH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       96 * 1024 + 64 * 1024));
         done = true;
     }
@@ -673,7 +683,7 @@ void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat) {
     const size_t smem = (size_t)G.smem;
     configure_wave<false>();
     configure_wave<true>();
-    configure<0, false>();
+    configure<0, false, false>();
     static size_t last_smem = 0;
     static int blocks = 0;
     if (smem != last_smem) {
@@ -694,28 +704,33 @@ void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat) {
 void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat) {
     const Geo G = make_geo(a.L);
     const size_t smem = (size_t)G.smem;
-    configure<0, false>();
-    configure<1, false>();
-    configure<0, true>();
-    configure<1, true>();
     static size_t last_smem = 0;
     static int blocks = 0;
     if (smem != last_smem) {
-        blocks = tma_blocks((const void*)sor_pass_tma<0, false>, smem);
+        configure<0, false, false>();
+        configure<1, false, false>();
+        configure<0, true, false>();
+        configure<1, true, false>();
+        configure<0, false, true>();
+        configure<1, false, true>();
+        configure<0, true, true>();
+        configure<1, true, true>();
+        blocks = tma_blocks((const void*)sor_pass_tma<0, false, false>, smem);
         last_smem = smem;
     }
     const long long items = (long long)G.njg * G.nkc * (a.l_hi - a.l_lo + 1);
     const unsigned grid = (unsigned)std::min<long long>(items, blocks);
-    if (colour == 0) {
-        if (heat)
-            sor_pass_tma<0, true><<<grid, kThreads, smem, s>>>(a);
-        else
-            sor_pass_tma<0, false><<<grid, kThreads, smem, s>>>(a);
-    } else {
-        if (heat)
-            sor_pass_tma<1, true><<<grid, kThreads, smem, s>>>(a);
-        else
-            sor_pass_tma<1, false><<<grid, kThreads, smem, s>>>(a);
+    const bool push = a.push_lo[0][0] != nullptr || a.push_hi[0][0] != nullptr;
+    const int v = (colour & 1) | (heat ? 2 : 0) | (push ? 4 : 0);
+    switch (v) {
+        case 0: sor_pass_tma<0, false, false><<<grid, kThreads, smem, s>>>(a); break;
+        case 1: sor_pass_tma<1, false, false><<<grid, kThreads, smem, s>>>(a); break;
+        case 2: sor_pass_tma<0, true, false><<<grid, kThreads, smem, s>>>(a); break;
+        case 3: sor_pass_tma<1, true, false><<<grid, kThreads, smem, s>>>(a); break;
+        case 4: sor_pass_tma<0, false, true><<<grid, kThreads, smem, s>>>(a); break;
+        case 5: sor_pass_tma<1, false, true><<<grid, kThreads, smem, s>>>(a); break;
+        case 6: sor_pass_tma<0, true, true><<<grid, kThreads, smem, s>>>(a); break;
+        default: sor_pass_tma<1, true, true><<<grid, kThreads, smem, s>>>(a); break;
     }
     SSB_LAUNCHED();
 }
