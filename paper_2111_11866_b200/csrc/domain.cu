@@ -407,6 +407,8 @@ Domain::Domain(const ss_grid& grid, int dev, int rank, int w, const unsigned cha
     slabs.emplace_back(new Slab(g, rank * chunk, n4l, rank, chunk, world, stream));
     sp.push_back(slabs.back().get());
     tr = make_nccl_transport(uid, rank, w);
+    const char* e = std::getenv("SSB_P2P");
+    if (w > 1 && e && std::atoi(e) != 0) setup_peer_links(*tr, *sp[0], rank, w, chunk, g.n4, peers);
     sync();
 }
 
@@ -578,6 +580,13 @@ void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>
     // the interior slices (the paper overlaps Isend/Irecv the same way)
     const bool push = a[0].push_lo[0][0] != nullptr || a[0].push_hi[0][0] != nullptr;
     auto pass = [&](int colour) {
+        if (push && distributed) {  // NVLink: wait for the neighbours' previous pass, push, signal
+            const unsigned long long k = ++peers.count;
+            launch_p2p_wait(stream, peers, k - 1);
+            launch_sor_pass(stream, a[0], colour, heat);
+            launch_p2p_signal(stream, peers, k);
+            return;
+        }
         if (push) {  // the pass kernels write the neighbours' halo planes themselves
             for (const SorArgs& x : a) launch_sor_pass(stream, x, colour, heat);
             return;
@@ -627,6 +636,30 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
     }
     // in-process slab group with the TMA pass: neighbours' halo planes are written by
     // the pass kernels themselves (no exchange copies between the passes)
+    if (distributed && peers.on && a[0].tma && !a[0].wave) {
+        // ranks: the neighbours' arrays of the same buffer roles, mapped with CUDA IPC
+        Slab& x = *sp[0];
+        const long long P1 = x.L.plane();
+        bool mapped = true;
+        for (int b = 0; b < kStateBuffers && mapped; ++b)
+            for (int c = 0; c < 2 && mapped; ++c) {
+                int k = -1;  // which of this slab's state arrays is role b
+                for (int q = 0; q < kStateBuffers; ++q)
+                    if (x.S[q].c[c].p == B[0][b].c[c]) k = q;
+                mapped = k >= 0;
+                if (mapped) {
+                    a[0].push_lo[b][c] = peers.S[0][k][c];
+                    a[0].push_hi[b][c] = peers.S[1][k][c];
+                }
+            }
+        if (mapped) {
+            a[0].push_lo_off = (long long)peers.n4[0] * P1;
+            a[0].push_hi_off = -(long long)x.L.n4 * P1;
+        } else {
+            for (int b = 0; b < kStateBuffers; ++b)
+                for (int c = 0; c < 2; ++c) a[0].push_lo[b][c] = a[0].push_hi[b][c] = nullptr;
+        }
+    }
     if (!distributed && sp.size() > 1 && a[0].tma && !a[0].wave && halo_push()) {
         const long long P1 = sp[0]->L.plane();
         for (size_t s = 0; s < sp.size(); ++s) {

@@ -163,6 +163,24 @@ struct LocalTransport : Transport {
 };
 
 std::unique_ptr<Transport> make_nccl_transport(const unsigned char* uid, int rank, int world);
+
+// NVLink peer links of one rank (opt-in, SSB_P2P=1): the l-neighbours' state
+// arrays and flag words mapped into this process with CUDA IPC, so the TMA pass
+// pushes its boundary planes straight into the neighbours' halo planes over
+// NVLink (no NCCL exchange), and per-pass completion counters order the passes.
+struct PeerLinks {
+    bool on = false;
+    double* S[2][kStateBuffers][2] = {};    // [0 = low neighbour, 1 = high][buffer][colour]
+    unsigned long long* peer_flag[2] = {};  // the word this rank writes in the low / high neighbour
+    Dev<unsigned long long> my_flags;       // [0] written by the low neighbour, [1] by the high one
+    unsigned long long count = 0;           // passes completed by this rank (identical on every rank)
+    int n4[2] = {0, 0};                     // owned slices of the low / high neighbour
+};
+// exchanges IPC handles of the slab's state arrays over the transport's NCCL
+// communicator and opens the neighbours' (transport_nccl.cu)
+void setup_peer_links(Transport& tr, Slab& s, int rank, int world, int chunk, int n4_global, PeerLinks& pl);
+void launch_p2p_wait(cudaStream_t st, const PeerLinks& pl, unsigned long long target);
+void launch_p2p_signal(cudaStream_t st, const PeerLinks& pl, unsigned long long value);
 void nccl_unique_id(unsigned char out[128]);
 
 // ------------------------------------------------------------------ domain
@@ -172,6 +190,7 @@ struct Domain {
     int chunk = 0;      // ceil(n4 / world)
     int device = 0;
     bool distributed = false;  // NCCL: slabs.size() == 1 < world
+    PeerLinks peers;           // NVLink halo push between ranks (SSB_P2P=1)
     cudaStream_t stream = nullptr, cap_stream = nullptr;
     cudaStream_t comm = nullptr;  // halo exchanges (overlapped with interior slices)
     cudaEvent_t ev_bnd = nullptr, ev_xchg = nullptr;

@@ -450,7 +450,9 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
                                                 ms, mph, s0, ph0, it, ucw, warp, lane, pol.ustore, plo, phi);
         if (lane == 0) a.part[n & 3][C][t * kWarps + warp] = r2;
     }
-
+    // halo push to another GPU: this thread's peer stores are performed before the
+    // pass completes (the signal kernel that follows publishes the pass)
+    if constexpr (PUSH) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------

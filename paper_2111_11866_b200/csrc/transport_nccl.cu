@@ -112,9 +112,76 @@ struct NcclTransport : Transport {
         check(api().AllGather(local[0], all[0], (size_t)chunk, ncclDouble, comm, slabs[0]->stream),
               "ncclAllGather");
     }
+    void allgather_bytes(const void* d_local, void* d_all, size_t bytes, cudaStream_t st) {
+        check(api().AllGather(d_local, d_all, bytes, ncclChar, comm, st), "ncclAllGather");
+    }
 };
 
+__global__ void p2p_wait_kernel(const unsigned long long* f, int lo, int hi, unsigned long long target) {
+    for (int i = 0; i < 2; ++i) {
+        if (!(i == 0 ? lo : hi)) continue;
+        while (true) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f + i) : "memory");
+            if (v >= target) break;
+            __nanosleep(200);
+        }
+    }
+}
+
+__global__ void p2p_signal_kernel(unsigned long long* lo, unsigned long long* hi, unsigned long long v) {
+    __threadfence_system();  // the pass kernel's peer stores are ordered before the counter
+    if (lo) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(lo), "l"(v) : "memory");
+    if (hi) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(hi), "l"(v) : "memory");
+}
+
 }  // namespace
+
+void launch_p2p_wait(cudaStream_t st, const PeerLinks& pl, unsigned long long target) {
+    p2p_wait_kernel<<<1, 1, 0, st>>>(pl.my_flags.p, pl.S[0][0][0] != nullptr, pl.S[1][0][0] != nullptr, target);
+    SSB_LAUNCHED();
+}
+
+void launch_p2p_signal(cudaStream_t st, const PeerLinks& pl, unsigned long long value) {
+    p2p_signal_kernel<<<1, 1, 0, st>>>(pl.peer_flag[0], pl.peer_flag[1], value);
+    SSB_LAUNCHED();
+}
+
+void setup_peer_links(Transport& t, Slab& s, int rank, int world, int chunk, int n4_global, PeerLinks& pl) {
+    auto* tr = dynamic_cast<NcclTransport*>(&t);
+    require(tr != nullptr, "peer links need the NCCL transport");
+    constexpr int H = 2 * kStateBuffers + 1;  // state arrays + the flag words
+    pl.my_flags.alloc(2);
+    SSB_CUDA(cudaMemset(pl.my_flags.p, 0, 2 * sizeof(unsigned long long)));
+    cudaIpcMemHandle_t mine[H];
+    for (int b = 0; b < kStateBuffers; ++b)
+        for (int c = 0; c < 2; ++c) SSB_CUDA(cudaIpcGetMemHandle(&mine[2 * b + c], s.S[b].c[c].p));
+    SSB_CUDA(cudaIpcGetMemHandle(&mine[H - 1], pl.my_flags.p));
+    Dev<unsigned char> dl, da;
+    dl.alloc(sizeof mine);
+    da.alloc(sizeof mine * world);
+    SSB_CUDA(cudaMemcpy(dl.p, mine, sizeof mine, cudaMemcpyHostToDevice));
+    tr->allgather_bytes(dl.p, da.p, sizeof mine, s.stream);
+    std::vector<cudaIpcMemHandle_t> all((size_t)H * world);
+    SSB_CUDA(cudaMemcpyAsync(all.data(), da.p, sizeof mine * world, cudaMemcpyDeviceToHost, s.stream));
+    SSB_CUDA(cudaStreamSynchronize(s.stream));
+    for (int side = 0; side < 2; ++side) {
+        const int r = side == 0 ? rank - 1 : rank + 1;
+        if (r < 0 || r >= world) continue;
+        pl.n4[side] = r == world - 1 ? n4_global - (world - 1) * chunk : chunk;
+        for (int b = 0; b < kStateBuffers; ++b)
+            for (int c = 0; c < 2; ++c) {
+                void* p = nullptr;
+                SSB_CUDA(cudaIpcOpenMemHandle(&p, all[(size_t)r * H + 2 * b + c], cudaIpcMemLazyEnablePeerAccess));
+                pl.S[side][b][c] = static_cast<double*>(p);
+            }
+        void* f = nullptr;
+        SSB_CUDA(cudaIpcOpenMemHandle(&f, all[(size_t)r * H + H - 1], cudaIpcMemLazyEnablePeerAccess));
+        // the low neighbour's word [1] is written by its high neighbour (this rank), and vice versa
+        pl.peer_flag[side] = static_cast<unsigned long long*>(f) + (side == 0 ? 1 : 0);
+    }
+    pl.on = true;
+}
 
 std::unique_ptr<Transport> make_nccl_transport(const unsigned char* uid, int rank, int world) {
     return std::unique_ptr<Transport>(new NcclTransport(uid, rank, world));
