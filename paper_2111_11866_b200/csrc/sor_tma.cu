@@ -36,7 +36,7 @@ namespace ssb {
 
 namespace {
 
-constexpr int kWarps = 8;  // "virtual" consumer warps: one row (segment) each, one residual partial each
+constexpr int kWarps = 8;  // consumer warps: one row (segment) each, one residual partial each
 constexpr int kConsumers = kWarps;
 constexpr int kThreads = (kConsumers + 2) * 32;  // + a producer warp per ring
 #ifndef SSB_MAIN_STAGES
