@@ -39,6 +39,45 @@ __device__ __forceinline__ double* at(const Layout& L, PField f, int i, int j, i
     return f.c[L.colour(i, j, k, l)] + L.packed(i, j, k, l);
 }
 
+// Ghost-shell enumeration: the two hyperplanes c[axis] = 0 / max of one axis
+// (face_count(axis) positions each, the other three coordinates over their whole
+// padded range, lowest axis fastest).  Kernels over ghosts walk these instead of
+// the whole padded box (config 1: 2.3 M instead of 19 M positions).
+__host__ __device__ __forceinline__ long long face_count(const Layout& L, int axis) {
+    const long long ext[4] = {L.iMax, L.jMax, L.kMax, L.lMax};
+    long long n = 1;
+    for (int b = 0; b < 4; ++b)
+        if (b != axis) n *= ext[b];
+    return n;
+}
+
+__device__ __forceinline__ void face_pos(const Layout& L, int axis, long long e, int c[4]) {
+    const long long F = face_count(L, axis);
+    const int ext[4] = {L.iMax, L.jMax, L.kMax, L.lMax};
+    const int side = (int)(e / F);
+    long long r = e - side * F;
+    for (int b = 0; b < 4; ++b) {
+        if (b == axis) continue;
+        c[b] = (int)(r % ext[b]);
+        r /= ext[b];
+    }
+    c[axis] = side ? ext[axis] - 1 : 0;
+}
+
+// e over the 8 hyperplanes of all axes -> a ghost position (edges repeat)
+__device__ __forceinline__ void shell_pos(const Layout& L, long long e, int c[4]) {
+    int axis = 0;
+    while (axis < 3 && e >= 2 * face_count(L, axis)) {
+        e -= 2 * face_count(L, axis);
+        ++axis;
+    }
+    face_pos(L, axis, e, c);
+}
+
+__host__ __device__ __forceinline__ long long shell_count(const Layout& L) {
+    return 2 * (face_count(L, 0) + face_count(L, 1) + face_count(L, 2) + face_count(L, 3));
+}
+
 __global__ void pack_kernel(const Layout L, const double* __restrict__ src, PField dst, PField t0,
                             PField t1, PField t2) {
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -62,24 +101,28 @@ __global__ void unpack_kernel(const Layout L, PField src, double* __restrict__ d
     dst[e] = src.c[L.colour(p.i, p.j, p.k, p.l)][p.row * L.W + (p.i >> 1)];
 }
 
-__global__ void fill_kernel(const Layout L, PField f, double v, int ghosts_only) {
+__global__ void fill_kernel(const Layout L, PField f, double v) {
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (e >= L.P) return;
     const Pos p = decode_padded(L, e);
-    const bool ghost = p.i == 0 || p.i > L.n1 || p.j == 0 || p.j > L.n2 || p.k == 0 ||
-                       p.k > L.n3 || p.l == 0 || p.l > L.n4;
-    if (ghosts_only && !ghost) return;
     f.c[L.colour(p.i, p.j, p.k, p.l)][p.row * L.W + (p.i >> 1)] = v;
+}
+
+__global__ void set_ghosts_kernel(const Layout L, PField f, double v) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= shell_count(L)) return;
+    int c[4];
+    shell_pos(L, e, c);
+    *at(L, f, c[0], c[1], c[2], c[3]) = v;
 }
 
 // grid.cpp:138-156, one launch per axis (axis order 0..3 carries edges/corners)
 __global__ void mirror_kernel(const Layout L, PField f, int axis) {
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (e >= L.P) return;
-    const Pos p = decode_padded(L, e);
-    int c[4] = {p.i, p.j, p.k, p.l};
+    if (e >= 2 * face_count(L, axis)) return;
+    int c[4];
+    face_pos(L, axis, e, c);
     const int hi[4] = {L.n1 + 1, L.n2 + 1, L.n3 + 1, L.n4 + 1};
-    if (c[axis] != 0 && c[axis] != hi[axis]) return;
     // slab halo planes are the neighbours' data, not ghosts
     if (axis == 3 && ((c[3] == 0 && !L.glo) || (c[3] == hi[3] && !L.ghi))) return;
     const int dst[4] = {c[0], c[1], c[2], c[3]};
@@ -95,13 +138,11 @@ __global__ void fill_raw_kernel(double* p, long long n, double v) {
 
 __global__ void copy_ghosts_kernel(const Layout L, PField dst, PField src) {
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (e >= L.P) return;
-    const Pos p = decode_padded(L, e);
-    const bool ghost = p.i == 0 || p.i > L.n1 || p.j == 0 || p.j > L.n2 || p.k == 0 ||
-                       p.k > L.n3 || p.l == 0 || p.l > L.n4;
-    if (!ghost) return;
-    const int c = L.colour(p.i, p.j, p.k, p.l);
-    const long long q = p.row * L.W + (p.i >> 1);
+    if (e >= shell_count(L)) return;
+    int p[4];
+    shell_pos(L, e, p);
+    const int c = L.colour(p[0], p[1], p[2], p[3]);
+    const long long q = L.packed(p[0], p[1], p[2], p[3]);
     dst.c[c][q] = src.c[c][q];
 }
 
@@ -265,7 +306,7 @@ void launch_fill_raw(cudaStream_t s, double* p, long long n, double v) {
 }
 
 void launch_copy_ghosts(cudaStream_t s, const Layout& L, PField dst, PField src) {
-    copy_ghosts_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, dst, src);
+    copy_ghosts_kernel<<<ceil_div(shell_count(L), 256), 256, 0, s>>>(L, dst, src);
     SSB_LAUNCHED();
 }
 
@@ -275,18 +316,18 @@ void launch_unpack(cudaStream_t s, const Layout& L, PField src, double* dst) {
 }
 
 void launch_fill(cudaStream_t s, const Layout& L, PField f, double v) {
-    fill_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, f, v, 0);
+    fill_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, f, v);
     SSB_LAUNCHED();
 }
 
 void launch_set_ghosts(cudaStream_t s, const Layout& L, PField f, double v) {
-    fill_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, f, v, 1);
+    set_ghosts_kernel<<<ceil_div(shell_count(L), 256), 256, 0, s>>>(L, f, v);
     SSB_LAUNCHED();
 }
 
 void launch_mirror_ghosts(cudaStream_t s, const Layout& L, PField f, int a0, int a1) {
     for (int axis = a0; axis < a1; ++axis) {
-        mirror_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, f, axis);
+        mirror_kernel<<<ceil_div(2 * face_count(L, axis), 256), 256, 0, s>>>(L, f, axis);
         SSB_LAUNCHED();
     }
 }
