@@ -78,27 +78,49 @@ __host__ __device__ __forceinline__ long long shell_count(const Layout& L) {
     return 2 * (face_count(L, 0) + face_count(L, 1) + face_count(L, 2) + face_count(L, 3));
 }
 
+// one warp per padded row (j, k, l): coalesced reads of the reference layout,
+// half-warp-contiguous writes into each colour's packed row
+struct RowPos {
+    int j, k, l;
+    bool ghost_row;  // j, k or l is a ghost/halo index: every doxel of the row is a ghost
+};
+__device__ __forceinline__ RowPos decode_row(const Layout& L, long long r) {
+    RowPos p;
+    p.j = (int)(r % L.jMax);
+    const long long t = r / L.jMax;
+    p.k = (int)(t % L.kMax);
+    p.l = (int)(t / L.kMax);
+    p.ghost_row = p.j == 0 || p.j > L.n2 || p.k == 0 || p.k > L.n3 || p.l == 0 || p.l > L.n4;
+    return p;
+}
+
 __global__ void pack_kernel(const Layout L, const double* __restrict__ src, PField dst, PField t0,
                             PField t1, PField t2) {
-    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (e >= L.P) return;
-    const Pos p = decode_padded(L, e);
-    const int c = L.colour(p.i, p.j, p.k, p.l);
-    const long long q = p.row * L.W + (p.i >> 1);
-    const double v = src[e];
-    dst.c[c][q] = v;
-    const bool ghost = p.i == 0 || p.i > L.n1 || p.j == 0 || p.j > L.n2 || p.k == 0 ||
-                       p.k > L.n3 || p.l == 0 || p.l > L.n4;
-    if (ghost && t0.c[c]) t0.c[c][q] = v;
-    if (ghost && t1.c[c]) t1.c[c][q] = v;
-    if (ghost && t2.c[c]) t2.c[c][q] = v;
+    const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= L.rows) return;
+    const RowPos p = decode_row(L, r);
+    const int par = (p.j + p.k + p.l + L.lpar) & 1;
+    for (int i = lane; i < L.iMax; i += 32) {
+        const int c = (i + par) & 1;
+        const long long q = r * L.W + (i >> 1);
+        const double v = src[r * L.iMax + i];
+        dst.c[c][q] = v;
+        if (p.ghost_row || i == 0 || i > L.n1) {
+            if (t0.c[c]) t0.c[c][q] = v;
+            if (t1.c[c]) t1.c[c][q] = v;
+            if (t2.c[c]) t2.c[c][q] = v;
+        }
+    }
 }
 
 __global__ void unpack_kernel(const Layout L, PField src, double* __restrict__ dst) {
-    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (e >= L.P) return;
-    const Pos p = decode_padded(L, e);
-    dst[e] = src.c[L.colour(p.i, p.j, p.k, p.l)][p.row * L.W + (p.i >> 1)];
+    const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= L.rows) return;
+    const RowPos p = decode_row(L, r);
+    const int par = (p.j + p.k + p.l + L.lpar) & 1;
+    for (int i = lane; i < L.iMax; i += 32) dst[r * L.iMax + i] = src.c[(i + par) & 1][r * L.W + (i >> 1)];
 }
 
 __global__ void fill_kernel(const Layout L, PField f, double v) {
@@ -296,7 +318,7 @@ __global__ void mask_kernel(const Layout L, PField f, double level, uint8_t* mas
 
 void launch_pack(cudaStream_t s, const Layout& L, const double* src, PField dst, PField t0,
                  PField t1, PField t2) {
-    pack_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, src, dst, t0, t1, t2);
+    pack_kernel<<<ceil_div(L.rows * 32, 256), 256, 0, s>>>(L, src, dst, t0, t1, t2);
     SSB_LAUNCHED();
 }
 
@@ -311,7 +333,7 @@ void launch_copy_ghosts(cudaStream_t s, const Layout& L, PField dst, PField src)
 }
 
 void launch_unpack(cudaStream_t s, const Layout& L, PField src, double* dst) {
-    unpack_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, src, dst);
+    unpack_kernel<<<ceil_div(L.rows * 32, 256), 256, 0, s>>>(L, src, dst);
     SSB_LAUNCHED();
 }
 
