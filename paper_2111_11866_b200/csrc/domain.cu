@@ -4,6 +4,8 @@
 #include "domain.cuh"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <climits>
 #include <cmath>
@@ -882,6 +884,16 @@ void Domain::get_mask(double level, uint8_t* mask) {
 }
 
 void Domain::prepare(const double* image, const ss_center* c, int n, const ss_seg_params& p, const double* u0) {
+    // SSB_TIMING=1: per-phase wall times of prepare on stderr (device synchronised)
+    static const bool timing = std::getenv("SSB_TIMING") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!timing) return;
+        sync();
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "prepare %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t_last).count());
+        t_last = t;
+    };
     validate_seg_params(p);
     validate_centers(g, c, n);
     require(image != nullptr, "null image");
@@ -900,6 +912,7 @@ void Domain::prepare(const double* image, const ss_center* c, int n, const ss_se
         }
         s->rescale(0);
     }
+    mark("u0 + rescale");
 
     // local_threshold, heat_smooth x2, face_coefficients (solver.cpp:419-422)
     std::vector<std::unique_ptr<DevField>> img, th, t1, t2, t3;
@@ -916,6 +929,7 @@ void Domain::prepare(const double* image, const ss_center* c, int n, const ss_se
         t3.back()->alloc(s->L);
         s->upload(host_slab(image, *s), img.back()->pf());
     }
+    mark("alloc + image upload");
     {
         std::vector<std::unique_ptr<BallSet>> bsets;
         std::vector<std::unique_ptr<Dev<double>>> abs;
@@ -951,23 +965,28 @@ void Domain::prepare(const double* image, const ss_center* c, int n, const ss_se
     std::vector<PField> thf;
     for (auto& f : th) thf.push_back(f->pf());
     exchange(thf, 3);  // halos of the thresholded image (the heat solve reads them)
+    mark("local_threshold");
 
     std::vector<Triple> b1, b2;
     for (size_t s = 0; s < sp.size(); ++s) b1.push_back({img[s]->pf(), t1[s]->pf(), t2[s]->pf(), t3[s]->pf()});
     const int r1 = heat_smooth(b1, p.sigma, p.smooth_steps, p.smooth_omega, p.smooth_tol, p.smooth_max_iter);
+    mark("heat_smooth(I0)");
     for (size_t s = 0; s < sp.size(); ++s)
         b2.push_back({th[s]->pf(), b1[s][(r1 + 1) % kStateBuffers], b1[s][(r1 + 2) % kStateBuffers],
                       b1[s][(r1 + 3) % kStateBuffers]});
     const int r2 = heat_smooth(b2, p.sigma, p.smooth_steps, p.smooth_omega, p.smooth_tol, p.smooth_max_iter);
+    mark("heat_smooth(ITH)");
     for (size_t s = 0; s < sp.size(); ++s)
         sp[s]->face_coefficients(b1[s][r1], b2[s][r2], p.K, p.delta, p.vartheta, nullptr);
     sync();
+    mark("face_coefficients");
 
     // apply_dirichlet(u, 0) (solver.cpp:425) on every state buffer; halo planes
     // are refreshed by the exchange at the start of every step
     for (Slab* s : sp)
         for (auto& f : s->S) launch_set_ghosts(stream, s->L, f.pf(), 0.0);
     sync();
+    mark("dirichlet");
     prepared = true;
 }
 
