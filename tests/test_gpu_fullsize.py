@@ -57,3 +57,29 @@ def test_config2_properties_and_slabs(gpu):
     inner = g.interior
     slack = 10 * d1["tol"]
     assert up[inner].min() - slack <= u1[inner].min() and u1[inner].max() <= up[inner].max() + slack
+
+
+def test_wide_rows_kernels_agree(gpu):
+    """512-wide rows (BASELINE config 3's x extent: one row per work item, 8 warps
+    across 256 slots): TMA two-pass == LDG two-pass bit for bit over two steps,
+    on 1 slab and on 3 slabs (halo push)."""
+    rng = np.random.default_rng(3003)
+    dims, h = (512, 48, 12, 6), 1.0 / 32
+    g = gpu.Grid.make(dims, h)
+    img = np.zeros(g.shape)
+    img[g.interior] = np.clip(rng.normal(0.3, 0.2, size=(dims[3], dims[2], dims[1], dims[0])), 0, 1)
+    img[g.interior] = img[g.interior].astype(np.float32)
+    rows = [(f, 255.5, 23.5, 5.5, 6.0) for f in range(dims[3])]
+    p = gpu.seg_params(tau=h, epsilon=1e-3, omega=1.4, sor_rel_tol=1e-8, n_steps=2, sigma=np.sqrt(2) * h,
+                       K=500.0, delta=0.5, vartheta=0.5, rescale_radius=8.0)
+    res = {}
+    for kernel, slabs in (("tma", 1), ("ldg", 1), ("tma", 3)):
+        with gpu.Session(g, n_slabs=slabs) as s:
+            s.set_kernel(kernel)
+            s.prepare(img, rows, p)
+            its = [s.step()["iterations"] for _ in range(2)]
+            res[(kernel, slabs)] = (its, s.get_u())
+    its0, u0 = res[("tma", 1)]
+    for key, (its, u) in res.items():
+        assert its == its0, key
+        assert np.array_equal(u.view(np.uint64), u0.view(np.uint64)), key
