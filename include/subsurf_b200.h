@@ -213,8 +213,10 @@ SS_API ss_status ss_session_eoc_row(ss_session* s, int n, double omega, double s
                                     double* err, long long* sweeps);
 /* 0 = host-driven chunked loop, 1 = CUDA-graph conditional loop (default) */
 SS_API ss_status ss_session_set_loop_mode(ss_session* s, int mode);
-/* SOR kernel: 1 = TMA-fed two-pass (default), 0 = plain LDG two-pass, 2 = two-iteration
- * TMA wavefront through L2 (experimental; measured slower on B200) */
+/* SOR kernel: 4 = auto (default: 3 when the solve's working set fits L2, else 1),
+ * 1 = TMA-fed two-pass, 0 = plain LDG two-pass, 3 = resident (the whole solve in one
+ * cooperative launch), 2 = two-iteration TMA wavefront (experimental; measured slower
+ * on B200) */
 SS_API ss_status ss_session_set_kernel(ss_session* s, int kernel);
 /* per-pass CUDA-event timing of the SOR kernels (forces the host-driven loop) */
 SS_API ss_status ss_session_set_profiling(ss_session* s, int enable);
