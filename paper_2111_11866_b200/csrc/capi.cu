@@ -122,7 +122,7 @@ ss_status ss_assemble_step(const ss_grid* g, const double* u_prev, const double*
         s.upload_state(u_prev, 0);
         if (G) {
             double* d8 = s.stage8_p();
-            SSB_CUDA(cudaMemcpyAsync(d8, G, s.L.P * 8 * sizeof(double), cudaMemcpyDefault, d.stream));
+            copy_h2d(d8, G, s.L.P * 8 * sizeof(double), d.stream);
             s.G[0].alloc(s.L.cs * 8);
             s.G[1].alloc(s.L.cs * 8);
             launch_pack8(d.stream, s.L, d8, s.G[0].p, s.G[1].p);
@@ -135,9 +135,9 @@ ss_status ss_assemble_step(const ss_grid* g, const double* u_prev, const double*
         SSB_CUDA(cudaMemsetAsync(dg.p, 0, s.L.P * sizeof(double), d.stream));
         SSB_CUDA(cudaMemsetAsync(ab.p, 0, s.L.P * sizeof(double), d.stream));
         s.assemble(s.S[0].pf(), G != nullptr, tau, epsilon, off, dg.p, ab.p);
-        SSB_CUDA(cudaMemcpyAsync(offdiag, off, s.L.P * 8 * sizeof(double), cudaMemcpyDefault, d.stream));
-        SSB_CUDA(cudaMemcpyAsync(diag, dg.p, s.L.P * sizeof(double), cudaMemcpyDefault, d.stream));
-        SSB_CUDA(cudaMemcpyAsync(abar, ab.p, s.L.P * sizeof(double), cudaMemcpyDefault, d.stream));
+        copy_d2h(offdiag, off, s.L.P * 8 * sizeof(double), d.stream);
+        copy_d2h(diag, dg.p, s.L.P * sizeof(double), d.stream);
+        copy_d2h(abar, ab.p, s.L.P * sizeof(double), d.stream);
         int bad = 0;
         SSB_CUDA(cudaMemcpyAsync(&bad, s.flags.p, sizeof(int), cudaMemcpyDeviceToHost, d.stream));
         d.sync();
@@ -159,9 +159,9 @@ ss_status ss_assemble_heat_step(const ss_grid* g, double dt, double* offdiag, do
         dg.alloc(s.L.P);
         ab.alloc(s.L.P);
         launch_heat_export(d.stream, s.L, hc, off, dg.p, ab.p);
-        SSB_CUDA(cudaMemcpyAsync(offdiag, off, s.L.P * 8 * sizeof(double), cudaMemcpyDefault, d.stream));
-        SSB_CUDA(cudaMemcpyAsync(diag, dg.p, s.L.P * sizeof(double), cudaMemcpyDefault, d.stream));
-        SSB_CUDA(cudaMemcpyAsync(abar, ab.p, s.L.P * sizeof(double), cudaMemcpyDefault, d.stream));
+        copy_d2h(offdiag, off, s.L.P * 8 * sizeof(double), d.stream);
+        copy_d2h(diag, dg.p, s.L.P * sizeof(double), d.stream);
+        copy_d2h(abar, ab.p, s.L.P * sizeof(double), d.stream);
         d.sync();
     });
 }
@@ -177,7 +177,7 @@ ss_status ss_redblack_sor(const ss_grid* g, const double* offdiag, const double*
         Domain& d = cached(*g);
         Slab& s = *d.sp[0];
         double* d8 = s.stage8_p();
-        SSB_CUDA(cudaMemcpyAsync(d8, offdiag, s.L.P * 8 * sizeof(double), cudaMemcpyDefault, d.stream));
+        copy_h2d(d8, offdiag, s.L.P * 8 * sizeof(double), d.stream);
         launch_pack_coef(d.stream, s.L, d8, s.coef[0].p, s.coef[1].p);  // pack_coefficients, solver.cpp:233-249
         s.rhs_sep.alloc(s.L);
         s.upload(rhs, s.rhs_sep.pf());
@@ -209,7 +209,7 @@ ss_status ss_face_coefficients(const ss_grid* g, const double* I0s, const double
         double* out = s.stage8_p();
         launch_fill_raw(d.stream, out, s.L.P * 8, 1.0);  // ghost entries = 1 (edge.hpp:73)
         s.face_coefficients(a.pf(), b.pf(), K, delta, vartheta, out);
-        SSB_CUDA(cudaMemcpyAsync(G, out, s.L.P * 8 * sizeof(double), cudaMemcpyDefault, d.stream));
+        copy_d2h(G, out, s.L.P * 8 * sizeof(double), d.stream);
         d.sync();
         s.have_G = false;
     });

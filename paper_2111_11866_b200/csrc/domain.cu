@@ -189,7 +189,7 @@ double* Slab::stage8_p() {
 
 void Slab::upload(const double* host, PField dst, PField t0, PField t1, PField t2) {
     double* d = stage_p();
-    SSB_CUDA(cudaMemcpyAsync(d, host, L.P * sizeof(double), cudaMemcpyDefault, stream));
+    copy_h2d(d, host, L.P * sizeof(double), stream);
     launch_pack(stream, L, d, dst, t0, t1, t2);
 }
 
@@ -201,7 +201,7 @@ void Slab::upload_state(const double* host, int role) {
 void Slab::download(PField src, double* host) {
     double* d = stage_p();
     launch_unpack(stream, L, src, d);
-    SSB_CUDA(cudaMemcpyAsync(host, d, L.P * sizeof(double), cudaMemcpyDefault, stream));
+    copy_d2h(host, d, L.P * sizeof(double), stream);
 }
 
 void Slab::sync_ghosts_from(int role) {
@@ -865,8 +865,7 @@ void Domain::get_u(double* host) {
         launch_unpack(stream, s->L, s->S[cur].pf(), d);
         const int p0 = s->L.glo ? 0 : 1;
         const int p1 = s->L.ghi ? s->L.n4 + 1 : s->L.n4;
-        SSB_CUDA(cudaMemcpyAsync(host_slab(host, *s) + p0 * hp, d + p0 * hp, (p1 - p0 + 1) * hp * sizeof(double),
-                                 cudaMemcpyDefault, stream));
+        copy_d2h(host_slab(host, *s) + p0 * hp, d + p0 * hp, (p1 - p0 + 1) * hp * sizeof(double), stream);
     }
     sync();
 }

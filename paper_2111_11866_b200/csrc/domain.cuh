@@ -164,6 +164,12 @@ struct LocalTransport : Transport {
 
 std::unique_ptr<Transport> make_nccl_transport(const unsigned char* uid, int rank, int world);
 
+// large host <-> device copies (hostio.cu): pinned host memory direct and async;
+// pageable memory through pinned chunks filled / drained by host threads.  Both
+// return with the host buffer reusable (d2h: data arrived).
+void copy_h2d(void* dev, const void* host, size_t bytes, cudaStream_t s);
+void copy_d2h(void* host, const void* dev, size_t bytes, cudaStream_t s);
+
 // NVLink peer links of one rank (opt-in, SSB_P2P=1): the l-neighbours' state
 // arrays and flag words mapped into this process with CUDA IPC, so the TMA pass
 // pushes its boundary planes straight into the neighbours' halo planes over
