@@ -178,6 +178,9 @@ def make_workload(workloads, ssd, config, rank, world):
             return workloads.config1()
         lb, cnt = ssd.partition(64 * world, world)[rank]
         return workloads.config1(replicas=world, planes=(lb - 1, lb + cnt))
+    if config == "config3" and world < 2:
+        # 2.1e9 doxels x ~130 B of device state = 280 GB: more than one B200 (BASELINE: 2/4/8 GPUs)
+        raise SystemExit("config3 needs >= 2 GPUs (280 GB of device state)")
     n4 = {"config2": 32, "config3": 64, "config4": 16 * world}[config]
     lb, cnt = ssd.partition(n4, world)[rank]
     planes = (lb - 1, lb + cnt) if world > 1 else None
