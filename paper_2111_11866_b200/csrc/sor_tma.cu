@@ -107,7 +107,7 @@ __device__ __forceinline__ Policies make_policies(int hint) {
 
 struct Geo {  // per-launch tiling (identical on host and device)
     int R;    // rows per item
-    int wpr;  // warps per row
+    int wpr;  // warps per row (wide rows), 0: flat slot mapping (R * nq <= 256)
     int njg;  // row groups per plane
     int nkc;  // plane chunks per slice
     long long items;
@@ -123,13 +123,25 @@ struct Geo {  // per-launch tiling (identical on host and device)
 __host__ __device__ inline Geo make_geo(const Layout& L) {
     Geo g;
     const uint32_t rb = (uint32_t)L.W * 8u;
-    int R = 8;
-    while (R > 1 && rb * (9u * R + 2u) > 24576u) R >>= 1;
-    if (R > L.n2) R = L.n2 < 1 ? 1 : L.n2;
-    // keep R a divisor of kWarps so warps map evenly onto rows
-    while (kWarps % R) --R;
+    const uint32_t crb = (uint32_t)L.Wc * 32u;
+    const int nq = (L.n1 + 1) / 2;  // slots of one colour per row
+    // Rows per item.  Rows up to 256 slots: the 256 consumer threads take one slot
+    // each over the item's R rows (flat mapping), so pick R <= 256 / nq filling the
+    // most threads (ties: more rows, fewer halo rows) within the stage budget --
+    // 32 slots: 8 rows, 128: 2, 40: 6, 80: 3.  Wider rows: one row, 8 warps along it.
+    int R = 1;
+    if (nq <= 256) {
+        int best = 0;
+        for (int r = 1; r <= 256 / nq && r <= L.n2; ++r) {
+            if (r > 1 && r * (crb + 4u * rb) + (r + 2u) * rb > 24576u) break;
+            if (r * nq >= best) {
+                best = r * nq;
+                R = r;
+            }
+        }
+    }
     g.R = R;
-    g.wpr = kWarps / R;
+    g.wpr = nq <= 256 ? 0 : kWarps;  // 0: flat mapping
     g.njg = (L.n2 + R - 1) / R;
     g.nkc = (L.n3 + kPlanesPerItem - 1) / kPlanesPerItem;
     g.items = (long long)g.njg * g.nkc * L.n4;
@@ -268,10 +280,15 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
                                                uint64_t pol_store, double* push_lo = nullptr,
                                                double* push_hi = nullptr) {
     const int W = L.W;
-    const int r = warp / G.wpr;
+    // this thread's row r and first slot: flat (one slot per thread over the item's
+    // R rows) or, for rows wider than 256 slots, 8 warps striding along the row
+    const int nq = (L.n1 + 1) / 2;
+    const int tid = warp * 32 + lane;
+    const int r = G.wpr ? warp / G.wpr : tid / nq;
+    const int q_begin = G.wpr ? lane + 32 * (warp % G.wpr) : tid - r * nq;
+    const int q_step = G.wpr ? 32 * G.wpr : 1 << 30;
     const int j = it.j0 + r;
-    const bool row_ok = r < it.rows;
-    const int q_begin = lane + 32 * (warp % G.wpr), q_step = 32 * G.wpr;
+    const bool row_ok = r < it.rows;  // (flat: tid < R * nq  <=>  r < R)
     // last slot q with i = 1 + par + 2q <= n1, per parity
     const int q_end0 = (L.n1 - 1) >> 1, q_end1 = (L.n1 - 2) >> 1;
     int par = (1 + j + it.k0 + it.l + L.lpar + C) & 1;
