@@ -29,7 +29,7 @@ for _ in range(S):
 u_gpu = s.get_u()
 s.close()
 res = {"workload": wl.name, "steps": S, "gpu_prepare_s": prep, "gpu_step_s": ours, "gpu_iterations": its}
-if op.ref_available():
+if op.ref_available() and not os.environ.get("NO_REF"):
     R = op.ref()
     og = op.Grid.make(wl.dims, wl.h)
     workers = min(R.lib.ref_hardware_threads(), wl.dims[3])
