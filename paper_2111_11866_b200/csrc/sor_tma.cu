@@ -40,10 +40,13 @@ constexpr int kWarps = 8;  // consumer warps: one row (segment) each, one residu
 constexpr int kConsumers = kWarps;
 constexpr int kThreads = (kConsumers + 2) * 32;  // + a producer warp per ring
 #ifndef SSB_MAIN_STAGES
-#define SSB_MAIN_STAGES 5
+#define SSB_MAIN_STAGES 4
 #endif
 #ifndef SSB_UK_STAGES
-#define SSB_UK_STAGES 5
+#define SSB_UK_STAGES 6
+#endif
+#ifndef SSB_STAGE_BUDGET
+#define SSB_STAGE_BUDGET 24576  // bytes of one main + one UK stage that bound the rows per item
 #endif
 constexpr int kMainStages = SSB_MAIN_STAGES;  // per-plane operands (consumed by one plane)
 constexpr int kUKStages = SSB_UK_STAGES;      // other-colour planes (held for three planes)
@@ -136,7 +139,7 @@ __host__ __device__ inline Geo make_geo(const Layout& L) {
     if (nq <= 256) {
         int best = 0;
         for (int r = 1; r <= 256 / nq && r <= L.n2; ++r) {
-            if (r > 1 && r * (crb + 4u * rb) + (r + 2u) * rb > 24576u) break;
+            if (r > 1 && r * (crb + 4u * rb) + (r + 2u) * rb > (uint32_t)SSB_STAGE_BUDGET) break;
             if (r * nq >= best) {
                 best = r * nq;
                 R = r;
