@@ -21,7 +21,8 @@ def test_header_declares_the_reference_entry_points():
     names = declared_symbols()
     for n in ["ss_assemble_step", "ss_assemble_heat_step", "ss_redblack_sor", "ss_face_coefficients",
               "ss_heat_smooth", "ss_local_threshold", "ss_build_initial", "ss_local_rescale",
-              "ss_extract_mask", "ss_segment", "ss_session_create", "ss_session_step"]:
+              "ss_extract_mask", "ss_segment", "ss_session_create", "ss_session_step",
+              "ss_label_components", "ss_distance_centers", "ss_backtrack_link", "ss_track", "ss_session_track"]:
         assert n in names
 
 
@@ -71,3 +72,16 @@ def test_pass_bytes():
     g = ss.Grid.make((64, 64, 64, 64), 1 / 64)
     # 56 B per doxel per sweep, half per colour pass
     assert ss.sor_pass_bytes(g) == 0.5 * 64 ** 4 * 56
+
+
+def test_tracking_validation_and_no_fallback(ss):
+    """tracking entry points: shape checks before the device; no CPU fallback without one"""
+    g = ss.Grid.make((4, 3, 2, 2), 1.0)
+    with pytest.raises(ss.ValidationError, match="mask shape"):
+        ss.label_components(np.zeros((2, 2, 3, 5), np.uint8), g)
+    if ss.device_available():
+        pytest.skip("a GPU is visible")
+    with pytest.raises(ss.DeviceError):
+        ss.label_components(np.zeros((2, 2, 3, 4), np.uint8), g)
+    with pytest.raises(ss.DeviceError):
+        ss.track(np.zeros(g.shape), g)
