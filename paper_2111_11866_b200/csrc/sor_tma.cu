@@ -36,8 +36,15 @@ namespace ssb {
 
 namespace {
 
-constexpr int kWarps = 8;  // consumer warps: one row (segment) each, one residual partial each
+#ifndef SSB_CONSUMER_WARPS
+#define SSB_CONSUMER_WARPS 8
+#endif
+#ifndef SSB_CTAS_PER_SM
+#define SSB_CTAS_PER_SM 2
+#endif
+constexpr int kWarps = SSB_CONSUMER_WARPS;  // consumer warps, one residual partial each per item
 constexpr int kConsumers = kWarps;
+constexpr int kSlotsPerPlane = kConsumers * 32;   // consumer threads: one slot each (flat mapping)
 constexpr int kThreads = (kConsumers + 2) * 32;  // + a producer warp per ring
 #ifndef SSB_MAIN_STAGES
 #define SSB_MAIN_STAGES 4
@@ -136,9 +143,9 @@ __host__ __device__ inline Geo make_geo(const Layout& L) {
     // most threads (ties: more rows, fewer halo rows) within the stage budget --
     // 32 slots: 8 rows, 128: 2, 40: 6, 80: 3.  Wider rows: one row, 8 warps along it.
     int R = 1;
-    if (nq <= 256) {
+    if (nq <= kSlotsPerPlane) {
         int best = 0;
-        for (int r = 1; r <= 256 / nq && r <= L.n2; ++r) {
+        for (int r = 1; r <= kSlotsPerPlane / nq && r <= L.n2; ++r) {
             if (r > 1 && r * (crb + 4u * rb) + (r + 2u) * rb > (uint32_t)SSB_STAGE_BUDGET) break;
             if (r * nq >= best) {
                 best = r * nq;
@@ -147,7 +154,7 @@ __host__ __device__ inline Geo make_geo(const Layout& L) {
         }
     }
     g.R = R;
-    g.wpr = nq <= 256 ? 0 : kWarps;  // 0: flat mapping
+    g.wpr = nq <= kSlotsPerPlane ? 0 : kWarps;  // 0: flat mapping
     g.njg = (L.n2 + R - 1) / R;
     g.nkc = (L.n3 + kPlanesPerItem - 1) / kPlanesPerItem;
     g.items = (long long)g.njg * g.nkc * L.n4;
@@ -424,7 +431,7 @@ __device__ __forceinline__ void init_barriers(Bars& b) {
 }
 
 template <int C, bool HEAT, bool PUSH>
-__global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
+__global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_pass_tma(const SorArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) Bars bars;
     __shared__ double ws[32];
@@ -467,7 +474,8 @@ __global__ void __launch_bounds__(kThreads, 2) sor_pass_tma(const SorArgs a) {
         }
         return;
     }
-    if (C == 1 && a.fuse_final) black_head_finalize(a, n, ws, &last, threadIdx.x);
+    if (C == 1 && a.fuse_final && threadIdx.x < 256)  // the finalize's fixed 256-thread tree
+        black_head_finalize(a, n, ws, &last, threadIdx.x);
     uint32_t ms = 0, mph = 0, s0 = 0, ph0 = 0;
     for (long long tt = blockIdx.x; tt < n_items; tt += gridDim.x) {
         Item it;
@@ -516,7 +524,7 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 }
 
 template <bool HEAT>
-__global__ void __launch_bounds__(kThreads, 2) sor_wave_tma(const SorArgs a) {
+__global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_wave_tma(const SorArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) Bars bars;
     const SorState* st = a.st;
@@ -615,7 +623,7 @@ void configure() {
     static bool done = false;
     if (!done) {
         SSB_CUDA(cudaFuncSetAttribute(sor_pass_tma<C, HEAT, PUSH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      96 * 1024 + 64 * 1024));
+                                      200 * 1024));
         done = true;
     }
 }
@@ -625,7 +633,7 @@ void configure_wave() {
     static bool done = false;
     if (!done) {
         SSB_CUDA(cudaFuncSetAttribute(sor_wave_tma<HEAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      96 * 1024 + 64 * 1024));
+                                      200 * 1024));
         done = true;
     }
 }
@@ -678,7 +686,7 @@ int pass_l2hint() {
 
 bool tma_pass_supported(const Layout& L) {
     const Geo G = make_geo(L);
-    return (size_t)G.smem <= 160 * 1024;
+    return (size_t)G.smem <= 200 * 1024;
 }
 
 void tma_pass_tiles(const Layout& L, SorArgs& a) {
