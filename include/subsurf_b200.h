@@ -193,7 +193,8 @@ SS_API void* ss_session_stream(ss_session* s);
 SS_API ss_status ss_session_prepare(ss_session* s, const double* image, const ss_center* c,
                                     int n, const ss_seg_params* p, const double* u0);
 /* one time step of the loop body (solver.cpp:428-438): assemble_step,
- * redblack_sor (rhs = guess = u), local_rescale.  diag may be NULL. */
+ * redblack_sor (rhs = guess = u), local_rescale.  diag may be NULL; on
+ * SS_ERR_NOCONVERGE it holds the iterations and the last residual. */
 SS_API ss_status ss_session_step(ss_session* s, ss_step_diag* diag);
 /* host <-> device copies of u (padded fp64, ghosts included) */
 SS_API ss_status ss_session_set_u(ss_session* s, const double* host_u);

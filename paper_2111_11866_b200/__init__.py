@@ -552,7 +552,8 @@ class Session:
 
     def step(self) -> dict:
         d = StepDiag()
-        _check(library().ss_session_step(self._h, C.byref(d)))
+        st = library().ss_session_step(self._h, C.byref(d))
+        _check(st, d.iterations, d.residual)  # SolverError carries iterations / last residual
         return dict(iterations=d.iterations, residual=d.residual, tol=d.tol, umin=d.umin, umax=d.umax)
 
     def step_nodiag(self) -> None:

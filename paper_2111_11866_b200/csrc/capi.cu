@@ -541,7 +541,15 @@ ss_status ss_session_step(ss_session* s, ss_step_diag* diag) {
     return guard([&] {
         require(s != nullptr, "null session");
         SSB_CUDA(cudaSetDevice(s->d->device));
-        s->d->step(diag);
+        try {
+            s->d->step(diag);
+        } catch (const SolverErrT& e) {  // SolverError{last_residual, iterations} (solver.cpp:391-395)
+            if (diag) {
+                diag->iterations = e.iterations;
+                diag->residual = e.residual;
+            }
+            throw;
+        }
     });
 }
 

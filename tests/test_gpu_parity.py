@@ -329,3 +329,24 @@ def test_per_call_api_thread_safe(gpu):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("kernel", ["auto", "tma", "ldg", "resident"])
+def test_segment_step_noconvergence(gpu, oracle, kernel):
+    """segment()'s SOR hitting sor_max_iter raises SolverError with the reference's
+    iteration count and last residual (solver.cpp:391-395), from every SOR kernel."""
+    d = load("segment")
+    g = G_of(gpu, d)
+    h = float(d["h"])
+    kw = dict(tau=h, epsilon=1e-3, omega=1.4, n_steps=1, sigma=np.sqrt(2) * h, K=200.0, delta=0.5,
+              vartheta=0.5, rescale_radius=3.0, sor_tol=1e-300, sor_max_iter=9)
+    from oracle.oracle_py import Grid as OG, seg_params as osp
+    st, _, info = oracle.segment(OG.make(tuple(int(x) for x in d["dims"]), h), d["image"], d["rows"], osp(**kw))
+    assert st == oracle_noconv()
+    with gpu.Session(g) as s:
+        s.set_kernel(kernel)
+        s.prepare(d["image"], d["rows"], gpu.seg_params(**kw))
+        with pytest.raises(gpu.SolverError) as e:
+            s.step()
+    assert e.value.iterations == 9
+    assert e.value.last_residual > 0
