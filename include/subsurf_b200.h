@@ -163,7 +163,8 @@ SS_API ss_status ss_track(const ss_grid* g, const double* u, double level, int w
                           double radius, ss_track_point* out, int capacity, int* n_points);
 
 /* segment (solver.hpp:91-92, solver.cpp:405-441).  u0 may be NULL
- * (build_initial); diags: n_steps entries or NULL. */
+ * (build_initial); diags: n_steps entries or NULL.  On SS_ERR_NOCONVERGE the
+ * failing step's diag holds the iterations and last residual, with tol = -1. */
 SS_API ss_status ss_segment(const ss_grid* g, const double* image, const ss_center* c, int n,
                             const ss_seg_params* p, const double* u0, double* u_out,
                             ss_step_diag* diags);

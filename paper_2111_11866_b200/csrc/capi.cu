@@ -469,7 +469,20 @@ ss_status ss_segment(const ss_grid* g, const double* image, const ss_center* c, 
         require(p != nullptr, "null params");
         Domain& d = cached(*g);
         d.prepare(image, c, n, *p, u0);
-        for (int step = 0; step < p->n_steps; ++step) d.step(diags ? diags + step : nullptr);
+        if (diags) std::memset(diags, 0, sizeof(ss_step_diag) * p->n_steps);
+        for (int step = 0; step < p->n_steps; ++step) {
+            try {
+                d.step(diags ? diags + step : nullptr);
+            } catch (const SolverErrT& e) {  // the failing step's diag: SolverError's payload
+                if (diags) {
+                    diags[step].iterations = e.iterations;
+                    diags[step].residual = e.residual;
+                    diags[step].tol = -1.0;  // marks the failing step
+                }
+                d.prepared = false;
+                throw;
+            }
+        }
         d.get_u(u_out);
         d.prepared = false;
     });

@@ -276,12 +276,25 @@ Field4D segment(const Field4D& image, const CentersTable& centers, const Segment
     std::vector<ss_step_diag> d(sp.solver.n_steps);
     const ss_grid g = grid_of(image.spec());
     const std::vector<ss_center> cs = centers_of(centers);
-    raise(ss_segment(&g, image.data(), cs.data(), (int)cs.size(), &p, nullptr, u.data(), d.data()));
+    const ss_status st = ss_segment(&g, image.data(), cs.data(), (int)cs.size(), &p, nullptr, u.data(), d.data());
+    // steps that completed print their diagnostics line (solver.cpp:433-438); a SolverError
+    // carries the failing step's iterations and last residual
+    int done = sp.solver.n_steps, failed = -1;
+    if (st == SS_ERR_NOCONVERGE)
+        for (int s = 0; s < sp.solver.n_steps; ++s)
+            if (d[s].tol < 0.0) {  // ss_segment marks the failing step
+                failed = s;
+                done = s;
+                break;
+            }
+    if (st != SS_OK && failed < 0) done = 0;
     if (diagnostics)
-        for (int s = 0; s < sp.solver.n_steps; ++s)  // solver.cpp:433-438
+        for (int s = 0; s < done; ++s)
             (*diagnostics) << "step " << s + 1 << "/" << sp.solver.n_steps << " sor_iters=" << d[s].iterations
                            << " residual=" << d[s].residual << " min=" << d[s].umin << " max=" << d[s].umax
                            << "\n";
+    if (failed >= 0) raise(st, d[failed].iterations, d[failed].residual);
+    raise(st);
     return u;
 }
 

@@ -1,6 +1,7 @@
 // C++ drop-in test: the namespace-subsurf API (include/subsurf_b200/subsurf.hpp)
 // against the oracle restatement (oracle/subsurf_oracle.c), bit for bit.
 // Built and run by tests/test_gpu_host_cpp.py on the GPU box.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -184,6 +185,28 @@ int main() {
     CHECK(same(us.data(), tmp.data(), P), "segment");
     CHECK(diag.str().find("step 2/2 sor_iters=" + std::to_string(od[1].iterations)) != std::string::npos,
           "segment diagnostics line");
+
+    // segment() with sor_max_iter too small for one of the steps: the completed steps'
+    // diagnostics lines, then SolverError with the failing solve's iterations
+    // (solver.cpp:391-395, :433-438)
+    {
+        SegmentationParams bad = seg;
+        const int M = od[1].iterations > od[0].iterations ? od[0].iterations
+                                                           : std::min(od[0].iterations, od[1].iterations) - 1;
+        const int fail = od[1].iterations > od[0].iterations ? 2 : (od[0].iterations > M ? 1 : 2);
+        bad.solver.sor_max_iter = M;
+        std::ostringstream bd;
+        bool thrown = false;
+        try {
+            segment(img, ct, bad, &bd);
+        } catch (const SolverError& e) {
+            thrown = e.iterations == M && e.last_residual > 0.0;
+        }
+        CHECK(thrown, "segment SolverError payload");
+        CHECK((bd.str().find("step 1/2") != std::string::npos) == (fail == 2) &&
+                  bd.str().find("step 2/2") == std::string::npos,
+              "segment diagnostics before SolverError");
+    }
 
     const MaskFrames m = extract_mask(us, 0.5);
     std::vector<unsigned char> om(spec.interior_size());
