@@ -151,11 +151,15 @@ int cmd_segment(const std::string& config_path, int workers, const std::string& 
     const ss_grid g{spec.n1, spec.n2, spec.n3, spec.n4, spec.h1, spec.h2, spec.h3, spec.h4};
     Field4D u(spec);
     std::vector<ss_step_diag> d(p.n_steps);
-    check(ss_segment(&g, image.data(), cs.data(), (int)cs.size(), &p, u0.size() ? u0.data() : nullptr, u.data(),
-                     d.data()));
-    for (int s = 0; s < p.n_steps; ++s)  // solver.cpp:433-438
+    const ss_status st = ss_segment(&g, image.data(), cs.data(), (int)cs.size(), &p,
+                                    u0.size() ? u0.data() : nullptr, u.data(), d.data());
+    for (int s = 0; s < p.n_steps && d[s].iterations > 0 && d[s].tol >= 0.0; ++s)  // completed steps (solver.cpp:433-438)
         std::cerr << "step " << s + 1 << "/" << p.n_steps << " sor_iters=" << d[s].iterations
                   << " residual=" << d[s].residual << " min=" << d[s].umin << " max=" << d[s].umax << "\n";
+    if (st == SS_ERR_NOCONVERGE)
+        for (int s = 0; s < p.n_steps; ++s)
+            if (d[s].tol < 0.0) throw SolverError(ss_last_error(), d[s].residual, d[s].iterations);
+    check(st);
     write_image4d(u, output + ".json", output + ".raw");
     if (cfg.boolean("export_vtk", false))
         for (int l = 1; l <= spec.n4; ++l) export_frame_vtk(u, l, output + "_f" + std::to_string(l - 1) + ".vtk");
