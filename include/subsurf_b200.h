@@ -215,8 +215,10 @@ SS_API ss_status ss_session_eoc_row(ss_session* s, int n, double omega, double s
                                     double* err, long long* sweeps);
 /* 0 = host-driven chunked loop, 1 = CUDA-graph conditional loop (default) */
 SS_API ss_status ss_session_set_loop_mode(ss_session* s, int mode);
-/* SOR kernel: 4 = auto (default: 3 when the solve's working set fits L2, else 1),
- * 1 = TMA-fed two-pass, 0 = plain LDG two-pass, 3 = resident (the whole solve in one
+/* SOR kernel: 4 = auto (default: 3 when the solve's working set fits L2, else the TMA
+ * two-pass with whole-row or 2D-tiled items, whichever keeps more lanes busy),
+ * 1 = TMA-fed two-pass with whole-row items, 5 = TMA two-pass with 2D-tiled items
+ * (tensor maps), 0 = plain LDG two-pass, 3 = resident (the whole solve in one
  * cooperative launch), 2 = two-iteration TMA wavefront (experimental; measured slower
  * on B200) */
 SS_API ss_status ss_session_set_kernel(ss_session* s, int kernel);

@@ -598,7 +598,7 @@ class Session:
         in one cooperative launch (LDG tiles, grid barriers); 'wave': two-iteration TMA
         wavefront through L2 (experimental, measured slower)."""
         _check(library().ss_session_set_kernel(
-            self._h, {"ldg": 0, "tma": 1, "wave": 2, "resident": 3, "auto": 4}[kernel]))
+            self._h, {"ldg": 0, "tma": 1, "wave": 2, "resident": 3, "auto": 4, "tma2d": 5}[kernel]))
 
     def set_profiling(self, on: bool) -> None:
         _check(library().ss_session_set_profiling(self._h, 1 if on else 0))

@@ -638,8 +638,8 @@ ss_status ss_session_set_loop_mode(ss_session* s, int mode) {
 ss_status ss_session_set_kernel(ss_session* s, int kernel) {
     return guard([&] {
         require(s != nullptr, "null session");
-        require(kernel >= 0 && kernel <= 4,
-                "kernel must be 0 (LDG), 1 (TMA), 2 (TMA wavefront), 3 (resident) or 4 (auto)");
+        require(kernel >= 0 && kernel <= 5,
+                "kernel must be 0 (LDG), 1 (TMA), 2 (TMA wavefront), 3 (resident), 4 (auto) or 5 (2D-tiled TMA)");
         s->d->kernel = kernel;
     });
 }

@@ -136,6 +136,10 @@ void build_balls(BallSet& bs, const ss_grid& gl, int l0, const ss_center* c, int
 }
 
 // ------------------------------------------------------------------ slab
+Slab::~Slab() {
+    for (auto& e : map_cache) cudaFree(e.dev);
+}
+
 Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int world, cudaStream_t s)
     : index(idx), stream(s) {
     gl = global;
@@ -318,6 +322,16 @@ SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool he
     a.order = pass_order();
     a.fuse_final = a.tma && world == 1 && !a.wave && pass_fuse_final() && tma_fuse_ok(L) ? 1 : 0;
     // halo push pointers are filled in by the Domain (it knows the neighbours)
+    // 2D-tiled items on request, or (auto) when whole-row items leave many lanes idle:
+    // rows of 150 / 284 slots (n1 = 300 / 567) -14..-29% per sweep; 16..256-slot rows
+    // that fill the 256 threads keep whole rows
+    const double u_rows = tma_lane_utilization(L, false), u_2d = tma_lane_utilization(L, true);
+    a.tile2d = a.tma && !a.wave && (kernel == 5 || pass_tile2d() || (kernel == 6 && u_rows < 0.8 && u_2d > u_rows))
+                   ? 1 : 0;
+    if (a.tile2d) {
+        a.maps = maps_for(a);
+        if (!a.maps) a.tile2d = 0;  // no tensor-map encoder: whole-row items
+    }
     if (a.tma)
         tma_pass_tiles(L, a);
     else
@@ -502,6 +516,37 @@ cudaEvent_t Domain::pool_event(size_t idx) {
     return ev_pool[idx];
 }
 
+// 2D-tiled TMA items (env SSB_TILE2D; kernel 5 selects them explicitly)
+bool pass_tile2d() {
+    static const int v = [] {
+        const char* e = std::getenv("SSB_TILE2D");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v != 0;
+}
+
+// device copies of the tensor maps, one per set of array pointers (the cached
+// graphs bake the map address in, so a map set is never rewritten)
+const TmaMaps* Slab::maps_for(const SorArgs& a) const {
+    const void* key[2 * kStateBuffers + 4];
+    for (int b = 0; b < kStateBuffers; ++b)
+        for (int c = 0; c < 2; ++c) key[2 * b + c] = a.U[b][c];
+    key[2 * kStateBuffers] = a.rhs[0];
+    key[2 * kStateBuffers + 1] = a.rhs[1];
+    key[2 * kStateBuffers + 2] = a.coef[0];
+    key[2 * kStateBuffers + 3] = a.coef[1];
+    for (const auto& e : map_cache)
+        if (std::memcmp(e.key, key, sizeof key) == 0) return e.dev;
+    TmaMaps h;
+    if (!encode_tma_maps(a, h)) return nullptr;
+    MapEntry e;
+    std::memcpy(e.key, key, sizeof key);
+    SSB_CUDA(cudaMalloc(&e.dev, sizeof(TmaMaps)));
+    SSB_CUDA(cudaMemcpy(e.dev, &h, sizeof h, cudaMemcpyHostToDevice));
+    map_cache.push_back(e);
+    return e.dev;
+}
+
 // halo push for in-process slab groups (env SSB_PUSH, default on)
 bool halo_push() {
     static const int v = [] {
@@ -627,7 +672,9 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
     std::vector<SorArgs> a;
     // resident loop: single slab whose working set fits L2 (auto) or on request
     bool resident = single() && (kernel == 3 || (kernel == 4 && resident_supported(sp[0]->L)));
-    int kern = resident ? 0 : (kernel == 4 || kernel == 3 ? 1 : kernel);  // LDG tiles for resident
+    // per-slab kernel code: 0 LDG (also the resident loop's tiles), 1 TMA whole rows,
+    // 2 wavefront, 5 TMA 2D-tiled, 6 TMA with the item shape chosen per grid (auto)
+    int kern = resident ? 0 : (kernel == 4 ? 6 : kernel == 3 ? 1 : kernel);
     solve_count = (solve_count + 1) & 0x3fff;
     const int epoch_base = (solve_count + 1) << 16;  // differs from the previous solve's
     for (size_t s = 0; s < sp.size(); ++s) {
@@ -683,7 +730,7 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
         }
         if (!launch_sor_resident(stream, a[0], heat)) {  // cannot be co-resident: pass kernels
             resident = false;
-            kern = 1;
+            kern = kernel == 4 ? 6 : 1;
             a[0] = sp[0]->sor_args(B[0].data(), rhs[0], heat, omega, hc, world, kern);
         }
     }

@@ -72,6 +72,8 @@ void build_balls(BallSet& bs, const ss_grid& g_local, int l0, const ss_center* c
                  double radius, bool fixed_radius);
 
 void require(bool ok, const std::string& msg);
+bool pass_tile2d();  // env SSB_TILE2D
+bool halo_push();    // env SSB_PUSH
 void validate_grid(const ss_grid* g);
 void validate_solver(double tau, double eps, double omega, double tol, int max_iter, int n_steps);
 void validate_smoothing(double sigma, int steps, double tol, int max_iter, double omega);
@@ -135,6 +137,14 @@ struct Slab {
     void initial(PField u, const ss_center* c, int n, double v, double R, int profile);
     SorArgs sor_args(const PField B[kStateBuffers], const PField& rhs, bool heat, double omega,
                      const double hc[4], int world, int kernel) const;
+    // tensor maps of the 2D-tiled pass, device copies cached per pointer set
+    struct MapEntry {
+        const void* key[2 * kStateBuffers + 4];
+        TmaMaps* dev = nullptr;
+    };
+    mutable std::vector<MapEntry> map_cache;
+    const TmaMaps* maps_for(const SorArgs& a) const;
+    ~Slab();
 };
 
 // ------------------------------------------------------------------ transports

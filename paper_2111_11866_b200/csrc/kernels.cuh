@@ -1,6 +1,8 @@
 // kernels.cuh -- device data structures and host launchers of every kernel.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point)
+
 #include "common.cuh"
 
 namespace ssb {
@@ -47,6 +49,9 @@ struct SorArgs {
     double* push_lo[kStateBuffers][2];
     double* push_hi[kStateBuffers][2];
     long long push_lo_off, push_hi_off;
+    // 2D-tiled TMA items (tile2d): rows x 32-slot segments loaded with tensor maps
+    int tile2d;
+    const struct TmaMaps* maps;  // device copy of the maps of U / rhs / coef (null: bulk copies)
     SorState* st;
     double omega, keep;
     double hc[4];           // heat stencil constants float(-dt/h_a^2) (solver.cpp:100-110)
@@ -64,6 +69,19 @@ struct SorArgs {
     int use_cond;
     cudaGraphConditionalHandle cond;
 };
+
+// Tensor maps of the 2D-tiled TMA pass (sor_tma.cu): 2D views [rows][slots] of the
+// colour-packed arrays, boxes of kTileR rows x (kTileS + 2) slots (fp64) or kTileS
+// slots x 8 faces (fp32 coefficients); the UK maps load kTileR + 2 rows.
+constexpr int kTileR = 8, kTileS = 32;
+struct TmaMaps {
+    CUtensorMap u_main[kStateBuffers][2];
+    CUtensorMap u_uk[kStateBuffers][2];
+    CUtensorMap rhs[2];
+    CUtensorMap coef[2];
+};
+// encode the maps of a's arrays into host memory (false: driver entry point unavailable)
+bool encode_tma_maps(const SorArgs& a, TmaMaps& m);
 
 constexpr int kPassBX = 32;  // doxels of one colour along a row
 constexpr int kPassBY = 8;   // rows (j) per block
@@ -84,7 +102,8 @@ void pass_tiles(const Layout& L, SorArgs& a);
 bool tma_pass_supported(const Layout& L);
 void tma_pass_tiles(const Layout& L, SorArgs& a);
 size_t tma_partials(const Layout& L);
-bool tma_fuse_ok(const Layout& L);  // the red pass can take the finalize into its tail
+bool tma_fuse_ok(const Layout& L);  // single slab: the finalize can move into the black pass
+double tma_lane_utilization(const Layout& L, bool tile2d);
 void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat);
 int pass_snake();   // SorArgs::snake default (env SSB_SNAKE)
 int pass_l2hint();  // SorArgs::l2hint default (env SSB_L2HINT)

@@ -27,6 +27,10 @@
 // item's canonical slice-major id, so per-slice sums do not depend on the
 // traversal or the grid size (same contract as sor.cu).
 #include <algorithm>
+#include <cstring>
+#include <string>
+
+#include <cudaTypedefs.h>
 #include <cstdlib>
 
 #include "sor_final.cuh"
@@ -102,6 +106,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// 2D tensor copy (box at coordinates {x, y}) with mbarrier completion
+__device__ __forceinline__ void tensor_g2s(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            sptr(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(sptr(bar))
+        : "memory");
+}
+
 // L2 eviction policies (createpolicy): streamed-once operands vs state rows
 struct Policies {
     uint64_t stream, uload, ustore;
@@ -131,13 +144,50 @@ struct Geo {  // per-launch tiling (identical on host and device)
     uint32_t off_coef, off_rhs, off_uc, off_ulm, off_ulp;
     uint32_t off_ukring;  // the UK ring follows the main ring
     uint32_t smem;
+    int S;     // 2D-tiled items: slots per segment (kTileS), 0: whole rows
+    int nsg;   // segments per row (1 for whole rows)
+    int pw;    // row pitch of a staged fp64 block, in slots (W, or kTileS + 2)
+    int cpw;   // row pitch of the staged coefficients, in floats (Wc * 8, or kTileS * 8)
 };
 
-__host__ __device__ inline Geo make_geo(const Layout& L) {
+__host__ __device__ inline Geo make_geo(const Layout& L, bool tile2d = false) {
     Geo g;
+    const int nq = (L.n1 + 1) / 2;  // slots of one colour per row
+    if (tile2d) {  // kTileR rows x kTileS-slot segments, every thread one slot
+        g.R = kTileR;
+        g.wpr = 0;
+        g.S = kTileS;
+        g.nsg = (nq + kTileS - 1) / kTileS;
+        g.pw = kTileS + 2;
+        g.cpw = kTileS * 8;
+        g.njg = (L.n2 + kTileR - 1) / kTileR;
+        g.nkc = (L.n3 + kPlanesPerItem - 1) / kPlanesPerItem;
+        g.items = (long long)g.nsg * g.njg * g.nkc * L.n4;
+        g.row_bytes = (uint32_t)g.pw * 8u;
+        g.coef_row_bytes = (uint32_t)g.cpw * 4u;
+        g.off_coef = 0;
+        g.off_rhs = g.R * g.coef_row_bytes;
+        g.off_uc = g.off_rhs + g.R * g.row_bytes;
+        g.off_ulm = g.off_uc + g.R * g.row_bytes;
+        g.off_ulp = g.off_ulm + g.R * g.row_bytes;
+        g.main_bytes = g.off_ulp + g.R * g.row_bytes;
+        // tensor copies land on 128-byte aligned shared addresses
+        auto up128 = [](uint32_t x) { return (x + 127u) & ~127u; };
+        g.off_uc = up128(g.off_uc);
+        g.off_ulm = up128(g.off_uc + g.R * g.row_bytes);
+        g.off_ulp = up128(g.off_ulm + g.R * g.row_bytes);
+        g.main_bytes = up128(g.off_ulp + g.R * g.row_bytes);
+        g.uk_bytes = up128((g.R + 2u) * g.row_bytes);
+        g.off_ukring = kMainStages * g.main_bytes;
+        g.smem = g.off_ukring + kUKStages * g.uk_bytes;
+        return g;
+    }
+    g.S = 0;
+    g.nsg = 1;
+    g.pw = L.W;
+    g.cpw = L.Wc * 8;
     const uint32_t rb = (uint32_t)L.W * 8u;
     const uint32_t crb = (uint32_t)L.Wc * 32u;
-    const int nq = (L.n1 + 1) / 2;  // slots of one colour per row
     // Rows per item.  Rows up to 256 slots: the 256 consumer threads take one slot
     // each over the item's R rows (flat mapping), so pick R <= 256 / nq filling the
     // most threads (ties: more rows, fewer halo rows) within the stage budget --
@@ -175,10 +225,12 @@ __host__ __device__ inline Geo make_geo(const Layout& L) {
 // Work item geometry (item = row group jg x plane chunk kc of slice l)
 struct Item {
     int l, j0, rows, k0, k1;
+    int s0;  // first slot (2D-tiled items), 0 for whole rows
 };
-__device__ __forceinline__ Item make_item(const Layout& L, const Geo& G, int l, int jg, int kc) {
+__device__ __forceinline__ Item make_item(const Layout& L, const Geo& G, int l, int jg, int kc, int sg = 0) {
     Item it;
     it.l = l;
+    it.s0 = sg * G.S;
     it.j0 = jg * G.R + 1;
     it.rows = min(G.R, L.n2 - it.j0 + 1);
     it.k0 = kc * kPlanesPerItem + 1;
@@ -194,26 +246,32 @@ __device__ __forceinline__ Item make_item(const Layout& L, const Geo& G, int l, 
 // grid is bigger than L2).
 __device__ __forceinline__ long long decode_item(const Layout& L, const Geo& G, int order, int l_lo, int nl,
                                                  long long t, Item& it) {
-    int l, jg, kc;
+    int l, jg, kc, sg;
     if (order == 0) {
-        const long long c = (long long)(l_lo - 1) * G.njg * G.nkc + t;
-        jg = (int)(c % G.njg);
-        const long long r = c / G.njg;
+        const long long c = (long long)(l_lo - 1) * G.nsg * G.njg * G.nkc + t;
+        sg = (int)(c % G.nsg);
+        const long long c2 = c / G.nsg;
+        jg = (int)(c2 % G.njg);
+        const long long r = c2 / G.njg;
         kc = (int)(r % G.nkc);
         l = (int)(r / G.nkc) + 1;
     } else if (order == 1) {
         l = l_lo + (int)(t % nl);
-        const long long r = t / nl;
+        const long long r0 = t / nl;
+        sg = (int)(r0 % G.nsg);
+        const long long r = r0 / G.nsg;
         jg = (int)(r % G.njg);
         kc = (int)(r / G.njg);
     } else {  // 2: slice fastest, then plane chunk (k-halo planes shared by neighbours in time)
         l = l_lo + (int)(t % nl);
-        const long long r = t / nl;
+        const long long r0 = t / nl;
+        sg = (int)(r0 % G.nsg);
+        const long long r = r0 / G.nsg;
         kc = (int)(r % G.nkc);
         jg = (int)(r / G.nkc);
     }
-    it = make_item(L, G, l, jg, kc);
-    return ((long long)(l - 1) * G.nkc + kc) * G.njg + jg;
+    it = make_item(L, G, l, jg, kc, sg);
+    return (((long long)(l - 1) * G.nkc + kc) * G.njg + jg) * G.nsg + sg;
 }
 
 template <int N>
@@ -245,10 +303,28 @@ template <bool HEAT>
 __device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsigned char* smem, uint64_t* full,
                                              uint64_t* empty, Ring<kMainStages>& rg, const Item& it,
                                              const float* coef, const double* rhs, const double* uc,
-                                             const double* uo, const Policies& pol) {
+                                             const double* uo, const Policies& pol,
+                                             const CUtensorMap* const* tm = nullptr) {
     const long long W = L.W;
     const long long plane_rows = (long long)L.jMax * L.kMax;
     const uint32_t rb = G.row_bytes;
+    if (G.S) {  // 2D-tiled: one tensor copy per stream, full boxes (out-of-range slots read as 0)
+        const CUtensorMap* const* m = tm;
+        for (int p = it.k0; p <= it.k1; ++p) {
+            rg.acquire(empty);
+            unsigned char* s = smem + rg.slot * G.main_bytes;
+            uint64_t* bar = &full[rg.slot];
+            mbar_expect_tx(bar, (HEAT ? 0u : G.R * G.coef_row_bytes) + 4u * G.R * rb);
+            const int row0 = (int)(((long long)it.l * L.kMax + p) * L.jMax + it.j0);
+            if (!HEAT) tensor_g2s(s + G.off_coef, m[0], it.s0 * 8, row0, bar);
+            tensor_g2s(s + G.off_rhs, m[1], it.s0, row0, bar);
+            tensor_g2s(s + G.off_uc, m[2], it.s0, row0, bar);
+            tensor_g2s(s + G.off_ulm, m[3], it.s0, row0 - (int)plane_rows, bar);
+            tensor_g2s(s + G.off_ulp, m[3], it.s0, row0 + (int)plane_rows, bar);
+            rg.advance();
+        }
+        return;
+    }
     for (int p = it.k0; p <= it.k1; ++p) {
         rg.acquire(empty);
         unsigned char* s = smem + rg.slot * G.main_bytes;
@@ -267,9 +343,21 @@ __device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsi
 // UK producer: the other colour's rows j0-1..j0+rows of planes k0-1 .. k1+1.
 __device__ __forceinline__ void produce_uk(const Layout& L, const Geo& G, unsigned char* smem, uint64_t* full,
                                            uint64_t* empty, Ring<kUKStages>& rg, const Item& it, const double* uo,
-                                           const Policies& pol) {
+                                           const Policies& pol, const CUtensorMap* uk_map = nullptr) {
     const long long W = L.W;
     const uint32_t rb = G.row_bytes;
+    if (G.S) {
+        for (int p = it.k0 - 1; p <= it.k1 + 1; ++p) {
+            rg.acquire(empty);
+            unsigned char* s = smem + G.off_ukring + rg.slot * G.uk_bytes;
+            uint64_t* bar = &full[rg.slot];
+            mbar_expect_tx(bar, (G.R + 2u) * rb);  // the box's bytes (the stage is padded to 128 B)
+            const int row0 = (int)(((long long)it.l * L.kMax + p) * L.jMax + it.j0);
+            tensor_g2s(s, uk_map, it.s0, row0 - 1, bar);
+            rg.advance();
+        }
+        return;
+    }
     for (int p = it.k0 - 1; p <= it.k1 + 1; ++p) {
         rg.acquire(empty);
         unsigned char* s = smem + G.off_ukring + rg.slot * G.uk_bytes;
@@ -302,16 +390,19 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
     // R rows) or, for rows wider than 256 slots, 8 warps striding along the row
     const int nq = (L.n1 + 1) / 2;
     const int tid = warp * 32 + lane;
-    const int r = G.wpr ? warp / G.wpr : tid / nq;
-    const int q_begin = G.wpr ? lane + 32 * (warp % G.wpr) : tid - r * nq;
-    const int q_step = G.wpr ? 32 * G.wpr : 1 << 30;
+    // 2D-tiled items (G.S): warp = row, lane = slot of the segment at it.s0
+    const int r = G.S ? warp : (G.wpr ? warp / G.wpr : tid / nq);
+    const int q_begin = G.S ? it.s0 + lane : (G.wpr ? lane + 32 * (warp % G.wpr) : tid - r * nq);
+    const int q_step = G.wpr && !G.S ? 32 * G.wpr : 1 << 30;
+    const int PW = G.pw;      // staged row pitch (slots)
+    const int sb0 = it.s0;    // global slot of the staged block's first column
     const int j = it.j0 + r;
     const bool row_ok = r < it.rows;  // (flat: tid < R * nq  <=>  r < R)
     // last slot q with i = 1 + par + 2q <= n1, per parity
     const int q_end0 = (L.n1 - 1) >> 1, q_end1 = (L.n1 - 2) >> 1;
     int par = (1 + j + it.k0 + it.l + L.lpar + C) & 1;
     // shared-memory element offsets of row r: R-row blocks / the (R+2)-row UK block
-    const int o_row = r * W, o_uk = (r + 1) * W;
+    const int o_row = r * PW - sb0, o_uk = (r + 1) * PW - sb0;  // index staged rows by GLOBAL slot
     double* wrow = ucw + L.row(j, it.k0, it.l) * (long long)W;  // this row at plane k0
     // halo push: the same row in the neighbours' arrays (first / last owned plane only)
     double* wlo = PUSH && push_lo ? push_lo + (wrow - ucw) + a.push_lo_off : nullptr;
@@ -334,7 +425,7 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
         const double* ukm = reinterpret_cast<const double*>(ukr + sm * G.uk_bytes) + o_uk;
         const double* ukc = reinterpret_cast<const double*>(ukr + sc * G.uk_bytes) + o_uk;
         const double* ukp = reinterpret_cast<const double*>(ukr + sp * G.uk_bytes) + o_uk;
-        const float* cf = reinterpret_cast<const float*>(mb + G.off_coef) + 8 * r * L.Wc;
+        const float* cf = reinterpret_cast<const float*>(mb + G.off_coef) + r * G.cpw - 8 * sb0;
         const double* rh = reinterpret_cast<const double*>(mb + G.off_rhs) + o_row;
         const double* u0r = reinterpret_cast<const double*>(mb + G.off_uc) + o_row;
         const double* ulm = reinterpret_cast<const double*>(mb + G.off_ulm) + o_row;
@@ -364,8 +455,8 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
                 d.u0 = u0r[m];
                 d.nb[0] = ukc[q];
                 d.nb[1] = ukc[q + 1];
-                d.nb[2] = ukc[m - W];
-                d.nb[3] = ukc[m + W];
+                d.nb[2] = ukc[m - PW];
+                d.nb[3] = ukc[m + PW];
                 d.nb[4] = ukm[m];
                 d.nb[5] = ukp[m];
                 d.nb[6] = ulm[m];
@@ -450,10 +541,10 @@ __global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_pass_tma(const 
     const double* uc = a.U[bin][C];
     const double* uo = C == 0 ? a.U[bin][1] : a.U[bout][0];
     double* ucw = a.U[bout][C];
-    const Geo G = make_geo(L);
+    const Geo G = make_geo(L, a.tile2d != 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nl = a.l_hi - a.l_lo + 1;
-    const long long n_items = (long long)G.njg * G.nkc * nl;
+    const long long n_items = (long long)G.nsg * G.njg * G.nkc * nl;
     // snake order: black passes walk the items backwards, so each pass starts on
     // the rows the previous pass touched last (still in L2)
     const bool rev = C == 1 && a.snake;
@@ -462,15 +553,26 @@ __global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_pass_tma(const 
 
     if (warp >= kConsumers) {  // producers: one thread per ring issues its bulk copies
         if (lane != 0) return;
+        // 2D-tiled: the tensor maps of the streams (coef, rhs, own colour, other colour)
+        const CUtensorMap* tm[4] = {nullptr, nullptr, nullptr, nullptr};
+        const CUtensorMap* tm_uk = nullptr;
+        if (G.S) {
+            const int bo = C == 0 ? bin : bout, co = C == 0 ? 1 : 0;
+            tm[0] = &a.maps->coef[C];
+            tm[1] = &a.maps->rhs[C];
+            tm[2] = &a.maps->u_main[bin][C];
+            tm[3] = &a.maps->u_main[bo][co];
+            tm_uk = &a.maps->u_uk[bo][co];
+        }
         Ring<kMainStages> rm;
         Ring<kUKStages> rk;
         for (long long tt = blockIdx.x; tt < n_items; tt += gridDim.x) {
             Item it;
             decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - tt : tt, it);
             if (warp == kConsumers)
-                produce_main<HEAT>(L, G, smem, bars.fullM, bars.emptyM, rm, it, a.coef[C], a.rhs[C], uc, uo, pol);
+                produce_main<HEAT>(L, G, smem, bars.fullM, bars.emptyM, rm, it, a.coef[C], a.rhs[C], uc, uo, pol, tm);
             else
-                produce_uk(L, G, smem, bars.fullK, bars.emptyK, rk, it, uo, pol);
+                produce_uk(L, G, smem, bars.fullK, bars.emptyK, rk, it, uo, pol, tm_uk);
         }
         return;
     }
@@ -532,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_wave_tma(const 
     const int n = *(volatile const int*)&st->n_red;
     const int epoch = *(volatile const int*)&st->epoch_base + n;
     const Layout& L = a.L;
-    const Geo G = make_geo(L);
+    const Geo G = make_geo(L, a.tile2d != 0);
     const int CH = G.njg * G.nkc;  // items per slice and phase
     // wavefront over sub-slices s = (l-1)*nkc + kc: phase d of step sigma works on
     // s = sigma - skew*d; each step has kWavePH phases x njg row groups
@@ -690,17 +792,66 @@ bool tma_pass_supported(const Layout& L) {
 }
 
 void tma_pass_tiles(const Layout& L, SorArgs& a) {
-    const Geo G = make_geo(L);
+    const Geo G = make_geo(L, a.tile2d != 0);
     a.tiles = G.items;
-    a.bps = G.njg * G.nkc * kWarps;  // partials per slice: one per (item, warp)
+    a.bps = G.nsg * G.njg * G.nkc * kWarps;  // partials per slice: one per (item, warp)
     a.tx = G.njg;
     a.ty = G.nkc;
-    a.tk = 1;
+    a.tk = G.nsg;
 }
 
 bool tma_fuse_ok(const Layout& L) { return L.glo && L.ghi; }  // single slab
 
-size_t tma_partials(const Layout& L) { return (size_t)make_geo(L).items * kWarps; }
+// fraction of the consumer threads that own a doxel slot in a plane step
+double tma_lane_utilization(const Layout& L, bool tile2d) {
+    const Geo G = make_geo(L, tile2d);
+    const int nq = (L.n1 + 1) / 2;
+    if (G.S) return nq / (double)(G.S * G.nsg);
+    if (G.wpr) return nq / (double)(kSlotsPerPlane * ((nq + kSlotsPerPlane - 1) / kSlotsPerPlane));
+    return G.R * nq / (double)kSlotsPerPlane;
+}
+
+size_t tma_partials(const Layout& L) {
+    return (size_t)std::max(make_geo(L).items, make_geo(L, true).items) * kWarps;
+}
+
+// ---- tensor maps of the 2D-tiled pass (driver API through the runtime's entry point)
+bool encode_tma_maps(const SorArgs& a, TmaMaps& m) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!enc) return false;
+    const Layout& L = a.L;
+    const cuuint32_t ones[2] = {1, 1};
+    auto map2d = [&](CUtensorMap* out, CUtensorMapDataType dt, const void* base, cuuint64_t cols, cuuint32_t esz,
+                     cuuint32_t bx, cuuint32_t by) {
+        const cuuint64_t dims[2] = {cols, (cuuint64_t)L.rows};
+        const cuuint64_t strides[1] = {cols * esz};
+        const cuuint32_t box[2] = {bx, by};
+        const CUresult r = enc(out, dt, 2, const_cast<void*>(base), dims, strides, box, ones,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error(SS_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    };
+    std::memset(&m, 0, sizeof m);
+    const cuuint32_t pw = kTileS + 2;
+    for (int b = 0; b < kStateBuffers; ++b)
+        for (int c = 0; c < 2; ++c) {
+            map2d(&m.u_main[b][c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, a.U[b][c], L.W, 8, pw, kTileR);
+            map2d(&m.u_uk[b][c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, a.U[b][c], L.W, 8, pw, kTileR + 2);
+        }
+    for (int c = 0; c < 2; ++c) {
+        map2d(&m.rhs[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, a.rhs[c], L.W, 8, pw, kTileR);
+        if (a.coef[c])
+            map2d(&m.coef[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.coef[c], (cuuint64_t)L.Wc * 8, 4, kTileS * 8, kTileR);
+    }
+    return true;
+}
 
 int wave_iters() { return kWavePH / 2; }
 
@@ -740,7 +891,7 @@ void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat) {
 }
 
 void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat) {
-    const Geo G = make_geo(a.L);
+    const Geo G = make_geo(a.L, a.tile2d != 0);
     const size_t smem = (size_t)G.smem;
     static size_t last_smem = 0;
     static int blocks = 0;
@@ -756,7 +907,7 @@ void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat
         blocks = tma_blocks((const void*)sor_pass_tma<0, false, false>, smem);
         last_smem = smem;
     }
-    const long long items = (long long)G.njg * G.nkc * (a.l_hi - a.l_lo + 1);
+    const long long items = (long long)G.nsg * G.njg * G.nkc * (a.l_hi - a.l_lo + 1);
     const unsigned grid = (unsigned)std::min<long long>(items, blocks);
     const bool push = a.push_lo[0][0] != nullptr || a.push_hi[0][0] != nullptr;
     const int v = (colour & 1) | (heat ? 2 : 0) | (push ? 4 : 0);

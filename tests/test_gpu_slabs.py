@@ -91,7 +91,7 @@ def test_nccl_session_world1(gpu):
     assert np.array_equal(u.view(np.uint64), d["u_rel"].view(np.uint64))
 
 
-@pytest.mark.parametrize("kernel", ["ldg", "tma", "wave", "resident", "auto"])
+@pytest.mark.parametrize("kernel", ["ldg", "tma", "wave", "resident", "auto", "tma2d"])
 def test_pass_kernels_agree(gpu, kernel):
     """Both SOR colour-pass kernels give the golden segment() result bit for bit."""
     d = dict(np.load(os.path.join(GOLD, "segment.npz")))
@@ -122,7 +122,7 @@ def test_kernels_agree_odd_shapes(gpu, oracle, dims):
               delta=0.5, vartheta=0.5, rescale_radius=2.0)
     st, uo, info = oracle.segment(cs.grid(dims, h), img, rows, oracle_params(kw))
     assert st == 0
-    for kernel in ("tma", "ldg", "resident"):
+    for kernel in ("tma", "ldg", "resident", "tma2d"):
         with gpu.Session(g) as s:
             s.set_kernel(kernel)
             s.prepare(img, rows, gpu.seg_params(**kw))
