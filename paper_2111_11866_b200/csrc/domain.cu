@@ -722,12 +722,10 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
         }
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (resident) {
-        if (profiling) {
-            e0 = pool_event(0);
-            e1 = pool_event(1);
-            SSB_CUDA(cudaEventRecord(e0, stream));
-        }
+    if (resident) {  // events around the single launch: profiling split and the live loop time
+        e0 = pool_event(0);
+        e1 = pool_event(1);
+        SSB_CUDA(cudaEventRecord(e0, stream));
         if (!launch_sor_resident(stream, a[0], heat)) {  // cannot be co-resident: pass kernels
             resident = false;
             kern = kernel == 4 ? 6 : 1;
@@ -735,12 +733,17 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
         }
     }
     if (resident) {
-        if (profiling) SSB_CUDA(cudaEventRecord(e1, stream));
+        SSB_CUDA(cudaEventRecord(e1, stream));
         SSB_CUDA(cudaMemcpyAsync(st_host, sp[0]->st.p, sizeof(SorState), cudaMemcpyDeviceToHost, stream));
         sync();
+        float lms = 0.f;
+        SSB_CUDA(cudaEventElapsedTime(&lms, e0, e1));
+        if (!heat) {  // passes run: red 1..it+1, black 1..it+1 (the last one speculative)
+            prof.loop_ms += lms;
+            prof.loop_passes += 2LL * st_host->iterations + 2;
+        }
         if (profiling) {  // one launch: split its time evenly over the colour passes it ran
-            float ms = 0.f;
-            SSB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            const float ms = lms;
             const int it = st_host->iterations;
             const double per = ms / (2.0 * it + 1.0);
             prof.red_ms += per * (it + 1);
@@ -764,9 +767,19 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
     const int limit = wave ? (max_iter + WI) / WI : max_iter + 1;
     if (single() && loop_mode == 1 && !profiling) {
         cudaGraphExec_t ex = graph_for(a[0], heat);
+        cudaEvent_t l0 = pool_event(0), l1 = pool_event(1);
+        SSB_CUDA(cudaEventRecord(l0, stream));
         SSB_CUDA(cudaGraphLaunch(ex, stream));
+        SSB_CUDA(cudaEventRecord(l1, stream));
         SSB_CUDA(cudaMemcpyAsync(st_host, sp[0]->st.p, sizeof(SorState), cudaMemcpyDeviceToHost, stream));
         sync();
+        if (!heat) {  // live SOR-loop time (the bench's roofline): events around the graph
+            float ms = 0.f;
+            SSB_CUDA(cudaEventElapsedTime(&ms, l0, l1));
+            prof.loop_ms += ms;
+            // passes run: red 1..it+1, black 1..it (+1 when the finalize sits in the black pass)
+            prof.loop_passes += 2LL * st_host->iterations + 1 + (a[0].fuse_final ? 1 : 0);
+        }
         const int bodies = wave ? st_host->iterations / WI + 1 : st_host->iterations + 1;
         const int U = graph_unroll();
         // kernels per loop body: red, finalize, black (finalize folded into black: 2;
