@@ -109,6 +109,7 @@ int pass_snake();   // SorArgs::snake default (env SSB_SNAKE)
 int pass_l2hint();  // SorArgs::l2hint default (env SSB_L2HINT)
 int pass_order();   // SorArgs::order default (env SSB_ORDER)
 int pass_fuse_final();  // SorArgs::fuse_final allowed (env SSB_FUSE_FINAL)
+int pass_pdl();         // programmatic dependent launch of the TMA passes (env SSB_PDL)
 bool wave_supported(const Layout& L);
 size_t wave_flags(const Layout& L);
 int wave_iters();  // SOR iterations per wavefront launch (SSB_WAVE_PHASES / 2)

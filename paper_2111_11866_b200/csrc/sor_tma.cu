@@ -527,6 +527,10 @@ __global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_pass_tma(const 
     __shared__ __align__(8) Bars bars;
     __shared__ double ws[32];
     __shared__ int last;
+    // prologue that touches no global memory, then wait for the previous kernel of the
+    // stream (programmatic dependent launch: this grid may start while it drains)
+    init_barriers(bars);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     SorState* st = a.st;
     if (*(volatile const int*)&st->done) return;
     const int n = C == 0 ? *(volatile const int*)&st->n_red : *(volatile const int*)&st->n_black;
@@ -549,7 +553,6 @@ __global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_pass_tma(const 
     // the rows the previous pass touched last (still in L2)
     const bool rev = C == 1 && a.snake;
     const Policies pol = make_policies(a.l2hint);
-    init_barriers(bars);
 
     if (warp >= kConsumers) {  // producers: one thread per ring issues its bulk copies
         if (lane != 0) return;
@@ -764,6 +767,13 @@ int pass_snake() {
     }();
     return v;
 }
+int pass_pdl() {
+    static const int v = [] {
+        const char* e = std::getenv("SSB_PDL");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
 int pass_fuse_final() {
     static const int v = [] {
         const char* e = std::getenv("SSB_FUSE_FINAL");
@@ -911,16 +921,24 @@ void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat
     const unsigned grid = (unsigned)std::min<long long>(items, blocks);
     const bool push = a.push_lo[0][0] != nullptr || a.push_hi[0][0] != nullptr;
     const int v = (colour & 1) | (heat ? 2 : 0) | (push ? 4 : 0);
-    switch (v) {
-        case 0: sor_pass_tma<0, false, false><<<grid, kThreads, smem, s>>>(a); break;
-        case 1: sor_pass_tma<1, false, false><<<grid, kThreads, smem, s>>>(a); break;
-        case 2: sor_pass_tma<0, true, false><<<grid, kThreads, smem, s>>>(a); break;
-        case 3: sor_pass_tma<1, true, false><<<grid, kThreads, smem, s>>>(a); break;
-        case 4: sor_pass_tma<0, false, true><<<grid, kThreads, smem, s>>>(a); break;
-        case 5: sor_pass_tma<1, false, true><<<grid, kThreads, smem, s>>>(a); break;
-        case 6: sor_pass_tma<0, true, true><<<grid, kThreads, smem, s>>>(a); break;
-        default: sor_pass_tma<1, true, true><<<grid, kThreads, smem, s>>>(a); break;
-    }
+    using K = void (*)(const SorArgs);
+    static const K fns[8] = {sor_pass_tma<0, false, false>, sor_pass_tma<1, false, false>,
+                             sor_pass_tma<0, true, false>,  sor_pass_tma<1, true, false>,
+                             sor_pass_tma<0, false, true>,  sor_pass_tma<1, false, true>,
+                             sor_pass_tma<0, true, true>,   sor_pass_tma<1, true, true>};
+    // programmatic dependent launch: the pass may be scheduled while the previous kernel
+    // drains; it waits (griddepcontrol.wait) before its first global read
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pass_pdl() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SSB_CUDA(cudaLaunchKernelEx(&cfg, fns[v], a));
     SSB_LAUNCHED();
 }
 
