@@ -2,9 +2,9 @@
 
 Loads ``oracle/liboracle.so`` (the C restatement, ``subsurf_oracle.c``) and,
 when present, ``oracle/_ref/libsubsurf_ref.so`` (the unmodified reference
-compiled in place).  Only tests/, ``__graft_entry__.smoke()`` and bench.py's
-cpu_baseline / reference legs import this module; the product package never
-does.
+compiled in place).  Only tests/ (incl. tests/perf/), ``__graft_entry__.smoke()``
+and bench.py's cpu_baseline / reference legs import this module; the product
+package never does.
 
 Arrays are numpy fp64 in the reference's ghost-padded layout, shape
 ``(n4+2, n3+2, n2+2, n1+2)`` (i fastest), coefficient arrays

@@ -2,8 +2,8 @@
  * subsurf_oracle.h -- CPU restatement of the reference SUBSURF hot path.
  *
  * TEST INFRASTRUCTURE ONLY.  This is the parity checker, never the product:
- * only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
- * legs may load it.  The product path (paper_2111_11866_b200) never links it
+ * only tests/ (incl. the reference-timing harnesses in tests/perf/),
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / reference legs may load it.  The product path (paper_2111_11866_b200) never links it
  * and has no CPU fallback.
  *
  * Every function restates one reference function in plain C with the same

@@ -4,7 +4,7 @@ threads, n4)) on the host cores of the same box, same workload, same steps.
 Both: steps 1..S after the same prepare; the reference's per-step wall times come
 from its own segment() loop (ref_segment step_seconds)."""
 import json, os, sys, time
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np
 import paper_2111_11866_b200 as ss

@@ -4,7 +4,7 @@ centres, predecessor candidates on the GPU; linking on the host) vs the
 reference's own track() (oracle/_ref, single-threaded CPU) on the same u.
 u = the config-2 nuclei image (256x256x64 x 32 frames, ~150 nuclei), level 0.3."""
 import json, os, sys, time
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np
 import paper_2111_11866_b200 as ss
