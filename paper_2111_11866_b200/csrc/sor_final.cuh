@@ -14,33 +14,53 @@
 
 namespace ssb {
 
-// 256 threads (tid 0..255) synchronised with named barrier 1: fixed-shape tree
-__device__ __forceinline__ double group256_sum(double v, double* ws, int tid) {
+// The fixed-shape 256-lane tree, run by NT = 256 or 128 threads (tid 0..NT-1,
+// named barrier 1): thread tid plays lanes tid + k*NT, k < 256/NT, so the sum is
+// the same bits whichever NT runs it.
+template <int NT = 256>
+__device__ __forceinline__ double group256_sum(const double (&v)[256 / NT], double* ws, int tid) {
+    constexpr int V = 256 / NT;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if ((tid & 31) == 0) ws[tid >> 5] = v;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    if (tid < 32) {
-        v = tid < 8 ? ws[tid] : 0.0;
+    for (int k = 0; k < V; ++k) {
+        double x = v[k];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if ((tid & 31) == 0) ws[(tid + k * NT) >> 5] = x;
     }
-    return v;  // valid in tid 0
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    double x = 0.0;
+    if (tid < 32) {
+        x = tid < 8 ? ws[tid] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    }
+    return x;  // valid in tid 0
+}
+__device__ __forceinline__ double group256_sum(double v, double* ws, int tid) {
+    const double a[1] = {v};
+    return group256_sum<256>(a, ws, tid);
 }
 
 // residual of slice l (local, 0-based) of state n-1; valid in tid 0
+template <int NT = 256>
 __device__ __forceinline__ double slice_residual(const SorArgs& a, int n, int l, double* ws, int tid) {
+    constexpr int V = 256 / NT;
     const double* pr = a.part[n & 3][0] + (long long)l * a.bps;        // red(n)
     const double* pb = a.part[(n - 1) & 3][1] + (long long)l * a.bps;  // black(n-1)
-    double r = 0.0, b = 0.0;
-    for (int q = tid; q < a.bps; q += 256) {
-        r += __ldcg(pr + q);
-        b += __ldcg(pb + q);
+    double r[V], b[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        r[k] = 0.0;
+        b[k] = 0.0;
+        for (int q = tid + k * NT; q < a.bps; q += 256) {
+            r[k] += __ldcg(pr + q);
+            b[k] += __ldcg(pb + q);
+        }
     }
-    r = group256_sum(r, ws, tid);
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    b = group256_sum(b, ws, tid);
-    return b + r;  // slice_black + red (solver.cpp:359)
+    const double rs = group256_sum<NT>(r, ws, tid);
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    const double bs = group256_sum<NT>(b, ws, tid);
+    return bs + rs;  // slice_black + red (solver.cpp:359)
 }
 
 // Decision of iteration n-1 from the per-slice residuals of ALL slices in
@@ -78,16 +98,17 @@ __device__ __forceinline__ void sor_decide_state(const SorArgs& a, SorState* st,
 // runs after it -- and the CTA that completes the last slice decides.  The
 // black pass of iteration n runs whatever the decision (if iterate n-1 has
 // converged it only writes buffer out(n), which nobody reads).  Called by the
-// 256 consumer threads of a CTA.
+// NT consumer threads of a CTA (the same bits for NT = 128 or 256).
+template <int NT = 256>
 __device__ __forceinline__ void black_head_finalize(const SorArgs& a, int n, double* ws, int* last, int tid) {
     int mine = 0;
     for (int l = blockIdx.x; l < a.L.n4; l += gridDim.x) {
         if (n >= 2) {
-            const double v = slice_residual(a, n, l, ws, tid);
+            const double v = slice_residual<NT>(a, n, l, ws, tid);
             if (tid == 0) a.slice_res[l] = v;
         }
         ++mine;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
     }
     if (!mine) return;
     if (tid == 0) {

@@ -20,16 +20,14 @@ __device__ __forceinline__ void store_u(double* p, double v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
-// The update of solver.cpp:292-313; returns the squared residual contribution
-// (black: in-sweep, :309-312; red: of the incoming state, :347-356).
+// The update of solver.cpp:292-313: the new value and the squared residual
+// contribution (black: in-sweep, :309-312; red: of the incoming state, :347-356).
 // Every rounding is the reference's: the products c_f * u_f are formed once and
 // feed both the update (acc -= p_f) and the red residual (res += p_f) -- the
 // reference evaluates the same products in both places -- so the three
 // dependency chains (diag sum, acc, residual) can overlap.
-template <int C, bool HINT = false, bool MIRROR = false>
-__device__ __forceinline__ double compute_doxel(const SorArgs& a, const DoxelIn& d,
-                                                double* __restrict__ ucw, uint64_t pol = 0,
-                                                double* mir_lo = nullptr, double* mir_hi = nullptr) {
+template <int C>
+__device__ __forceinline__ void doxel_update(const SorArgs& a, const DoxelIn& d, double& unew, double& r2) {
     const double c0 = (double)d.c[0], c1 = (double)d.c[1], c2 = (double)d.c[2];
     const double c3 = (double)d.c[3], c4 = (double)d.c[4], c5 = (double)d.c[5];
     const double c6 = (double)d.c[6], c7 = (double)d.c[7];
@@ -56,30 +54,32 @@ __device__ __forceinline__ double compute_doxel(const SorArgs& a, const DoxelIn&
         res += p6;
         res += p7;
         const double ubar = acc / dg;
-        const double unew = a.omega * ubar + a.keep * d.u0;
-        if constexpr (HINT)
-            store_u(ucw + d.p, unew, pol);
-        else
-            ucw[d.p] = unew;
-        if constexpr (MIRROR) {  // halo push (uniform per work item)
-            if (mir_lo) mir_lo[d.p] = unew;
-            if (mir_hi) mir_hi[d.p] = unew;
-        }
-        return res * res;
+        unew = a.omega * ubar + a.keep * d.u0;
+        r2 = res * res;
     } else {
         const double ubar = acc / dg;
-        const double unew = a.omega * ubar + a.keep * d.u0;
-        if constexpr (HINT)
-            store_u(ucw + d.p, unew, pol);
-        else
-            ucw[d.p] = unew;
-        if constexpr (MIRROR) {
-            if (mir_lo) mir_lo[d.p] = unew;
-            if (mir_hi) mir_hi[d.p] = unew;
-        }
+        unew = a.omega * ubar + a.keep * d.u0;
         const double res = dg * (unew - ubar);
-        return res * res;
+        r2 = res * res;
     }
+}
+
+// doxel_update + the store(s) of the new value; returns the squared residual
+template <int C, bool HINT = false, bool MIRROR = false>
+__device__ __forceinline__ double compute_doxel(const SorArgs& a, const DoxelIn& d,
+                                                double* __restrict__ ucw, uint64_t pol = 0,
+                                                double* mir_lo = nullptr, double* mir_hi = nullptr) {
+    double unew, r2;
+    doxel_update<C>(a, d, unew, r2);
+    if constexpr (HINT)
+        store_u(ucw + d.p, unew, pol);
+    else
+        ucw[d.p] = unew;
+    if constexpr (MIRROR) {  // halo push (uniform per work item)
+        if (mir_lo) mir_lo[d.p] = unew;
+        if (mir_hi) mir_hi[d.p] = unew;
+    }
+    return r2;
 }
 
 }  // namespace ssb

@@ -50,6 +50,14 @@ constexpr int kWarps = SSB_CONSUMER_WARPS;  // consumer warps, one residual part
 constexpr int kConsumers = kWarps;
 constexpr int kSlotsPerPlane = kConsumers * 32;   // consumer threads: one slot each (flat mapping)
 constexpr int kThreads = (kConsumers + 2) * 32;  // + a producer warp per ring
+#ifndef SSB_FLAT_WARPS
+#define SSB_FLAT_WARPS 8
+#endif
+// flat-mapping kernels: kFlatWarps consumer warps, each thread kFlatV of the 256 slots
+constexpr int kFlatWarps = SSB_FLAT_WARPS;
+constexpr int kFlatV = kWarps / kFlatWarps;
+static_assert(kFlatWarps * kFlatV == kWarps && (kFlatV == 1 || kFlatV == 2), "SSB_FLAT_WARPS: 8 or 4");
+__host__ __device__ constexpr int pass_threads(bool flat) { return ((flat ? kFlatWarps : kConsumers) + 2) * 32; }
 #ifndef SSB_MAIN_STAGES
 #define SSB_MAIN_STAGES 4
 #endif
@@ -77,6 +85,22 @@ constexpr int kDefaultOrder = 1;
 constexpr int kWavePH = SSB_WAVE_PHASES;
 
 __device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// shared-memory loads at a 32-bit shared address (+ a constant byte offset).  volatile:
+// they stay behind the mbarrier waits (also volatile asm) that publish the stage.
+template <int OFF>
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(addr), "n"(OFF));
+    return v;
+}
+template <int OFF>
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+%5];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr), "n"(OFF));
+    return v;
+}
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sptr(bar)), "r"(count) : "memory");
@@ -245,33 +269,36 @@ __device__ __forceinline__ Item make_item(const Layout& L, const Geo& G, int l, 
 // concurrently and share their other-colour rows through L2 (a slice of a large
 // grid is bigger than L2).
 __device__ __forceinline__ long long decode_item(const Layout& L, const Geo& G, int order, int l_lo, int nl,
-                                                 long long t, Item& it) {
-    int l, jg, kc, sg;
+                                                 long long t64, Item& it) {
+    // item counts stay far below 2^31 (host_launch checks), so 32-bit division suffices
+    const unsigned t = (unsigned)t64;
+    unsigned l, jg, kc, sg;
+    const unsigned nsg = (unsigned)G.nsg, njg = (unsigned)G.njg, nkc = (unsigned)G.nkc;
     if (order == 0) {
-        const long long c = (long long)(l_lo - 1) * G.nsg * G.njg * G.nkc + t;
-        sg = (int)(c % G.nsg);
-        const long long c2 = c / G.nsg;
-        jg = (int)(c2 % G.njg);
-        const long long r = c2 / G.njg;
-        kc = (int)(r % G.nkc);
-        l = (int)(r / G.nkc) + 1;
+        const unsigned c = (unsigned)(l_lo - 1) * nsg * njg * nkc + t;
+        sg = c % nsg;
+        const unsigned c2 = c / nsg;
+        jg = c2 % njg;
+        const unsigned r = c2 / njg;
+        kc = r % nkc;
+        l = r / nkc + 1;
     } else if (order == 1) {
-        l = l_lo + (int)(t % nl);
-        const long long r0 = t / nl;
-        sg = (int)(r0 % G.nsg);
-        const long long r = r0 / G.nsg;
-        jg = (int)(r % G.njg);
-        kc = (int)(r / G.njg);
+        const unsigned r0 = t / (unsigned)nl;
+        l = (unsigned)l_lo + (t - r0 * (unsigned)nl);
+        const unsigned r = nsg == 1 ? r0 : r0 / nsg;
+        sg = r0 - r * nsg;
+        kc = r / njg;
+        jg = r - kc * njg;
     } else {  // 2: slice fastest, then plane chunk (k-halo planes shared by neighbours in time)
-        l = l_lo + (int)(t % nl);
-        const long long r0 = t / nl;
-        sg = (int)(r0 % G.nsg);
-        const long long r = r0 / G.nsg;
-        kc = (int)(r % G.nkc);
-        jg = (int)(r / G.nkc);
+        const unsigned r0 = t / (unsigned)nl;
+        l = (unsigned)l_lo + (t - r0 * (unsigned)nl);
+        const unsigned r = nsg == 1 ? r0 : r0 / nsg;
+        sg = r0 - r * nsg;
+        jg = r / nkc;
+        kc = r - jg * nkc;
     }
-    it = make_item(L, G, l, jg, kc, sg);
-    return (((long long)(l - 1) * G.nkc + kc) * G.njg + jg) * G.nsg + sg;
+    it = make_item(L, G, (int)l, (int)jg, (int)kc, (int)sg);
+    return (((long long)(l - 1) * nkc + kc) * njg + jg) * nsg + sg;
 }
 
 template <int N>
@@ -304,7 +331,7 @@ __device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsi
                                              uint64_t* empty, Ring<kMainStages>& rg, const Item& it,
                                              const float* coef, const double* rhs, const double* uc,
                                              const double* uo, const Policies& pol,
-                                             const CUtensorMap* const* tm = nullptr) {
+                                             const CUtensorMap* const* tm = nullptr, bool issue = true) {
     const long long W = L.W;
     const long long plane_rows = (long long)L.jMax * L.kMax;
     const uint32_t rb = G.row_bytes;
@@ -314,13 +341,15 @@ __device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsi
             rg.acquire(empty);
             unsigned char* s = smem + rg.slot * G.main_bytes;
             uint64_t* bar = &full[rg.slot];
-            mbar_expect_tx(bar, (HEAT ? 0u : G.R * G.coef_row_bytes) + 4u * G.R * rb);
             const int row0 = (int)(((long long)it.l * L.kMax + p) * L.jMax + it.j0);
-            if (!HEAT) tensor_g2s(s + G.off_coef, m[0], it.s0 * 8, row0, bar);
-            tensor_g2s(s + G.off_rhs, m[1], it.s0, row0, bar);
-            tensor_g2s(s + G.off_uc, m[2], it.s0, row0, bar);
-            tensor_g2s(s + G.off_ulm, m[3], it.s0, row0 - (int)plane_rows, bar);
-            tensor_g2s(s + G.off_ulp, m[3], it.s0, row0 + (int)plane_rows, bar);
+            if (issue) {
+                mbar_expect_tx(bar, (HEAT ? 0u : G.R * G.coef_row_bytes) + 4u * G.R * rb);
+                if (!HEAT) tensor_g2s(s + G.off_coef, m[0], it.s0 * 8, row0, bar);
+                tensor_g2s(s + G.off_rhs, m[1], it.s0, row0, bar);
+                tensor_g2s(s + G.off_uc, m[2], it.s0, row0, bar);
+                tensor_g2s(s + G.off_ulm, m[3], it.s0, row0 - (int)plane_rows, bar);
+                tensor_g2s(s + G.off_ulp, m[3], it.s0, row0 + (int)plane_rows, bar);
+            }
             rg.advance();
         }
         return;
@@ -329,13 +358,15 @@ __device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsi
         rg.acquire(empty);
         unsigned char* s = smem + rg.slot * G.main_bytes;
         uint64_t* bar = &full[rg.slot];
-        mbar_expect_tx(bar, (HEAT ? 0u : it.rows * G.coef_row_bytes) + 4u * it.rows * rb);
         const long long row0 = ((long long)it.l * L.kMax + p) * L.jMax + it.j0;  // row (j0, p, l)
-        if (!HEAT) bulk_g2s(s + G.off_coef, coef + row0 * L.Wc * 8, it.rows * G.coef_row_bytes, bar, pol.stream);
-        bulk_g2s(s + G.off_rhs, rhs + row0 * W, it.rows * rb, bar, pol.stream);
-        bulk_g2s(s + G.off_uc, uc + row0 * W, it.rows * rb, bar, pol.uload);
-        bulk_g2s(s + G.off_ulm, uo + (row0 - plane_rows) * W, it.rows * rb, bar, pol.uload);
-        bulk_g2s(s + G.off_ulp, uo + (row0 + plane_rows) * W, it.rows * rb, bar, pol.uload);
+        if (issue) {
+            mbar_expect_tx(bar, (HEAT ? 0u : it.rows * G.coef_row_bytes) + 4u * it.rows * rb);
+            if (!HEAT) bulk_g2s(s + G.off_coef, coef + row0 * L.Wc * 8, it.rows * G.coef_row_bytes, bar, pol.stream);
+            bulk_g2s(s + G.off_rhs, rhs + row0 * W, it.rows * rb, bar, pol.stream);
+            bulk_g2s(s + G.off_uc, uc + row0 * W, it.rows * rb, bar, pol.uload);
+            bulk_g2s(s + G.off_ulm, uo + (row0 - plane_rows) * W, it.rows * rb, bar, pol.uload);
+            bulk_g2s(s + G.off_ulp, uo + (row0 + plane_rows) * W, it.rows * rb, bar, pol.uload);
+        }
         rg.advance();
     }
 }
@@ -343,7 +374,8 @@ __device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsi
 // UK producer: the other colour's rows j0-1..j0+rows of planes k0-1 .. k1+1.
 __device__ __forceinline__ void produce_uk(const Layout& L, const Geo& G, unsigned char* smem, uint64_t* full,
                                            uint64_t* empty, Ring<kUKStages>& rg, const Item& it, const double* uo,
-                                           const Policies& pol, const CUtensorMap* uk_map = nullptr) {
+                                           const Policies& pol, const CUtensorMap* uk_map = nullptr,
+                                           bool issue = true) {
     const long long W = L.W;
     const uint32_t rb = G.row_bytes;
     if (G.S) {
@@ -351,9 +383,11 @@ __device__ __forceinline__ void produce_uk(const Layout& L, const Geo& G, unsign
             rg.acquire(empty);
             unsigned char* s = smem + G.off_ukring + rg.slot * G.uk_bytes;
             uint64_t* bar = &full[rg.slot];
-            mbar_expect_tx(bar, (G.R + 2u) * rb);  // the box's bytes (the stage is padded to 128 B)
             const int row0 = (int)(((long long)it.l * L.kMax + p) * L.jMax + it.j0);
-            tensor_g2s(s, uk_map, it.s0, row0 - 1, bar);
+            if (issue) {
+                mbar_expect_tx(bar, (G.R + 2u) * rb);  // the box's bytes (the stage is padded to 128 B)
+                tensor_g2s(s, uk_map, it.s0, row0 - 1, bar);
+            }
             rg.advance();
         }
         return;
@@ -362,9 +396,11 @@ __device__ __forceinline__ void produce_uk(const Layout& L, const Geo& G, unsign
         rg.acquire(empty);
         unsigned char* s = smem + G.off_ukring + rg.slot * G.uk_bytes;
         uint64_t* bar = &full[rg.slot];
-        mbar_expect_tx(bar, (it.rows + 2) * rb);
         const long long row0 = ((long long)it.l * L.kMax + p) * L.jMax + it.j0;
-        bulk_g2s(s, uo + (row0 - 1) * W, (it.rows + 2) * rb, bar, pol.uload);
+        if (issue) {
+            mbar_expect_tx(bar, (it.rows + 2) * rb);
+            bulk_g2s(s, uo + (row0 - 1) * W, (it.rows + 2) * rb, bar, pol.uload);
+        }
         rg.advance();
     }
 }
@@ -472,10 +508,8 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
 #endif
             }
         __syncwarp();
-        if (lane == 0) {
-            mbar_arrive(&emptyM[ms]);  // plane p's operands are done
-            mbar_arrive(&emptyK[sm]);  // and plane p-1's other-colour rows
-        }
+        mbar_arrive(&emptyM[ms]);  // plane p's operands are done (every consumer thread arrives)
+        mbar_arrive(&emptyK[sm]);  // and plane p-1's other-colour rows
         next_stage<kMainStages>(ms, mph);
         sm = sc;
         pm = pc;
@@ -490,10 +524,8 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
     }
     // the last two UK stages of the item (planes k1, k1+1)
     __syncwarp();
-    if (lane == 0) {
-        mbar_arrive(&emptyK[sm]);
-        mbar_arrive(&emptyK[sc]);
-    }
+    mbar_arrive(&emptyK[sm]);
+    mbar_arrive(&emptyK[sc]);
     next_stage<kUKStages>(sc, pc);
     s0 = sc;
     ph0 = pc;
@@ -502,34 +534,177 @@ __device__ __forceinline__ double consume_item(const SorArgs& a, const Layout& L
     return r2;
 }
 
+// Per-thread constants of the flat slot mapping (rows of <= 256 slots, whole-row
+// items): thread tid owns row r = tid / nq, slot q = tid % nq of every item.
+struct FlatThread {
+    int r, q;
+    uint32_t t_coef;  // byte offset of its 8 coefficients in a main stage
+    uint32_t t_row;   // byte offset of slot q of row r in an R-row block
+    uint32_t t_uk;    // byte offset of slot q of row r + 1 in the (R+2)-row UK block
+    uint32_t act;     // bit par: slot q holds a doxel of parity par (q <= q_end[par])
+};
+__device__ __forceinline__ FlatThread flat_thread(const Layout& L, const Geo& G, int tid) {
+    FlatThread f;
+    const int nq = (L.n1 + 1) / 2;
+    f.r = tid / nq;
+    f.q = tid - f.r * nq;
+    const int ra = f.r < G.R ? f.r : 0;  // idle threads (r >= R) read row 0's operands
+    f.t_coef = G.off_coef + (uint32_t)(ra * G.cpw + 8 * f.q) * 4u;
+    f.t_row = (uint32_t)(ra * G.pw + f.q) * 8u;
+    f.t_uk = (uint32_t)((ra + 1) * G.pw + f.q) * 8u;
+    f.act = (f.q <= ((L.n1 - 1) >> 1) ? 1u : 0u) | (f.q <= ((L.n1 - 2) >> 1) ? 2u : 0u);
+    return f;
+}
+
+// consume_item for the flat mapping: the same update, with every shared-memory
+// address a per-thread constant plus a stage base carried from plane to plane
+// (the general version re-derives its addresses per plane: ~35 integer
+// instructions per warp-plane against ~90 for the arithmetic itself).
+template <int C, bool PUSH, int V>
+__device__ __forceinline__ void consume_item_flat(const SorArgs& a, const Layout& L, const Geo& G,
+                                                  const FlatThread (&ft)[V], uint32_t sbase, uint64_t* fullM,
+                                                  uint64_t* emptyM, uint64_t* fullK, uint64_t* emptyK, uint32_t& ms,
+                                                  uint32_t& mph, uint32_t& s0, uint32_t& ph0, const Item& it,
+                                                  double* __restrict__ ucw, double* push_lo, double* push_hi,
+                                                  double (&r2)[V]) {
+    // V virtual threads per thread (slots tid + k * consumer threads): their updates
+    // are independent, so they are computed branch-free side by side and stored
+    // under a predicate
+    uint32_t act[V], par[V], trow[V];
+    double* wq[V];
+    double* wlo[V];
+    double* whi[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        const int j = it.j0 + ft[k].r;
+        act[k] = ft[k].r < it.rows ? ft[k].act : 0u;
+        par[k] = (uint32_t)(1 + j + it.k0 + it.l + L.lpar + C) & 1u;
+        const long long row0 = L.row(j, it.k0, it.l) * (long long)L.W + ft[k].q;
+        wq[k] = ucw + row0;  // slot q of this row at plane k0 (+ par: the doxel's slot)
+        wlo[k] = PUSH && push_lo ? push_lo + row0 + a.push_lo_off : nullptr;
+        whi[k] = PUSH && push_hi ? push_hi + row0 + a.push_hi_off : nullptr;
+        trow[k] = ft[k].t_row;
+        r2[k] = 0.0;
+    }
+    long long wstep = (long long)L.jMax * L.W;
+    asm("" : "+l"(wstep));  // opaque: keep it in registers, not re-derived per plane
+    const uint32_t pwb = (uint32_t)G.pw * 8u;
+    // shared addresses: UK stages of planes p-1, p, p+1 (stage bases), main stage of p
+    const uint32_t ukb = sbase + G.off_ukring;
+    uint32_t sm = s0, pm = ph0;
+    uint32_t sc = sm, pc = pm;
+    next_stage<kUKStages>(sc, pc);
+    uint32_t am = ukb + sm * G.uk_bytes, ac = ukb + sc * G.uk_bytes;
+    uint32_t amain = sbase + ms * G.main_bytes;
+    mbar_wait(&fullK[sm], pm);
+    mbar_wait(&fullK[sc], pc);
+    for (int p = it.k0; p <= it.k1; ++p) {
+        uint32_t sp = sc, pp = pc;
+        next_stage<kUKStages>(sp, pp);
+        const uint32_t ap = sp == 0 ? ukb : ac + G.uk_bytes;
+        mbar_wait(&fullK[sp], pp);
+        mbar_wait(&fullM[ms], mph);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const bool on = (act[k] >> par[k]) & 1u;
+            if (V == 1 && !on) continue;
+            const uint32_t par8 = par[k] * 8u;
+            const uint32_t cf = amain + ft[k].t_coef;
+            const uint32_t x = amain + trow[k] + par8;  // slot m = q + par of row r
+            const uint32_t yc = ac + ft[k].t_uk;         // slot q of the UK row r + 1
+            const uint32_t y = yc + par8;                // slot m of the UK row r + 1
+            const float4 lo = lds_f4<0>(cf), hi = lds_f4<16>(cf);
+            DoxelIn d;
+            d.c[0] = lo.x; d.c[1] = lo.y; d.c[2] = lo.z; d.c[3] = lo.w;
+            d.c[4] = hi.x; d.c[5] = hi.y; d.c[6] = hi.z; d.c[7] = hi.w;
+            d.rhs = lds_f64<0>(x + G.off_rhs);
+            d.u0 = lds_f64<0>(x + G.off_uc);
+            d.nb[0] = lds_f64<0>(yc);  // slot q   <-> i - 1
+            d.nb[1] = lds_f64<8>(yc);  // slot q+1 <-> i + 1
+            d.nb[2] = lds_f64<0>(y - pwb);
+            d.nb[3] = lds_f64<0>(y + pwb);
+            d.nb[4] = lds_f64<0>(am + ft[k].t_uk + par8);
+            d.nb[5] = lds_f64<0>(ap + ft[k].t_uk + par8);
+            d.nb[6] = lds_f64<0>(x + G.off_ulm);
+            d.nb[7] = lds_f64<0>(x + G.off_ulp);
+            double unew, e2;
+            doxel_update<C>(a, d, unew, e2);
+            if (on) {
+                wq[k][par[k]] = unew;
+                if constexpr (PUSH) {
+                    if (wlo[k]) wlo[k][par[k]] = unew;
+                    if (whi[k]) whi[k][par[k]] = unew;
+                }
+                r2[k] += e2;
+            }
+        }
+        // every consumer thread arrives for itself (release: its reads are done)
+        mbar_arrive(&emptyM[ms]);  // plane p's operands
+        mbar_arrive(&emptyK[sm]);  // plane p-1's other-colour rows
+        if (++ms == kMainStages) {
+            ms = 0;
+            mph ^= 1u;
+            amain = sbase;
+        } else {
+            amain += G.main_bytes;
+        }
+        sm = sc;
+        pm = pc;
+        sc = sp;
+        pc = pp;
+        am = ac;
+        ac = ap;
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            par[k] ^= 1u;
+            wq[k] += wstep;
+            if constexpr (PUSH) {
+                if (wlo[k]) wlo[k] += wstep;
+                if (whi[k]) whi[k] += wstep;
+            }
+        }
+    }
+    mbar_arrive(&emptyK[sm]);
+    mbar_arrive(&emptyK[sc]);
+    next_stage<kUKStages>(sc, pc);
+    s0 = sc;
+    ph0 = pc;
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r2[k] += __shfl_down_sync(0xffffffffu, r2[k], o);
+}
+
 struct Bars {
     uint64_t fullM[kMainStages], emptyM[kMainStages], fullK[kUKStages], emptyK[kUKStages];
 };
 
-__device__ __forceinline__ void init_barriers(Bars& b) {
+__device__ __forceinline__ void init_barriers(Bars& b, uint32_t consumer_threads = kConsumers * 32) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < kMainStages; ++s) {
             mbar_init(&b.fullM[s], 1);
-            mbar_init(&b.emptyM[s], kConsumers);
+            mbar_init(&b.emptyM[s], consumer_threads);
         }
         for (int s = 0; s < kUKStages; ++s) {
             mbar_init(&b.fullK[s], 1);
-            mbar_init(&b.emptyK[s], kConsumers);
+            mbar_init(&b.emptyK[s], consumer_threads);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 }
 
-template <int C, bool HEAT, bool PUSH>
-__global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_pass_tma(const SorArgs a) {
+template <int C, bool HEAT, bool PUSH, bool FLAT>
+__global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_tma(const SorArgs a) {
+    constexpr int NW = FLAT ? kFlatWarps : kConsumers;  // consumer warps of this kernel
+    constexpr int V = FLAT ? kFlatV : 1;                 // slots per consumer thread
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) Bars bars;
     __shared__ double ws[32];
     __shared__ int last;
     // prologue that touches no global memory, then wait for the previous kernel of the
     // stream (programmatic dependent launch: this grid may start while it drains)
-    init_barriers(bars);
+    init_barriers(bars, NW * 32);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     SorState* st = a.st;
     if (*(volatile const int*)&st->done) return;
@@ -554,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_pass_tma(const 
     const bool rev = C == 1 && a.snake;
     const Policies pol = make_policies(a.l2hint);
 
-    if (warp >= kConsumers) {  // producers: one thread per ring issues its bulk copies
+    if (warp >= NW) {  // producers: one thread per ring issues its bulk copies
         if (lane != 0) return;
         // 2D-tiled: the tensor maps of the streams (coef, rhs, own colour, other colour)
         const CUtensorMap* tm[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -572,24 +747,37 @@ __global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_pass_tma(const 
         for (long long tt = blockIdx.x; tt < n_items; tt += gridDim.x) {
             Item it;
             decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - tt : tt, it);
-            if (warp == kConsumers)
+            if (warp == NW)
                 produce_main<HEAT>(L, G, smem, bars.fullM, bars.emptyM, rm, it, a.coef[C], a.rhs[C], uc, uo, pol, tm);
             else
                 produce_uk(L, G, smem, bars.fullK, bars.emptyK, rk, it, uo, pol, tm_uk);
         }
         return;
     }
-    if (C == 1 && a.fuse_final && threadIdx.x < 256)  // the finalize's fixed 256-thread tree
-        black_head_finalize(a, n, ws, &last, threadIdx.x);
+    if (C == 1 && a.fuse_final)  // the finalize's fixed 256-lane tree, NW * 32 threads
+        black_head_finalize<NW * 32>(a, n, ws, &last, threadIdx.x);
     uint32_t ms = 0, mph = 0, s0 = 0, ph0 = 0;
+    // FLAT (host-chosen): whole-row items with the flat slot mapping, not heat.  Thread
+    // tid plays the 8-warp mapping's threads tid + k * NW * 32 (k < V), and writes
+    // their warps' residual partials, so the partials are the same bits for any V.
+    FlatThread ft[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) ft[k] = FLAT ? flat_thread(L, G, threadIdx.x + k * NW * 32) : FlatThread{};
     for (long long tt = blockIdx.x; tt < n_items; tt += gridDim.x) {
         Item it;
         const long long t = decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - tt : tt, it);
         double* plo = PUSH && it.l == 1 ? a.push_lo[bout][C] : nullptr;
         double* phi = PUSH && it.l == L.n4 ? a.push_hi[bout][C] : nullptr;
-        const double r2 = consume_item<C, HEAT, PUSH>(a, L, G, smem, bars.fullM, bars.emptyM, bars.fullK, bars.emptyK,
-                                                ms, mph, s0, ph0, it, ucw, warp, lane, pol.ustore, plo, phi);
-        if (lane == 0) a.part[n & 3][C][t * kWarps + warp] = r2;
+        double r2[V];
+        if constexpr (FLAT)
+            consume_item_flat<C, PUSH, V>(a, L, G, ft, sptr(smem), bars.fullM, bars.emptyM, bars.fullK, bars.emptyK, ms,
+                                          mph, s0, ph0, it, ucw, plo, phi, r2);
+        else
+            r2[0] = consume_item<C, HEAT, PUSH>(a, L, G, smem, bars.fullM, bars.emptyM, bars.fullK, bars.emptyK, ms,
+                                                mph, s0, ph0, it, ucw, warp, lane, pol.ustore, plo, phi);
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < V; ++k) a.part[n & 3][C][t * kWarps + warp + k * NW] = r2[k];
     }
     // halo push to another GPU: this thread's peer stores are performed before the
     // pass completes (the signal kernel that follows publishes the pass)
@@ -723,11 +911,11 @@ __global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_wave_tma(const 
     }
 }
 
-template <int C, bool HEAT, bool PUSH>
+template <int C, bool HEAT, bool PUSH, bool FLAT = false>
 void configure() {
     static bool done = false;
     if (!done) {
-        SSB_CUDA(cudaFuncSetAttribute(sor_pass_tma<C, HEAT, PUSH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SSB_CUDA(cudaFuncSetAttribute(sor_pass_tma<C, HEAT, PUSH, FLAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       200 * 1024));
         done = true;
     }
@@ -745,7 +933,7 @@ void configure_wave() {
 
 // resident CTAs for this kernel and shared-memory size (the wavefront kernel
 // relies on every CTA being resident: items wait only on earlier items)
-int tma_blocks(const void* fn, size_t smem_bytes) {
+int tma_blocks(const void* fn, size_t smem_bytes, int threads = kThreads) {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -753,7 +941,7 @@ int tma_blocks(const void* fn, size_t smem_bytes) {
         SSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
     int per = 0;
-    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, smem_bytes));
+    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem_bytes));
     return sms * std::max(1, per);
 }
 
@@ -798,7 +986,9 @@ int pass_l2hint() {
 
 bool tma_pass_supported(const Layout& L) {
     const Geo G = make_geo(L);
-    return (size_t)G.smem <= 200 * 1024;
+    // decode_item works in 32 bits
+    const long long lim = 1LL << 31;
+    return (size_t)G.smem <= 200 * 1024 && G.items < lim && make_geo(L, true).items < lim;
 }
 
 void tma_pass_tiles(const Layout& L, SorArgs& a) {
@@ -904,7 +1094,7 @@ void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat
     const Geo G = make_geo(a.L, a.tile2d != 0);
     const size_t smem = (size_t)G.smem;
     static size_t last_smem = 0;
-    static int blocks = 0;
+    static int blocks[2] = {0, 0};  // general / flat kernels
     if (smem != last_smem) {
         configure<0, false, false>();
         configure<1, false, false>();
@@ -914,23 +1104,33 @@ void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat
         configure<1, false, true>();
         configure<0, true, true>();
         configure<1, true, true>();
-        blocks = tma_blocks((const void*)sor_pass_tma<0, false, false>, smem);
+        configure<0, false, false, true>();
+        configure<1, false, false, true>();
+        configure<0, false, true, true>();
+        configure<1, false, true, true>();
+        blocks[0] = tma_blocks((const void*)sor_pass_tma<0, false, false, false>, smem, pass_threads(false));
+        blocks[1] = tma_blocks((const void*)sor_pass_tma<0, false, false, true>, smem, pass_threads(true));
         last_smem = smem;
     }
+    const bool flat = !heat && !G.S && !G.wpr;
     const long long items = (long long)G.nsg * G.njg * G.nkc * (a.l_hi - a.l_lo + 1);
-    const unsigned grid = (unsigned)std::min<long long>(items, blocks);
+    const unsigned grid = (unsigned)std::min<long long>(items, blocks[flat]);
     const bool push = a.push_lo[0][0] != nullptr || a.push_hi[0][0] != nullptr;
-    const int v = (colour & 1) | (heat ? 2 : 0) | (push ? 4 : 0);
+    const int v = (colour & 1) | (heat ? 2 : 0) | (push ? 4 : 0) | (flat ? 8 : 0);
     using K = void (*)(const SorArgs);
-    static const K fns[8] = {sor_pass_tma<0, false, false>, sor_pass_tma<1, false, false>,
-                             sor_pass_tma<0, true, false>,  sor_pass_tma<1, true, false>,
-                             sor_pass_tma<0, false, true>,  sor_pass_tma<1, false, true>,
-                             sor_pass_tma<0, true, true>,   sor_pass_tma<1, true, true>};
+    static const K fns[16] = {sor_pass_tma<0, false, false, false>, sor_pass_tma<1, false, false, false>,
+                              sor_pass_tma<0, true, false, false>,  sor_pass_tma<1, true, false, false>,
+                              sor_pass_tma<0, false, true, false>,  sor_pass_tma<1, false, true, false>,
+                              sor_pass_tma<0, true, true, false>,   sor_pass_tma<1, true, true, false>,
+                              sor_pass_tma<0, false, false, true>,  sor_pass_tma<1, false, false, true>,
+                              nullptr,                              nullptr,
+                              sor_pass_tma<0, false, true, true>,   sor_pass_tma<1, false, true, true>,
+                              nullptr,                              nullptr};
     // programmatic dependent launch: the pass may be scheduled while the previous kernel
     // drains; it waits (griddepcontrol.wait) before its first global read
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(pass_threads(flat));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];

@@ -10,9 +10,10 @@ make -s -C $C >/dev/null
 mkdir -p $ROOT/variants/$1
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 SRC=${3:-sor_tma.cu}
-OBJ=${SRC%.cu}.o
+case $SRC in /*) ;; *) SRC=$C/$SRC ;; esac  # a path outside csrc/ replaces the same-named source
+OBJ=$(basename ${SRC%.cu}).o
 nvcc $ARCH -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC,-fvisibility=hidden -I$ROOT/include $2 \
-    -c -o $ROOT/variants/$1/$OBJ $C/$SRC
+    -I$C -c -o $ROOT/variants/$1/$OBJ $SRC
 OBJS=$(ls $C/build/*.o | grep -v "/$OBJ")
 nvcc $ARCH -shared -o $ROOT/variants/$1.so $OBJS $ROOT/variants/$1/$OBJ -Xlinker -z,defs -lcudart_static -lrt -lpthread -ldl
 echo variants/$1.so

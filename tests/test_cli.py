@@ -106,9 +106,18 @@ def test_cli_threshold_and_eoc(cli, oracle, tmp_path):
     assert np.array_equal(th, tho[1:-1, 1:-1, 1:-1, 1:-1].astype("<f4"))
     r = subprocess.run([cli, "eoc", "--max-n", "20"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
-    lines = r.stdout.strip().splitlines()
+    lines = r.stdout.rstrip("\n").splitlines()
     assert len(lines) == 3 and float(lines[1].split()[3]) == pytest.approx(1.684177e-2, rel=1e-6)
     assert float(lines[2].split()[4]) == pytest.approx(1.851052, rel=1e-5)
+    # print_report's exact layout (eoc.cpp:193-203): header, setw(4)/setw(9)/setw(10) columns,
+    # scientific error, fixed EOC from the second row on
+    assert lines[0] == "   n          h  final step         error        EOC"
+    for q, (n, steps) in enumerate(((10, 1), (20, 4))):
+        err = float(lines[q + 1].split()[3])
+        want = f"{n:4d}  {2.5 / n:>9g}  {steps:10d}  {err:.6e}"
+        if q:
+            want += f"   {float(lines[q + 1].split()[4]):.6f}"
+        assert lines[q + 1] == want
 
 
 @pytest.mark.gpu
