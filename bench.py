@@ -365,6 +365,18 @@ def main():
             traffic = json.load(open(tf)).get(args.config, {}).get("sor_pass_bytes")
         except Exception:
             traffic = None
+    # halo exchange (t-slabs, N > 1): its device time on the comm stream and the part the
+    # compute stream waited for after the interior slices (max over ranks)
+    halo = None
+    if pr.get("halo_n"):
+        h = torch.tensor([pr["halo_ms"] / pr["halo_n"], pr["halo_exposed_ms"] / pr["halo_n"]], device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(h, op=torch.distributed.ReduceOp.MAX)
+        xm, ex = (float(v) for v in h.tolist())
+        halo = {"exchanges_timed": int(pr["halo_n"]), "exchange_ms": xm, "exposed_ms": ex,
+                "overlapped_ms": max(0.0, xm - ex), "pass_ms": pass_ms_kernel,
+                "source": "profiling run: events on the comm stream around each colour pass's "
+                          "exchange and on the compute stream after its interior slices (max over ranks)"}
     sor_share = (pr["red_ms"] + pr["black_ms"]) / max(1e-9, pr["red_ms"] + pr["black_ms"] + pr["assemble_ms"] + pr["rescale_ms"])
 
     if rank == 0:
@@ -392,6 +404,8 @@ def main():
                          "peak_source": peak_src, "sor_share_of_step": sor_share},
             "clocks": clk.summary(),
         }
+        if halo:
+            line["halo"] = halo
         if world == 1 and not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline_sample(wl)

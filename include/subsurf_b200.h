@@ -227,13 +227,20 @@ SS_API ss_status ss_session_set_profiling(ss_session* s, int enable);
 /* accumulated since the last call (then reset): total ms in red passes, black
  * passes, assembly kernels and rescale, and the number of each (profiling mode);
  * loop_ms / loop_passes: device time of the SOR loops (events around each CUDA-graph
- * solve, recorded in normal running at no cost) and the colour passes they ran */
+ * solve, recorded in normal running at no cost) and the colour passes they ran;
+ * halo_*: exchange time exposed vs overlapped (multi-slab, profiling mode) */
 typedef struct {
     double red_ms, black_ms, assemble_ms, rescale_ms;
     long long red_n, black_n, assemble_n, rescale_n;
     long long sweeps; /* completed red+black sweeps */
     double loop_ms;
     long long loop_passes;
+    /* multi-slab solves with the halo exchange on the comm stream (profiling mode):
+     * halo_ms = device time of the exchanges (the comm stream, events around each),
+     * halo_exposed_ms = how much of it the compute stream waited for after its interior
+     * slices were done (the rest overlapped them), halo_n = exchanges timed */
+    double halo_ms, halo_exposed_ms;
+    long long halo_n;
 } ss_profile;
 SS_API ss_status ss_session_profile(ss_session* s, ss_profile* out);
 /* algorithmic bytes of one SOR colour pass: 28 B x interior doxels (SURVEY 8(d):

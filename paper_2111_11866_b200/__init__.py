@@ -132,7 +132,8 @@ class Profile(C.Structure):
     _fields_ = [("red_ms", C.c_double), ("black_ms", C.c_double), ("assemble_ms", C.c_double),
                 ("rescale_ms", C.c_double), ("red_n", C.c_longlong), ("black_n", C.c_longlong),
                 ("assemble_n", C.c_longlong), ("rescale_n", C.c_longlong),
-                ("sweeps", C.c_longlong), ("loop_ms", C.c_double), ("loop_passes", C.c_longlong)]
+                ("sweeps", C.c_longlong), ("loop_ms", C.c_double), ("loop_passes", C.c_longlong),
+                ("halo_ms", C.c_double), ("halo_exposed_ms", C.c_double), ("halo_n", C.c_longlong)]
 
 
 def seg_params(**kw) -> SegParams:

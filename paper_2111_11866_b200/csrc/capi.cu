@@ -98,7 +98,7 @@ struct ss_session {
 extern "C" {
 
 const char* ss_last_error(void) { return t_err.c_str(); }
-int ss_abi_version(void) { return 3; }
+int ss_abi_version(void) { return 4; }
 unsigned long long ss_launch_count(void) { return g_launches.load(); }
 
 int ss_device_available(void) {

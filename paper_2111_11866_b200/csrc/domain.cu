@@ -507,6 +507,9 @@ std::vector<double> Domain::gather_values(const std::vector<std::vector<double>>
     return out;
 }
 
+// profiling events per host-driven loop body: the red/black pass bounds + 3 per exchange
+constexpr int kBodyEvents = 10;
+
 cudaEvent_t Domain::pool_event(size_t idx) {
     while (ev_pool.size() <= idx) {
         cudaEvent_t e;
@@ -643,12 +646,16 @@ void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>
             launch_sor_pass_range(stream, x, colour, heat, 1, 1);
             if (n4 > 1) launch_sor_pass_range(stream, x, colour, heat, n4, n4);
         }
+        // profiling: x[0] exchange start (comm), x[1] exchange end (comm), x[2] interior done
+        cudaEvent_t* xe = ev4 ? ev4 + 4 + 3 * colour : nullptr;
         SSB_CUDA(cudaEventRecord(ev_bnd, stream));
         SSB_CUDA(cudaStreamWaitEvent(comm, ev_bnd, 0));
+        if (xe) SSB_CUDA(cudaEventRecord(xe[0], comm));
         tr->exchange(sp, F, colour == 0 ? 1 : 2, comm);
-        SSB_CUDA(cudaEventRecord(ev_xchg, comm));
+        SSB_CUDA(cudaEventRecord(xe ? xe[1] : ev_xchg, comm));
         for (const SorArgs& x : a) launch_sor_pass_range(stream, x, colour, heat, 2, x.L.n4 - 1);
-        SSB_CUDA(cudaStreamWaitEvent(stream, ev_xchg, 0));
+        if (xe) SSB_CUDA(cudaEventRecord(xe[2], stream));
+        SSB_CUDA(cudaStreamWaitEvent(stream, xe ? xe[1] : ev_xchg, 0));
     };
     if (ev4) SSB_CUDA(cudaEventRecord(ev4[0], stream));
     pass(0);
@@ -761,6 +768,9 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
         return o;
     }
     const bool wave = a[0].wave != 0;
+    // exchanges on the comm stream (not the in-kernel halo push): timed in profiling mode
+    const bool halo_timed = profiling && !single() && !wave && a[0].push_lo[0][0] == nullptr &&
+                            a[0].push_hi[0][0] == nullptr;
     // loop bodies: red(max_iter+1) evaluates the last residual; a wavefront body
     // covers two iterations
     const int WI = wave_iters();
@@ -797,12 +807,13 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
             const int nb = std::min(nb_chunk, limit - launched);
             for (int b = 0; b < nb; ++b) {
                 const int n = launched + b + 1;
-                cudaEvent_t evs[4];
+                // per body: red/black pass bounds (4) + the two exchanges' events (multi-slab, 6)
+                cudaEvent_t evs[kBodyEvents];
                 cudaEvent_t* e4 = nullptr;
                 if (profiling) {
-                    for (int q = 0; q < 4; ++q) evs[q] = pool_event(ev_used + q);
+                    for (int q = 0; q < kBodyEvents; ++q) evs[q] = pool_event(ev_used + q);
                     body_ev.push_back(ev_used);
-                    ev_used += 4;
+                    ev_used += kBodyEvents;
                     e4 = evs;
                 }
                 if (single())
@@ -850,6 +861,17 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
                     prof.black_ms += ms;
                     prof.black_n++;
                 }
+                if (halo_timed)  // both exchanges of the body: duration, and the part not hidden
+                    for (int c = 0; c < 2; ++c) {
+                        if (c == 0 ? (int)b > it : (int)b >= it) continue;
+                        const size_t x = base + 4 + 3 * c;
+                        float xm = 0.f, wait = 0.f;
+                        SSB_CUDA(cudaEventElapsedTime(&xm, ev_pool[x], ev_pool[x + 1]));
+                        SSB_CUDA(cudaEventElapsedTime(&wait, ev_pool[x + 2], ev_pool[x + 1]));
+                        prof.halo_ms += xm;
+                        prof.halo_exposed_ms += wait > 0.f ? wait : 0.f;
+                        prof.halo_n++;
+                    }
             }
         }
     }

@@ -69,6 +69,13 @@ __host__ __device__ constexpr int pass_threads(bool flat) { return ((flat ? kFla
 #endif
 constexpr int kMainStages = SSB_MAIN_STAGES;  // per-plane operands (consumed by one plane)
 constexpr int kUKStages = SSB_UK_STAGES;      // other-colour planes (held for three planes)
+#ifndef SSB_FULL_ROWS
+// 1: the flat consumer also rewrites a row's ghost/pad slots, so row stores cover whole
+// 32-byte sectors.  MEASURED (config 1 red pass, ncu): DRAM reads 502.6 -> 493.1 MB (the
+// L2 fills of partial sectors), but +25% instructions; per sweep config 1 -1%, config 2
+// +5.5% (power-capped clock).  Off.
+#define SSB_FULL_ROWS 0
+#endif
 #ifndef SSB_PLANES_PER_ITEM
 #define SSB_PLANES_PER_ITEM 16  // measured: 8 -> 16 planes: config 2/4 -6%, config 1 -1% per sweep (fewer k-halo rows)
 #endif
@@ -542,6 +549,12 @@ struct FlatThread {
     uint32_t t_row;   // byte offset of slot q of row r in an R-row block
     uint32_t t_uk;    // byte offset of slot q of row r + 1 in the (R+2)-row UK block
     uint32_t act;     // bit par: slot q holds a doxel of parity par (q <= q_end[par])
+    // slots of the row no doxel of parity par covers (the i-ghost and the even-W pad):
+    // [0, par) and [hi[par], W).  The row's first / last thread rewrites them with the
+    // input row's values (equal in every state buffer), so the row store covers whole
+    // 32-byte sectors and L2 does not fill the partial ones from DRAM.
+    uint32_t fill;    // bit 0: first thread of its row, bit 1: last thread of its row
+    int hi0, hi1;     // hi[par] - q: first high fill slot relative to q
 };
 __device__ __forceinline__ FlatThread flat_thread(const Layout& L, const Geo& G, int tid) {
     FlatThread f;
@@ -553,6 +566,9 @@ __device__ __forceinline__ FlatThread flat_thread(const Layout& L, const Geo& G,
     f.t_row = (uint32_t)(ra * G.pw + f.q) * 8u;
     f.t_uk = (uint32_t)((ra + 1) * G.pw + f.q) * 8u;
     f.act = (f.q <= ((L.n1 - 1) >> 1) ? 1u : 0u) | (f.q <= ((L.n1 - 2) >> 1) ? 2u : 0u);
+    f.fill = SSB_FULL_ROWS && f.r < G.R ? (f.q == 0 ? 1u : 0u) | (f.q == nq - 1 ? 2u : 0u) : 0u;
+    f.hi0 = ((L.n1 - 1) >> 1) + 1 - f.q;
+    f.hi1 = ((L.n1 - 2) >> 1) + 2 - f.q;
     return f;
 }
 
@@ -636,6 +652,13 @@ __device__ __forceinline__ void consume_item_flat(const SorArgs& a, const Layout
                     if (whi[k]) whi[k][par[k]] = unew;
                 }
                 r2[k] += e2;
+            }
+            if (SSB_FULL_ROWS && ft[k].fill && ft[k].r < it.rows) {  // ghost / pad slots of the row
+                const uint32_t xu = amain + trow[k] + G.off_uc;         // slot q of the input row
+                if ((ft[k].fill & 1u) && par[k]) wq[k][0] = lds_f64<0>(xu);
+                if (ft[k].fill & 2u)
+                    for (int e = par[k] ? ft[k].hi1 : ft[k].hi0; ft[k].q + e < L.W; ++e)
+                        wq[k][e] = lds_f64<0>(xu + 8u * (uint32_t)e);
             }
         }
         // every consumer thread arrives for itself (release: its reads are done)

@@ -135,3 +135,31 @@ def test_kernels_agree_odd_shapes(gpu, oracle, dims):
 def oracle_params(kw):
     from oracle.oracle_py import seg_params
     return seg_params(**kw)
+
+
+def test_halo_exchange_timing(gpu):
+    """Profiling mode times the halo exchanges of a multi-slab solve (comm stream) and the
+    part the compute stream waited for (bench.py's "halo" object for N > 1): every
+    exchange of the timed passes is counted, and results are unchanged by the timing."""
+    dims = (12, 10, 8, 8)
+    h = 1.0 / 12
+    g = gpu.Grid.make(dims, h)
+    img = cs.f32_image(dims, 9)
+    rows = [(f, 5.5, 4.5, 3.5, 1.5) for f in range(dims[3])]
+    p = gpu.seg_params(tau=h, epsilon=1e-3, omega=1.4, n_steps=1, sigma=np.sqrt(2) * h, K=100.0,
+                       delta=0.5, vartheta=0.5, rescale_radius=3.0)
+    outs = []
+    for prof in (False, True):
+        with gpu.Session(g, n_slabs=4) as s:
+            s.set_kernel("ldg")  # exchange copies between the passes (no in-kernel halo push)
+            s.prepare(img, rows, p)
+            s.set_profiling(prof)
+            s.profile()
+            r = s.fixed_sweeps(12)
+            pr = s.profile()
+            outs.append((r, s.get_u()))
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][1].view(np.uint64), outs[1][1].view(np.uint64))
+    assert pr["halo_n"] == pr["red_n"] + pr["black_n"] >= 2 * 12  # one exchange per colour pass
+    assert pr["halo_ms"] > 0.0
+    assert 0.0 <= pr["halo_exposed_ms"] <= pr["red_ms"] + pr["black_ms"]
