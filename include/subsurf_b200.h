@@ -222,6 +222,9 @@ SS_API ss_status ss_session_set_loop_mode(ss_session* s, int mode);
  * cooperative launch), 2 = two-iteration TMA wavefront (experimental; measured slower
  * on B200) */
 SS_API ss_status ss_session_set_kernel(ss_session* s, int kernel);
+/* kernel code (as above; 7 = one-sweep k-wavefront) the session's last segmentation
+ * SOR solve ran after the support checks (-1: none yet) */
+SS_API ss_status ss_session_sor_kernel(ss_session* s, int* kernel);
 /* per-pass CUDA-event timing of the SOR kernels (forces the host-driven loop) */
 SS_API ss_status ss_session_set_profiling(ss_session* s, int enable);
 /* accumulated since the last call (then reset): total ms in red passes, black

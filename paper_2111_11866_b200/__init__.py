@@ -216,6 +216,7 @@ def library() -> C.CDLL:
                                C.POINTER(C.c_longlong)])
     sig("ss_session_set_profiling", [C.c_void_p, C.c_int])
     sig("ss_session_set_kernel", [C.c_void_p, C.c_int])
+    sig("ss_session_sor_kernel", [C.c_void_p, C.POINTER(C.c_int)])
     sig("ss_session_profile", [C.c_void_p, C.POINTER(Profile)])
     _lib = L
     return L
@@ -599,7 +600,14 @@ class Session:
         in one cooperative launch (LDG tiles, grid barriers); 'wave': two-iteration TMA
         wavefront through L2 (experimental, measured slower)."""
         _check(library().ss_session_set_kernel(
-            self._h, {"ldg": 0, "tma": 1, "wave": 2, "resident": 3, "auto": 4, "tma2d": 5}[kernel]))
+            self._h, {"ldg": 0, "tma": 1, "wave": 2, "resident": 3, "auto": 4, "tma2d": 5,
+                       "kwave": 7}[kernel]))
+
+    def sor_kernel(self) -> str:
+        """The SOR kernel the last segmentation solve ran (after the support checks)."""
+        k = C.c_int(-1)
+        _check(library().ss_session_sor_kernel(self._h, C.byref(k)))
+        return {-1: "none", 0: "ldg", 1: "tma", 2: "wave", 3: "resident", 5: "tma2d", 7: "kwave"}[k.value]
 
     def set_profiling(self, on: bool) -> None:
         _check(library().ss_session_set_profiling(self._h, 1 if on else 0))

@@ -638,9 +638,17 @@ ss_status ss_session_set_loop_mode(ss_session* s, int mode) {
 ss_status ss_session_set_kernel(ss_session* s, int kernel) {
     return guard([&] {
         require(s != nullptr, "null session");
-        require(kernel >= 0 && kernel <= 5,
-                "kernel must be 0 (LDG), 1 (TMA), 2 (TMA wavefront), 3 (resident), 4 (auto) or 5 (2D-tiled TMA)");
+        require(kernel >= 0 && kernel <= 7 && kernel != 6,
+                "kernel must be 0 (LDG), 1 (TMA), 2 (TMA wavefront), 3 (resident), 4 (auto), 5 (2D-tiled TMA) "
+                "or 7 (one-sweep k-wavefront)");
         s->d->kernel = kernel;
+    });
+}
+
+ss_status ss_session_sor_kernel(ss_session* s, int* kernel) {
+    return guard([&] {
+        require(s != nullptr && kernel != nullptr, "null argument");
+        *kernel = s->d->last_kernel;
     });
 }
 

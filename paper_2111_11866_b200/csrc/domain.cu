@@ -150,7 +150,8 @@ Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int 
     coef[1].alloc(L.rows * L.Wc * 8);
     SorArgs t{};
     pass_tiles(L, t);
-    const size_t nparts = std::max({(size_t)t.tiles * kPassBY, tma_partials(L), resident_partials(L)});
+    const size_t nparts = std::max({(size_t)t.tiles * kPassBY, tma_partials(L), resident_partials(L),
+                                    kwave_supported(L) ? kwave_partials(L) : (size_t)0});
     for (auto& pp : part) {
         pp[0].alloc(nparts);
         pp[1].alloc(nparts);
@@ -166,8 +167,9 @@ Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int 
     }
     gloc.alloc(8);
     gall.alloc((size_t)world * 8);
-    if (world == 1 && wave_supported(L)) {
-        wflags.alloc(wave_flags(L));
+    if (world == 1 && (wave_supported(L) || kwave_supported(L))) {
+        wflags.alloc(std::max(wave_supported(L) ? wave_flags(L) : (size_t)0,
+                              kwave_supported(L) ? kwave_flags(L) : (size_t)0));
         SSB_CUDA(cudaMemsetAsync(wflags.p, 0, wflags.n * sizeof(int), stream));
     }
     SSB_CUDA(cudaMemsetAsync(slice_res.p, 0, slice_res.n * sizeof(double), stream));
@@ -315,7 +317,8 @@ SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool he
     a.tma = kernel >= 1 && tma_pass_supported(L) ? 1 : 0;
     a.l_lo = 1;
     a.l_hi = L.n4;
-    a.wave = kernel == 2 && world == 1 && wflags.p != nullptr ? 1 : 0;
+    a.wave = kernel == 2 && world == 1 && wflags.p != nullptr && wave_supported(L) ? 1 : 0;
+    if (kernel == 7 && !heat && world == 1 && wflags.p != nullptr && kwave_supported(L)) a.wave = 2;
     a.flags = wflags.p;
     a.snake = pass_snake();
     a.l2hint = pass_l2hint();
@@ -336,6 +339,7 @@ SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool he
         tma_pass_tiles(L, a);
     else
         pass_tiles(L, a);
+    if (a.wave == 2) a.bps = kwave_bps(L);  // one partial per (plane-chunk item, warp)
     a.use_cond = 0;
     return a;
 }
@@ -728,6 +732,8 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
             a[s].push_hi_off = -(long long)sp[s]->L.n4 * P1;                 // my plane n4 -> its plane 0
         }
     }
+    if (!heat)
+        last_kernel = resident ? 3 : a[0].wave == 2 ? 7 : a[0].wave == 1 ? 2 : !a[0].tma ? 0 : a[0].tile2d ? 5 : 1;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (resident) {  // events around the single launch: profiling split and the live loop time
         e0 = pool_event(0);
@@ -737,6 +743,7 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
             resident = false;
             kern = kernel == 4 ? 6 : 1;
             a[0] = sp[0]->sor_args(B[0].data(), rhs[0], heat, omega, hc, world, kern);
+            if (!heat) last_kernel = a[0].tile2d ? 5 : 1;
         }
     }
     if (resident) {
@@ -773,7 +780,7 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
                             a[0].push_hi[0][0] == nullptr;
     // loop bodies: red(max_iter+1) evaluates the last residual; a wavefront body
     // covers two iterations
-    const int WI = wave_iters();
+    const int WI = a[0].wave == 1 ? wave_iters() : 1;
     const int limit = wave ? (max_iter + WI) / WI : max_iter + 1;
     if (single() && loop_mode == 1 && !profiling) {
         cudaGraphExec_t ex = graph_for(a[0], heat);
@@ -788,7 +795,8 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
             SSB_CUDA(cudaEventElapsedTime(&ms, l0, l1));
             prof.loop_ms += ms;
             // passes run: red 1..it+1, black 1..it (+1 when the finalize sits in the black pass)
-            prof.loop_passes += 2LL * st_host->iterations + 1 + (a[0].fuse_final ? 1 : 0);
+            prof.loop_passes += a[0].wave == 2 ? 2LL * (st_host->iterations + 1)  // k-wavefront bodies
+                                               : 2LL * st_host->iterations + 1 + (a[0].fuse_final ? 1 : 0);
         }
         const int bodies = wave ? st_host->iterations / WI + 1 : st_host->iterations + 1;
         const int U = graph_unroll();

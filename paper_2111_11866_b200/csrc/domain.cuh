@@ -219,6 +219,7 @@ struct Domain {
     ss_seg_params prm{};
 
     int loop_mode = 1;
+    int last_kernel = -1;  // kernel code the last non-heat solve ran (ss_session_sor_kernel)
     int kernel = 4;   // SOR: 4 = auto (default: resident when the working set fits L2, else TMA),
                       // 1 = TMA two-pass, 0 = LDG two-pass, 3 = resident (one cooperative launch
                       // per solve), 2 = TMA wavefront (experimental, slower; sor_tma.cu)

@@ -60,7 +60,7 @@ struct SorArgs {
     long long tiles;
     int tma;                // 1: TMA-fed pass kernel (sor_tma.cu), 0: LDG pass (sor.cu)
     int l_lo, l_hi;         // slices (local, 1-based) a pass launch covers (default 1 .. n4)
-    int wave;               // 1: two-iteration wavefront kernel per loop body
+    int wave;               // 1: two-iteration wavefront kernel per loop body, 2: one-sweep k-wavefront
     int* flags;             // wavefront item completion flags (epochs)
     int snake;              // TMA pass: black passes walk the items in reverse (L2 reuse at the turn)
     int order;              // TMA pass item order: 0 slice-major, 1 slice-fastest
@@ -112,6 +112,13 @@ int pass_fuse_final();  // SorArgs::fuse_final allowed (env SSB_FUSE_FINAL)
 int pass_pdl();         // programmatic dependent launch of the TMA passes (env SSB_PDL)
 bool wave_supported(const Layout& L);
 size_t wave_flags(const Layout& L);
+// one-sweep k-wavefront (kernel 7, sor_tma.cu): support test, flag / partial sizes,
+// partials per slice, launch (one iteration: red + black)
+bool kwave_supported(const Layout& L);
+size_t kwave_flags(const Layout& L);
+size_t kwave_partials(const Layout& L);
+int kwave_bps(const Layout& L);
+void launch_sor_kwave(cudaStream_t s, const SorArgs& a);
 int wave_iters();  // SOR iterations per wavefront launch (SSB_WAVE_PHASES / 2)
 void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat);
 dim3 pass_grid(const Layout& L);

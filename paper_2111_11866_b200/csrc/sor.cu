@@ -433,6 +433,18 @@ bool launch_sor_resident(cudaStream_t s, const SorArgs& a, bool heat) {
 }
 
 void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* ev) {
+    if (a.wave == 2) {  // one sweep (red + black) in one k-wavefront launch, then the decision
+        if (ev) SSB_CUDA(cudaEventRecord(ev[0], s));
+        launch_sor_kwave(s, a);
+        if (ev) SSB_CUDA(cudaEventRecord(ev[1], s));
+        sor_finalize<<<a.L.n4, 256, 0, s>>>(a);
+        SSB_LAUNCHED();
+        if (ev) {
+            SSB_CUDA(cudaEventRecord(ev[2], s));
+            SSB_CUDA(cudaEventRecord(ev[3], s));
+        }
+        return;
+    }
     if (a.wave) {  // iterations n and n+1 in one wavefront launch, then both decisions
         if (ev) SSB_CUDA(cudaEventRecord(ev[0], s));
         launch_sor_wave(s, a, heat);

@@ -57,7 +57,13 @@ constexpr int kThreads = (kConsumers + 2) * 32;  // + a producer warp per ring
 constexpr int kFlatWarps = SSB_FLAT_WARPS;
 constexpr int kFlatV = kWarps / kFlatWarps;
 static_assert(kFlatWarps * kFlatV == kWarps && (kFlatV == 1 || kFlatV == 2), "SSB_FLAT_WARPS: 8 or 4");
-__host__ __device__ constexpr int pass_threads(bool flat) { return ((flat ? kFlatWarps : kConsumers) + 2) * 32; }
+#ifndef SSB_SPLIT_MAIN
+#define SSB_SPLIT_MAIN 0  // flat kernels: a second main-ring producer thread issues the l-1 / l+1 rows
+#endif
+constexpr int kSplitMain = SSB_SPLIT_MAIN;
+__host__ __device__ constexpr int pass_threads(bool flat) {
+    return ((flat ? kFlatWarps + kSplitMain : kConsumers) + 2) * 32;
+}
 #ifndef SSB_MAIN_STAGES
 #define SSB_MAIN_STAGES 4
 #endif
@@ -338,7 +344,8 @@ __device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsi
                                              uint64_t* empty, Ring<kMainStages>& rg, const Item& it,
                                              const float* coef, const double* rhs, const double* uc,
                                              const double* uo, const Policies& pol,
-                                             const CUtensorMap* const* tm = nullptr, bool issue = true) {
+                                             const CUtensorMap* const* tm = nullptr, bool issue = true,
+                                             int part = 0) {
     const long long W = L.W;
     const long long plane_rows = (long long)L.jMax * L.kMax;
     const uint32_t rb = G.row_bytes;
@@ -367,12 +374,19 @@ __device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsi
         uint64_t* bar = &full[rg.slot];
         const long long row0 = ((long long)it.l * L.kMax + p) * L.jMax + it.j0;  // row (j0, p, l)
         if (issue) {
-            mbar_expect_tx(bar, (HEAT ? 0u : it.rows * G.coef_row_bytes) + 4u * it.rows * rb);
-            if (!HEAT) bulk_g2s(s + G.off_coef, coef + row0 * L.Wc * 8, it.rows * G.coef_row_bytes, bar, pol.stream);
-            bulk_g2s(s + G.off_rhs, rhs + row0 * W, it.rows * rb, bar, pol.stream);
-            bulk_g2s(s + G.off_uc, uc + row0 * W, it.rows * rb, bar, pol.uload);
-            bulk_g2s(s + G.off_ulm, uo + (row0 - plane_rows) * W, it.rows * rb, bar, pol.uload);
-            bulk_g2s(s + G.off_ulp, uo + (row0 + plane_rows) * W, it.rows * rb, bar, pol.uload);
+            // part 0: every stream; split producers: part 1 coef / rhs / own colour, part 2 the l +- 1 rows
+            const uint32_t b1 = (HEAT ? 0u : it.rows * G.coef_row_bytes) + 2u * it.rows * rb, b2 = 2u * it.rows * rb;
+            mbar_expect_tx(bar, part == 0 ? b1 + b2 : part == 1 ? b1 : b2);
+            if (part != 2) {
+                if (!HEAT)
+                    bulk_g2s(s + G.off_coef, coef + row0 * L.Wc * 8, it.rows * G.coef_row_bytes, bar, pol.stream);
+                bulk_g2s(s + G.off_rhs, rhs + row0 * W, it.rows * rb, bar, pol.stream);
+                bulk_g2s(s + G.off_uc, uc + row0 * W, it.rows * rb, bar, pol.uload);
+            }
+            if (part != 1) {
+                bulk_g2s(s + G.off_ulm, uo + (row0 - plane_rows) * W, it.rows * rb, bar, pol.uload);
+                bulk_g2s(s + G.off_ulp, uo + (row0 + plane_rows) * W, it.rows * rb, bar, pol.uload);
+            }
         }
         rg.advance();
     }
@@ -702,10 +716,11 @@ struct Bars {
     uint64_t fullM[kMainStages], emptyM[kMainStages], fullK[kUKStages], emptyK[kUKStages];
 };
 
-__device__ __forceinline__ void init_barriers(Bars& b, uint32_t consumer_threads = kConsumers * 32) {
+__device__ __forceinline__ void init_barriers(Bars& b, uint32_t consumer_threads = kConsumers * 32,
+                                              uint32_t main_producers = 1) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < kMainStages; ++s) {
-            mbar_init(&b.fullM[s], 1);
+            mbar_init(&b.fullM[s], main_producers);
             mbar_init(&b.emptyM[s], consumer_threads);
         }
         for (int s = 0; s < kUKStages; ++s) {
@@ -727,7 +742,8 @@ __global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_
     __shared__ int last;
     // prologue that touches no global memory, then wait for the previous kernel of the
     // stream (programmatic dependent launch: this grid may start while it drains)
-    init_barriers(bars, NW * 32);
+    constexpr int SPLIT = FLAT ? kSplitMain : 0;  // second main-ring producer warp
+    init_barriers(bars, NW * 32, 1 + SPLIT);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     SorState* st = a.st;
     if (*(volatile const int*)&st->done) return;
@@ -771,7 +787,11 @@ __global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_
             Item it;
             decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - tt : tt, it);
             if (warp == NW)
-                produce_main<HEAT>(L, G, smem, bars.fullM, bars.emptyM, rm, it, a.coef[C], a.rhs[C], uc, uo, pol, tm);
+                produce_main<HEAT>(L, G, smem, bars.fullM, bars.emptyM, rm, it, a.coef[C], a.rhs[C], uc, uo, pol, tm,
+                                   true, SPLIT ? 1 : 0);
+            else if (SPLIT && warp == NW + 2)
+                produce_main<HEAT>(L, G, smem, bars.fullM, bars.emptyM, rm, it, a.coef[C], a.rhs[C], uc, uo, pol, tm,
+                                   true, 2);
             else
                 produce_uk(L, G, smem, bars.fullK, bars.emptyK, rk, it, uo, pol, tm_uk);
         }
@@ -931,6 +951,252 @@ __global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_wave_tma(const 
             int* q = a.flags + ((long long)d * L.n4 + (l - 1)) * CH + c;
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(q), "r"(epoch) : "memory");
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// One-sweep k-wavefront (kernel 7, "kwave": red and black of one iteration in one launch).
+//
+// Items are R rows x kKwP planes (a plane chunk) of one slice, consumed with the two-pass
+// rings and flat mapping.  The launch walks the plane chunks in order across ALL slices
+// and row groups at once: step s holds the red items of chunk s (every (jg, l), l
+// fastest), then the black items of chunk s - LAG.  A black item (kc, jg, l) reads the
+// new red values of (kc, jg, l), (kc, jg, l +- 1), (kc, jg +- 1, l) and (kc +- 1, jg, l)
+// (the first / last plane); the producers poll those seven red items' completion flags
+// (epochs; relaxed loads issued one black item ahead, one acquire fence) before issuing
+// the item's bulk copies.  A publisher thread per CTA publishes each finished red item
+// (consumers' stores -> mbarrier -> __threadfence -> flag) so consumers never block on
+// a fence.  Why: the red values a black item reads, and the black values the red items
+// of the following chunks read, were touched ~LAG + 2 chunks earlier and are still in L2
+// (coefficient / rhs streams evict_first), so a sweep moves ~59 B per doxel from DRAM
+// instead of the two-pass ~67 B.  Iterates are the two-pass ones bit for bit (tests);
+// residual partials are one per (item, warp) at the item's canonical slice-major index.
+// MEASURED (config 1, B200, scripts/gpu_kwave_var.sh): DRAM 997 vs 1128 MB per sweep, but
+// 226 us per sweep vs 198 us for the two-pass (P = 4, LAG = 2; P = 8: 217; P = 1: 330);
+// with the flag waits compiled out (wrong results, timing only) 193 us -- the cross-CTA
+// dependency waits cost more than the 12% of DRAM bytes saved.  Opt-in, not the default.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+#ifndef SSB_KWAVE_LAG
+#define SSB_KWAVE_LAG 2  // black items of plane chunk c follow the red items of chunk c + LAG
+#endif
+#ifndef SSB_KWAVE_PLANES
+#define SSB_KWAVE_PLANES 4  // planes per item (one ring stage each)
+#endif
+constexpr int kKwP = SSB_KWAVE_PLANES;
+#ifndef SSB_KWAVE_L2MB
+#define SSB_KWAVE_L2MB 48  // L2 share the live u rows of the wavefront may take
+#endif
+#ifndef SSB_KWAVE_L2HINT
+#define SSB_KWAVE_L2HINT 1  // bit0: coefficient / rhs streams evict_first (the u rows are the reused data)
+#endif
+constexpr int kKwLag = SSB_KWAVE_LAG;
+constexpr int kKwPub = 4;  // publisher ring: items a consumer may finish ahead of the publisher
+struct KwGeo {
+    int nkc;        // plane chunks of kKwP planes
+    int M;          // items per chunk and colour: njg * n4
+    long long NT;   // items of the launch: (nkc + LAG) steps x 2 colours x M (empty halves skipped)
+};
+__host__ __device__ __forceinline__ KwGeo make_kwgeo(const Layout& L, const Geo& G) {
+    KwGeo k;
+    k.nkc = (L.n3 + kKwP - 1) / kKwP;
+    k.M = G.njg * L.n4;
+    k.NT = (long long)(k.nkc + kKwLag) * 2 * k.M;
+    return k;
+}
+
+#ifndef SSB_KWAVE_NODEP
+#define SSB_KWAVE_NODEP 0
+#endif
+constexpr int kKwThreads = (kFlatWarps + 3) * 32;  // consumers + main producer + UK producer + publisher
+__host__ __device__ __forceinline__ uint32_t kwave_smem(const Layout& L) { return (uint32_t)make_geo(L).smem; }
+
+__global__ void __launch_bounds__(kKwThreads, SSB_CTAS_PER_SM) sor_kwave_tma(const SorArgs a) {
+    constexpr int NW = kFlatWarps, V = kFlatV;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) Bars bars;  // the two-pass rings: main (per plane), UK (other-colour rows)
+    __shared__ __align__(8) uint64_t doneB[kKwPub], pubB[kKwPub];
+    init_barriers(bars, NW * 32);
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < kKwPub; ++q) {
+            mbar_init(&doneB[q], NW * 32);  // consumers: item finished (stores issued)
+            mbar_init(&pubB[q], 1);         // publisher: item published, slot free again
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const SorState* st = a.st;
+    if (*(volatile const int*)&st->done) return;
+    const int n = *(volatile const int*)&st->n_red;
+    const int epoch = *(volatile const int*)&st->epoch_base + n;
+    const Layout& L = a.L;
+    const Geo G = make_geo(L, false);
+    const KwGeo K = make_kwgeo(L, G);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bin = in_buf(n), bout = out_buf(n);
+    int* const flg = a.flags;  // per red item: the epoch of the launch that completed it
+    // item cursor: block blk (2 per step: red, black), row group jg, slice l0 + 1 (l fastest);
+    // advanced by gridDim.x items with additions only
+    struct Cur {
+        int blk, jg, l0;
+    };
+    const int NB = 2 * (K.nkc + kKwLag);
+    const int gq = (int)(gridDim.x / (unsigned)L.n4), gr = (int)(gridDim.x % (unsigned)L.n4);
+    auto first = [&]() {
+        Cur c;
+        const int x0 = (int)blockIdx.x % K.M;
+        c.blk = (int)blockIdx.x / K.M;
+        c.jg = x0 / L.n4;
+        c.l0 = x0 - c.jg * L.n4;
+        return c;
+    };
+    auto advance = [&](Cur& c) {
+        c.l0 += gr;
+        c.jg += gq;
+        if (c.l0 >= L.n4) {
+            c.l0 -= L.n4;
+            ++c.jg;
+        }
+        while (c.jg >= G.njg) {
+            c.jg -= G.njg;
+            ++c.blk;
+        }
+    };
+    // colour and Item of the cursor's item; false: empty half-step (no such chunk)
+    auto item_of = [&](const Cur& c, int& C, Item& it) -> bool {
+        C = c.blk & 1;
+        const int kc = (c.blk >> 1) - C * kKwLag;  // plane chunk
+        if (kc < 0 || kc >= K.nkc) return false;
+        it.l = c.l0 + 1;
+        it.s0 = 0;
+        it.j0 = c.jg * G.R + 1;
+        it.rows = min(G.R, L.n2 - it.j0 + 1);
+        it.k0 = kc * kKwP + 1;
+        it.k1 = min(it.k0 + kKwP - 1, L.n3);
+        return true;
+    };
+    auto chunk = [&](const Item& it) { return (it.k0 - 1) / kKwP; };
+    auto flag_of = [&](int kc, int jg, int l) -> const int* {
+        return flg + ((long long)kc * G.njg + jg) * L.n4 + (l - 1);
+    };
+
+    if (warp == NW + 2) {  // publisher: after the consumers finish a red item, fence + flag
+        if (lane != 0) return;
+        uint32_t ps = 0, pph = 0;
+        for (Cur c = first(); c.blk < NB; advance(c)) {
+            int C;
+            Item it;
+            if (!item_of(c, C, it)) continue;
+            mbar_wait(&doneB[ps], pph);
+            if (C == 0) {
+#ifndef SSB_KWAVE_NOFENCE  // (timing experiment only: without it the flag may overtake the data)
+                __threadfence();  // the consumers' stores (ordered before their arrivals) -> gpu scope
+#endif
+                asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(flag_of(chunk(it), c.jg, it.l)),
+                             "r"(epoch)
+                             : "memory");
+            }
+            mbar_arrive(&pubB[ps]);
+            next_stage<kKwPub>(ps, pph);
+        }
+        return;
+    }
+    if (warp >= NW) {  // producers: lane 0 of warp NW (main ring), of warp NW + 1 (UK ring)
+        if (lane != 0) return;
+        const Policies pol = make_policies(SSB_KWAVE_L2HINT);
+        Ring<kMainStages> rm;
+        Ring<kUKStages> rk;
+        // the red items a black item (kc, jg, l) reads: (kc, jg, l), (kc, jg, l +- 1),
+        // (kc, jg +- 1, l), (kc +- 1, jg, l); their flags for this CTA's next black item are
+        // loaded one black item ahead (relaxed, in parallel), re-polled only if not yet set
+        Cur nb{-1, 0, 0};
+        int nbv[7];
+        auto deps = [&](const Cur& c, const Item& it, const int*(&q)[7]) {
+            const int kc = chunk(it), jg = c.jg, l = it.l;
+            const int* self = flag_of(kc, jg, l);
+            q[0] = self;
+            q[1] = l > 1 ? self - 1 : self;
+            q[2] = l < L.n4 ? self + 1 : self;
+            q[3] = jg > 0 ? self - L.n4 : self;
+            q[4] = jg + 1 < G.njg ? self + L.n4 : self;
+            q[5] = kc > 0 ? self - (long long)G.njg * L.n4 : self;
+            q[6] = kc + 1 < K.nkc ? self + (long long)G.njg * L.n4 : self;
+        };
+        auto prefetch_next_black = [&](Cur c) {
+            nb.blk = -1;
+            for (advance(c); c.blk < NB; advance(c)) {
+                int C2;
+                Item it2;
+                if (item_of(c, C2, it2) && C2 == 1) {
+                    const int* q[7];
+                    deps(c, it2, q);
+#pragma unroll
+                    for (int u = 0; u < 7; ++u) nbv[u] = ld_relaxed(q[u]);
+                    nb = c;
+                    return;
+                }
+            }
+        };
+        for (Cur c = first(); c.blk < NB; advance(c)) {
+            int C;
+            Item it;
+            if (!item_of(c, C, it)) continue;
+            if (C == 1 && !SSB_KWAVE_NODEP) {  // (NODEP: timing experiment only, wrong results)
+                const int* q[7];
+                deps(c, it, q);
+                const bool pre = nb.blk == c.blk && nb.jg == c.jg && nb.l0 == c.l0;
+                int v[7];
+#pragma unroll
+                for (int u = 0; u < 7; ++u) v[u] = pre ? nbv[u] : ld_relaxed(q[u]);
+#pragma unroll
+                for (int u = 0; u < 7; ++u)
+                    while (v[u] != epoch) {
+                        __nanosleep(32);
+                        v[u] = ld_relaxed(q[u]);
+                    }
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+                prefetch_next_black(c);
+            }
+            const double* uc = a.U[bin][C];
+            const double* uo = C == 0 ? a.U[bin][1] : a.U[bout][0];
+            if (warp == NW) {
+                produce_main<false>(L, G, smem, bars.fullM, bars.emptyM, rm, it, a.coef[C], a.rhs[C], uc, uo, pol);
+            } else {
+                produce_uk(L, G, smem, bars.fullK, bars.emptyK, rk, it, uo, pol);
+            }
+        }
+        return;
+    }
+    uint32_t ms = 0, mph = 0, s0 = 0, ph0 = 0, ds = 0, dph = 0;
+    int ci = 0;  // item ordinal
+    FlatThread ft[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) ft[k] = flat_thread(L, G, threadIdx.x + k * NW * 32);
+    for (Cur c = first(); c.blk < NB; advance(c)) {
+        int C;
+        Item it;
+        if (!item_of(c, C, it)) continue;
+        double r2[V];
+        if (C == 0)
+            consume_item_flat<0, false, V>(a, L, G, ft, sptr(smem), bars.fullM, bars.emptyM, bars.fullK, bars.emptyK,
+                                           ms, mph, s0, ph0, it, a.U[bout][0], nullptr, nullptr, r2);
+        else
+            consume_item_flat<1, false, V>(a, L, G, ft, sptr(smem), bars.fullM, bars.emptyM, bars.fullK, bars.emptyK,
+                                           ms, mph, s0, ph0, it, a.U[bout][1], nullptr, nullptr, r2);
+        const long long canon = ((long long)(it.l - 1) * K.nkc + chunk(it)) * G.njg + c.jg;
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < V; ++k) a.part[n & 3][C][canon * kWarps + warp + k * NW] = r2[k];
+        // hand the item to the publisher (its slot must have been released kKwPub items ago)
+        if (ci >= kKwPub) mbar_wait(&pubB[ds], dph ^ 1u);
+        mbar_arrive(&doneB[ds]);
+        next_stage<kKwPub>(ds, dph);
+        ++ci;
     }
 }
 
@@ -1110,6 +1376,47 @@ void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat) {
         sor_wave_tma<true><<<grid, kThreads, smem, s>>>(a);
     else
         sor_wave_tma<false><<<grid, kThreads, smem, s>>>(a);
+    SSB_LAUNCHED();
+}
+
+bool kwave_supported(const Layout& L) {
+    // whole-row flat items, one slab; a plane of the whole grid (all i, j, l; ~60 B per
+    // doxel) must leave L2 room for the ~3 planes the wavefront keeps live
+    const Geo G = make_geo(L);
+    // u rows live in L2 between a chunk's first red read and its last black read: about
+    // LAG + 2 chunks of (red-new + black-old) = 8 B per doxel of a plane (the coefficient /
+    // rhs streams are evict_first)
+    const double plane_u = (double)L.n1 * L.n2 * L.n4 * 8.0;
+    return tma_pass_supported(L) && !G.wpr && !G.S && L.glo && L.ghi && kwave_smem(L) <= 110u * 1024u &&
+           (kKwLag + 2.0) * kKwP * plane_u <= SSB_KWAVE_L2MB * 1024.0 * 1024;
+}
+size_t kwave_flags(const Layout& L) {
+    const Geo G = make_geo(L);
+    const int nkc = make_kwgeo(L, G).nkc;
+    return (size_t)nkc * G.njg * L.n4;
+}
+size_t kwave_partials(const Layout& L) {
+    const Geo G = make_geo(L);
+    return (size_t)make_kwgeo(L, G).nkc * G.njg * L.n4 * kWarps;
+}
+int kwave_bps(const Layout& L) {
+    const Geo G = make_geo(L);
+    return make_kwgeo(L, G).nkc * G.njg * kWarps;
+}
+
+void launch_sor_kwave(cudaStream_t s, const SorArgs& a) {
+    const Geo G = make_geo(a.L);
+    const KwGeo K = make_kwgeo(a.L, G);
+    const size_t smem = kwave_smem(a.L);
+    static size_t last_smem = 0;
+    static int blocks = 0;
+    if (smem != last_smem) {
+        SSB_CUDA(cudaFuncSetAttribute(sor_kwave_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        blocks = tma_blocks((const void*)sor_kwave_tma, smem, kKwThreads);
+        last_smem = smem;
+    }
+    const unsigned grid = (unsigned)std::min<long long>(K.NT, blocks);
+    sor_kwave_tma<<<grid, kKwThreads, smem, s>>>(a);
     SSB_LAUNCHED();
 }
 

@@ -37,7 +37,7 @@ if os.environ.get("CHECK_VS_TMA"):  # bitwise check of the selected kernel again
     s.set_u(wl.u0 if wl.u0 is not None else a)
     s.fixed_sweeps(7)
     print("bitwise_equal_to_tma", bool(np.array_equal(a, s.get_u())))
-print(json.dumps(dict(config=cfg, slabs=int(os.environ.get("SLABS", "1")), kernel=os.environ.get("SUBSURF_KERNEL"), lib=os.environ.get("SUBSURF_B200_LIB"), snake=os.environ.get("SSB_SNAKE"), l2hint=os.environ.get("SSB_L2HINT"),
+print(json.dumps(dict(config=cfg, ran=s.sor_kernel(), slabs=int(os.environ.get("SLABS", "1")), kernel=os.environ.get("SUBSURF_KERNEL"), lib=os.environ.get("SUBSURF_B200_LIB"), snake=os.environ.get("SSB_SNAKE"), l2hint=os.environ.get("SSB_L2HINT"),
                       us_per_sweep=1e3 * ms / N,
                       red_us=1e3 * pr["red_ms"] / max(1, pr["red_n"]),
                       black_us=1e3 * pr["black_ms"] / max(1, pr["black_n"]))))

@@ -91,7 +91,7 @@ def test_nccl_session_world1(gpu):
     assert np.array_equal(u.view(np.uint64), d["u_rel"].view(np.uint64))
 
 
-@pytest.mark.parametrize("kernel", ["ldg", "tma", "wave", "resident", "auto", "tma2d"])
+@pytest.mark.parametrize("kernel", ["ldg", "tma", "wave", "resident", "auto", "tma2d", "kwave"])
 def test_pass_kernels_agree(gpu, kernel):
     """Both SOR colour-pass kernels give the golden segment() result bit for bit."""
     d = dict(np.load(os.path.join(GOLD, "segment.npz")))
@@ -122,7 +122,7 @@ def test_kernels_agree_odd_shapes(gpu, oracle, dims):
               delta=0.5, vartheta=0.5, rescale_radius=2.0)
     st, uo, info = oracle.segment(cs.grid(dims, h), img, rows, oracle_params(kw))
     assert st == 0
-    for kernel in ("tma", "ldg", "resident", "tma2d"):
+    for kernel in ("tma", "ldg", "resident", "tma2d", "kwave"):
         with gpu.Session(g) as s:
             s.set_kernel(kernel)
             s.prepare(img, rows, gpu.seg_params(**kw))
@@ -163,3 +163,30 @@ def test_halo_exchange_timing(gpu):
     assert pr["halo_n"] == pr["red_n"] + pr["black_n"] >= 2 * 12  # one exchange per colour pass
     assert pr["halo_ms"] > 0.0
     assert 0.0 <= pr["halo_exposed_ms"] <= pr["red_ms"] + pr["black_ms"]
+
+
+@pytest.mark.parametrize("dims", [(64, 16, 12, 10), (32, 24, 9, 7), (40, 8, 5, 13), (1, 3, 2, 5)])
+def test_kwave_matches_two_pass(gpu, dims):
+    """The one-sweep k-wavefront kernel (red and black items of one iteration in one
+    launch, black items waiting on per-item flags of the red items they read) gives the
+    two-pass TMA kernel's iterates bit for bit, with the same iteration counts."""
+    h = 1.0 / max(dims[:3])
+    g = gpu.Grid.make(dims, h)
+    img = cs.f32_image(dims, 3 + sum(dims), noise=0.05)
+    rows = [(f, (dims[0] - 1) / 2, (dims[1] - 1) / 2, (dims[2] - 1) / 2, 2.5) for f in range(dims[3])]
+    p = gpu.seg_params(tau=h, epsilon=1e-3, omega=1.4, sor_rel_tol=1e-8, n_steps=3, sigma=np.sqrt(2) * h,
+                       K=100.0, delta=0.5, vartheta=0.5, rescale_radius=3.0)
+    out = {}
+    for kernel in ("tma", "kwave"):
+        for mode in (0, 1):  # host-driven loop / CUDA-graph conditional loop
+            with gpu.Session(g) as s:
+                s.set_kernel(kernel)
+                s.set_loop_mode(mode)
+                s.prepare(img, rows, p)
+                its = [s.step()["iterations"] for _ in range(3)]
+                assert s.sor_kernel() == kernel
+                out[kernel, mode] = (its, s.get_u())
+    ref_its, ref_u = out["tma", 1]
+    for key, (its, u) in out.items():
+        assert its == ref_its, key
+        assert np.array_equal(u.view(np.uint64), ref_u.view(np.uint64)), key
