@@ -19,6 +19,7 @@ struct SorState {
     int iterations, max_iter;
     int fixed, pad;
     unsigned int counter;
+    unsigned int item_ctr[2];  // dynamic item counters of the TMA colour passes (zeroed by the other pass)
     int epoch_base;  // distinct per solve: completion flags of the wavefront kernel compare to epoch_base + n
     double tol, residual;
 };

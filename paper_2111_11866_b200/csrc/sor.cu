@@ -314,6 +314,7 @@ __global__ void sor_init(SorState* st, double tol, const double* norm_slices, in
     st->max_iter = max_iter;
     st->fixed = fixed;
     st->counter = 0;
+    st->item_ctr[0] = st->item_ctr[1] = 0;
     st->residual = 0.0;
     if (norm_slices) {
         double s = 0.0;
