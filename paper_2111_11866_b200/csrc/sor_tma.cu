@@ -844,7 +844,8 @@ __global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_
         return;
     }
     if (C == 1 && a.fuse_final)  // the finalize's fixed 256-lane tree, NW * 32 threads
-        black_head_finalize<NW * 32>(a, n, ws, &last, threadIdx.x);
+        if (threadIdx.x < 256)  // the tree is played by <= 256 threads (same bits for 128 or 256)
+            black_head_finalize<(NW * 32 > 256 ? 256 : NW * 32)>(a, n, ws, &last, threadIdx.x);
     uint32_t ms = 0, mph = 0, s0 = 0, ph0 = 0;
     // FLAT (host-chosen): whole-row items with the flat slot mapping, not heat.  Thread
     // tid plays the 8-warp mapping's threads tid + k * NW * 32 (k < V), and writes
