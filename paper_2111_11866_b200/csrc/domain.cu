@@ -317,6 +317,8 @@ SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool he
     a.tma = kernel >= 1 && tma_pass_supported(L) ? 1 : 0;
     a.l_lo = 1;
     a.l_hi = L.n4;
+    a.l_step = 1;
+    a.dyn = 1;  // whole-slab pass launches; ranges clear it (sor.cu)
     a.wave = kernel == 2 && world == 1 && wflags.p != nullptr && wave_supported(L) ? 1 : 0;
     if (kernel == 7 && !heat && world == 1 && wflags.p != nullptr && kwave_supported(L)) a.wave = 2;
     a.flags = wflags.p;
@@ -388,6 +390,10 @@ void Domain::init_common() {
     SSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     SSB_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
     SSB_CUDA(cudaStreamCreateWithFlags(&comm, cudaStreamNonBlocking));
+    int prio_lo = 0, prio_hi = 0;
+    SSB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    SSB_CUDA(cudaStreamCreateWithPriority(&bnd, cudaStreamNonBlocking, prio_hi));
+    SSB_CUDA(cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming));
     SSB_CUDA(cudaEventCreateWithFlags(&ev_bnd, cudaEventDisableTiming));
     SSB_CUDA(cudaEventCreateWithFlags(&ev_xchg, cudaEventDisableTiming));
     SSB_CUDA(cudaMallocHost(&st_host, sizeof(SorState)));
@@ -447,6 +453,8 @@ Domain::~Domain() {
     if (scal_host) cudaFreeHost(scal_host);
     if (comm) cudaStreamSynchronize(comm);
     if (ev_bnd) cudaEventDestroy(ev_bnd);
+    if (ev_pre) cudaEventDestroy(ev_pre);
+    if (bnd) cudaStreamDestroy(bnd);
     if (ev_xchg) cudaEventDestroy(ev_xchg);
     if (stream) cudaStreamDestroy(stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
@@ -645,19 +653,19 @@ void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>
             for (const SorArgs& x : a) launch_sor_pass(stream, x, colour, heat);
             return;
         }
-        for (const SorArgs& x : a) {
-            const int n4 = x.L.n4;
-            launch_sor_pass_range(stream, x, colour, heat, 1, 1);
-            if (n4 > 1) launch_sor_pass_range(stream, x, colour, heat, n4, n4);
-        }
+        // the end slices (the planes the neighbours need) on the high-priority stream, one
+        // launch per slab, running concurrently with the interior slices on the main stream
+        SSB_CUDA(cudaEventRecord(ev_pre, stream));
+        SSB_CUDA(cudaStreamWaitEvent(bnd, ev_pre, 0));
+        for (const SorArgs& x : a) launch_sor_pass_ends(bnd, x, colour, heat);
         // profiling: x[0] exchange start (comm), x[1] exchange end (comm), x[2] interior done
         cudaEvent_t* xe = ev4 ? ev4 + 4 + 3 * colour : nullptr;
-        SSB_CUDA(cudaEventRecord(ev_bnd, stream));
+        SSB_CUDA(cudaEventRecord(ev_bnd, bnd));
         SSB_CUDA(cudaStreamWaitEvent(comm, ev_bnd, 0));
         if (xe) SSB_CUDA(cudaEventRecord(xe[0], comm));
         tr->exchange(sp, F, colour == 0 ? 1 : 2, comm);
         SSB_CUDA(cudaEventRecord(xe ? xe[1] : ev_xchg, comm));
-        for (const SorArgs& x : a) launch_sor_pass_range(stream, x, colour, heat, 2, x.L.n4 - 1);
+        for (const SorArgs& x : a) launch_sor_pass_range(stream, x, colour, heat, 2, x.L.n4 - 1, true);
         if (xe) SSB_CUDA(cudaEventRecord(xe[2], stream));
         SSB_CUDA(cudaStreamWaitEvent(stream, xe ? xe[1] : ev_xchg, 0));
     };

@@ -209,6 +209,8 @@ struct Domain {
     PeerLinks peers;           // NVLink halo push between ranks (SSB_P2P=1)
     cudaStream_t stream = nullptr, cap_stream = nullptr;
     cudaStream_t comm = nullptr;  // halo exchanges (overlapped with interior slices)
+    cudaStream_t bnd = nullptr;   // high priority: a colour pass's end slices, concurrent with its interior
+    cudaEvent_t ev_pre = nullptr; // the pass's start on the main stream (the end-slice launch waits for it)
     cudaEvent_t ev_bnd = nullptr, ev_xchg = nullptr;
     std::vector<std::unique_ptr<Slab>> slabs;
     std::vector<Slab*> sp;  // raw pointers, rank order

@@ -61,6 +61,9 @@ struct SorArgs {
     long long tiles;
     int tma;                // 1: TMA-fed pass kernel (sor_tma.cu), 0: LDG pass (sor.cu)
     int l_lo, l_hi;         // slices (local, 1-based) a pass launch covers (default 1 .. n4)
+    int l_step;             // ... every l_step-th of them (TMA pass; 1: all, n4 - 1: the two end slices)
+    int pdl_off;            // launch without programmatic dependent launch (side-stream launches)
+    int dyn;                // TMA pass: items from the colour's atomic counter (one such launch per pass)
     int wave;               // 1: two-iteration wavefront kernel per loop body, 2: one-sweep k-wavefront
     int* flags;             // wavefront item completion flags (epochs)
     int snake;              // TMA pass: black passes walk the items in reverse (L2 reuse at the turn)
@@ -130,7 +133,10 @@ void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* e
 // pieces for the multi-slab body (halo exchange / all-gather between them)
 void launch_sor_pass(cudaStream_t s, const SorArgs& a, int colour, bool heat);
 // the same pass restricted to slices [lo, hi] (boundary-first halo overlap)
-void launch_sor_pass_range(cudaStream_t s, const SorArgs& a, int colour, bool heat, int lo, int hi);
+void launch_sor_pass_range(cudaStream_t s, const SorArgs& a, int colour, bool heat, int lo, int hi,
+                           bool dyn = false);
+// the two end slices (1 and n4: the planes a t-slab exchanges) of a colour pass
+void launch_sor_pass_ends(cudaStream_t s, const SorArgs& a, int colour, bool heat);
 void launch_sor_finalize(cudaStream_t s, const SorArgs& a);
 // whole solve in one cooperative launch (LDG tiles, state in L2); single slab
 bool resident_supported(const Layout& L);

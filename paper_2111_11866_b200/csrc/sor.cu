@@ -382,11 +382,29 @@ void launch_sor_pass(cudaStream_t s, const SorArgs& a, int colour, bool heat) {
     SSB_LAUNCHED();
 }
 
-void launch_sor_pass_range(cudaStream_t s, const SorArgs& a, int colour, bool heat, int lo, int hi) {
+void launch_sor_pass_range(cudaStream_t s, const SorArgs& a, int colour, bool heat, int lo, int hi, bool dyn) {
     if (lo > hi) return;
     SorArgs b = a;
     b.l_lo = lo;
     b.l_hi = hi;
+    b.l_step = 1;
+    b.dyn = dyn ? 1 : 0;  // only the interior launch of a pass takes items from the counter
+    launch_sor_pass(s, b, colour, heat);
+}
+
+void launch_sor_pass_ends(cudaStream_t s, const SorArgs& a, int colour, bool heat) {
+    const int n4 = a.L.n4;
+    if (n4 <= 2 || !a.tma || a.wave) {  // contiguous, or kernels without strided slice ranges
+        launch_sor_pass_range(s, a, colour, heat, 1, 1);
+        if (n4 > 1) launch_sor_pass_range(s, a, colour, heat, n4, n4);
+        return;
+    }
+    SorArgs b = a;  // slices 1 and n4 in one launch
+    b.l_lo = 1;
+    b.l_hi = n4;
+    b.l_step = n4 - 1;
+    b.pdl_off = 1;
+    b.dyn = 0;
     launch_sor_pass(s, b, colour, heat);
 }
 

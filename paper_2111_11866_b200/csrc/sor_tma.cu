@@ -287,29 +287,28 @@ __device__ __forceinline__ Item make_item(const Layout& L, const Geo& G, int l, 
 // concurrently and share their other-colour rows through L2 (a slice of a large
 // grid is bigger than L2).
 __device__ __forceinline__ long long decode_item(const Layout& L, const Geo& G, int order, int l_lo, int nl,
-                                                 long long t64, Item& it) {
+                                                 long long t64, Item& it, int l_step = 1) {
     // item counts stay far below 2^31 (host_launch checks), so 32-bit division suffices
     const unsigned t = (unsigned)t64;
     unsigned l, jg, kc, sg;
     const unsigned nsg = (unsigned)G.nsg, njg = (unsigned)G.njg, nkc = (unsigned)G.nkc;
     if (order == 0) {
-        const unsigned c = (unsigned)(l_lo - 1) * nsg * njg * nkc + t;
-        sg = c % nsg;
-        const unsigned c2 = c / nsg;
+        sg = t % nsg;
+        const unsigned c2 = t / nsg;
         jg = c2 % njg;
         const unsigned r = c2 / njg;
         kc = r % nkc;
-        l = r / nkc + 1;
+        l = (unsigned)l_lo + (r / nkc) * (unsigned)l_step;
     } else if (order == 1) {
         const unsigned r0 = t / (unsigned)nl;
-        l = (unsigned)l_lo + (t - r0 * (unsigned)nl);
+        l = (unsigned)l_lo + (t - r0 * (unsigned)nl) * (unsigned)l_step;
         const unsigned r = nsg == 1 ? r0 : r0 / nsg;
         sg = r0 - r * nsg;
         kc = r / njg;
         jg = r - kc * njg;
     } else {  // 2: slice fastest, then plane chunk (k-halo planes shared by neighbours in time)
         const unsigned r0 = t / (unsigned)nl;
-        l = (unsigned)l_lo + (t - r0 * (unsigned)nl);
+        l = (unsigned)l_lo + (t - r0 * (unsigned)nl) * (unsigned)l_step;
         const unsigned r = nsg == 1 ? r0 : r0 / nsg;
         sg = r0 - r * nsg;
         jg = r / nkc;
@@ -776,13 +775,13 @@ __global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_
     double* ucw = a.U[bout][C];
     const Geo G = make_geo(L, a.tile2d != 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nl = a.l_hi - a.l_lo + 1;
+    const int nl = (a.l_hi - a.l_lo) / a.l_step + 1;  // slices l_lo, l_lo + l_step, .. l_hi
     const long long n_items = (long long)G.nsg * G.njg * G.nkc * nl;
     // snake order: black passes walk the items backwards, so each pass starts on
     // the rows the previous pass touched last (still in L2)
     const bool rev = C == 1 && a.snake;
     const Policies pol = make_policies(a.l2hint);
-    const bool dyn = DYN && a.l_lo == 1 && a.l_hi == L.n4;  // uniform over the grid
+    const bool dyn = DYN && a.dyn && a.l_step == 1;  // uniform over the grid; one such launch per pass
     // the other colour's pass is complete (and its successor not started): reset its counter
     if (dyn && blockIdx.x == 0 && threadIdx.x == 0) st->item_ctr[C ^ 1] = 0;
     // queue reader: the next item index (-1: none left)
@@ -822,7 +821,7 @@ __global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_
                 // claim the next item now: the atomic's latency overlaps this item's copies
                 const unsigned nxt = atomicAdd(&st->item_ctr[C], 1u);
                 Item it;
-                decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - cur : cur, it);
+                decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - cur : cur, it, a.l_step);
                 produce_main<HEAT>(L, G, smem, bars.fullM, bars.emptyM, rm, it, a.coef[C], a.rhs[C], uc, uo, pol, tm);
                 tt = (long long)gridDim.x + nxt;
             }
@@ -831,7 +830,7 @@ __global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_
         for (long long tt = dyn ? q_take() : blockIdx.x; tt >= 0 && tt < n_items;
              tt = dyn ? q_take() : tt + gridDim.x) {
             Item it;
-            decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - tt : tt, it);
+            decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - tt : tt, it, a.l_step);
             if (warp == NW)
                 produce_main<HEAT>(L, G, smem, bars.fullM, bars.emptyM, rm, it, a.coef[C], a.rhs[C], uc, uo, pol, tm,
                                    true, SPLIT ? 1 : 0);
@@ -855,7 +854,7 @@ __global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_
     for (int k = 0; k < V; ++k) ft[k] = FLAT ? flat_thread(L, G, threadIdx.x + k * NW * 32) : FlatThread{};
     for (long long tt = dyn ? q_take() : blockIdx.x; tt >= 0 && tt < n_items; tt = dyn ? q_take() : tt + gridDim.x) {
         Item it;
-        const long long t = decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - tt : tt, it);
+        const long long t = decode_item(L, G, a.order, a.l_lo, nl, rev ? n_items - 1 - tt : tt, it, a.l_step);
         double* plo = PUSH && it.l == 1 ? a.push_lo[bout][C] : nullptr;
         double* phi = PUSH && it.l == L.n4 ? a.push_hi[bout][C] : nullptr;
         double r2[V];
@@ -1490,7 +1489,7 @@ void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat
         last_smem = smem;
     }
     const bool flat = !heat && !G.S && !G.wpr;
-    const long long items = (long long)G.nsg * G.njg * G.nkc * (a.l_hi - a.l_lo + 1);
+    const long long items = (long long)G.nsg * G.njg * G.nkc * ((a.l_hi - a.l_lo) / a.l_step + 1);
     const unsigned grid = (unsigned)std::min<long long>(items, blocks[flat]);
     const bool push = a.push_lo[0][0] != nullptr || a.push_hi[0][0] != nullptr;
     const int v = (colour & 1) | (heat ? 2 : 0) | (push ? 4 : 0) | (flat ? 8 : 0);
@@ -1512,7 +1511,7 @@ void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pass_pdl() ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = pass_pdl() && !a.pdl_off ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     SSB_CUDA(cudaLaunchKernelEx(&cfg, fns[v], a));
