@@ -62,14 +62,21 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        # started (and its first sample read) BEFORE the timed region: nvidia-smi's start-up
+        # (NVML init) stalls driver calls for milliseconds and must not land inside it
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
                  "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 10.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.pre = list(self.lines)  # samples before the region: used only if none fall inside
+        self.lines = []
         return self
 
     def _read(self):
@@ -85,9 +92,10 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        lines = self.lines or getattr(self, "pre", [])
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
