@@ -389,9 +389,14 @@ void Domain::init_common() {
     SSB_CUDA(cudaSetDevice(device));
     SSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     SSB_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
-    SSB_CUDA(cudaStreamCreateWithFlags(&comm, cudaStreamNonBlocking));
+    // the end slices and the halo exchange run on high-priority streams: the interior
+    // pass is a persistent grid that fills every CTA slot, and pending CTAs of a
+    // higher-priority stream (the end slices, the NCCL exchange kernels) are scheduled
+    // first on the slots that free up, so the exchange overlaps the interior instead of
+    // waiting for its end
     int prio_lo = 0, prio_hi = 0;
     SSB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    SSB_CUDA(cudaStreamCreateWithPriority(&comm, cudaStreamNonBlocking, prio_hi));
     SSB_CUDA(cudaStreamCreateWithPriority(&bnd, cudaStreamNonBlocking, prio_hi));
     SSB_CUDA(cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming));
     SSB_CUDA(cudaEventCreateWithFlags(&ev_bnd, cudaEventDisableTiming));
