@@ -365,11 +365,11 @@ void LocalTransport::exchange(std::vector<Slab*>& slabs, const std::vector<PFiel
 }
 
 void LocalTransport::allgather(std::vector<Slab*>& slabs, const std::vector<double*>& local,
-                               const std::vector<double*>& all, int chunk) {
+                               const std::vector<double*>& all, int chunk, cudaStream_t st) {
     for (size_t d = 0; d < slabs.size(); ++d)
         for (size_t s = 0; s < slabs.size(); ++s)
             SSB_CUDA(cudaMemcpyAsync(all[d] + s * chunk, local[s], chunk * sizeof(double),
-                                     cudaMemcpyDeviceToDevice, slabs[d]->stream));
+                                     cudaMemcpyDeviceToDevice, st ? st : slabs[d]->stream));
 }
 
 // ------------------------------------------------------------------ domain
@@ -398,6 +398,9 @@ void Domain::init_common() {
     SSB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     SSB_CUDA(cudaStreamCreateWithPriority(&comm, cudaStreamNonBlocking, prio_hi));
     SSB_CUDA(cudaStreamCreateWithPriority(&bnd, cudaStreamNonBlocking, prio_hi));
+    SSB_CUDA(cudaStreamCreateWithPriority(&dec, cudaStreamNonBlocking, prio_hi));
+    SSB_CUDA(cudaEventCreateWithFlags(&ev_red, cudaEventDisableTiming));
+    SSB_CUDA(cudaEventCreateWithFlags(&ev_dec, cudaEventDisableTiming));
     SSB_CUDA(cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming));
     SSB_CUDA(cudaEventCreateWithFlags(&ev_bnd, cudaEventDisableTiming));
     SSB_CUDA(cudaEventCreateWithFlags(&ev_xchg, cudaEventDisableTiming));
@@ -460,6 +463,9 @@ Domain::~Domain() {
     if (ev_bnd) cudaEventDestroy(ev_bnd);
     if (ev_pre) cudaEventDestroy(ev_pre);
     if (bnd) cudaStreamDestroy(bnd);
+    if (dec) cudaStreamDestroy(dec);
+    if (ev_red) cudaEventDestroy(ev_red);
+    if (ev_dec) cudaEventDestroy(ev_dec);
     if (ev_xchg) cudaEventDestroy(ev_xchg);
     if (stream) cudaStreamDestroy(stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
@@ -677,17 +683,24 @@ void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>
     if (ev4) SSB_CUDA(cudaEventRecord(ev4[0], stream));
     pass(0);
     if (ev4) SSB_CUDA(cudaEventRecord(ev4[1], stream));
-    for (const SorArgs& x : a) launch_sor_finalize(stream, x);
+    // the decision of iteration n-1 (slice residuals, their all-gather, the test) on the side
+    // stream, overlapped with the black pass n: black(n) does not depend on it (the red pass
+    // handed it n; if n-1 turns out converged, black(n) only wrote out(n), which nobody reads)
+    SSB_CUDA(cudaEventRecord(ev_red, stream));
+    SSB_CUDA(cudaStreamWaitEvent(dec, ev_red, 0));
+    for (const SorArgs& x : a) launch_sor_finalize(dec, x);
     std::vector<double*> loc, all;
     for (Slab* s : sp) {
         loc.push_back(s->slice_res.p);
         all.push_back(s->all_slices.p);
     }
-    tr->allgather(sp, loc, all, chunk);
-    for (const SorArgs& x : a) launch_sor_decide(stream, x);
+    tr->allgather(sp, loc, all, chunk, dec);
+    for (const SorArgs& x : a) launch_sor_decide(dec, x);
+    SSB_CUDA(cudaEventRecord(ev_dec, dec));
     if (ev4) SSB_CUDA(cudaEventRecord(ev4[2], stream));
     pass(1);
     if (ev4) SSB_CUDA(cudaEventRecord(ev4[3], stream));
+    SSB_CUDA(cudaStreamWaitEvent(stream, ev_dec, 0));  // the next red pass reads the decision
 }
 
 SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& rhs, bool heat, double omega,

@@ -155,21 +155,22 @@ struct Transport {
     virtual void exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours,
                           cudaStream_t s) = 0;
     // every slab's local[s] (chunk doubles) -> all[s'][rank * chunk] for all s'
+    // on stream st (nullptr: the slabs' own stream)
     virtual void allgather(std::vector<Slab*>& slabs, const std::vector<double*>& local,
-                           const std::vector<double*>& all, int chunk) = 0;
+                           const std::vector<double*>& all, int chunk, cudaStream_t st = nullptr) = 0;
 };
 
 struct NullTransport : Transport {
     void exchange(std::vector<Slab*>&, const std::vector<PField>&, int, cudaStream_t) override {}
-    void allgather(std::vector<Slab*>&, const std::vector<double*>&, const std::vector<double*>&,
-                   int) override {}
+    void allgather(std::vector<Slab*>&, const std::vector<double*>&, const std::vector<double*>&, int,
+                   cudaStream_t) override {}
 };
 
 struct LocalTransport : Transport {
     void exchange(std::vector<Slab*>& slabs, const std::vector<PField>& F, int colours,
                   cudaStream_t s) override;
     void allgather(std::vector<Slab*>& slabs, const std::vector<double*>& local,
-                   const std::vector<double*>& all, int chunk) override;
+                   const std::vector<double*>& all, int chunk, cudaStream_t st = nullptr) override;
 };
 
 std::unique_ptr<Transport> make_nccl_transport(const unsigned char* uid, int rank, int world);
@@ -211,6 +212,8 @@ struct Domain {
     cudaStream_t comm = nullptr;  // halo exchanges (overlapped with interior slices)
     cudaStream_t bnd = nullptr;   // high priority: a colour pass's end slices, concurrent with its interior
     cudaEvent_t ev_pre = nullptr; // the pass's start on the main stream (the end-slice launch waits for it)
+    cudaStream_t dec = nullptr;   // high priority: slab-group residual + decision, overlapped with the black pass
+    cudaEvent_t ev_red = nullptr, ev_dec = nullptr;
     cudaEvent_t ev_bnd = nullptr, ev_xchg = nullptr;
     std::vector<std::unique_ptr<Slab>> slabs;
     std::vector<Slab*> sp;  // raw pointers, rank order

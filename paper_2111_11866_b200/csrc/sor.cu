@@ -135,9 +135,11 @@ __device__ __forceinline__ void pass_body(const SorArgs& a, int n) {
 
 template <int C, bool HEAT>
 __global__ void __launch_bounds__(kPassBX * kPassBY, SSB_PASS_MINB) sor_pass(const SorArgs a) {
-    const SorState* st = a.st;
+    SorState* st = a.st;
     if (*(volatile const int*)&st->done) return;
     const int n = C == 0 ? *(volatile const int*)&st->n_red : *(volatile const int*)&st->n_black;
+    // the red pass hands its n to the black pass (the decision may run concurrently)
+    if (C == 0 && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) st->n_black = n;
     pass_body<C, HEAT, false>(a, n);
 }
 

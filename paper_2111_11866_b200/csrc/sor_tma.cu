@@ -766,7 +766,8 @@ __global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_
     // n to the black pass (n_black: black CTAs read it, nobody else writes it
     // during the red pass); the black pass's first CTAs take the finalize's
     // place before their own items (black_head_finalize).
-    if (C == 0 && a.fuse_final && blockIdx.x == 0 && threadIdx.x == 0) st->n_black = n;
+    // (also on slab groups: their decision runs concurrently with the black pass)
+    if (C == 0 && blockIdx.x == 0 && threadIdx.x == 0) st->n_black = n;
     const int bout = out_buf(n);
     const int bin = in_buf(n);
     const Layout& L = a.L;

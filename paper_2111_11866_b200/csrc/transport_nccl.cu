@@ -108,8 +108,8 @@ struct NcclTransport : Transport {
         check(a.GroupEnd(), "ncclGroupEnd");
     }
     void allgather(std::vector<Slab*>& slabs, const std::vector<double*>& local, const std::vector<double*>& all,
-                   int chunk) override {
-        check(api().AllGather(local[0], all[0], (size_t)chunk, ncclDouble, comm, slabs[0]->stream),
+                   int chunk, cudaStream_t st) override {
+        check(api().AllGather(local[0], all[0], (size_t)chunk, ncclDouble, comm, st ? st : slabs[0]->stream),
               "ncclAllGather");
     }
     void allgather_bytes(const void* d_local, void* d_all, size_t bytes, cudaStream_t st) {
