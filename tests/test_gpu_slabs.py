@@ -190,3 +190,52 @@ def test_kwave_matches_two_pass(gpu, dims):
     for key, (its, u) in out.items():
         assert its == ref_its, key
         assert np.array_equal(u.view(np.uint64), ref_u.view(np.uint64)), key
+
+
+_NOPUSH_SCRIPT = r"""
+import os, sys, json
+import numpy as np
+sys.path.insert(0, os.environ["REPO"])
+import paper_2111_11866_b200 as ss
+d = dict(np.load(os.path.join(os.environ["REPO"], "tests", "golden", "segment.npz")))
+dims = tuple(int(x) for x in d["dims"])
+h = float(d["h"])
+g = ss.Grid.make(dims, h)
+p = ss.seg_params(tau=h, epsilon=1e-3, omega=1.4, n_steps=3, sigma=np.sqrt(2) * h, K=200.0,
+                  delta=0.5, vartheta=0.5, rescale_radius=3.0, sor_rel_tol=1e-8)
+out = {}
+for n_slabs in (2, 3):
+    with ss.Session(g, n_slabs=n_slabs) as s:
+        s.set_kernel(os.environ["KERNEL"])
+        s.prepare(d["image"], d["rows"], p)
+        s.set_profiling(True)  # counts the exchanges: proves the exchange (not push) path ran
+        s.profile()
+        its = [s.step()["iterations"] for _ in range(3)]
+        halo_n = s.profile()["halo_n"]
+        u = s.get_u()
+    out[n_slabs] = (its == list(d["iters_rel"]),
+                    bool(np.array_equal(u.view(np.uint64), d["u_rel"].view(np.uint64))), halo_n,
+                    list(dims))
+print(json.dumps({str(k): v for k, v in out.items()}))
+"""
+
+
+@pytest.mark.parametrize("kernel", ["tma", "tma2d"])
+def test_slabs_exchange_path_tma(gpu, kernel):
+    """Slab groups WITHOUT the in-kernel halo push (SSB_PUSH=0, the path NCCL ranks take):
+    the two end slices in one strided TMA launch on the high-priority stream, the interior
+    with dynamic items on the main stream, exchange copies on the comm stream, the decision
+    on its own stream overlapped with the black pass -- bit-identical to the golden
+    single-domain run.  (SSB_PUSH is read once per process: a subprocess.)"""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SSB_PUSH="0", REPO=repo, KERNEL=kernel)
+    r = subprocess.run([sys.executable, "-c", _NOPUSH_SCRIPT], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for k, (its_ok, u_ok, halo_n, dims) in res.items():
+        assert its_ok and u_ok, (kernel, k, res)
+        assert halo_n > 0, (kernel, k, res)
