@@ -1020,8 +1020,8 @@ __global__ void __launch_bounds__(kThreads, SSB_CTAS_PER_SM) sor_wave_tma(const 
 // residual partials are one per (item, warp) at the item's canonical slice-major index.
 // MEASURED (config 1, B200, scripts/gpu_kwave_var.sh): DRAM 997 vs 1128 MB per sweep, but
 // 226 us per sweep vs 198 us for the two-pass (P = 4, LAG = 2; P = 8: 217; P = 1: 330);
-// with the flag waits compiled out (wrong results, timing only) 193 us -- the cross-CTA
-// dependency waits cost more than the 12% of DRAM bytes saved.  Opt-in, not the default.
+// with the flag waits compiled out (a timing-only build, wrong results; removed) 193 us -- the
+// cross-CTA dependency waits cost more than the 12% of DRAM bytes saved.  Opt-in, not the default.
 __device__ __forceinline__ int ld_relaxed(const int* p) {
     int v;
     asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1056,9 +1056,6 @@ __host__ __device__ __forceinline__ KwGeo make_kwgeo(const Layout& L, const Geo&
     return k;
 }
 
-#ifndef SSB_KWAVE_NODEP
-#define SSB_KWAVE_NODEP 0
-#endif
 constexpr int kKwThreads = (kFlatWarps + 3) * 32;  // consumers + main producer + UK producer + publisher
 __host__ __device__ __forceinline__ uint32_t kwave_smem(const Layout& L) { return (uint32_t)make_geo(L).smem; }
 
@@ -1140,9 +1137,7 @@ __global__ void __launch_bounds__(kKwThreads, SSB_CTAS_PER_SM) sor_kwave_tma(con
             if (!item_of(c, C, it)) continue;
             mbar_wait(&doneB[ps], pph);
             if (C == 0) {
-#ifndef SSB_KWAVE_NOFENCE  // (timing experiment only: without it the flag may overtake the data)
                 __threadfence();  // the consumers' stores (ordered before their arrivals) -> gpu scope
-#endif
                 asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(flag_of(chunk(it), c.jg, it.l)),
                              "r"(epoch)
                              : "memory");
@@ -1192,7 +1187,7 @@ __global__ void __launch_bounds__(kKwThreads, SSB_CTAS_PER_SM) sor_kwave_tma(con
             int C;
             Item it;
             if (!item_of(c, C, it)) continue;
-            if (C == 1 && !SSB_KWAVE_NODEP) {  // (NODEP: timing experiment only, wrong results)
+            if (C == 1) {
                 const int* q[7];
                 deps(c, it, q);
                 const bool pre = nb.blk == c.blk && nb.jg == c.jg && nb.l0 == c.l0;
