@@ -93,7 +93,12 @@ constexpr int kUKStages = SSB_UK_STAGES;      // other-colour planes (held for t
 constexpr int kPlanesPerItem = SSB_PLANES_PER_ITEM;
 constexpr int kDefaultSnake = 1;
 constexpr int kDefaultL2Hint = 0;
-constexpr int kDefaultOrder = 1;
+// -1 = auto: slice-major (0) when a slice has at most half a grid of items -- several
+// slices are in flight, so the l +- 1 rows AND the row-group / plane-chunk halo rows of
+// an item come from L2 (config 1: 197 -> 190 us per sweep) -- else slice-fastest (1),
+// which keeps the l +- 1 rows in L2 when a slice is larger than the grid (config 2:
+// slice-major 1619 vs 1446 us)
+constexpr int kDefaultOrder = -1;
 #ifndef SSB_WAVE_SKEW
 #define SSB_WAVE_SKEW 0  // 0: 2 * nkc sub-slices (measured: nkc+1 starves, 16..48 equal)
 #endif
@@ -1487,6 +1492,8 @@ void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat
     const bool flat = !heat && !G.S && !G.wpr;
     const long long items = (long long)G.nsg * G.njg * G.nkc * ((a.l_hi - a.l_lo) / a.l_step + 1);
     const unsigned grid = (unsigned)std::min<long long>(items, blocks[flat]);
+    SorArgs b = a;
+    if (b.order < 0) b.order = 2LL * G.nsg * G.njg * G.nkc <= blocks[flat] ? 0 : 1;
     const bool push = a.push_lo[0][0] != nullptr || a.push_hi[0][0] != nullptr;
     const int v = (colour & 1) | (heat ? 2 : 0) | (push ? 4 : 0) | (flat ? 8 : 0);
     using K = void (*)(const SorArgs);
@@ -1510,7 +1517,7 @@ void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat
     attr[0].val.programmaticStreamSerializationAllowed = pass_pdl() && !a.pdl_off ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    SSB_CUDA(cudaLaunchKernelEx(&cfg, fns[v], a));
+    SSB_CUDA(cudaLaunchKernelEx(&cfg, fns[v], b));
     SSB_LAUNCHED();
 }
 
