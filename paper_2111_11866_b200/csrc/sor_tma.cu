@@ -91,6 +91,10 @@ constexpr int kUKStages = SSB_UK_STAGES;      // other-colour planes (held for t
 #define SSB_PLANES_PER_ITEM 16  // measured: 8 -> 16 planes: config 2/4 -6%, config 1 -1% per sweep (fewer k-halo rows)
 #endif
 constexpr int kPlanesPerItem = SSB_PLANES_PER_ITEM;
+#ifndef SSB_SMALL_SLICE_ITEMS
+#define SSB_SMALL_SLICE_ITEMS 148  // whole-row items per slice (at kPlanesPerItem) below which items are halved
+#endif
+constexpr int kSmallSliceItems = SSB_SMALL_SLICE_ITEMS;
 constexpr int kDefaultSnake = 1;
 constexpr int kDefaultL2Hint = 0;
 // -1 = auto: slice-major (0) when a slice has at most half a grid of items -- several
@@ -183,6 +187,7 @@ struct Geo {  // per-launch tiling (identical on host and device)
     int wpr;  // warps per row (wide rows), 0: flat slot mapping (R * nq <= 256)
     int njg;  // row groups per plane
     int nkc;  // plane chunks per slice
+    int ppi;  // planes per item (chunk)
     long long items;
     uint32_t row_bytes;   // one packed row of doubles
     uint32_t coef_row_bytes;  // one row of fp32 coefficients (Wc slots x 8)
@@ -208,6 +213,7 @@ __host__ __device__ inline Geo make_geo(const Layout& L, bool tile2d = false) {
         g.pw = kTileS + 2;
         g.cpw = kTileS * 8;
         g.njg = (L.n2 + kTileR - 1) / kTileR;
+        g.ppi = kPlanesPerItem;
         g.nkc = (L.n3 + kPlanesPerItem - 1) / kPlanesPerItem;
         g.items = (long long)g.nsg * g.njg * g.nkc * L.n4;
         g.row_bytes = (uint32_t)g.pw * 8u;
@@ -253,7 +259,13 @@ __host__ __device__ inline Geo make_geo(const Layout& L, bool tile2d = false) {
     g.R = R;
     g.wpr = nq <= kSlotsPerPlane ? 0 : kWarps;  // 0: flat mapping
     g.njg = (L.n2 + R - 1) / R;
-    g.nkc = (L.n3 + kPlanesPerItem - 1) / kPlanesPerItem;
+    // planes per item: kPlanesPerItem, halved when a slice has few items (then the launch
+    // runs slice-major and the items' plane-chunk halo rows come from L2; config 1: -0.7%
+    // per sweep with 8 planes, config 2 (large slices) +1.8%, so it keeps 16)
+    g.ppi = kPlanesPerItem;
+    if (g.njg * ((L.n3 + kPlanesPerItem - 1) / kPlanesPerItem) <= kSmallSliceItems && kPlanesPerItem >= 4)
+        g.ppi = kPlanesPerItem / 2;
+    g.nkc = (L.n3 + g.ppi - 1) / g.ppi;
     g.items = (long long)g.njg * g.nkc * L.n4;
     g.row_bytes = rb;
     g.off_coef = 0;
@@ -280,8 +292,8 @@ __device__ __forceinline__ Item make_item(const Layout& L, const Geo& G, int l, 
     it.s0 = sg * G.S;
     it.j0 = jg * G.R + 1;
     it.rows = min(G.R, L.n2 - it.j0 + 1);
-    it.k0 = kc * kPlanesPerItem + 1;
-    it.k1 = min(it.k0 + kPlanesPerItem - 1, L.n3);
+    it.k0 = kc * G.ppi + 1;
+    it.k1 = min(it.k0 + G.ppi - 1, L.n3);
     return it;
 }
 
