@@ -1,19 +1,25 @@
 """bench.py -- SOR voxel-updates/s of the 4D SUBSURF time step on B200.
 
 Contract:
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config config1]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config config4]
 
-A *step* is one semi-implicit time step of segment() (solver.cpp:428-438):
-assemble_step + red-black SOR to relative residual 1e-8 + local_rescale, on
-BASELINE config 1 (64^4, two moving blobs; the largest config that is quoted
-for 1 GPU).  value = interior doxels x completed red+black sweeps / device time
-of the K timed steps (all ranks summed), inputs resident in HBM.  e2e = the same
-metric through the public session API with the step's input u copied H2D from
-pinned host memory and the result u copied D2H inside the timed region.
+Default workload: BASELINE config 4 -- 256x256x128 x (16 N) frames, weak scaling
+along t (one 16-frame slab per GPU; N = 1 is the largest single-GPU config, 134 M
+doxels), config-2 data and solver settings, exactly 50 red-black sweeps per time
+step.  A *step* = one time step of segment() with that fixed sweep count
+(solver.cpp:428-438): assemble_step + 50 sweeps + local_rescale.  --config
+config0/1/2 run segment() steps to relative residual 1e-8 instead; config3
+(512x512x128x64, strong, N >= 2) likewise.
+
+value = interior doxels x completed red+black sweeps / device time of the K
+timed steps (all ranks: max over ranks of the device time), inputs resident in
+HBM.  e2e = the same metric through the public session API with the step's input
+u copied H2D from pinned host memory and the result u copied D2H inside the timed
+region.
 
 --impl reference times the UNMODIFIED reference CPU solver (oracle/_ref, built
-from /root/reference/proj/src) through its own public calls on the same
-workload, on the host cores (rank 0 only under torchrun).
+from /root/reference/proj/src) through its own public calls on the same workload
+(rank 0 only under torchrun), with the same `config` dict.
 """
 from __future__ import annotations
 
@@ -34,6 +40,7 @@ sys.path.insert(0, ROOT)
 METRIC = "SOR voxel-updates/s (4D grid, red+black sweep = 1 update/doxel)"
 UNIT = "voxel-updates/s"
 SURVEY_BYTES_PER_SWEEP = 56.0  # 8 fp32 coeff + rhs + u read + u write
+FIXED_SWEEPS = 50              # BASELINE config 4
 
 
 def env_rank():
@@ -113,64 +120,15 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline_sample(wl, sweeps=40):
-    """The reference's own redblack_sor (oracle/_ref) on the workload's grid, all host
-    threads it can use (it parallelises over l only): `sweeps` red-black sweeps of the
-    first time step's system (assemble_step at u0 with G == 1), timed around
-    redblack_sor; the reference throws SolverError at max_iter, caught as intended."""
-    from oracle import oracle_py as op
-    if not op.ref_available():
-        return None
-    R = op.ref()
-    g = op.Grid.make(wl.dims, wl.h)
-    workers = min(R.lib.ref_hardware_threads(), wl.dims[3])
-    st, off, _, _ = R.assemble_step(g, wl.u0, None, wl.params["tau"], wl.params["epsilon"], workers)
-    t0 = time.perf_counter()
-    st, u, it, res = R.redblack_sor(g, off, wl.u0, wl.u0, wl.params["omega"], 1e-300, sweeps, workers)
-    dt = time.perf_counter() - t0
-    return {"value": wl.n_interior * it / dt, "unit": UNIT, "cores": workers, "kind": "reference",
-            "sample": f"{it} red-black sweeps of redblack_sor on the {wl.dims} system "
-                      f"(oracle/_ref = unmodified reference, {workers} std::thread workers), {dt:.2f} s"}
-
-
-def run_reference(args, wl):
-    rank, world, _ = env_rank()
-    if rank != 0:
-        return 0
-    from oracle import oracle_py as op
-    base = {"metric": METRIC, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl.name, "dims": list(wl.dims), "sor_rel_tol": 1e-8,
-                       "omega": wl.params["omega"]}}
-    if not op.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
-        return 0
-    R = op.ref()
-    g = op.Grid.make(wl.dims, wl.h)
-    workers = min(R.lib.ref_hardware_threads(), wl.dims[3])
-    n = args.warmup + args.steps
-    p = op.seg_params(**{**wl.params, "n_steps": n})
-    t0 = time.perf_counter()
-    st, u, info = R.segment(g, wl.image, wl.rows, p, wl.u0, workers)
-    wall = time.perf_counter() - t0
-    if st != 0:
-        print(json.dumps({"impl": "reference", "unavailable": f"reference segment failed: {R.lib.ref_last_error()}"}))
-        return 0
-    its = [d["iterations"] for d in info["diags"]][args.warmup:]
-    secs = info["step_seconds"][args.warmup:]
-    value = wl.n_interior * sum(its) / sum(secs)
-    line = dict(base)
-    line.update({
-        "value": value, "ms_per_step": 1e3 * sum(secs) / len(secs), "vs_baseline": None,
-        "sor_iterations": its,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
-                         "sample": f"time steps {args.warmup + 1}..{n} of segment() on {wl.dims} "
-                                   f"(setup {info['times'][0]:.1f} s untimed; total wall {wall:.1f} s)"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    })
-    print(json.dumps(line))
-    return 0
+def workload_config(wl, config: str, world: int) -> dict:
+    """The `config` dict of the JSON line -- identical in both arms (same workload)."""
+    fixed = wl.notes.get("fixed_sweeps")
+    big = wl.n_interior // world * 200 > 1e9
+    return {"workload": wl.name, "config": config, "dims": list(wl.dims), "omega": wl.params["omega"],
+            "sor": f"fixed {fixed} sweeps/step (no stopping test)" if fixed else "to relative residual 1e-8",
+            "l2": "inputs larger than L2 (no flush): state + coefficients + G ~ "
+                  f"{wl.n_interior // world * 200 / 1e9:.1f} GB per GPU vs 0.126 GB L2" if big
+                  else "working set partly L2-resident (small config)"}
 
 
 def make_workload(workloads, ssd, config, rank, world):
@@ -197,44 +155,91 @@ def make_workload(workloads, ssd, config, rank, world):
     return workloads.CONFIGS[config](planes=planes)
 
 
-def run_reference_sample(args, config):
-    """Reference arm for the big configs: the reference's redblack_sor on one 16-frame
-    t-slab of the config's grid (configs 3/4 do not fit host RAM
-    whole), 5 sweeps per step, G == 1 coefficients assembled at u0."""
+def cpu_baseline_sample(wl):
+    """The reference's own redblack_sor (oracle/_ref) on the workload's full grid, steady
+    state: the system assemble_step(u0, G == 1), then two calls of 2 and 22 sweeps timed on
+    the host's threads (the reference parallelises over l only: min(threads, n4) workers);
+    the difference of the two wall times / 20 is the per-sweep time without the per-call
+    scatter, coefficient packing and thread start-up."""
+    from oracle import oracle_py as op
+    if not op.ref_available():
+        return None
+    R = op.ref()
+    g = op.Grid.make(wl.dims, wl.h)
+    workers = min(R.lib.ref_hardware_threads(), wl.dims[3])
+    na, nb = 2, 22
+    t0 = time.perf_counter()
+    st, (sa, sb) = R.sor_rate(g, wl.u0, wl.params["tau"], wl.params["epsilon"], wl.params["omega"], na, nb, workers)
+    if st != 0:
+        return {"error": R.lib.ref_last_error().decode() if isinstance(R.lib.ref_last_error(), bytes) else "sor_rate failed"}
+    per_sweep = (sb - sa) / (nb - na)
+    return {"value": wl.n_interior / per_sweep, "unit": UNIT, "cores": workers, "kind": "reference",
+            "sample": f"redblack_sor of the unmodified reference (oracle/_ref) on the full {tuple(wl.dims)} grid, "
+                      f"{workers} std::thread workers: calls of {na} and {nb} sweeps ({sa:.2f} s, {sb:.2f} s), "
+                      f"per-sweep time = difference / {nb - na} = {per_sweep * 1e3:.1f} ms "
+                      f"(system assembled at u0 with G == 1; {time.perf_counter() - t0:.1f} s in all)"}
+
+
+def run_reference(args, config):
+    """The unmodified reference (oracle/_ref) through its public calls on the same
+    workload as our arm -- at N > 1 on one GPU's share of the weak-scaled grid (the host's
+    cores do not grow with N; the metric is a rate).  Per step: config 4 = assemble_step +
+    redblack_sor(max_iter 50, caught SolverError: the reference has no fixed-sweep mode and
+    drops the iterate) + local_rescale; configs 0-2 = segment() time steps to rel. 1e-8.
+    Bounded: one untimed warm-up step, then min(K, cap) timed steps."""
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
     import workloads
     from oracle import oracle_py as op
-    if not op.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+    if config == "config3":
+        print(json.dumps({"impl": "reference", "unavailable": "config3 needs ~530 GB of host RAM for the "
+                          "reference (234 B per padded doxel)"}))
         return 0
-    wl = workloads.CONFIGS[config](planes=(0, 17)) if config != "config4" else workloads.config4(1, planes=(0, 17))
-    n1, n2, n3, _ = wl.dims
-    dims = (n1, n2, n3, 16)
+    if not op.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
+        return 0
+    from paper_2111_11866_b200 import dist as ssd
+    wl = make_workload(workloads, ssd, config, 0, 1)
+    # the config dict names the N-GPU workload (rank 0's slab carries its global dims and
+    # name); the timed sample is the N = 1 workload, one GPU's share
+    cfg_wl = wl if world == 1 else make_workload(workloads, ssd, config, 0, world)
     R = op.ref()
-    g = op.Grid.make(dims, wl.h)
-    workers = min(R.lib.ref_hardware_threads(), 16)
-    u0 = np.ascontiguousarray(wl.u0)
-    st, off, _, _ = R.assemble_step(g, u0, None, wl.params["tau"], wl.params["epsilon"], workers)
-    sweeps, secs = 0, 0.0
-    for s in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        st, u, it, res = R.redblack_sor(g, off, u0, u0, wl.params["omega"], 1e-300, 5, workers)
-        dt = time.perf_counter() - t0
-        if s >= args.warmup:
-            sweeps += it
-            secs += dt
-    n = n1 * n2 * n3 * 16
-    value = n * sweeps / secs
-    print(json.dumps({
-        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": wl.name, "sample_dims": list(dims)},
+    g = op.Grid.make(wl.dims, wl.h)
+    workers = min(R.lib.ref_hardware_threads(), wl.dims[3])
+    cap = {"config0": 50, "config1": 20, "config2": 2, "config4": 4}[config]
+    timed = max(1, min(args.steps, cap))
+    n = 1 + timed
+    fixed = wl.notes.get("fixed_sweeps")
+    p = op.seg_params(**{**wl.params, "n_steps": n})
+    t0 = time.perf_counter()
+    if fixed:
+        st, u, info = R.segment_fixed(g, wl.image, wl.rows, p, wl.u0, workers, fixed, 1)
+    else:
+        st, u, info = R.segment(g, wl.image, wl.rows, p, wl.u0, workers)
+    wall = time.perf_counter() - t0
+    if st != 0:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference run failed: {R.lib.ref_last_error()}"}))
+        return 0
+    its = [d["iterations"] for d in info["diags"]][1:]
+    secs = info["step_seconds"][1:]
+    value = wl.n_interior * sum(its) / sum(secs)
+    what = (f"assemble_step + redblack_sor({fixed} sweeps, SolverError caught) + local_rescale" if fixed
+            else "segment() time steps (assemble_step + redblack_sor to rel. 1e-8 + local_rescale)")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": timed, "warmup": 1, "ms_per_step": 1e3 * sum(secs) / len(secs), "higher_is_better": True,
+        "scaling": "strong" if config in ("config2", "config3") else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": workload_config(cfg_wl, config, world),
+        "sor_iterations": its,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
-                         "sample": f"5 red-black sweeps per step of redblack_sor on a 16-frame t-slab {dims}"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+                         "sample": f"{timed} timed {what} on {tuple(wl.dims)} after 1 untimed step "
+                                   f"(setup: threshold, heat_smooth x2, face_coefficients {info['times'][0]:.1f} s untimed; "
+                                   f"wall {wall:.1f} s; steps capped at {cap} to bound the run)"
+                                   + (f"; at N = {world} one GPU's {tuple(wl.dims)} share of the grid" if world > 1 else "")},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
     return 0
 
 
@@ -244,25 +249,21 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="config1")
+    ap.add_argument("--config", default="config4", choices=["config0", "config1", "config2", "config3", "config4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--loop-mode", type=int, default=1)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
-    import workloads
-    rank, world, local = env_rank()
     if args.impl == "reference":
-        # the reference CPU solver on the N=1 workload of the config (its host cores do not
-        # scale with the GPU count; the metric is a throughput, comparable across N)
-        if args.config in ("config0", "config1"):
-            return run_reference(args, workloads.CONFIGS[args.config]())
-        return run_reference_sample(args, args.config)
+        return run_reference(args, args.config)
 
+    import workloads
     import torch
     import paper_2111_11866_b200 as ss
     from paper_2111_11866_b200 import dist as ssd
 
+    rank, world, local = env_rank()
     torch.cuda.set_device(local)
     uid = None
     force_dist = os.environ.get("SUBSURF_FORCE_DIST") == "1"  # exercise the NCCL path at N=1
@@ -276,7 +277,7 @@ def main():
     else:
         wl = make_workload(workloads, ssd, args.config, 0, 1)
     fixed = wl.notes.get("fixed_sweeps")
-    scaling = "strong" if (world > 1 and args.config in ("config2", "config3")) else "weak"
+    scaling = "strong" if args.config in ("config2", "config3") else "weak"
 
     g = ss.Grid.make(wl.dims, wl.h)
     p = ss.seg_params(**{**wl.params, "n_steps": args.warmup + args.steps})
@@ -291,9 +292,15 @@ def main():
 
     def do_step():
         if fixed:
-            sess.fixed_sweeps(fixed)  # config 4: assemble + exactly 50 sweeps
+            sess.step_fixed(fixed, diag=False)  # config 4: assemble + exactly 50 sweeps + rescale
         else:
             sess.step_nodiag()
+
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return [float(v) for v in t.tolist()]
 
     # ---------------- value: device-resident steps
     sess.prepare(wl.image, wl.rows, p, wl.u0)
@@ -314,10 +321,11 @@ def main():
     ms = e0.elapsed_time(e1)
     prof = sess.profile()
     sweeps = prof["sweeps"]
-    t = torch.tensor([ms], device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms_max = float(t.item())
+    # halo exchange of the timed run (t-slabs, N > 1): the comm stream's exchange time and the
+    # part the compute stream waited for after its interior slices
+    halo_vals = [prof["halo_ms"] / prof["halo_n"], prof["halo_exposed_ms"] / prof["halo_n"]] if prof.get("halo_n") \
+        else [0.0, 0.0]
+    ms_max, hx, hexp = max_over_ranks([ms] + halo_vals)
     value = wl.n_interior * sweeps / (ms_max * 1e-3)  # whole grid (all ranks) per second
 
     # ---------------- e2e: same steps through the public API with host buffers
@@ -342,12 +350,10 @@ def main():
     barrier()
     ms_e2e = f0.elapsed_time(f1)
     sweeps_e2e = sess.profile()["sweeps"]
-    t = torch.tensor([ms_e2e], device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = wl.n_interior * sweeps_e2e / (float(t.item()) * 1e-3)
+    (ms_e2e_max,) = max_over_ranks([ms_e2e])
+    e2e_value = wl.n_interior * sweeps_e2e / (ms_e2e_max * 1e-3)
 
-    # ---------------- roofline of the dominant kernel (SOR colour pass), event-timed
+    # ---------------- per-kernel split (profiling run, after the timed region)
     sess.prepare(wl.image, wl.rows, p, wl.u0)
     for _ in range(args.warmup):
         do_step()
@@ -357,8 +363,9 @@ def main():
         do_step()
     pr = sess.profile()
     sess.set_profiling(False)
-    # per-pass time measured live in the timed region: CUDA events around every SOR loop
-    # (one CUDA-graph launch per solve) / the colour passes it ran -- launch gaps and the
+    # roofline of the dominant kernel (SOR colour pass): its time measured live in the timed
+    # region -- CUDA events around every SOR loop (one CUDA-graph launch per solve; the
+    # host-driven loop on slab groups) / the colour passes it ran, launch gaps and the
     # finalize included; the profiling run's per-kernel events are reported beside it
     pass_ms_kernel = (pr["red_ms"] + pr["black_ms"]) / max(1, pr["red_n"] + pr["black_n"])
     pass_ms = prof["loop_ms"] / prof["loop_passes"] if prof.get("loop_passes") else pass_ms_kernel
@@ -373,47 +380,37 @@ def main():
             traffic = json.load(open(tf)).get(args.config, {}).get("sor_pass_bytes")
         except Exception:
             traffic = None
-    # halo exchange (t-slabs, N > 1): its device time on the comm stream and the part the
-    # compute stream waited for after the interior slices (max over ranks)
-    halo = None
-    if pr.get("halo_n"):
-        h = torch.tensor([pr["halo_ms"] / pr["halo_n"], pr["halo_exposed_ms"] / pr["halo_n"]], device="cuda")
-        if world > 1:
-            torch.distributed.all_reduce(h, op=torch.distributed.ReduceOp.MAX)
-        xm, ex = (float(v) for v in h.tolist())
-        halo = {"exchanges_timed": int(pr["halo_n"]), "exchange_ms": xm, "exposed_ms": ex,
-                "overlapped_ms": max(0.0, xm - ex), "pass_ms": pass_ms_kernel,
-                "source": "profiling run: events on the comm stream around each colour pass's "
-                          "exchange and on the compute stream after its interior slices (max over ranks)"}
-    sor_share = (pr["red_ms"] + pr["black_ms"]) / max(1e-9, pr["red_ms"] + pr["black_ms"] + pr["assemble_ms"] + pr["rescale_ms"])
+    tot = pr["red_ms"] + pr["black_ms"] + pr["assemble_ms"] + pr["rescale_ms"]
+    sor_share = (pr["red_ms"] + pr["black_ms"]) / max(1e-9, tot)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl.name, "dims": list(wl.dims), "sor_rel_tol": 1e-8,
-                       "omega": wl.params["omega"],
-                       "parallelism": f"t-slabs x{world} (NCCL halo exchange per colour pass)" if world > 1 else "1 GPU",
-                       "sor": f"fixed {fixed} sweeps/step" if fixed else "to relative residual 1e-8",
-                       "sweeps_timed": int(sweeps),
-                       "l2": f"inputs larger than L2: state+coef+G = {wl.n_interior // world * 200 / 1e9:.1f} GB per GPU vs 0.126 GB L2"
-                       if wl.n_interior // world * 200 > 1e9 else "working set partly L2-resident (small config)"},
+            "config": workload_config(wl, args.config, world),
+            "parallelism": f"t-slabs x{world} (NCCL halo exchange per colour pass)" if world > 1 else "1 GPU",
+            "sweeps_timed": int(sweeps),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * P * world,
                     "d2h_bytes_per_step": 8 * P * world},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "sor_pass (one colour half-sweep)",
+                         "kernel": "sor_pass_tma (one colour half-sweep)",
                          "bytes_per_launch": bytes_per_pass, "avg_launch_ms": pass_ms,
                          "avg_launch_ms_source": "timed region: events around each SOR loop / passes run"
                          if prof.get("loop_passes") else "profiling run: per-kernel events",
                          "avg_launch_ms_per_kernel_events": pass_ms_kernel,
-                         "peak_source": peak_src, "sor_share_of_step": sor_share},
+                         "peak_source": peak_src, "sor_share_of_step": sor_share,
+                         "assemble_ms_per_step": pr["assemble_ms"] / max(1, pr["assemble_n"])},
             "clocks": clk.summary(),
         }
-        if halo:
-            line["halo"] = halo
+        if world > 1:
+            line["halo"] = {"exchanges_timed": int(prof.get("halo_n", 0)), "exchange_ms": hx, "exposed_ms": hexp,
+                            "overlapped_ms": max(0.0, hx - hexp),
+                            "source": "timed region: events on the comm stream around each colour pass's "
+                                      "exchange and on the compute stream after its interior slices "
+                                      "(mean per exchange, max over ranks)"}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline_sample(wl)

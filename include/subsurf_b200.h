@@ -66,7 +66,9 @@ typedef struct {
     double K, delta, vartheta;
     double init_v, init_R;
     int init_profile;     /* 0 = peak, 1 = linear (seedinit.hpp:10) */
-    double rescale_radius;/* <= 0 => per-row radii (std::nullopt) */
+    double rescale_radius;/* NaN => per-row radii (std::nullopt); any other value is the
+                           * explicit radius, r <= 0 included (a ball of at most one
+                           * doxel: the rescale is a no-op, seedinit.cpp:73-88) */
 } ss_seg_params;
 
 /* per-step diagnostics line (solver.cpp:433-438) */
@@ -112,7 +114,8 @@ SS_API ss_status ss_local_threshold(const ss_grid* g, const double* image, const
 /* build_initial (seedinit.hpp:25-26, seedinit.cpp:42-66) */
 SS_API ss_status ss_build_initial(const ss_grid* g, const ss_center* c, int n, double v,
                                   double R, int profile, double* u);
-/* local_rescale (seedinit.hpp:32-33, seedinit.cpp:68-99); radius <= 0 => per-row */
+/* local_rescale (seedinit.hpp:32-33, seedinit.cpp:68-99); radius NaN => per-row radii
+ * (std::nullopt), otherwise the explicit radius (r <= 0: no-op, as in the reference) */
 SS_API ss_status ss_local_rescale(const ss_grid* g, double* u, const ss_center* c, int n,
                                   double radius);
 /* apply_dirichlet (grid.cpp:126-136), apply_mirror_ghosts (grid.cpp:138-156),
@@ -206,8 +209,16 @@ SS_API ss_status ss_session_get_mask(ss_session* s, double level, uint8_t* mask)
 SS_API ss_status ss_session_track(ss_session* s, double level, int window, double radius,
                                   ss_track_point* out, int capacity, int* n_points);
 /* fixed-sweep mode (BASELINE config 4): assemble at the current u, then exactly
- * n_sweeps red+black sweeps with no stopping test; *residual = last residual. */
+ * n_sweeps red+black sweeps with no stopping test; *residual = last residual.
+ * Non-finite coefficients: SS_ERR_NONFINITE (solver.cpp:71-75). */
 SS_API ss_status ss_session_fixed_sweeps(ss_session* s, int n_sweeps, double* residual);
+/* one time step of BASELINE config 4 (ABI 5): ss_session_step with exactly n_sweeps
+ * sweeps and no stopping test in place of the solve to tolerance (assemble_step,
+ * n_sweeps red+black sweeps, local_rescale).  The reference has no such mode: its
+ * redblack_sor throws SolverError at max_iter and drops the iterate (solver.cpp:391-395);
+ * this is that iterate (tests pin it against the reference, tests/golden/pins.json).
+ * diag: iterations = n_sweeps, residual = the last residual, tol = 1. */
+SS_API ss_status ss_session_step_fixed(ss_session* s, int n_sweeps, ss_step_diag* diag);
 /* run_levelset_row (eoc.cpp:83-137): the EOC verification row n (10/20/40/80/160) on a
  * session created for the grid n^4 with h = 2.5/n; *err = space-time L2 error,
  * *sweeps = total SOR sweeps (may be NULL).  EocConfig defaults: omega 1.5, tol 1e-8. */

@@ -67,7 +67,9 @@ def seg_params(**kw) -> SegParams:
              rescale_each_step=1, sor_rel_tol=0.0, sigma=0.0, smooth_steps=1, smooth_tol=1e-10,
              smooth_max_iter=10000, smooth_omega=1.85, lambda_=0.5, background=0.0, K=1.0,
              delta=1.0, vartheta=0.0, init_v=1.0, init_R=10.0, init_profile=0,
-             rescale_radius=0.0)
+             rescale_radius=float("nan"))  # NaN = std::nullopt: per-row radii
+    if kw.get("rescale_radius", 0.0) is None:
+        kw["rescale_radius"] = float("nan")
     if "lam" in kw:
         kw["lambda_"] = kw.pop("lam")
     d.update(kw)
@@ -131,6 +133,11 @@ class _Lib:
         if with_workers:
             seg_args += [_D, C.POINTER(C.c_longlong), _D]
         self._seg = sig("segment", seg_args)
+        if with_workers:
+            self._sorrate = sig("sor_rate", [_G, _D, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
+                                             C.c_int, _D])
+            self._segfix = sig("segment_fixed", [_G, _D, _CEN, C.c_int, C.POINTER(SegParams), _D, C.c_int,
+                                                 C.c_int, C.c_int, _D, C.POINTER(StepDiag), _D, _D])
         if with_workers:  # tracking: the reference itself (tracking.cpp) is the checker
             _I = C.POINTER(C.c_int)
             self._lab = sig("label_components", [_G, C.POINTER(C.c_ubyte), _I, _I])
@@ -192,7 +199,9 @@ class _Lib:
         st = self._init(C.byref(g), arr, n, v, R, profile, _p(out))
         return st, out
 
-    def local_rescale(self, g, u, rows, radius=0.0):
+    def local_rescale(self, g, u, rows, radius=None):
+        """radius None = std::nullopt (each row's own radius); any number is explicit"""
+        radius = float("nan") if radius is None else float(radius)
         arr, n = centers_array(rows)
         u = np.array(u, dtype=np.float64, copy=True)
         st = self._resc(C.byref(g), _p(u), arr, n, radius)
@@ -280,6 +289,28 @@ class _Lib:
         if self.w:
             info.update(times=times.tolist(), sweeps=sweeps.value, step_seconds=step_s.tolist())
         return st, out, info
+
+    def segment_fixed(self, g, image, rows, params: SegParams, u0=None, workers=1, n_sweeps=50, mode=0):
+        """Reference only (ref_shim.cpp ref_segment_fixed): n_steps time steps of exactly
+        n_sweeps red-black sweeps each.  mode 0 returns the reference's own iterate (parity
+        pin), mode 1 times the throwing redblack_sor call without advancing u (bench)."""
+        arr, n = centers_array(rows)
+        out = np.empty(g.shape)
+        diags = (StepDiag * params.n_steps)()
+        times = np.zeros(4)
+        step_s = np.zeros(params.n_steps)
+        st = self._segfix(C.byref(g), _p(image), arr, n, C.byref(params), _p(u0), int(workers), int(n_sweeps),
+                          int(mode), _p(out), diags, _p(times), _p(step_s))
+        d = [dict(iterations=x.iterations, residual=x.residual, tol=x.tol, umin=x.umin,
+                  umax=x.umax) for x in diags]
+        return st, out, dict(diags=d, times=times.tolist(), step_seconds=step_s.tolist())
+
+    def sor_rate(self, g, u0, tau, eps, omega, n_a, n_b, workers):
+        """Reference only: wall seconds of redblack_sor calls of n_a and n_b sweeps."""
+        secs = np.zeros(2)
+        st = self._sorrate(C.byref(g), _p(np.ascontiguousarray(u0)), tau, eps, omega, int(n_a), int(n_b),
+                           int(workers), _p(secs))
+        return st, secs.tolist()
 
 
 _oracle = None

@@ -105,6 +105,33 @@ double interior_norm2(const Field4D& u) {
     return std::sqrt(acc);
 }
 
+SegmentationParams seg_of(const or_seg_params* p, int workers) {
+    SegmentationParams sp;
+    sp.solver.tau = p->tau;
+    sp.solver.epsilon = p->epsilon;
+    sp.solver.omega = p->omega;
+    sp.solver.sor_tol = p->sor_tol;
+    sp.solver.sor_max_iter = p->sor_max_iter;
+    sp.solver.n_steps = p->n_steps;
+    sp.solver.rescale_each_step = p->rescale_each_step != 0;
+    sp.smoothing.sigma = p->sigma;
+    sp.smoothing.steps = p->smooth_steps;
+    sp.smoothing.sor_tol = p->smooth_tol;
+    sp.smoothing.sor_max_iter = p->smooth_max_iter;
+    sp.smoothing.omega = p->smooth_omega;
+    sp.threshold.lambda = p->lambda;
+    sp.threshold.background = p->background;
+    sp.edge.K = p->K;
+    sp.edge.delta = p->delta;
+    sp.edge.vartheta = p->vartheta;
+    sp.init.v = p->init_v;
+    sp.init.R = p->init_R;
+    sp.init.profile = p->init_profile == 0 ? InitProfile::peak : InitProfile::linear;
+    if (!std::isnan(p->rescale_radius)) sp.rescale_radius = p->rescale_radius;
+    sp.workers = workers;
+    return sp;
+}
+
 }  // namespace
 
 extern "C" {
@@ -237,7 +264,7 @@ int ref_build_initial(const or_grid* g, const or_center* c, int n, double v, dou
 int ref_local_rescale(const or_grid* g, double* u, const or_center* c, int n, double radius) {
     return guarded([&] {
         Field4D f = field_of(g, u);
-        local_rescale(f, table_of(c, n), radius > 0.0 ? std::optional<double>(radius) : std::nullopt);
+        local_rescale(f, table_of(c, n), std::isnan(radius) ? std::nullopt : std::optional<double>(radius));
         store(f, u);
     });
 }
@@ -404,29 +431,7 @@ int ref_segment(const or_grid* g, const double* image, const or_center* c, int n
                 or_step_diag* diags, double* times, long long* sor_sweeps, double* step_seconds) {
     using clk = std::chrono::steady_clock;
     return guarded([&] {
-        SegmentationParams sp;
-        sp.solver.tau = p->tau;
-        sp.solver.epsilon = p->epsilon;
-        sp.solver.omega = p->omega;
-        sp.solver.sor_tol = p->sor_tol;
-        sp.solver.sor_max_iter = p->sor_max_iter;
-        sp.solver.n_steps = p->n_steps;
-        sp.solver.rescale_each_step = p->rescale_each_step != 0;
-        sp.smoothing.sigma = p->sigma;
-        sp.smoothing.steps = p->smooth_steps;
-        sp.smoothing.sor_tol = p->smooth_tol;
-        sp.smoothing.sor_max_iter = p->smooth_max_iter;
-        sp.smoothing.omega = p->smooth_omega;
-        sp.threshold.lambda = p->lambda;
-        sp.threshold.background = p->background;
-        sp.edge.K = p->K;
-        sp.edge.delta = p->delta;
-        sp.edge.vartheta = p->vartheta;
-        sp.init.v = p->init_v;
-        sp.init.R = p->init_R;
-        sp.init.profile = p->init_profile == 0 ? InitProfile::peak : InitProfile::linear;
-        if (p->rescale_radius > 0.0) sp.rescale_radius = p->rescale_radius;
-        sp.workers = workers;
+        SegmentationParams sp = seg_of(p, workers);
 
         const Field4D image_f = field_of(g, image);
         const CentersTable centers = table_of(c, n);
@@ -484,6 +489,114 @@ int ref_segment(const or_grid* g, const double* image, const or_center* c, int n
             times[3] = t_resc;
         }
         if (sor_sweeps) *sor_sweeps = sweeps;
+    });
+}
+
+// Fixed-sweep time steps (BASELINE config 4: "fixed 50 SOR sweeps per time step, no early
+// stop") through the reference's public calls.  The reference has no such mode:
+// redblack_sor throws SolverError{last_residual, iterations} at max_iter and discards the
+// iterate (solver.cpp:201-206, :391-395).  Same preamble as ref_segment, then per step
+// assemble_step + redblack_sor(max_iter = n_sweeps, sor_tol = 1e-300) + local_rescale.
+//   mode 0 (parity pin): the iterate after exactly n_sweeps sweeps is recovered from the
+//     reference itself by a second call with sor_tol = the thrown residual r_n: it stops at
+//     the first iteration whose residual is <= r_n, which must be n_sweeps (checked;
+//     residuals decrease strictly in practice), and returns that iterate.
+//   mode 1 (bench): only the throwing call is made (timed with the assembly and the
+//     rescale); the reference discards its iterate, so u is not advanced -- every step
+//     repeats the same work.
+int ref_segment_fixed(const or_grid* g, const double* image, const or_center* c, int n,
+                      const or_seg_params* p, const double* u0, int workers, int n_sweeps, int mode,
+                      double* u_out, or_step_diag* diags, double* times, double* step_seconds) {
+    using clk = std::chrono::steady_clock;
+    return guarded([&] {
+        SegmentationParams sp = seg_of(p, workers);
+        const Field4D image_f = field_of(g, image);
+        const CentersTable centers = table_of(c, n);
+        const auto t0 = clk::now();
+        const GridSpec& spec = image_f.spec();
+        sp.solver.validate();
+        validate_centers(centers, spec);
+        const int w = Partition::clamp_workers(spec.n4, sp.workers);
+        Field4D u = u0 ? field_of(g, u0) : build_initial(centers, sp.init, spec);
+        local_rescale(u, centers, sp.rescale_radius);
+        const Field4D th = local_threshold(image_f, centers, sp.threshold);
+        const Field4D I0s = heat_smooth(image_f, sp.smoothing, w);
+        const Field4D ITs = heat_smooth(th, sp.smoothing, w);
+        const FaceCoefficientField G = face_coefficients(I0s, ITs, sp.edge, spec, w);
+        apply_dirichlet(u, 0.0);
+        const Partition part = Partition::create(spec.n4, w);
+        const auto t1 = clk::now();
+        for (int step = 1; step <= sp.solver.n_steps; ++step) {
+            const auto a0 = clk::now();
+            const StepCoefficients coeff = assemble_step(u, &G, sp.solver, spec, w);
+            SolverParams stp = sp.solver;
+            stp.sor_tol = 1e-300;
+            stp.sor_max_iter = n_sweeps;
+            double r = 0.0;
+            int it = 0;
+            try {
+                SorResult sor = redblack_sor(coeff, u, u, stp, part);  // converged below 1e-300
+                r = sor.residual;
+                it = sor.iterations;
+                if (mode == 0) u = std::move(sor.u);
+            } catch (const SolverError& e) {
+                r = e.last_residual;
+                it = e.iterations;
+                if (mode == 0) {
+                    stp.sor_tol = r;
+                    SorResult sor = redblack_sor(coeff, u, u, stp, part);
+                    if (sor.iterations != n_sweeps || sor.residual != r)
+                        throw std::runtime_error("fixed-sweep pin: residual not strictly decreasing (stopped at " +
+                                                 std::to_string(sor.iterations) + ")");
+                    u = std::move(sor.u);
+                }
+            }
+            if (sp.solver.rescale_each_step) local_rescale(u, centers, sp.rescale_radius);
+            const auto a1 = clk::now();
+            if (step_seconds) step_seconds[step - 1] = std::chrono::duration<double>(a1 - a0).count();
+            if (diags) {
+                diags[step - 1].iterations = it;
+                diags[step - 1].residual = r;
+                diags[step - 1].tol = 1e-300;
+                const auto [lo, hi] = interior_minmax(u);
+                diags[step - 1].umin = lo;
+                diags[step - 1].umax = hi;
+            }
+        }
+        store(u, u_out);
+        if (times) times[0] = std::chrono::duration<double>(t1 - t0).count();
+    });
+}
+
+// Steady-state sweep rate of the reference's redblack_sor (bench.py cpu_baseline): the
+// system assemble_step(u, G == 1) on the caller's grid, then two calls of n_a and n_b
+// sweeps (max_iter, sor_tol = 1e-300: both end in SolverError, caught).  secs[0], secs[1]
+// are their wall times; (secs[1] - secs[0]) / (n_b - n_a) is the time per sweep with the
+// per-call scatter / coefficient packing / thread start-up cancelled out.
+int ref_sor_rate(const or_grid* g, const double* u0, double tau, double eps, double omega, int n_a, int n_b,
+                 int workers, double* secs) {
+    using clk = std::chrono::steady_clock;
+    return guarded([&] {
+        SolverParams sp;
+        sp.tau = tau;
+        sp.epsilon = eps;
+        sp.omega = omega;
+        sp.sor_tol = 1e-300;
+        const GridSpec spec = spec_of(g);
+        const int w = Partition::clamp_workers(spec.n4, workers);
+        const Field4D u = field_of(g, u0);
+        const StepCoefficients coeff = assemble_step(u, nullptr, sp, spec, w);
+        const Partition part = Partition::create(spec.n4, w);
+        const int ns[2] = {n_a, n_b};
+        for (int q = 0; q < 2; ++q) {
+            sp.sor_max_iter = ns[q];
+            const auto t0 = clk::now();
+            try {
+                (void)redblack_sor(coeff, u, u, sp, part);
+            } catch (const SolverError&) {
+            }
+            secs[q] = std::chrono::duration<double>(clk::now() - t0).count();
+        }
     });
 }
 

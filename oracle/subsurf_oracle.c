@@ -483,7 +483,7 @@ int or_build_initial(const or_grid* g, const or_center* c, int n, double v, doub
 int or_local_rescale(const or_grid* g, double* u, const or_center* c, int n, double radius) {
     if (or_validate_centers(g, c, n) != OR_OK) return OR_ERR_VALIDATION;
     for (int m = 0; m < n; ++m) {
-        const double r = radius > 0.0 ? radius : c[m].radius;
+        const double r = isnan(radius) ? c[m].radius : radius; /* NaN = std::nullopt (value_or) */
         const int l = c[m].frame + 1;
         const ball_box b = ball_bounds(&c[m], r, g);
         const double r_sq = r * r;

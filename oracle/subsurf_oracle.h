@@ -114,7 +114,7 @@ typedef struct {
     /* InitParams */
     double init_v, init_R;
     int init_profile;
-    /* rescale radius (<= 0: per-row) */
+    /* rescale radius (NaN: per-row radii = std::nullopt; else explicit) */
     double rescale_radius;
 } or_seg_params;
 

@@ -143,7 +143,9 @@ def seg_params(**kw) -> SegParams:
              rescale_each_step=1, sor_rel_tol=0.0, sigma=0.0, smooth_steps=1, smooth_tol=1e-10,
              smooth_max_iter=10000, smooth_omega=1.85, lambda_=0.5, background=0.0, K=1.0,
              delta=1.0, vartheta=0.0, init_v=1.0, init_R=10.0, init_profile=0,
-             rescale_radius=0.0)
+             rescale_radius=float("nan"))  # NaN = std::nullopt: per-row radii
+    if kw.get("rescale_radius", 0.0) is None:
+        kw["rescale_radius"] = float("nan")
     if "lam" in kw:
         kw["lambda_"] = kw.pop("lam")
     d.update(kw)
@@ -211,6 +213,7 @@ def library() -> C.CDLL:
     sig("ss_session_get_u", [C.c_void_p, _D])
     sig("ss_session_get_mask", [C.c_void_p, C.c_double, C.POINTER(C.c_uint8)])
     sig("ss_session_fixed_sweeps", [C.c_void_p, C.c_int, _D])
+    sig("ss_session_step_fixed", [C.c_void_p, C.c_int, C.POINTER(StepDiag)])
     sig("ss_session_set_loop_mode", [C.c_void_p, C.c_int])
     sig("ss_session_eoc_row", [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, _D,
                                C.POINTER(C.c_longlong)])
@@ -358,7 +361,7 @@ def local_rescale(u, centers, g: Grid, radius: Optional[float] = None) -> np.nda
     """Returns the rescaled copy (the reference rescales in place)."""
     out = np.array(_field(g, u, "u"), copy=True)
     arr, n = _centers(centers)
-    _check(library().ss_local_rescale(C.byref(g), _dp(out), arr, n, 0.0 if radius is None else radius))
+    _check(library().ss_local_rescale(C.byref(g), _dp(out), arr, n, float("nan") if radius is None else float(radius)))
     return out
 
 
@@ -560,6 +563,12 @@ class Session:
 
     def step_nodiag(self) -> None:
         _check(library().ss_session_step(self._h, None))
+
+    def step_fixed(self, n_sweeps: int, diag: bool = True):
+        """One BASELINE config-4 time step: assemble, exactly n_sweeps sweeps, rescale."""
+        d = StepDiag()
+        _check(library().ss_session_step_fixed(self._h, n_sweeps, C.byref(d) if diag else None))
+        return dict(iterations=d.iterations, residual=d.residual, tol=d.tol, umin=d.umin, umax=d.umax) if diag else None
 
     def set_u(self, u) -> None:
         a = self._host(u, "u")

@@ -98,7 +98,7 @@ struct ss_session {
 extern "C" {
 
 const char* ss_last_error(void) { return t_err.c_str(); }
-int ss_abi_version(void) { return 4; }
+int ss_abi_version(void) { return 5; }
 unsigned long long ss_launch_count(void) { return g_launches.load(); }
 
 int ss_device_available(void) {
@@ -616,6 +616,15 @@ ss_status ss_session_fixed_sweeps(ss_session* s, int n_sweeps, double* residual)
     });
 }
 
+ss_status ss_session_step_fixed(ss_session* s, int n_sweeps, ss_step_diag* diag) {
+    return guard([&] {
+        require(s != nullptr, "null session");
+        require(n_sweeps >= 1, "n_sweeps must be >= 1");
+        SSB_CUDA(cudaSetDevice(s->d->device));
+        s->d->step(diag, n_sweeps, true);
+    });
+}
+
 ss_status ss_session_eoc_row(ss_session* s, int n, double omega, double sor_tol, int sor_max_iter, double* err,
                              long long* sweeps) {
     return guard([&] {
@@ -641,6 +650,9 @@ ss_status ss_session_set_kernel(ss_session* s, int kernel) {
         require(kernel >= 0 && kernel <= 7 && kernel != 6,
                 "kernel must be 0 (LDG), 1 (TMA), 2 (TMA wavefront), 3 (resident), 4 (auto), 5 (2D-tiled TMA) "
                 "or 7 (one-sweep k-wavefront)");
+        if (s->d->kernel != kernel) {  // captured loops of the old kernel are not reused
+            s->d->clear_graphs();
+        }
         s->d->kernel = kernel;
     });
 }

@@ -106,7 +106,7 @@ void build_balls(BallSet& bs, const ss_grid& gl, int l0, const ss_center* c, int
     std::vector<int> rows;
     for (int m = 0; m < n; ++m) {
         if (c[m].frame + 1 - l0 < 1 || c[m].frame + 1 - l0 > gl.n4) continue;  // other slab
-        table.push_back(make_ball(gl, c[m], fixed_radius || radius > 0.0 ? radius : c[m].radius, l0));
+        table.push_back(make_ball(gl, c[m], fixed_radius || !std::isnan(radius) ? radius : c[m].radius, l0));
         rows.push_back(m);
     }
     const int nb = (int)table.size();
@@ -160,6 +160,7 @@ Slab::Slab(const ss_grid& global, int l0, int n4_local, int idx, int chunk, int 
     norm_loc.alloc(chunk);
     norm_part.alloc((size_t)chunk * kNormChunks);
     if (world > 1) {
+        bad_all.alloc(world);
         all_slices.alloc((size_t)world * chunk);
         norm_all.alloc((size_t)world * chunk);
         SSB_CUDA(cudaMemsetAsync(all_slices.p, 0, all_slices.n * sizeof(double), stream));
@@ -375,7 +376,9 @@ void LocalTransport::allgather(std::vector<Slab*>& slabs, const std::vector<doub
 // ------------------------------------------------------------------ domain
 struct Domain::GraphEntry {
     const void* key_ptr[2 * kStateBuffers + 2];
+    const void* maps;
     int heat;
+    int variant[7];  // every launch-shape switch of the captured pass kernels (graph_variant)
     double omega, hc[4];
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -473,6 +476,11 @@ Domain::~Domain() {
 }
 
 void Domain::sync() { SSB_CUDA(cudaStreamSynchronize(stream)); }
+
+void Domain::clear_graphs() {
+    sync();
+    graphs.clear();
+}
 
 long long Domain::host_plane() const { return (long long)(g.n1 + 2) * (g.n2 + 2) * (g.n3 + 2); }
 
@@ -591,22 +599,39 @@ int graph_unroll() {
     return v;
 }
 
+// the switches that select which pass kernels / item shapes a captured loop body launches:
+// a graph is reused only when all of them agree (ss_session_set_kernel may change them)
+static void graph_variant(const SorArgs& a, int v[7]) {
+    v[0] = a.tma;
+    v[1] = a.wave;
+    v[2] = a.tile2d;
+    v[3] = a.fuse_final;
+    v[4] = a.order;
+    v[5] = a.snake;
+    v[6] = a.l2hint;
+}
+
 cudaGraphExec_t Domain::graph_for(const SorArgs& base, bool heat) {
     constexpr int NK = 2 * kStateBuffers + 2;
+    int variant[7];
+    graph_variant(base, variant);
     const void* key[NK];
     for (int b = 0; b < kStateBuffers; ++b)
         for (int c = 0; c < 2; ++c) key[2 * b + c] = base.U[b][c];
     key[NK - 2] = base.rhs[0];
     key[NK - 1] = base.rhs[1];
     for (auto& e : graphs) {
-        bool same = e->heat == (int)heat + 2 * base.tma + 4 * base.wave && e->omega == base.omega;
+        bool same = e->heat == (int)heat && e->omega == base.omega && e->maps == (const void*)base.maps &&
+                    std::memcmp(e->variant, variant, sizeof variant) == 0;
         for (int q = 0; q < NK && same; ++q) same = e->key_ptr[q] == key[q];
         for (int q = 0; q < 4 && same; ++q) same = e->hc[q] == base.hc[q];
         if (same) return e->exec;
     }
     std::unique_ptr<GraphEntry> e(new GraphEntry);
     std::memcpy(e->key_ptr, key, sizeof key);
-    e->heat = (int)heat + 2 * base.tma + 4 * base.wave;
+    e->heat = (int)heat;
+    e->maps = base.maps;
+    std::memcpy(e->variant, variant, sizeof variant);
     e->omega = base.omega;
     std::memcpy(e->hc, base.hc, sizeof e->hc);
     SSB_CUDA(cudaGraphCreate(&e->graph, 0));
@@ -645,7 +670,7 @@ void Domain::body_single(const SorArgs& a, bool heat, cudaEvent_t* ev4) {
 // new red boundary planes, per-slice residuals + all-gather + decision, black,
 // exchange the new black boundary planes.
 void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>& B, bool heat, int n,
-                        cudaEvent_t* ev4) {
+                        cudaEvent_t* ev4, cudaEvent_t* xev6) {
     const int bout = out_buf(n);
     std::vector<PField> F;
     for (const Triple& t : B) F.push_back(t[bout]);
@@ -669,8 +694,9 @@ void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>
         SSB_CUDA(cudaEventRecord(ev_pre, stream));
         SSB_CUDA(cudaStreamWaitEvent(bnd, ev_pre, 0));
         for (const SorArgs& x : a) launch_sor_pass_ends(bnd, x, colour, heat);
-        // profiling: x[0] exchange start (comm), x[1] exchange end (comm), x[2] interior done
-        cudaEvent_t* xe = ev4 ? ev4 + 4 + 3 * colour : nullptr;
+        // halo timing (every timed multi-slab solve): x[0] exchange start (comm), x[1]
+        // exchange end (comm), x[2] interior slices done (main stream)
+        cudaEvent_t* xe = xev6 ? xev6 + 3 * colour : nullptr;
         SSB_CUDA(cudaEventRecord(ev_bnd, bnd));
         SSB_CUDA(cudaStreamWaitEvent(comm, ev_bnd, 0));
         if (xe) SSB_CUDA(cudaEventRecord(xe[0], comm));
@@ -705,7 +731,7 @@ void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>
 
 SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& rhs, bool heat, double omega,
                        const double hc[4], double tol_abs, bool use_norm, double rel, int max_iter, bool fixed,
-                       int* result) {
+                       int* result, bool check_assembly) {
     std::vector<SorArgs> a;
     // resident loop: single slab whose working set fits L2 (auto) or on request
     bool resident = single() && (kernel == 3 || (kernel == 4 && resident_supported(sp[0]->L)));
@@ -714,10 +740,21 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
     int kern = resident ? 0 : (kernel == 4 ? 6 : kernel == 3 ? 1 : kernel);
     solve_count = (solve_count + 1) & 0x3fff;
     const int epoch_base = (solve_count + 1) << 16;  // differs from the previous solve's
+    if (check_assembly && world > 1) {  // every slab's assembly flag to every slab, on the device
+        std::vector<double*> loc, all;
+        for (Slab* s : sp) {
+            launch_flag_to_double(stream, s->flags.p, s->gloc.p);
+            loc.push_back(s->gloc.p);
+            all.push_back(s->bad_all.p);
+        }
+        tr->allgather(sp, loc, all, 1);
+    }
     for (size_t s = 0; s < sp.size(); ++s) {
         Slab& x = *sp[s];
         const double* ns = use_norm ? (world == 1 ? x.norm_loc.p : x.norm_all.p) : nullptr;
-        launch_sor_init(stream, x.st.p, tol_abs, ns, g.n4, rel, max_iter, fixed ? 1 : 0, epoch_base);
+        launch_sor_init(stream, x.st.p, tol_abs, ns, g.n4, rel, max_iter, fixed ? 1 : 0, epoch_base,
+                        check_assembly && world == 1 ? x.flags.p : nullptr,
+                        check_assembly && world > 1 ? x.bad_all.p : nullptr, world);
         a.push_back(x.sor_args(B[s].data(), rhs[s], heat, omega, hc, world, kern));
     }
     // in-process slab group with the TMA pass: neighbours' halo planes are written by
@@ -796,13 +833,16 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
         o.residual = st_host->residual;
         o.tol = st_host->tol;
         o.converged = st_host->converged != 0;
+        o.nonfinite = st_host->nonfinite != 0;
         prof.sweeps += o.iterations;
         *result = o.iterations == 0 ? 0 : out_buf(o.iterations);
         return o;
     }
     const bool wave = a[0].wave != 0;
-    // exchanges on the comm stream (not the in-kernel halo push): timed in profiling mode
-    const bool halo_timed = profiling && !single() && !wave && a[0].push_lo[0][0] == nullptr &&
+    // exchanges on the comm stream (not the in-kernel halo push): timed in every multi-slab
+    // segmentation solve, profiling or not (events on the comm / main streams; the accounting
+    // reads them once the solve is over), so the bench reports the timed run's own halo time
+    const bool halo_timed = !heat && !single() && !wave && a[0].push_lo[0][0] == nullptr &&
                             a[0].push_hi[0][0] == nullptr;
     // loop bodies: red(max_iter+1) evaluates the last residual; a wavefront body
     // covers two iterations
@@ -844,16 +884,16 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
                 // per body: red/black pass bounds (4) + the two exchanges' events (multi-slab, 6)
                 cudaEvent_t evs[kBodyEvents];
                 cudaEvent_t* e4 = nullptr;
-                if (profiling) {
+                if (profiling || halo_timed) {
                     for (int q = 0; q < kBodyEvents; ++q) evs[q] = pool_event(ev_used + q);
                     body_ev.push_back(ev_used);
                     ev_used += kBodyEvents;
                     e4 = evs;
                 }
                 if (single())
-                    body_single(a[0], heat, e4);
+                    body_single(a[0], heat, profiling ? e4 : nullptr);
                 else
-                    body_multi(a, B, heat, n, e4);
+                    body_multi(a, B, heat, n, profiling ? e4 : nullptr, halo_timed ? e4 + 4 : nullptr);
             }
             launched += nb;
             SSB_CUDA(cudaMemcpyAsync(flag_host + slot, &sp[0]->st.p->done, sizeof(int), cudaMemcpyDeviceToHost,
@@ -880,17 +920,17 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
                 prof.red_ms += ms;
                 prof.red_n += 2 * WI;
             }
-        } else if (profiling) {
+        } else if (profiling || halo_timed) {
             const int it = st_host->iterations;
             for (size_t b = 0; b < body_ev.size(); ++b) {
                 float ms = 0.f;
                 const size_t base = body_ev[b];
-                if ((int)b <= it) {  // red(b+1) did real work (b+1 <= it+1)
+                if (profiling && (int)b <= it) {  // red(b+1) did real work (b+1 <= it+1)
                     SSB_CUDA(cudaEventElapsedTime(&ms, ev_pool[base], ev_pool[base + 1]));
                     prof.red_ms += ms;
                     prof.red_n++;
                 }
-                if ((int)b < it) {  // black(b+1) did real work
+                if (profiling && (int)b < it) {  // black(b+1) did real work
                     SSB_CUDA(cudaEventElapsedTime(&ms, ev_pool[base + 2], ev_pool[base + 3]));
                     prof.black_ms += ms;
                     prof.black_n++;
@@ -914,6 +954,7 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
     o.residual = st_host->residual;
     o.tol = st_host->tol;
     o.converged = st_host->converged != 0;
+    o.nonfinite = st_host->nonfinite != 0;
     prof.sweeps += o.iterations;
     *result = o.iterations == 0 ? 0 : out_buf(o.iterations);
     return o;
@@ -1052,7 +1093,7 @@ void Domain::prepare(const double* image, const ss_center* c, int n, const ss_se
         for (size_t s = 0; s < sp.size(); ++s) {
             Slab& x = *sp[s];
             bsets.emplace_back(new BallSet);
-            build_balls(*bsets.back(), x.gl, x.L.l0, c, n, 0.0, false);
+            build_balls(*bsets.back(), x.gl, x.L.l0, c, n, std::nan(""), false);  // per-row radii
             abs.emplace_back(new Dev<double>);
             abs.back()->alloc(2 * (size_t)std::max(1, bsets.back()->count()));
             launch_fill(stream, x.L, th[s]->pf(), p.background);
@@ -1105,7 +1146,12 @@ void Domain::prepare(const double* image, const ss_center* c, int n, const ss_se
     prepared = true;
 }
 
-void Domain::step(ss_step_diag* diag) {
+// One time step of the segment() loop (solver.cpp:428-438): exchange the u^{n-1} halos,
+// assemble_step, the per-step tolerance, redblack_sor (rhs = guess = u^{n-1}), local_rescale.
+// Everything up to the end of the SOR loop is one stream sequence: the assembly's
+// non-finite flag (solver.cpp:71-75) reaches the loop control on the device (sor_init,
+// all-gathered across slabs), and the host learns of it with the solve's final state.
+SolveOut Domain::step(ss_step_diag* diag, int fixed, bool rescale) {
     if (!prepared) throw Error(SS_ERR_STATE, "session not prepared");
     int roles[kStateBuffers];
     for (int q = 0; q < kStateBuffers; ++q) roles[q] = (cur + q) % kStateBuffers;
@@ -1113,7 +1159,7 @@ void Domain::step(ss_step_diag* diag) {
     if (profiling) SSB_CUDA(cudaEventRecord(ev[2], stream));
     for (Slab* s : sp) s->assemble(s->S[cur].pf(), s->have_G, prm.tau, prm.epsilon, nullptr, nullptr, nullptr);
     if (profiling) SSB_CUDA(cudaEventRecord(ev[3], stream));
-    const bool rel = prm.sor_rel_tol > 0.0;
+    const bool rel = !fixed && prm.sor_rel_tol > 0.0;
     if (rel) {
         std::vector<double*> loc, all;
         for (Slab* s : sp) {
@@ -1123,31 +1169,24 @@ void Domain::step(ss_step_diag* diag) {
         }
         if (world > 1) tr->allgather(sp, loc, all, chunk);
     }
-    // non-finite coefficients anywhere => NumericalError everywhere (solver.cpp:71-75)
-    std::vector<int> fh(sp.size(), 0);
-    for (size_t s = 0; s < sp.size(); ++s)
-        SSB_CUDA(cudaMemcpyAsync(&fh[s], sp[s]->flags.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    sync();
-    std::vector<std::vector<double>> bad(sp.size(), std::vector<double>(1, 0.0));
-    for (size_t s = 0; s < sp.size(); ++s) bad[s][0] = fh[s] ? 1.0 : 0.0;
-    const std::vector<double> anybad = gather_values(bad, 1);
-    if (*std::max_element(anybad.begin(), anybad.end()) > 0.0)
-        throw Error(SS_ERR_NONFINITE, "assemble_step: non-finite coefficient (bad input field?)");
+    const std::vector<Triple> B = role_triples(roles);
+    std::vector<PField> rhs;
+    for (const Triple& t : B) rhs.push_back(t[0]);  // rhs = guess = u^{n-1} (solver.cpp:430)
+    int rr = 0;
+    const SolveOut o = fixed ? solve(B, rhs, false, prm.omega, nullptr, 1.0, false, 0.0, fixed, true, &rr, true)
+                             : solve(B, rhs, false, prm.omega, nullptr, prm.sor_tol, rel, prm.sor_rel_tol,
+                                     prm.sor_max_iter, false, &rr, true);
     if (profiling) {
         float ms = 0.f;
         SSB_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[3]));
         prof.assemble_ms += ms;
         prof.assemble_n++;
     }
-    const std::vector<Triple> B = role_triples(roles);
-    std::vector<PField> rhs;
-    for (const Triple& t : B) rhs.push_back(t[0]);  // rhs = guess = u^{n-1} (solver.cpp:430)
-    int rr = 0;
-    const SolveOut o = solve(B, rhs, false, prm.omega, nullptr, prm.sor_tol, rel, prm.sor_rel_tol,
-                             prm.sor_max_iter, false, &rr);
+    if (o.nonfinite) throw Error(SS_ERR_NONFINITE, "assemble_step: non-finite coefficient (bad input field?)");
     if (!o.converged) throw SolverErrT(o);
     cur = roles[rr];
-    if (prm.rescale_each_step) {
+    const bool do_rescale = rescale && prm.rescale_each_step;
+    if (do_rescale) {
         if (profiling) SSB_CUDA(cudaEventRecord(ev[2], stream));
         for (Slab* s : sp) s->rescale(cur);
         if (profiling) SSB_CUDA(cudaEventRecord(ev[3], stream));
@@ -1159,8 +1198,8 @@ void Domain::step(ss_step_diag* diag) {
             SSB_CUDA(cudaMemcpyAsync(&mh[2 * s], sp[s]->scal.p + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                                      stream));
         }
-    sync();
-    if (profiling && prm.rescale_each_step) {
+    if (diag || profiling) sync();
+    if (profiling && do_rescale) {
         float ms = 0.f;
         SSB_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[3]));
         prof.rescale_ms += ms;
@@ -1181,21 +1220,11 @@ void Domain::step(ss_step_diag* diag) {
         diag->umin = lo;
         diag->umax = hi;
     }
+    return o;
 }
 
-double Domain::fixed_sweeps(int n_sweeps) {
-    if (!prepared) throw Error(SS_ERR_STATE, "session not prepared");
-    int roles[kStateBuffers];
-    for (int q = 0; q < kStateBuffers; ++q) roles[q] = (cur + q) % kStateBuffers;
-    exchange_role(cur, 3);
-    for (Slab* s : sp) s->assemble(s->S[cur].pf(), s->have_G, prm.tau, prm.epsilon, nullptr, nullptr, nullptr);
-    const std::vector<Triple> B = role_triples(roles);
-    std::vector<PField> rhs;
-    for (const Triple& t : B) rhs.push_back(t[0]);
-    int rr = 0;
-    const SolveOut o = solve(B, rhs, false, prm.omega, nullptr, 1.0, false, 0.0, n_sweeps, true, &rr);
-    cur = roles[rr];
-    return o.residual;
-}
+// fixed-sweep mode without the rescale (ss_session_fixed_sweeps): assemble + exactly
+// n_sweeps sweeps; non-finite coefficients are reported like step()'s
+double Domain::fixed_sweeps(int n_sweeps) { return step(nullptr, n_sweeps, false).residual; }
 
 }  // namespace ssb

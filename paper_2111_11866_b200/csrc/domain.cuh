@@ -85,6 +85,7 @@ struct SolveOut {
     int iterations = 0;
     double residual = 0.0, tol = 0.0;
     bool converged = false;
+    bool nonfinite = false;  // the assembly flagged a non-finite coefficient (no solve was made)
 };
 
 struct SolverErrT : Error {
@@ -115,6 +116,7 @@ struct Slab {
     Dev<SorState> st;
     Dev<double> scratch, scal;
     Dev<int> flags;
+    Dev<double> bad_all;     // all-gathered assembly flags (world doubles; slab groups / ranks)
     Dev<double> stage, stage8;
     BallSet rescale_balls;
 
@@ -246,6 +248,7 @@ struct Domain {
     ~Domain();
 
     void sync();
+    void clear_graphs();  // drop the captured SOR loops (after a kernel switch)
     int slabs_local() const { return (int)sp.size(); }
     bool single() const { return sp.size() == 1 && world == 1; }
     long long host_plane() const;  // padded doubles per l-plane of a host array
@@ -264,7 +267,7 @@ struct Domain {
     // result lands in B[s][*result].  Non-convergence is reported, not thrown.
     SolveOut solve(const std::vector<Triple>& B, const std::vector<PField>& rhs, bool heat,
                    double omega, const double hc[4], double tol_abs, bool use_norm, double rel,
-                   int max_iter, bool fixed, int* result);
+                   int max_iter, bool fixed, int* result, bool check_assembly = false);
     // heat_smooth over per-slab buffer triples; returns the index of the result
     int heat_smooth(const std::vector<Triple>& B, double sigma, int steps, double omega, double tol,
                     int max_iter);
@@ -275,7 +278,9 @@ struct Domain {
     void get_mask(double level, uint8_t* mask);
     void prepare(const double* image, const ss_center* c, int n, const ss_seg_params& p,
                  const double* u0);
-    void step(ss_step_diag* diag);
+    // one time step (solver.cpp:428-438); fixed > 0: exactly `fixed` sweeps, no stopping
+    // test (BASELINE config 4); rescale = false skips local_rescale (ss_session_fixed_sweeps)
+    SolveOut step(ss_step_diag* diag, int fixed = 0, bool rescale = true);
     double fixed_sweeps(int n_sweeps);
     // EOC verification row (eoc.cpp:83-137) on an n^4 session; returns the space-time L2 error
     double eoc_row(int n, double omega, double sor_tol, int max_iter, long long* total_sweeps);
@@ -286,7 +291,7 @@ private:
     cudaGraphExec_t graph_for(const SorArgs& a, bool heat);
     void body_single(const SorArgs& a, bool heat, cudaEvent_t* ev4);
     void body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>& B, bool heat, int n,
-                    cudaEvent_t* ev4);
+                    cudaEvent_t* ev4, cudaEvent_t* xev6);
 };
 
 }  // namespace ssb

@@ -17,7 +17,8 @@ struct SorState {
     int n_red, n_black;
     int done, converged;
     int iterations, max_iter;
-    int fixed, pad;
+    int fixed;
+    int nonfinite;  // assemble_step found a non-finite coefficient (solver.cpp:71-75): no solve
     unsigned int counter;
     unsigned int item_ctr[2];  // dynamic item counters of the TMA colour passes (zeroed by the other pass)
     int epoch_base;  // distinct per solve: completion flags of the wavefront kernel compare to epoch_base + n
@@ -126,8 +127,15 @@ void launch_sor_kwave(cudaStream_t s, const SorArgs& a);
 int wave_iters();  // SOR iterations per wavefront launch (SSB_WAVE_PHASES / 2)
 void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat);
 dim3 pass_grid(const Layout& L);
+// bad_local: this slab's assembly flag (int, non-zero = a non-finite diag), bad_all: the
+// all-gathered flags of every slab (n_all doubles); either may be null.  A set flag makes the
+// solve stop after its first decision with nonfinite = 1 -- the host reads it with the final
+// state, so no host round trip sits between the assembly and the SOR loop.
 void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_slices,
-                     int n_slices, double rel, int max_iter, int fixed, int epoch_base);
+                     int n_slices, double rel, int max_iter, int fixed, int epoch_base,
+                     const int* bad_local = nullptr, const double* bad_all = nullptr, int n_all = 0);
+// out[0] = flag[0] != 0 (the value a slab contributes to the flag all-gather)
+void launch_flag_to_double(cudaStream_t s, const int* flag, double* out);
 // single-slab loop body: red, finalize (inline decision), black
 void launch_sor_body(cudaStream_t s, const SorArgs& a, bool heat, cudaEvent_t* ev /*4 or null*/);
 // pieces for the multi-slab body (halo exchange / all-gather between them)

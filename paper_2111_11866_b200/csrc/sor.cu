@@ -306,7 +306,8 @@ __global__ void sor_decide(const SorArgs a) {
 
 // tol = rel * sqrt(sum over all slices in global l order) when norm_slices is given
 __global__ void sor_init(SorState* st, double tol, const double* norm_slices, int n_slices, double rel,
-                         int max_iter, int fixed, int epoch_base) {
+                         int max_iter, int fixed, int epoch_base, const int* bad_local,
+                         const double* bad_all, int n_all) {
     st->epoch_base = epoch_base;
     st->n_red = 1;
     st->n_black = 0;
@@ -325,7 +326,18 @@ __global__ void sor_init(SorState* st, double tol, const double* norm_slices, in
     } else {
         st->tol = tol;
     }
+    // NumericalError (solver.cpp:71-75) decided on the device: one iteration, not converged,
+    // flagged (every slab sees the same all-gathered flags, so every rank stops alike)
+    int bad = bad_local && *bad_local != 0;
+    for (int q = 0; bad_all && q < n_all; ++q) bad |= bad_all[q] != 0.0;
+    st->nonfinite = bad;
+    if (bad) {
+        st->max_iter = 1;
+        st->fixed = 0;
+    }
 }
+
+__global__ void flag_to_double(const int* flag, double* out) { out[0] = flag[0] != 0 ? 1.0 : 0.0; }
 
 }  // namespace
 
@@ -357,8 +369,15 @@ static int resident_blocks() {
 }
 
 void launch_sor_init(cudaStream_t s, SorState* st, double tol, const double* norm_slices,
-                     int n_slices, double rel, int max_iter, int fixed, int epoch_base) {
-    sor_init<<<1, 1, 0, s>>>(st, tol, norm_slices, n_slices, rel, max_iter, fixed, epoch_base);
+                     int n_slices, double rel, int max_iter, int fixed, int epoch_base,
+                     const int* bad_local, const double* bad_all, int n_all) {
+    sor_init<<<1, 1, 0, s>>>(st, tol, norm_slices, n_slices, rel, max_iter, fixed, epoch_base, bad_local,
+                             bad_all, n_all);
+    SSB_LAUNCHED();
+}
+
+void launch_flag_to_double(cudaStream_t s, const int* flag, double* out) {
+    flag_to_double<<<1, 1, 0, s>>>(flag, out);
     SSB_LAUNCHED();
 }
 

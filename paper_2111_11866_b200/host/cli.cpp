@@ -117,7 +117,9 @@ ss_seg_params params_of(const Config& c, const GridSpec& spec) {
     if (prof != "peak" && prof != "linear")
         throw ValidationError("config: init_profile must be peak or linear, got " + prof);
     p.init_profile = prof == "peak" ? 0 : 1;
-    p.rescale_radius = c.has("rescale_radius") ? c.num("rescale_radius", 0.0) : 0.0;
+    // set => explicit radius, even <= 0 (cli.cpp:104: the optional is engaged); unset =>
+    // std::nullopt, NaN on the ABI (per-row radii)
+    p.rescale_radius = c.has("rescale_radius") ? c.num("rescale_radius", 0.0) : std::nan("");
     return p;
 }
 

@@ -152,11 +152,14 @@ CentersTable read_centers(const std::string& path, const GridSpec& spec) {
             continue;
         }
         first = false;
-        for (char& c : line)
-            if (c == ',') c = ' ';
+        // exactly the reference's grammar (io.cpp:158-163): a value, then each of the four
+        // separators must be the character ',' (whitespace before a token is skipped by >>)
         std::istringstream ss(line);
         CenterRow r;
-        if (!(ss >> r.frame >> r.x >> r.y >> r.z >> r.radius))
+        char sep[4] = {0, 0, 0, 0};
+        ss >> r.frame >> sep[0] >> r.x >> sep[1] >> r.y >> sep[2] >> r.z >> sep[3] >> r.radius;
+        const bool commas = sep[0] == ',' && sep[1] == ',' && sep[2] == ',' && sep[3] == ',';
+        if (!ss || !commas)
             throw FormatError(path + ":" + std::to_string(lineno) + ": expected frame,x,y,z,radius");
         t.rows.push_back(r);
     }

@@ -186,7 +186,7 @@ void local_rescale(Field4D& u, const CentersTable& c, std::optional<double> radi
     validate_centers(c, u.spec());
     const ss_grid g = grid_of(u.spec());
     const std::vector<ss_center> cs = centers_of(c);
-    raise(ss_local_rescale(&g, u.data(), cs.data(), (int)cs.size(), radius.value_or(0.0)));
+    raise(ss_local_rescale(&g, u.data(), cs.data(), (int)cs.size(), radius.value_or(std::nan(""))));
 }
 
 StepCoefficients assemble_step(const Field4D& u_prev, const FaceCoefficientField* G, const SolverParams& p,
@@ -271,7 +271,7 @@ Field4D segment(const Field4D& image, const CentersTable& centers, const Segment
     p.init_v = sp.init.v;
     p.init_R = sp.init.R;
     p.init_profile = sp.init.profile == InitProfile::peak ? 0 : 1;
-    p.rescale_radius = sp.rescale_radius.value_or(0.0);
+    p.rescale_radius = sp.rescale_radius.value_or(std::nan(""));
     Field4D u(image.spec());
     std::vector<ss_step_diag> d(sp.solver.n_steps);
     const ss_grid g = grid_of(image.spec());

@@ -73,7 +73,7 @@ def main():
     st, u0l = R.build_initial(g, rows, 0.5, 2.5, 1)
     assert st == 0
     noisy = cs.rand_field(dims, 31)
-    st, resc_row = R.local_rescale(g, noisy, rows, 0.0)
+    st, resc_row = R.local_rescale(g, noisy, rows, None)
     assert st == 0
     st, resc_r2 = R.local_rescale(g, noisy, rows, 2.2)
     assert st == 0

@@ -57,6 +57,17 @@ def test_cli_usage_and_errors(cli, tmp_path):
     assert r.returncode == 1 and "payload is" in r.stderr  # io.cpp:83-86 FormatError
 
 
+@pytest.mark.parametrize("row", ["0 1.5 1.5 1.0 1.0", "0,1.5 1.5,1.0,1.0", "0;1.5;1.5;1.0;1.0", "0,1.5,1.5,1.0"])
+def test_cli_centers_grammar(cli, tmp_path, row):
+    """read_centers accepts exactly frame,x,y,z,radius with ',' separators (io.cpp:158-163):
+    whitespace- or partly comma-separated rows are a FormatError, like the reference's."""
+    dims = (4, 4, 3, 3)
+    write_case(str(tmp_path), dims, 0.25, cs.f32_image(dims, 1), [(0, 1.5, 1.5, 1.0, 1.0)])
+    (tmp_path / "centers.csv").write_text("frame,x,y,z,radius\n" + row + "\n")
+    r = subprocess.run([cli, "segment", "--config", str(tmp_path / "cfg.txt")], capture_output=True, text=True)
+    assert r.returncode == 1 and "expected frame,x,y,z,radius" in r.stderr, r.stderr
+
+
 def test_cli_no_cpu_fallback(cli, tmp_path):
     try:
         import torch

@@ -253,7 +253,7 @@ def test_balls_random(gpu, oracle, dims):
     st, th = oracle.local_threshold(og, img, rows, 0.3, -1.0)
     assert st == 0
     assert_bits(gpu.local_threshold(img, rows, g, 0.3, -1.0), th, "threshold, 40 balls")
-    st, rs = oracle.local_rescale(og, img, rows, 0.0)
+    st, rs = oracle.local_rescale(og, img, rows, None)
     assert_bits(gpu.local_rescale(img, rows, g), rs, "rescale, 40 balls")
     st, u0 = oracle.build_initial(og, rows, 0.7, 2.2, 0)
     assert_bits(gpu.build_initial(rows, g, 0.7, 2.2, 0), u0, "initial, 40 balls")

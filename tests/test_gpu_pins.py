@@ -1,0 +1,64 @@
+"""Full-size parity of every BASELINE config against the UNMODIFIED reference.
+
+tests/golden/pins.json holds what the reference itself produced on the bench's
+seeded workloads (tests/golden/make_pins.py, run in the build container through
+oracle/_ref): per time step the SOR iteration count, stopping residual, tolerance
+and min/max of u, the sha256 of the final u's bits and the 0.5-mask voxel count.
+
+  config0  32^4            all 10 segment() steps
+  config1  64^4            all 20 steps
+  config2  256x256x64x32   steps 1-3
+  config4  256x256x128x16  2 steps of exactly 50 sweeps (the reference's own iterate,
+                           recovered past its SolverError, oracle/ref_shim.cpp)
+
+The device session recomputes them here and must match: iterations exactly, u bit
+for bit (so the 0.5-mask too), min/max exactly.  Residual and tolerance are
+sums of squares formed in a different order (per-slice 256-lane trees vs the
+reference's sequential sweep) and are compared to 1e-12 relative -- equal
+iteration counts show no stopping decision flipped.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PINS = json.load(open(os.path.join(HERE, "golden", "pins.json")))
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def build(name):
+    import workloads
+    return {"config0": workloads.config0, "config1": workloads.config1, "config2": workloads.config2,
+            "config4": lambda: workloads.config4(1)}[name]()
+
+
+@pytest.mark.parametrize("name", sorted(PINS))
+def test_config_pinned_to_reference(gpu, name):
+    pin = PINS[name]
+    wl = build(name)
+    assert list(wl.dims) == pin["dims"]
+    got = {"image": sha(wl.image), "u0": sha(wl.u0), "rows": sha(np.asarray(wl.rows, dtype=np.float64))}
+    assert got == pin["inputs"], "this host generated different workload inputs than the pinning host"
+    g = gpu.Grid.make(wl.dims, wl.h)
+    steps, fixed = pin["steps"], pin["fixed_sweeps"]
+    with gpu.Session(g) as s:
+        s.prepare(wl.image, wl.rows, gpu.seg_params(**{**wl.params, "n_steps": steps}), wl.u0)
+        diags = [s.step_fixed(fixed) if fixed else s.step() for _ in range(steps)]
+        u = s.get_u()
+        mask = s.get_mask(0.5)
+    assert [d["iterations"] for d in diags] == pin["iterations"]
+    np.testing.assert_allclose([d["residual"] for d in diags], pin["residual"], rtol=1e-12, atol=0)
+    if not fixed:
+        np.testing.assert_allclose([d["tol"] for d in diags], pin["tol"], rtol=1e-12, atol=0)
+    assert [d["umin"] for d in diags] == pin["umin"]
+    assert [d["umax"] for d in diags] == pin["umax"]
+    assert sha(u) == pin["u_sha256"], "u differs from the reference's bits"
+    assert int(mask.sum()) == pin["mask_voxels"]

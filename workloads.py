@@ -251,7 +251,7 @@ def _nuclei_workload(name, dims, n_nuclei, seed, n_steps, planes, h=1.0 / 32, **
                 sub = v[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]]
                 np.maximum(sub, 1.0 / (d / h + 1.0), out=sub)
             u0[q, 1:-1, 1:-1, 1:-1] = v
-    params = _base_params(h, n_steps, K=5000.0, lambda_=0.7, rescale_radius=0.0, **over)
+    params = _base_params(h, n_steps, K=5000.0, lambda_=0.7, rescale_radius=None, **over)
     return Workload(name, dims, h, image, u0, rows, params, n_steps,
                     notes=dict(nuclei=n_nuclei, h=h, threshold="0.3 -> lambda 0.7", planes=(p0, p1)))
 
