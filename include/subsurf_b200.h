@@ -187,6 +187,19 @@ SS_API ss_status ss_session_create_group(const ss_grid* g, int n_slabs, int devi
 SS_API ss_status ss_nccl_unique_id(uint8_t out[128]);
 SS_API ss_status ss_session_create_dist(const ss_grid* g, int rank, int world, const uint8_t uid[128],
                                         int device, ss_session** out);
+/* one rank's slab with the halo exchanges and all-gathers staged through the host and
+ * the caller's callbacks (ABI 5): sendrecv sends `bytes` to rank `peer` and receives as many
+ * from it; allgather concatenates every rank's `bytes` in rank order.  Return 0 on success.
+ * Same messages as the NCCL transport, so results equal the single domain's bit for bit;
+ * synchronous -- for running the multi-process path where one GPU serves several ranks
+ * (tests), not a data path. */
+typedef struct {
+    void* ctx;
+    int (*sendrecv)(void* ctx, int peer, const void* send, void* recv, size_t bytes);
+    int (*allgather)(void* ctx, const void* local, void* all, size_t bytes);
+} ss_host_comm;
+SS_API ss_status ss_session_create_dist_host(const ss_grid* g, int rank, int world, const ss_host_comm* comm,
+                                             int device, ss_session** out);
 /* 1-based first owned slice, owned slice count (whole grid unless distributed), world size */
 SS_API ss_status ss_session_slab(ss_session* s, int* l_begin, int* l_count, int* world);
 SS_API ss_status ss_session_destroy(ss_session* s);

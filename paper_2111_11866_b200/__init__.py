@@ -204,6 +204,7 @@ def library() -> C.CDLL:
     sig("ss_session_create_group", [_GP, C.c_int, C.c_int, C.POINTER(C.c_void_p)])
     sig("ss_nccl_unique_id", [C.POINTER(C.c_uint8)])
     sig("ss_session_create_dist", [_GP, C.c_int, C.c_int, C.POINTER(C.c_uint8), C.c_int, C.POINTER(C.c_void_p)])
+    sig("ss_session_create_dist_host", [_GP, C.c_int, C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)])
     sig("ss_session_slab", [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)])
     sig("ss_session_destroy", [C.c_void_p])
     sig("ss_session_stream", [C.c_void_p], C.c_void_p)
@@ -509,8 +510,13 @@ class Session:
         h = C.c_void_p()
         if dist is not None:
             rank, world, uid = dist
-            ub = (C.c_uint8 * 128).from_buffer_copy(uid)
-            _check(library().ss_session_create_dist(C.byref(g), rank, world, ub, device, C.byref(h)))
+            if hasattr(uid, "as_abi"):  # dist.HostComm: exchanges staged through the host
+                self._comm = uid
+                _check(library().ss_session_create_dist_host(C.byref(g), rank, world, uid.as_abi(), device,
+                                                             C.byref(h)))
+            else:
+                ub = (C.c_uint8 * 128).from_buffer_copy(uid)
+                _check(library().ss_session_create_dist(C.byref(g), rank, world, ub, device, C.byref(h)))
         else:
             _check(library().ss_session_create_group(C.byref(g), n_slabs, device, C.byref(h)))
         self._h = h

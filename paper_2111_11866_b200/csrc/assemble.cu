@@ -351,6 +351,9 @@ void launch_assemble(cudaStream_t s, const AsmArgs& a0) {
         p2 = p2 && pow2(a.h[q]);
         a.hinv[q] = 1.0 / a.h[q];
     }
+    // the TMA-staged tile kernel (both colours in one launch) unless the per-call API asks
+    // for the padded fp64 exports
+    if (!a.off_out && assemble_tile_supported(a.L) && launch_assemble_tile(s, a, p2)) return;
     if (a.off_out) {
         if (p2) { asm_launch<0, true, true>(s, a); asm_launch<1, true, true>(s, a); }
         else { asm_launch<0, true, false>(s, a); asm_launch<1, true, false>(s, a); }
@@ -367,6 +370,7 @@ void launch_face_coefficients(cudaStream_t s, const EdgeArgs& a0) {
         p2 = p2 && pow2(a.h[q]);
         a.hinv[q] = 1.0 / a.h[q];
     }
+    if (!a.G_out && assemble_tile_supported(a.L) && launch_edge_tile(s, a, p2)) return;
     if (a.G_out) {
         if (p2) { edge_launch<0, true, true>(s, a); edge_launch<1, true, true>(s, a); }
         else { edge_launch<0, true, false>(s, a); edge_launch<1, true, false>(s, a); }

@@ -1,0 +1,570 @@
+// assemble_tile.cu -- the per-step coefficient assembly (assemble_step,
+// solver.cpp:23-77, face gradients edge.cpp:16-57) and the one-off edge
+// coefficients (face_coefficients, edge.cpp:73-99) as tile kernels that stage u
+// (I0s / ITs) in shared memory with TMA.
+//
+// Tile = one slice l x 8 rows (j) x 4 planes (k) x 32 padded doxels along i (16
+// of each colour).  The 33-point diamond-cell stencil of every doxel of the tile
+// lies in the brick  i-1..i+32 x j-1..j+8 x k-1..k+4 x l-1..l+1  of the two
+// colour-packed arrays: six 3D tensor copies (3 slices x 2 colours, boxes of
+// 18 slots x 10 rows x 6 planes, cp.async.bulk.tensor.3d with mbarrier
+// completion) bring it into shared memory, double-buffered so the next tile's
+// brick streams in while this one is computed.  256 threads = 8 rows x (16
+// doxels x 2 colours); each computes its doxel in the tile's 4 planes from
+// shared memory only (ld.shared with compile-time offsets from four per-thread
+// bases).  G (8 fp64 per doxel, 64 B) is streamed with 128-bit evict-first
+// loads; the fp32 coefficients go out as two 128-bit stores per doxel.
+//
+// Bit-exactness: the face gradients keep the reference's expression order
+// (-fmad=false).  The tail replaces the correctly rounded sqrt / div chain of
+// solver.cpp:48-66 by a reciprocal square root with two Newton steps: the
+// quotient q' = ((t_a Abar') G_f) rsqrt'(A_f^2) lies within ~20 double ulps of
+// the reference's q = ((t_a Abar) G_f) / sqrt(A_f^2), and the only output is
+// float(-q).  When q' is at least 512 double ulps away from a float rounding
+// midpoint (its low 29 mantissa bits differ from 2^28 by >= 512) and its
+// exponent lies in the normal float range, float(-q') == float(-q) exactly;
+// otherwise (probability ~2e-6 per face) the doxel is recomputed with the
+// reference's exact sequence.  So every coefficient is the reference's bits.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include <cudaTypedefs.h>
+
+#include "kernels.cuh"
+
+namespace ssb {
+
+namespace {
+
+constexpr int kTI = 32;                  // padded doxels along i per tile (16 per colour)
+constexpr int kTJ = 8;                   // rows per tile
+constexpr int kTK = 4;                   // planes per tile
+constexpr int kSS = 18;                  // shared slots per colour row (16 + i halo; 144 B)
+constexpr int kSR = kTJ + 2;             // rows with the j halo
+constexpr int kSP = kTK + 2;             // planes with the k halo
+constexpr int kBoxBytes = kSS * kSR * kSP * 8;         // 8640 B: one (slice, colour) brick
+constexpr int kBoxStride = (kBoxBytes + 127) / 128 * 128;  // 8704 B: TMA destinations 128-B aligned
+constexpr int kFieldBytes = 6 * kBoxStride;            // 3 slices x 2 colours
+constexpr int kThreadsT = kTJ * 32;
+
+__device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int OFF>
+__device__ __forceinline__ double lds(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(addr), "n"(OFF));
+    return v;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sptr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sptr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sptr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(sptr(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 3D tensor copy of the box at {x (slot), y (row j), z (plane l*kMax + k)}
+__device__ __forceinline__ void tensor3_g2s(uint32_t dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(dst),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(sptr(bar))
+        : "memory");
+}
+
+// L2 prefetch of a 3D tensor box (no shared-memory destination)
+__device__ __forceinline__ void tensor3_prefetch(const CUtensorMap* map, int x, int y, int z) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(x), "r"(y),
+                 "r"(z)
+                 : "memory");
+}
+
+struct TileGeo {
+    int nb, njb, nkc;  // i blocks, row blocks, plane chunks
+    long long tiles;
+};
+__host__ __device__ __forceinline__ TileGeo tile_geo(const Layout& L) {
+    TileGeo g;
+    g.nb = (L.n1 + kTI - 1) / kTI;
+    g.njb = (L.n2 + kTJ - 1) / kTJ;
+    g.nkc = (L.n3 + kTK - 1) / kTK;
+    g.tiles = (long long)g.nb * g.njb * g.nkc * L.n4;
+    return g;
+}
+
+// tile t -> (l, b, jb, kc), slices fastest: the tiles in flight together share their
+// (i block, row block, plane chunk), so a slice's brick, read by the tiles of l-1, l and
+// l+1, comes from L2 after the first read
+struct Tile {
+    int l, b, jb, kc;
+};
+__device__ __forceinline__ Tile tile_of(const Layout& L, const TileGeo& g, long long t) {
+    Tile x;
+    x.l = (int)(t % L.n4) + 1;
+    long long r = t / L.n4;
+    x.b = (int)(r % g.nb);
+    r /= g.nb;
+    x.jb = (int)(r % g.njb);
+    x.kc = (int)(r / g.njb);
+    return x;
+}
+
+template <int NF>
+struct Maps {
+    CUtensorMap m[NF][2];  // per field, per colour: 3D view [planes l*kMax+k][rows j][slots]
+};
+
+// issue the bricks of tile t of every field into buffer `buf` (one elected thread)
+template <int NF>
+__device__ __forceinline__ void load_tile(const Layout& L, const Maps<NF>& M, const Tile& x, uint32_t buf,
+                                          uint64_t* bar) {
+    mbar_expect_tx(bar, NF * 6 * kBoxBytes);
+    const int x0 = x.b * (kTI / 2);       // slot of padded i = 32 b (the i-1 halo of i0 = 32 b + 1)
+    const int y0 = x.jb * kTJ;            // row j0 - 1
+    const int z0 = x.kc * kTK;            // plane k0 - 1
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+#pragma unroll
+        for (int sl = 0; sl < 3; ++sl)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                tensor3_g2s(buf + f * kFieldBytes + (sl * 2 + c) * kBoxStride, &M.m[f][c], x0, y0,
+                            (x.l - 1 + sl) * L.kMax + z0, bar);
+}
+
+// The stencil of one doxel read from a staged brick.  Four per-thread bases: the
+// doxel's own colour c / the other colour, each at slot s (i-1 / i+1 neighbours: slot s,
+// s+1) or s+e (the doxel's own slot); everything else is a compile-time offset.
+struct SStencil {
+    uint32_t bc, bce, bnc, bnce;
+    template <int DI, int DJ, int DK, int DL>
+    __device__ __forceinline__ double at() const {
+        constexpr int par = (DI + DJ + DK + DL) & 1;
+        constexpr int off = (1 + DL) * 2 * kBoxStride + ((1 + DK) * kSR + (1 + DJ)) * kSS * 8 + (DI > 0 ? 8 : 0);
+        const uint32_t b = par ? (DI != 0 ? bnc : bnce) : (DI != 0 ? bc : bce);
+        return lds<off>(b);
+    }
+};
+
+template <bool POW2>
+__device__ __forceinline__ double scale_h(double x, const double* h, const double* hinv, int a) {
+    if constexpr (POW2)
+        return x * hinv[a];  // x / h == x * (1/h) exactly for h = 2^-k
+    else
+        return x / h[a];
+}
+
+// corner-average difference along tangent T of face F (edge.cpp:16-22, :43-45):
+// (0.25*(((p0 + pn) + p_t) + p_nt) - 0.25*(((p0 + pn) + p_-t) + p_n-t)) / h_T
+template <int F, int T, bool POW2>
+__device__ __forceinline__ double tangent(const SStencil& S, const double* h, const double* hinv, double p0pn) {
+    constexpr int A = F >> 1, SG = (F & 1) ? 1 : -1;
+    constexpr int ai = A == 0 ? SG : 0, aj = A == 1 ? SG : 0, ak = A == 2 ? SG : 0, al = A == 3 ? SG : 0;
+    constexpr int ti = T == 0, tj = T == 1, tk = T == 2, tl = T == 3;
+    const double plus = 0.25 * (p0pn + S.at<ti, tj, tk, tl>() + S.at<ai + ti, aj + tj, ak + tk, al + tl>());
+    const double minus = 0.25 * (p0pn + S.at<-ti, -tj, -tk, -tl>() + S.at<ai - ti, aj - tj, ak - tk, al - tl>());
+    return scale_h<POW2>(plus - minus, h, hinv, T);
+}
+
+// face_gradient (edge.cpp:33-48) of face F
+template <int F, bool POW2>
+__device__ __forceinline__ void face_grad(const SStencil& S, const double* h, const double* hinv, double p0,
+                                          double g[4]) {
+    constexpr int A = F >> 1, SG = (F & 1) ? 1 : -1;
+    const double pn = S.at<A == 0 ? SG : 0, A == 1 ? SG : 0, A == 2 ? SG : 0, A == 3 ? SG : 0>();
+    g[A] = scale_h<POW2>((double)SG * (pn - p0), h, hinv, A);
+    const double p0pn = p0 + pn;
+    if constexpr (A != 0) g[0] = tangent<F, 0, POW2>(S, h, hinv, p0pn);
+    if constexpr (A != 1) g[1] = tangent<F, 1, POW2>(S, h, hinv, p0pn);
+    if constexpr (A != 2) g[2] = tangent<F, 2, POW2>(S, h, hinv, p0pn);
+    if constexpr (A != 3) g[3] = tangent<F, 3, POW2>(S, h, hinv, p0pn);
+}
+
+template <int F, bool POW2>
+__device__ __forceinline__ double face_sq(const SStencil& S, const double* h, const double* hinv, double p0) {
+    double g[4];
+    face_grad<F, POW2>(S, h, hinv, p0, g);
+    return g[0] * g[0] + g[1] * g[1] + g[2] * g[2] + g[3] * g[3];  // edge.cpp:53-54
+}
+
+// 1/sqrt(x) to ~1 ulp for normal x: hardware approximation + two Newton steps
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = __fma_rn(-__dmul_rn(x, y), y, 1.0);
+    y = __fma_rn(__dmul_rn(y, 0.5), e, y);
+    e = __fma_rn(-__dmul_rn(x, y), y, 1.0);
+    y = __fma_rn(__dmul_rn(y, 0.5), e, y);
+    return y;
+}
+
+// float(q') is float(q) for every q within ~20 ulps of q' unless q' sits near a float
+// rounding midpoint or outside the normal float range: then take the exact path
+__device__ __forceinline__ bool near_midpoint(double q) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(q);
+    const int low = (int)(b & 0x1FFFFFFFull);
+    const int ex = (int)((b >> 52) & 0x7FF);
+    const int d = low - (1 << 28);
+    return (d < 512 && d > -512) || ex < 1023 - 120 || ex > 1023 + 120;
+}
+
+// G of a tile (both colours) into L2 ahead of the tile: 3D view of a colour's G array
+// [planes][rows][W * 8 doubles], box 17 slots x 8 faces, 8 rows, 4 planes
+constexpr int kGBoxX = (kTI / 2 + 1) * 8;
+struct AsmTileArgs {
+    Maps<1> maps;
+    CUtensorMap gmap[2];
+    int gpref;  // G maps valid
+    AsmArgs a;
+    TileGeo g;
+};
+
+__device__ __forceinline__ void prefetch_G(const AsmTileArgs& p, const Tile& x) {
+    const int z = x.l * p.a.L.kMax + x.kc * kTK + 1;
+    tensor3_prefetch(&p.gmap[0], x.b * (kTI / 2) * 8, x.jb * kTJ + 1, z);
+    tensor3_prefetch(&p.gmap[1], x.b * (kTI / 2) * 8, x.jb * kTJ + 1, z);
+}
+
+template <bool POW2, int STAGES, int MINB>
+__global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __grid_constant__ AsmTileArgs p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[STAGES], empty[STAGES];
+    const AsmArgs& a = p.a;
+    const Layout& L = a.L;
+    const TileGeo& g = p.g;
+    const int tid = threadIdx.x;
+    const int ty = tid >> 5, c = (tid >> 4) & 1, s = tid & 15;
+    const uint32_t sbase = sptr(smem);
+    if (tid == 0) {
+        for (int q = 0; q < STAGES; ++q) {
+            mbar_init(&bars[q], 1);
+            mbar_init(&empty[q], kTJ);  // one arrival per warp when it is done with the buffer
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    long long t = blockIdx.x;
+    if (tid == 0) {
+        for (int q = 0; q < STAGES; ++q) {
+            const long long tq = t + (long long)q * gridDim.x;
+            if (tq < g.tiles) load_tile<1>(L, p.maps, tile_of(L, g, tq), sbase + q * kFieldBytes, &bars[q]);
+        }
+        if (p.gpref && t < g.tiles) prefetch_G(p, tile_of(L, g, t));
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    bool bad = false;
+    for (; t < g.tiles; t += gridDim.x) {
+        const Tile x = tile_of(L, g, t);
+        const uint32_t buf = sbase + stage * kFieldBytes;
+        if (tid == 32 && p.gpref && t + gridDim.x < g.tiles) prefetch_G(p, tile_of(L, g, t + gridDim.x));
+        mbar_wait(&bars[stage], phase);
+        const int j = x.jb * kTJ + 1 + ty;
+        // this thread's bases at plane kk = 0 of the brick (row ty, slot s)
+        const uint32_t rb = buf + (uint32_t)(ty * kSS + s) * 8;
+#pragma unroll 1
+        for (int kk = 0; kk < kTK; ++kk) {
+            const int k = x.kc * kTK + 1 + kk;
+            const int e = (c + 1 + j + k + x.l + L.lpar) & 1;
+            const int i = x.b * kTI + 1 + 2 * s + e;
+            if (j > L.n2 || k > L.n3 || i > L.n1) continue;
+            SStencil S;
+            const uint32_t pb = rb + (uint32_t)(kk * kSR * kSS) * 8;
+            S.bc = pb + c * kBoxStride;
+            S.bnc = pb + (1 - c) * kBoxStride;
+            S.bce = S.bc + e * 8;
+            S.bnce = S.bnc + e * 8;
+            const long long row = L.row(j, k, x.l);
+            const long long pg = row * L.W + (i >> 1);
+            double gv[8];
+            if (a.G[c]) {
+                const double2* gp = reinterpret_cast<const double2*>(a.G[c] + pg * 8);
+#pragma unroll
+                for (int h2 = 0; h2 < 4; ++h2) {
+                    const double2 v = __ldcs(gp + h2);
+                    gv[2 * h2] = v.x;
+                    gv[2 * h2 + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int f = 0; f < 8; ++f) gv[f] = 1.0;
+            }
+            const double p0 = S.at<0, 0, 0, 0>();
+            double x2[8];
+            x2[0] = a.eps + face_sq<0, POW2>(S, a.h, a.hinv, p0);  // A_f^2 = eps + |grad_f u|^2
+            x2[1] = a.eps + face_sq<1, POW2>(S, a.h, a.hinv, p0);
+            x2[2] = a.eps + face_sq<2, POW2>(S, a.h, a.hinv, p0);
+            x2[3] = a.eps + face_sq<3, POW2>(S, a.h, a.hinv, p0);
+            x2[4] = a.eps + face_sq<4, POW2>(S, a.h, a.hinv, p0);
+            x2[5] = a.eps + face_sq<5, POW2>(S, a.h, a.hinv, p0);
+            x2[6] = a.eps + face_sq<6, POW2>(S, a.h, a.hinv, p0);
+            x2[7] = a.eps + face_sq<7, POW2>(S, a.h, a.hinv, p0);
+            double a_sq_sum = 0.0;
+#pragma unroll
+            for (int f = 0; f < 8; ++f) a_sq_sum += x2[f];  // solver.cpp:51-55, sequential f
+            const double sbar = a.eps + 0.125 * a_sq_sum;   // Abar^2 (solver.cpp:56)
+            const double abar_f = sbar * rsqrt_nr(sbar);
+            double th[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) th[q] = a.t_h2[q] * abar_f;
+            float cf[8];
+            bool slow = false;
+#pragma unroll
+            for (int f = 0; f < 8; ++f) {
+                const double q = th[f >> 1] * gv[f] * rsqrt_nr(x2[f]);
+                slow |= near_midpoint(q);
+                cf[f] = __double2float_rn(-q);
+            }
+            if (slow) {  // the reference's exact sequence (solver.cpp:51-66)
+                const double abar = sqrt(sbar);
+#pragma unroll
+                for (int f = 0; f < 8; ++f) cf[f] = __double2float_rn(-(a.t_h2[f >> 1] * abar * gv[f] / sqrt(x2[f])));
+            }
+            // diag = 1 - sum of the 8 (float-valued) doubles is non-finite iff some
+            // coefficient is (a sum of 8 finite floats cannot overflow a double), solver.cpp:68-75
+#pragma unroll
+            for (int f = 0; f < 8; ++f) bad |= (__float_as_uint(cf[f]) & 0x7F800000u) == 0x7F800000u;
+            float4* cw = reinterpret_cast<float4*>(a.coef[c] + (row * L.Wc + ((i - 1) >> 1)) * 8);
+            __stcs(cw, make_float4(cf[0], cf[1], cf[2], cf[3]));
+            __stcs(cw + 1, make_float4(cf[4], cf[5], cf[6], cf[7]));
+        }
+        // this warp is done with the buffer; the producer (thread 0) refills it once all
+        // eight warps are -- the other warps go on with the next (already loaded) tile
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[stage]);
+        if (tid == 0) {
+            const long long tn = t + (long long)STAGES * gridDim.x;
+            if (tn < g.tiles) {
+                mbar_wait(&empty[stage], phase);
+                load_tile<1>(L, p.maps, tile_of(L, g, tn), buf, &bars[stage]);
+            }
+        }
+        if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+        }
+    }
+    if (bad) atomicOr(a.bad, 1);
+}
+
+struct EdgeTileArgs {
+    Maps<2> maps;
+    EdgeArgs a;
+    TileGeo g;
+};
+
+// face_coefficients (edge.cpp:73-99): G_f = 1 / (1 + K s^2), s = delta |grad_f I0s| +
+// vartheta |grad_f ITs|, fp64 output (exact sequence: sqrt / div as the reference)
+template <bool POW2>
+__global__ void __launch_bounds__(kThreadsT, 1) edge_tile_kernel(const __grid_constant__ EdgeTileArgs p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[2];
+    const EdgeArgs& a = p.a;
+    const Layout& L = a.L;
+    const TileGeo& g = p.g;
+    const int tid = threadIdx.x;
+    const int ty = tid >> 5, c = (tid >> 4) & 1, s = tid & 15;
+    const uint32_t sbase = sptr(smem);
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    long long t = blockIdx.x;
+    if (tid == 0)
+        for (int q = 0; q < 2; ++q) {
+            const long long tq = t + (long long)q * gridDim.x;
+            if (tq < g.tiles) load_tile<2>(L, p.maps, tile_of(L, g, tq), sbase + q * 2 * kFieldBytes, &bars[q]);
+        }
+    int stage = 0;
+    uint32_t phase = 0;
+    for (; t < g.tiles; t += gridDim.x) {
+        const Tile x = tile_of(L, g, t);
+        const uint32_t buf = sbase + stage * 2 * kFieldBytes;
+        mbar_wait(&bars[stage], phase);
+        const int j = x.jb * kTJ + 1 + ty;
+        const uint32_t rb = buf + (uint32_t)(ty * kSS + s) * 8;
+#pragma unroll 1
+        for (int kk = 0; kk < kTK; ++kk) {
+            const int k = x.kc * kTK + 1 + kk;
+            const int e = (c + 1 + j + k + x.l + L.lpar) & 1;
+            const int i = x.b * kTI + 1 + 2 * s + e;
+            if (j > L.n2 || k > L.n3 || i > L.n1) continue;
+            SStencil SI, ST;
+            const uint32_t pb = rb + (uint32_t)(kk * kSR * kSS) * 8;
+            SI.bc = pb + c * kBoxStride;
+            SI.bnc = pb + (1 - c) * kBoxStride;
+            SI.bce = SI.bc + e * 8;
+            SI.bnce = SI.bnc + e * 8;
+            ST.bc = SI.bc + kFieldBytes;
+            ST.bnc = SI.bnc + kFieldBytes;
+            ST.bce = SI.bce + kFieldBytes;
+            ST.bnce = SI.bnce + kFieldBytes;
+            const double pi0 = SI.at<0, 0, 0, 0>(), pt0 = ST.at<0, 0, 0, 0>();
+            double G[8];
+#define SSB_EDGE_TILE_FACE(F)                                                                   \
+    {                                                                                           \
+        double gi[4], gt[4];                                                                    \
+        face_grad<F, POW2>(SI, a.h, a.hinv, pi0, gi);                                           \
+        face_grad<F, POW2>(ST, a.h, a.hinv, pt0, gt);                                           \
+        const double ni = sqrt(gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2] + gi[3] * gi[3]);  \
+        const double nt = sqrt(gt[0] * gt[0] + gt[1] * gt[1] + gt[2] * gt[2] + gt[3] * gt[3]);  \
+        const double sv = a.delta * ni + a.vartheta * nt;                                       \
+        G[F] = 1.0 / (1.0 + a.K * sv * sv);                                                     \
+    }
+            SSB_EDGE_TILE_FACE(0)
+            SSB_EDGE_TILE_FACE(1)
+            SSB_EDGE_TILE_FACE(2)
+            SSB_EDGE_TILE_FACE(3)
+            SSB_EDGE_TILE_FACE(4)
+            SSB_EDGE_TILE_FACE(5)
+            SSB_EDGE_TILE_FACE(6)
+            SSB_EDGE_TILE_FACE(7)
+#undef SSB_EDGE_TILE_FACE
+            const long long pg = L.row(j, k, x.l) * L.W + (i >> 1);
+            double2* gw = reinterpret_cast<double2*>(a.G[c] + pg * 8);
+#pragma unroll
+            for (int h2 = 0; h2 < 4; ++h2) gw[h2] = make_double2(G[2 * h2], G[2 * h2 + 1]);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const long long tn = t + 2LL * gridDim.x;
+            if (tn < g.tiles) load_tile<2>(L, p.maps, tile_of(L, g, tn), buf, &bars[stage]);
+        }
+        if (++stage == 2) {
+            stage = 0;
+            phase ^= 1;
+        }
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    return enc;
+}
+
+// 3D view of a colour's G array: [planes][rows][W * 8], box kGBoxX x 8 rows x 4 planes
+bool encode_G(CUtensorMap* out, const Layout& L, const double* base) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = encoder();
+    if (!enc || !base) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)L.W * 8, (cuuint64_t)L.jMax, (cuuint64_t)L.kMax * L.lMax};
+    const cuuint64_t strides[2] = {(cuuint64_t)L.W * 64, (cuuint64_t)L.W * L.jMax * 64};
+    const cuuint32_t box[3] = {kGBoxX, kTJ, kTK};
+    const cuuint32_t ones[3] = {1, 1, 1};
+    return enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, ones,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 3D view of one colour array: [planes (l*kMax + k)][rows j][slots], box 18 x 10 x 6
+bool encode_brick(CUtensorMap* out, const Layout& L, const double* base) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = encoder();
+    if (!enc || !base) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)L.W, (cuuint64_t)L.jMax, (cuuint64_t)L.kMax * L.lMax};
+    const cuuint64_t strides[2] = {(cuuint64_t)L.W * 8, (cuuint64_t)L.W * L.jMax * 8};
+    const cuuint32_t box[3] = {kSS, kSR, kSP};
+    const cuuint32_t ones[3] = {1, 1, 1};
+    return enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, ones,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+#ifndef SSB_ASMT_STAGES
+#define SSB_ASMT_STAGES 2
+#endif
+#ifndef SSB_ASMT_MINB
+#define SSB_ASMT_MINB 2
+#endif
+
+template <class K>
+unsigned grid_for(K kernel, size_t smem, long long tiles) {
+    int dev = 0, sms = 0, per = 0;
+    SSB_CUDA(cudaGetDevice(&dev));
+    SSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kThreadsT, smem));
+    return (unsigned)std::min<long long>(tiles, (long long)sms * std::max(1, per));
+}
+
+}  // namespace
+
+bool assemble_tile_supported(const Layout& L) {
+    // TMA box bounds / alignment hold for every grid (W even); off by SSB_ASM_TILE=0
+    static const int on = env_int("SSB_ASM_TILE", 1);
+    return on != 0 && encoder() != nullptr && L.n1 >= 1;
+}
+
+bool launch_assemble_tile(cudaStream_t s, const AsmArgs& a, bool pow2) {
+    AsmTileArgs p;
+    std::memset(&p, 0, sizeof p);
+    p.a = a;
+    p.g = tile_geo(a.L);
+    if (!encode_brick(&p.maps.m[0][0], a.L, a.u[0]) || !encode_brick(&p.maps.m[0][1], a.L, a.u[1])) return false;
+    static const int gpref = env_int("SSB_ASM_GPREF", 0);  // measured neutral (+12% DRAM reads): off
+    p.gpref = gpref && a.G[0] && encode_G(&p.gmap[0], a.L, a.G[0]) && encode_G(&p.gmap[1], a.L, a.G[1]) ? 1 : 0;
+    constexpr int ST = SSB_ASMT_STAGES;
+    const size_t smem = (size_t)ST * kFieldBytes;
+    auto k = pow2 ? assemble_tile_kernel<true, ST, SSB_ASMT_MINB> : assemble_tile_kernel<false, ST, SSB_ASMT_MINB>;
+    static bool configured[2] = {false, false};
+    if (!configured[pow2]) {
+        SSB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured[pow2] = true;
+    }
+    static unsigned grid[2] = {0, 0};
+    if (!grid[pow2]) grid[pow2] = grid_for(k, smem, 1LL << 40);
+    k<<<(unsigned)std::min<long long>(p.g.tiles, grid[pow2]), kThreadsT, smem, s>>>(p);
+    SSB_LAUNCHED();
+    return true;
+}
+
+bool launch_edge_tile(cudaStream_t s, const EdgeArgs& a, bool pow2) {
+    EdgeTileArgs p;
+    std::memset(&p, 0, sizeof p);
+    p.a = a;
+    p.g = tile_geo(a.L);
+    if (!encode_brick(&p.maps.m[0][0], a.L, a.I0[0]) || !encode_brick(&p.maps.m[0][1], a.L, a.I0[1]) ||
+        !encode_brick(&p.maps.m[1][0], a.L, a.IT[0]) || !encode_brick(&p.maps.m[1][1], a.L, a.IT[1]))
+        return false;
+    const size_t smem = 4 * (size_t)kFieldBytes;
+    auto k = pow2 ? edge_tile_kernel<true> : edge_tile_kernel<false>;
+    static bool configured[2] = {false, false};
+    if (!configured[pow2]) {
+        SSB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured[pow2] = true;
+    }
+    static unsigned grid[2] = {0, 0};
+    if (!grid[pow2]) grid[pow2] = grid_for(k, smem, 1LL << 40);
+    k<<<(unsigned)std::min<long long>(p.g.tiles, grid[pow2]), kThreadsT, smem, s>>>(p);
+    SSB_LAUNCHED();
+    return true;
+}
+
+}  // namespace ssb

@@ -248,7 +248,7 @@ ss_status ss_local_threshold(const ss_grid* g, const double* image, const ss_cen
         b.alloc(s.L);
         s.upload(image, a.pf());
         BallSet bs;
-        build_balls(bs, s.gl, 0, c, n, 0.0, false);
+        build_balls(bs, s.gl, 0, c, n, std::nan(""), false);  // per-row radii
         Dev<double> ab;
         ab.alloc(2 * (size_t)std::max(1, bs.count()));
         launch_fill(d.stream, s.L, b.pf(), background);
@@ -521,6 +521,20 @@ ss_status ss_session_create_dist(const ss_grid* g, int rank, int world, const ui
         SSB_CUDA(cudaSetDevice(device));
         std::unique_ptr<ss_session> h(new ss_session);
         h->d.reset(new Domain(*g, device, rank, world, uid));
+        *out = h.release();
+    });
+}
+
+ss_status ss_session_create_dist_host(const ss_grid* g, int rank, int world, const ss_host_comm* comm, int device,
+                                      ss_session** out) {
+    return guard([&] {
+        validate_grid(g);
+        require(out != nullptr && comm != nullptr, "null argument");
+        require_device();
+        *out = nullptr;
+        SSB_CUDA(cudaSetDevice(device));
+        std::unique_ptr<ss_session> h(new ss_session);
+        h->d.reset(new Domain(*g, device, rank, world, *comm));
         *out = h.release();
     });
 }

@@ -432,17 +432,28 @@ Domain::Domain(const ss_grid& grid, int dev, int n_slabs) : g(grid), world(n_sla
     sync();
 }
 
-Domain::Domain(const ss_grid& grid, int dev, int rank, int w, const unsigned char* uid)
-    : g(grid), world(w), device(dev), distributed(true) {
-    require(w >= 1 && rank >= 0 && rank < w, "invalid rank / world size");
-    chunk = (g.n4 + w - 1) / w;
-    const int last = g.n4 - (w - 1) * chunk;
-    require(last >= 1, "Partition: " + std::to_string(w) + " workers leave the last one with " +
+void Domain::init_rank(int rank) {
+    require(world >= 1 && rank >= 0 && rank < world, "invalid rank / world size");
+    chunk = (g.n4 + world - 1) / world;
+    const int last = g.n4 - (world - 1) * chunk;
+    require(last >= 1, "Partition: " + std::to_string(world) + " workers leave the last one with " +
                            std::to_string(last) + " slices of " + std::to_string(g.n4));
     init_common();
-    const int n4l = rank == w - 1 ? last : chunk;
+    const int n4l = rank == world - 1 ? last : chunk;
     slabs.emplace_back(new Slab(g, rank * chunk, n4l, rank, chunk, world, stream));
     sp.push_back(slabs.back().get());
+}
+
+Domain::Domain(const ss_grid& grid, int dev, int rank, int w, const ss_host_comm& comm)
+    : g(grid), world(w), device(dev), distributed(true) {
+    init_rank(rank);
+    tr = make_host_transport(comm, rank, w);
+    sync();
+}
+
+Domain::Domain(const ss_grid& grid, int dev, int rank, int w, const unsigned char* uid)
+    : g(grid), world(w), device(dev), distributed(true) {
+    init_rank(rank);
     tr = make_nccl_transport(uid, rank, w);
     const char* e = std::getenv("SSB_P2P");
     if (w > 1 && e && std::atoi(e) != 0) setup_peer_links(*tr, *sp[0], rank, w, chunk, g.n4, peers);

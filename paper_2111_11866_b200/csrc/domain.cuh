@@ -176,6 +176,8 @@ struct LocalTransport : Transport {
 };
 
 std::unique_ptr<Transport> make_nccl_transport(const unsigned char* uid, int rank, int world);
+// host-staged exchanges / all-gathers through the caller's callbacks (transport_host.cu)
+std::unique_ptr<Transport> make_host_transport(const ss_host_comm& c, int rank, int world);
 
 // large host <-> device copies (hostio.cu): pinned host memory direct and async;
 // pageable memory through pinned chunks filled / drained by host threads.  Both
@@ -245,6 +247,8 @@ struct Domain {
     Domain(const ss_grid& grid, int device, int n_slabs);
     // one rank of an NCCL job
     Domain(const ss_grid& grid, int device, int rank, int world, const unsigned char* uid);
+    // one rank of a job whose exchanges go through the host (ss_host_comm callbacks)
+    Domain(const ss_grid& grid, int device, int rank, int world, const ss_host_comm& comm);
     ~Domain();
 
     void sync();
@@ -287,6 +291,7 @@ struct Domain {
 
 private:
     void init_common();
+    void init_rank(int rank);  // the rank's slab (distributed constructors)
     cudaEvent_t pool_event(size_t idx);
     cudaGraphExec_t graph_for(const SorArgs& a, bool heat);
     void body_single(const SorArgs& a, bool heat, cudaEvent_t* ev4);

@@ -182,6 +182,10 @@ struct EdgeArgs {
     double hinv[4];
 };
 void launch_face_coefficients(cudaStream_t s, const EdgeArgs& a);
+// TMA-staged tile kernels (assemble_tile.cu); false = not launched (no tensor-map encoder)
+bool assemble_tile_supported(const Layout& L);
+bool launch_assemble_tile(cudaStream_t s, const AsmArgs& a, bool pow2);
+bool launch_edge_tile(cudaStream_t s, const EdgeArgs& a, bool pow2);
 
 // padded fp64 off-diagonals (8 per doxel) -> colour-packed fp32 rows
 // (pack_coefficients, solver.cpp:233-249)

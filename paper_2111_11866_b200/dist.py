@@ -57,3 +57,53 @@ def reduce_slice_partials(partials_by_rank):
         for v in part:
             total += float(v)
     return total
+
+
+class HostComm:
+    """Host-staged transport callbacks (ss_host_comm, ABI 5) over a torch.distributed
+    group -- gloo works on any host.  Lets several processes run the distributed
+    Domain on ONE GPU: each rank's halo planes and residual partials go device -> host
+    -> gloo -> host -> device, with the NCCL transport's message pattern, so the
+    results equal the single domain's bit for bit.  Synchronous; a test / debugging
+    path, not the multi-GPU data path."""
+
+    def __init__(self, group=None):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+
+        def sendrecv(ctx, peer, send, recv, nbytes):
+            try:
+                s = torch.frombuffer((C.c_uint8 * nbytes).from_address(send), dtype=torch.uint8)
+                r = torch.frombuffer((C.c_uint8 * nbytes).from_address(recv), dtype=torch.uint8)
+                reqs = [dist.isend(s, peer, group=group), dist.irecv(r, peer, group=group)]
+                for q in reqs:
+                    q.wait()
+                return 0
+            except Exception:  # reported to the library as a transport failure
+                return 1
+
+        def allgather(ctx, local, allbuf, nbytes):
+            try:
+                loc = torch.frombuffer((C.c_uint8 * nbytes).from_address(local), dtype=torch.uint8)
+                out = torch.frombuffer((C.c_uint8 * (nbytes * self.world)).from_address(allbuf), dtype=torch.uint8)
+                dist.all_gather(list(out.chunk(self.world)), loc, group=group)
+                return 0
+            except Exception:
+                return 1
+
+        SR = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t)
+        AG = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+
+        class _Abi(C.Structure):
+            _fields_ = [("ctx", C.c_void_p), ("sendrecv", SR), ("allgather", AG)]
+
+        self._sr, self._ag = SR(sendrecv), AG(allgather)  # kept alive with the session
+        self._abi = _Abi(None, self._sr, self._ag)
+
+    def as_abi(self):
+        import ctypes as C
+        return C.cast(C.pointer(self._abi), C.c_void_p)
