@@ -225,6 +225,18 @@ SS_API ss_status ss_session_track(ss_session* s, double level, int window, doubl
  * n_sweeps red+black sweeps with no stopping test; *residual = last residual.
  * Non-finite coefficients: SS_ERR_NONFINITE (solver.cpp:71-75). */
 SS_API ss_status ss_session_fixed_sweeps(ss_session* s, int n_sweeps, double* residual);
+/* one time step with the host's copy of u (ABI 5): u_in (or NULL: keep the device's u)
+ * becomes the interior of u^{n-1}, then the time step of ss_session_step (n_sweeps = 0,
+ * to tolerance) or ss_session_step_fixed (n_sweeps > 0), and the interior of u^n goes to
+ * u_out (or NULL).  Host arrays are COMPACT interiors: n1*n2*n3*n4 doubles of the owned
+ * slices, i fastest, no ghost layer (the ghosts are the session's Dirichlet data, 0 in
+ * segment(), solver.cpp:425).  With page-locked u_in on a single-slab session the upload
+ * streams in slice chunks and the assembly of each chunk starts as soon as its l+1
+ * neighbour is in.  ss_session_set_u_interior / _get_u_interior: the copies alone. */
+SS_API ss_status ss_session_step_host(ss_session* s, const double* u_in, double* u_out, int n_sweeps,
+                                      ss_step_diag* diag);
+SS_API ss_status ss_session_set_u_interior(ss_session* s, const double* u);
+SS_API ss_status ss_session_get_u_interior(ss_session* s, double* u);
 /* one time step of BASELINE config 4 (ABI 5): ss_session_step with exactly n_sweeps
  * sweeps and no stopping test in place of the solve to tolerance (assemble_step,
  * n_sweeps red+black sweeps, local_rescale).  The reference has no such mode: its

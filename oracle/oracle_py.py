@@ -136,6 +136,10 @@ class _Lib:
         if with_workers:
             self._sorrate = sig("sor_rate", [_G, _D, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
                                              C.c_int, _D])
+            self._wimg = sig("write_image4d", [_G, _D, C.c_char_p, C.c_char_p])
+            self._wvtk = sig("export_frame_vtk", [_G, _D, C.c_int, C.c_char_p])
+            self._wtrj = sig("write_trajectories", [C.c_int, C.POINTER(C.c_int), _D, C.c_char_p])
+            self._wlab = sig("export_label_vtks", [_G, _D, C.c_double, C.c_char_p])
             self._segfix = sig("segment_fixed", [_G, _D, _CEN, C.c_int, C.POINTER(SegParams), _D, C.c_int,
                                                  C.c_int, C.c_int, _D, C.POINTER(StepDiag), _D, _D])
         if with_workers:  # tracking: the reference itself (tracking.cpp) is the checker
@@ -311,6 +315,21 @@ class _Lib:
         st = self._sorrate(C.byref(g), _p(np.ascontiguousarray(u0)), tau, eps, omega, int(n_a), int(n_b),
                            int(workers), _p(secs))
         return st, secs.tolist()
+
+    # ---- the reference's writers (io.cpp), reference only
+    def write_image4d(self, g, u, header, data):
+        return self._wimg(C.byref(g), _p(np.ascontiguousarray(u)), header.encode(), data.encode())
+
+    def export_frame_vtk(self, g, u, l, path):
+        return self._wvtk(C.byref(g), _p(np.ascontiguousarray(u)), int(l), path.encode())
+
+    def write_trajectories(self, points, path):
+        idf = np.ascontiguousarray(np.array([p[:2] for p in points], dtype=np.int32).reshape(-1, 2))
+        xyz = np.ascontiguousarray(np.array([p[2:] for p in points], dtype=np.float64).reshape(-1, 3))
+        return self._wtrj(len(points), idf.ctypes.data_as(C.POINTER(C.c_int)), _p(xyz), path.encode())
+
+    def export_label_vtks(self, g, u, level, prefix):
+        return self._wlab(C.byref(g), _p(np.ascontiguousarray(u)), float(level), prefix.encode())
 
 
 _oracle = None

@@ -20,6 +20,7 @@
 #include "subsurf/edge.hpp"
 #include "subsurf/eoc.hpp"
 #include "subsurf/grid.hpp"
+#include "subsurf/io.hpp"
 #include "subsurf/preprocess.hpp"
 #include "subsurf/seedinit.hpp"
 #include "subsurf/solver.hpp"
@@ -597,6 +598,50 @@ int ref_sor_rate(const or_grid* g, const double* u0, double tau, double eps, dou
             }
             secs[q] = std::chrono::duration<double>(clk::now() - t0).count();
         }
+    });
+}
+
+// The reference's own writers (io.cpp), for byte-for-byte comparison of the CLI drop-in's
+// output files: write_image4d (io.cpp:99-119), export_frame_vtk (io.cpp:198-223),
+// write_trajectories (io.cpp:170-177), and the track subcommand's label-field VTKs
+// (cli.cpp:174-188: label_components of extract_mask, exported frame by frame).
+int ref_write_image4d(const or_grid* g, const double* u, const char* header, const char* data) {
+    return guarded([&] { write_image4d(field_of(g, u), header, data); });
+}
+
+int ref_export_frame_vtk(const or_grid* g, const double* u, int l, const char* path) {
+    return guarded([&] { export_frame_vtk(field_of(g, u), l, path); });
+}
+
+int ref_write_trajectories(int n, const int* id_frame, const double* xyz, const char* path) {
+    return guarded([&] {
+        TrajectoryFile t;
+        for (int q = 0; q < n; ++q) {
+            TrajectoryPoint pt;
+            pt.trajectory_id = id_frame[2 * q];
+            pt.frame = id_frame[2 * q + 1];
+            pt.x = xyz[3 * q];
+            pt.y = xyz[3 * q + 1];
+            pt.z = xyz[3 * q + 2];
+            t.points.push_back(pt);
+        }
+        write_trajectories(t, path);
+    });
+}
+
+int ref_export_label_vtks(const or_grid* g, const double* u, double level, const char* prefix) {
+    return guarded([&] {
+        const Field4D f = field_of(g, u);
+        const LabelField labels = label_components(extract_mask(f, level));
+        const GridSpec& spec = f.spec();
+        Field4D label_field(spec, 0.0);
+        for (int l = 1; l <= spec.n4; ++l)
+            for (int k = 1; k <= spec.n3; ++k)
+                for (int j = 1; j <= spec.n2; ++j)
+                    for (int i = 1; i <= spec.n1; ++i)
+                        label_field.at(i, j, k, l) = double(labels.frames[l - 1][labels.voxel(i - 1, j - 1, k - 1)]);
+        for (int l = 1; l <= spec.n4; ++l)
+            export_frame_vtk(label_field, l, std::string(prefix) + "_f" + std::to_string(l - 1) + ".vtk");
     });
 }
 

@@ -215,6 +215,9 @@ def library() -> C.CDLL:
     sig("ss_session_get_mask", [C.c_void_p, C.c_double, C.POINTER(C.c_uint8)])
     sig("ss_session_fixed_sweeps", [C.c_void_p, C.c_int, _D])
     sig("ss_session_step_fixed", [C.c_void_p, C.c_int, C.POINTER(StepDiag)])
+    sig("ss_session_step_host", [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(StepDiag)])
+    sig("ss_session_set_u_interior", [C.c_void_p, C.c_void_p])
+    sig("ss_session_get_u_interior", [C.c_void_p, C.c_void_p])
     sig("ss_session_set_loop_mode", [C.c_void_p, C.c_int])
     sig("ss_session_eoc_row", [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, _D,
                                C.POINTER(C.c_longlong)])
@@ -575,6 +578,39 @@ class Session:
         d = StepDiag()
         _check(library().ss_session_step_fixed(self._h, n_sweeps, C.byref(d) if diag else None))
         return dict(iterations=d.iterations, residual=d.residual, tol=d.tol, umin=d.umin, umax=d.umax) if diag else None
+
+    @property
+    def interior_shape(self):
+        g = self.g
+        return (self.l_count if self.distributed else g.n4, g.n3, g.n2, g.n1)
+
+    def step_host(self, u_in=None, u_out=None, n_sweeps: int = 0, diag: bool = True):
+        """One time step with the host's copy of u as compact interiors (interior_shape):
+        u_in (or None) -> u^{n-1}, then step (n_sweeps = 0) or step_fixed(n_sweeps), and u^n
+        -> u_out (a new array when None and diag is requested).  numpy arrays or raw
+        pointers (int, e.g. a pinned torch tensor's data_ptr())."""
+        def ptr(a, name, write):
+            if a is None:
+                return None
+            if isinstance(a, int):
+                return C.c_void_p(a)
+            if a.shape != self.interior_shape or a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ValidationError(f"{name}: expected a C-contiguous float64 array of shape {self.interior_shape}")
+            return C.c_void_p(a.ctypes.data)
+        d = StepDiag()
+        st = library().ss_session_step_host(self._h, ptr(u_in, "u_in", False), ptr(u_out, "u_out", True), n_sweeps,
+                                            C.byref(d) if diag else None)
+        _check(st, d.iterations, d.residual)
+        return dict(iterations=d.iterations, residual=d.residual, tol=d.tol, umin=d.umin, umax=d.umax) if diag else None
+
+    def set_u_interior(self, u) -> None:
+        a = np.ascontiguousarray(u, dtype=np.float64).reshape(self.interior_shape)
+        _check(library().ss_session_set_u_interior(self._h, C.c_void_p(a.ctypes.data)))
+
+    def get_u_interior(self) -> np.ndarray:
+        out = np.empty(self.interior_shape)
+        _check(library().ss_session_get_u_interior(self._h, C.c_void_p(out.ctypes.data)))
+        return out
 
     def set_u(self, u) -> None:
         a = self._host(u, "u")

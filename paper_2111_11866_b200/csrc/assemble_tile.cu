@@ -97,14 +97,17 @@ __device__ __forceinline__ void tensor3_prefetch(const CUtensorMap* map, int x, 
 
 struct TileGeo {
     int nb, njb, nkc;  // i blocks, row blocks, plane chunks
+    int l_lo, nl;      // slices l_lo .. l_lo + nl - 1
     long long tiles;
 };
-__host__ __device__ __forceinline__ TileGeo tile_geo(const Layout& L) {
+__host__ __device__ __forceinline__ TileGeo tile_geo(const Layout& L, int l_lo = 1, int l_hi = -1) {
     TileGeo g;
     g.nb = (L.n1 + kTI - 1) / kTI;
     g.njb = (L.n2 + kTJ - 1) / kTJ;
     g.nkc = (L.n3 + kTK - 1) / kTK;
-    g.tiles = (long long)g.nb * g.njb * g.nkc * L.n4;
+    g.l_lo = l_lo;
+    g.nl = (l_hi < 0 ? L.n4 : l_hi) - l_lo + 1;
+    g.tiles = (long long)g.nb * g.njb * g.nkc * g.nl;
     return g;
 }
 
@@ -116,8 +119,8 @@ struct Tile {
 };
 __device__ __forceinline__ Tile tile_of(const Layout& L, const TileGeo& g, long long t) {
     Tile x;
-    x.l = (int)(t % L.n4) + 1;
-    long long r = t / L.n4;
+    x.l = (int)(t % g.nl) + g.l_lo;
+    long long r = t / g.nl;
     x.b = (int)(r % g.nb);
     r /= g.nb;
     x.jb = (int)(r % g.njb);
@@ -516,10 +519,28 @@ unsigned grid_for(K kernel, size_t smem, long long tiles) {
 
 }  // namespace
 
+static bool launch_tile(cudaStream_t s, AsmTileArgs& p, bool pow2);
+
 bool assemble_tile_supported(const Layout& L) {
     // TMA box bounds / alignment hold for every grid (W even); off by SSB_ASM_TILE=0
     static const int on = env_int("SSB_ASM_TILE", 1);
     return on != 0 && encoder() != nullptr && L.n1 >= 1;
+}
+
+bool launch_assemble_tile_range(cudaStream_t s, const AsmArgs& a0, int l_lo, int l_hi) {
+    if (l_hi < l_lo) return true;
+    AsmArgs a = a0;
+    bool pow2 = true;
+    for (int q = 0; q < 4; ++q) {
+        int e = 0;
+        pow2 = pow2 && std::frexp(a.h[q], &e) == 0.5;
+        a.hinv[q] = 1.0 / a.h[q];
+    }
+    AsmTileArgs p;
+    std::memset(&p, 0, sizeof p);
+    p.a = a;
+    p.g = tile_geo(a.L, l_lo, l_hi);
+    return launch_tile(s, p, pow2);
 }
 
 bool launch_assemble_tile(cudaStream_t s, const AsmArgs& a, bool pow2) {
@@ -527,6 +548,11 @@ bool launch_assemble_tile(cudaStream_t s, const AsmArgs& a, bool pow2) {
     std::memset(&p, 0, sizeof p);
     p.a = a;
     p.g = tile_geo(a.L);
+    return launch_tile(s, p, pow2);
+}
+
+static bool launch_tile(cudaStream_t s, AsmTileArgs& p, bool pow2) {
+    const AsmArgs& a = p.a;
     if (!encode_brick(&p.maps.m[0][0], a.L, a.u[0]) || !encode_brick(&p.maps.m[0][1], a.L, a.u[1])) return false;
     static const int gpref = env_int("SSB_ASM_GPREF", 0);  // measured neutral (+12% DRAM reads): off
     p.gpref = gpref && a.G[0] && encode_G(&p.gmap[0], a.L, a.G[0]) && encode_G(&p.gmap[1], a.L, a.G[1]) ? 1 : 0;

@@ -639,6 +639,40 @@ ss_status ss_session_step_fixed(ss_session* s, int n_sweeps, ss_step_diag* diag)
     });
 }
 
+ss_status ss_session_step_host(ss_session* s, const double* u_in, double* u_out, int n_sweeps, ss_step_diag* diag) {
+    return guard([&] {
+        require(s != nullptr, "null session");
+        require(n_sweeps >= 0, "n_sweeps must be >= 0");
+        SSB_CUDA(cudaSetDevice(s->d->device));
+        try {
+            s->d->step_host(u_in, u_out, n_sweeps, diag);
+        } catch (const SolverErrT& e) {
+            if (diag) {
+                diag->iterations = e.iterations;
+                diag->residual = e.residual;
+            }
+            throw;
+        }
+    });
+}
+
+ss_status ss_session_set_u_interior(ss_session* s, const double* u) {
+    return guard([&] {
+        require(s && u, "null session / buffer");
+        SSB_CUDA(cudaSetDevice(s->d->device));
+        s->d->set_u_interior(u);
+        s->d->sync();
+    });
+}
+
+ss_status ss_session_get_u_interior(ss_session* s, double* u) {
+    return guard([&] {
+        require(s && u, "null session / buffer");
+        SSB_CUDA(cudaSetDevice(s->d->device));
+        s->d->get_u_interior(u);
+    });
+}
+
 ss_status ss_session_eoc_row(ss_session* s, int n, double omega, double sor_tol, int sor_max_iter, double* err,
                              long long* sweeps) {
     return guard([&] {

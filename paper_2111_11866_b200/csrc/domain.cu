@@ -216,6 +216,25 @@ void Slab::sync_ghosts_from(int role) {
         if (r != role) launch_copy_ghosts(stream, L, S[r].pf(), S[role].pf());
 }
 
+AsmArgs Slab::asm_args(PField u, bool with_G, double tau, double eps) const {
+    AsmArgs a{};
+    a.L = L;
+    a.u[0] = u.c[0];
+    a.u[1] = u.c[1];
+    a.G[0] = with_G ? G[0].p : nullptr;
+    a.G[1] = with_G ? G[1].p : nullptr;
+    a.coef[0] = coef[0].p;
+    a.coef[1] = coef[1].p;
+    const double h[4] = {gl.h1, gl.h2, gl.h3, gl.h4};
+    for (int q = 0; q < 4; ++q) {
+        a.t_h2[q] = tau / (h[q] * h[q]);  // solver.cpp:36-38
+        a.h[q] = h[q];
+    }
+    a.eps = eps;
+    a.bad = flags.p;
+    return a;
+}
+
 void Slab::assemble(PField u, bool with_G, double tau, double eps, double* off_out, double* diag_out,
                     double* abar_out) {
     AsmArgs a{};
@@ -392,6 +411,7 @@ void Domain::init_common() {
     SSB_CUDA(cudaSetDevice(device));
     SSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     SSB_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+    SSB_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
     // the end slices and the halo exchange run on high-priority streams: the interior
     // pass is a persistent grid that fills every CTA slot, and pending CTAs of a
     // higher-priority stream (the end slices, the NCCL exchange kernels) are scheduled
@@ -483,6 +503,9 @@ Domain::~Domain() {
     if (ev_xchg) cudaEventDestroy(ev_xchg);
     if (stream) cudaStreamDestroy(stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (h2d) cudaStreamSynchronize(h2d);
+    for (auto e : up_ev) cudaEventDestroy(e);
+    if (h2d) cudaStreamDestroy(h2d);
     if (comm) cudaStreamDestroy(comm);
 }
 
@@ -1162,13 +1185,80 @@ void Domain::prepare(const double* image, const ss_center* c, int n, const ss_se
 // Everything up to the end of the SOR loop is one stream sequence: the assembly's
 // non-finite flag (solver.cpp:71-75) reaches the loop control on the device (sor_init,
 // all-gathered across slabs), and the host learns of it with the solve's final state.
-SolveOut Domain::step(ss_step_diag* diag, int fixed, bool rescale) {
+SolveOut Domain::step(ss_step_diag* diag, int fixed, bool rescale) { return step_impl(diag, fixed, rescale, nullptr); }
+
+void Domain::set_u_interior(const double* host) {
+    const long long fr = (long long)g.n1 * g.n2 * g.n3;
+    for (Slab* s : sp) {
+        double* d = s->stage_p();
+        copy_h2d(d, host + (distributed ? 0 : fr * s->L.l0), fr * s->L.n4 * sizeof(double), stream);
+        launch_pack_interior(stream, s->L, d, s->S[cur].pf(), 1, s->L.n4);
+    }
+}
+
+void Domain::get_u_interior(double* host) {
+    const long long fr = (long long)g.n1 * g.n2 * g.n3;
+    for (Slab* s : sp) {
+        double* d = s->stage_p();
+        launch_unpack_interior(stream, s->L, s->S[cur].pf(), d);
+        copy_d2h(host + (distributed ? 0 : fr * s->L.l0), d, fr * s->L.n4 * sizeof(double), stream);
+    }
+    sync();
+}
+
+// single slab, page-locked input: slice chunks H2D on the copy stream; per chunk the main
+// stream packs it and assembles the slices whose l+1 neighbour is in (the last chunk: all)
+void Domain::upload_assemble(const double* host) {
+    Slab& x = *sp[0];
+    const long long fr = (long long)g.n1 * g.n2 * g.n3;
+    const int n4 = x.L.n4, C = std::min(n4, 8);
+    while ((int)up_ev.size() < C + 1) {
+        cudaEvent_t e;
+        SSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        up_ev.push_back(e);
+    }
+    double* st = x.stage_p();
+    SSB_CUDA(cudaEventRecord(up_ev[C], stream));  // earlier users of the staging buffer are done
+    SSB_CUDA(cudaStreamWaitEvent(h2d, up_ev[C], 0));
+    auto lo = [&](int q) { return 1 + (int)((long long)q * n4 / C); };
+    for (int q = 0; q < C; ++q) {
+        const int a = lo(q), b = lo(q + 1) - 1;
+        SSB_CUDA(cudaMemcpyAsync(st + (a - 1) * fr, host + (a - 1) * fr, (size_t)(b - a + 1) * fr * sizeof(double),
+                                 cudaMemcpyHostToDevice, h2d));
+        SSB_CUDA(cudaEventRecord(up_ev[q], h2d));
+    }
+    SSB_CUDA(cudaMemsetAsync(x.flags.p, 0, sizeof(int), stream));
+    const AsmArgs args = x.asm_args(x.S[cur].pf(), x.have_G, prm.tau, prm.epsilon);
+    int done = 0;
+    for (int q = 0; q < C; ++q) {
+        const int a = lo(q), b = lo(q + 1) - 1;
+        SSB_CUDA(cudaStreamWaitEvent(stream, up_ev[q], 0));
+        launch_pack_interior(stream, x.L, st, x.S[cur].pf(), a, b);
+        const int hi = q == C - 1 ? n4 : b - 1;
+        if (!launch_assemble_tile_range(stream, args, done + 1, hi))
+            throw Error(SS_ERR_CUDA, "assemble: tensor-map encoding failed");
+        done = std::max(done, hi);
+    }
+}
+
+SolveOut Domain::step_host(const double* in, double* out, int fixed, ss_step_diag* diag) {
+    const SolveOut o = step_impl(diag, fixed, true, in);
+    if (out) get_u_interior(out);
+    return o;
+}
+
+SolveOut Domain::step_impl(ss_step_diag* diag, int fixed, bool rescale, const double* host_in) {
     if (!prepared) throw Error(SS_ERR_STATE, "session not prepared");
     int roles[kStateBuffers];
     for (int q = 0; q < kStateBuffers; ++q) roles[q] = (cur + q) % kStateBuffers;
+    const bool overlap = host_in && single() && assemble_tile_supported(sp[0]->L) && host_pinned(host_in);
+    if (host_in && !overlap) set_u_interior(host_in);
     exchange_role(cur, 3);  // u^{n-1} halos for the face gradients and the first red pass
     if (profiling) SSB_CUDA(cudaEventRecord(ev[2], stream));
-    for (Slab* s : sp) s->assemble(s->S[cur].pf(), s->have_G, prm.tau, prm.epsilon, nullptr, nullptr, nullptr);
+    if (overlap)
+        upload_assemble(host_in);
+    else
+        for (Slab* s : sp) s->assemble(s->S[cur].pf(), s->have_G, prm.tau, prm.epsilon, nullptr, nullptr, nullptr);
     if (profiling) SSB_CUDA(cudaEventRecord(ev[3], stream));
     const bool rel = !fixed && prm.sor_rel_tol > 0.0;
     if (rel) {

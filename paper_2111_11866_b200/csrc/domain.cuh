@@ -131,6 +131,7 @@ struct Slab {
     void sync_ghosts_from(int role);
     void assemble(PField u, bool with_G, double tau, double eps, double* off_out, double* diag_out,
                   double* abar_out);
+    AsmArgs asm_args(PField u, bool with_G, double tau, double eps) const;
     void face_coefficients(PField I0s, PField ITs, double K, double delta, double vartheta,
                            double* G_out);
     void rescale(int role);
@@ -184,6 +185,7 @@ std::unique_ptr<Transport> make_host_transport(const ss_host_comm& c, int rank, 
 // return with the host buffer reusable (d2h: data arrived).
 void copy_h2d(void* dev, const void* host, size_t bytes, cudaStream_t s);
 void copy_d2h(void* host, const void* dev, size_t bytes, cudaStream_t s);
+bool host_pinned(const void* p);  // page-locked (or registered) host memory
 
 // NVLink peer links of one rank (opt-in, SSB_P2P=1): the l-neighbours' state
 // arrays and flag words mapped into this process with CUDA IPC, so the TMA pass
@@ -286,10 +288,22 @@ struct Domain {
     // test (BASELINE config 4); rescale = false skips local_rescale (ss_session_fixed_sweeps)
     SolveOut step(ss_step_diag* diag, int fixed = 0, bool rescale = true);
     double fixed_sweeps(int n_sweeps);
+    // step() with the step's input / result as compact host interiors (n1*n2*n3*n4 doubles of
+    // this domain's owned slices, i fastest; ghosts stay the device's Dirichlet data); either
+    // may be null.  Single slab + page-locked input: the upload streams in slice chunks on a
+    // copy stream and the assembly of each chunk's slices starts as soon as their l+1
+    // neighbours have arrived (ss_session_step_host)
+    SolveOut step_host(const double* in, double* out, int fixed, ss_step_diag* diag);
+    void set_u_interior(const double* host);
+    void get_u_interior(double* host);
     // EOC verification row (eoc.cpp:83-137) on an n^4 session; returns the space-time L2 error
     double eoc_row(int n, double omega, double sor_tol, int max_iter, long long* total_sweeps);
 
 private:
+    cudaStream_t h2d = nullptr;        // step_host: chunked upload of the step's input
+    std::vector<cudaEvent_t> up_ev;   // ... one event per chunk (+ the staging-free event)
+    SolveOut step_impl(ss_step_diag* diag, int fixed, bool rescale, const double* host_in);
+    void upload_assemble(const double* host);
     void init_common();
     void init_rank(int rank);  // the rank's slab (distributed constructors)
     cudaEvent_t pool_event(size_t idx);

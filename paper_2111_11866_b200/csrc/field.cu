@@ -114,6 +114,36 @@ __global__ void pack_kernel(const Layout L, const double* __restrict__ src, PFie
     }
 }
 
+// compact interior rows (n1 doubles, i fastest, then j, k, l; no ghosts) of slices
+// [l_lo, l_hi] <-> the colour-packed field: one warp per interior row
+__global__ void pack_interior_kernel(const Layout L, const double* __restrict__ src, PField dst, int l_lo,
+                                     long long nrows) {
+    const long long q = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= nrows) return;
+    const int j = (int)(q % L.n2) + 1;
+    const long long t = q / L.n2;
+    const int k = (int)(t % L.n3) + 1;
+    const int l = (int)(t / L.n3) + l_lo;
+    const long long r = L.row(j, k, l);
+    const long long cq = ((long long)(l - 1) * L.n3 + (k - 1)) * L.n2 + (j - 1);
+    const int par = (j + k + l + L.lpar) & 1;
+    for (int i = 1 + lane; i <= L.n1; i += 32) dst.c[(i + par) & 1][r * L.W + (i >> 1)] = src[cq * L.n1 + i - 1];
+}
+
+__global__ void unpack_interior_kernel(const Layout L, PField src, double* __restrict__ dst, long long nrows) {
+    const long long q = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= nrows) return;
+    const int j = (int)(q % L.n2) + 1;
+    const long long t = q / L.n2;
+    const int k = (int)(t % L.n3) + 1;
+    const int l = (int)(t / L.n3) + 1;
+    const long long r = L.row(j, k, l);
+    const int par = (j + k + l + L.lpar) & 1;
+    for (int i = 1 + lane; i <= L.n1; i += 32) dst[q * L.n1 + i - 1] = src.c[(i + par) & 1][r * L.W + (i >> 1)];
+}
+
 __global__ void unpack_kernel(const Layout L, PField src, double* __restrict__ dst) {
     const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -329,6 +359,19 @@ void launch_fill_raw(cudaStream_t s, double* p, long long n, double v) {
 
 void launch_copy_ghosts(cudaStream_t s, const Layout& L, PField dst, PField src) {
     copy_ghosts_kernel<<<ceil_div(shell_count(L), 256), 256, 0, s>>>(L, dst, src);
+    SSB_LAUNCHED();
+}
+
+void launch_pack_interior(cudaStream_t s, const Layout& L, const double* src, PField dst, int l_lo, int l_hi) {
+    const long long nrows = (long long)L.n2 * L.n3 * (l_hi - l_lo + 1);
+    if (nrows <= 0) return;
+    pack_interior_kernel<<<ceil_div(nrows * 32, 256), 256, 0, s>>>(L, src, dst, l_lo, nrows);
+    SSB_LAUNCHED();
+}
+
+void launch_unpack_interior(cudaStream_t s, const Layout& L, PField src, double* dst) {
+    const long long nrows = (long long)L.n2 * L.n3 * L.n4;
+    unpack_interior_kernel<<<ceil_div(nrows * 32, 256), 256, 0, s>>>(L, src, dst, nrows);
     SSB_LAUNCHED();
 }
 

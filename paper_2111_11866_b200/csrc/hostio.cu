@@ -72,6 +72,8 @@ void par_memcpy(void* dst, const void* src, size_t n) {
 
 }  // namespace
 
+bool host_pinned(const void* p) { return pinned(p); }
+
 void copy_h2d(void* dev, const void* host, size_t bytes, cudaStream_t s) {
     if (bytes < (4u << 20) || pinned(host)) {
         SSB_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, s));

@@ -185,6 +185,8 @@ void launch_face_coefficients(cudaStream_t s, const EdgeArgs& a);
 // TMA-staged tile kernels (assemble_tile.cu); false = not launched (no tensor-map encoder)
 bool assemble_tile_supported(const Layout& L);
 bool launch_assemble_tile(cudaStream_t s, const AsmArgs& a, bool pow2);
+// the same restricted to slices [l_lo, l_hi] (the upload-overlapped assembly of step_host)
+bool launch_assemble_tile_range(cudaStream_t s, const AsmArgs& a, int l_lo, int l_hi);
 bool launch_edge_tile(cudaStream_t s, const EdgeArgs& a, bool pow2);
 
 // padded fp64 off-diagonals (8 per doxel) -> colour-packed fp32 rows
@@ -203,6 +205,10 @@ void launch_pack(cudaStream_t s, const Layout& L, const double* src, PField dst,
                  PField twin1, PField twin2);
 void launch_fill_raw(cudaStream_t s, double* p, long long n, double v);
 void launch_unpack(cudaStream_t s, const Layout& L, PField src, double* dst);
+// compact interior arrays (n1*n2*n3*n4 doubles, i fastest, no ghosts): slices [l_lo, l_hi]
+// of src (indexed from slice 1) into dst's interior / every interior doxel of src out
+void launch_pack_interior(cudaStream_t s, const Layout& L, const double* src, PField dst, int l_lo, int l_hi);
+void launch_unpack_interior(cudaStream_t s, const Layout& L, PField src, double* dst);
 void launch_fill(cudaStream_t s, const Layout& L, PField f, double v);
 void launch_set_ghosts(cudaStream_t s, const Layout& L, PField f, double v);
 // ghost doxels of src copied into dst

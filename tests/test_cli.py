@@ -82,7 +82,7 @@ def test_cli_no_cpu_fallback(cli, tmp_path):
 
 
 @pytest.mark.gpu
-def test_cli_segment_matches_oracle(cli, oracle, tmp_path):
+def test_cli_segment_matches_oracle(cli, oracle, ref, tmp_path):
     from oracle import oracle_py as op
     dims, h = (10, 8, 7, 6), 0.125
     img = cs.f32_image(dims, 3)
@@ -99,7 +99,17 @@ def test_cli_segment_matches_oracle(cli, oracle, tmp_path):
     st, uo, info = oracle.segment(op.Grid.make(dims, h), img, rows, p)
     assert st == 0
     assert np.array_equal(u, uo[1:-1, 1:-1, 1:-1, 1:-1].astype("<f4"))
-    assert os.path.exists(str(tmp_path / "out_f0.vtk"))
+    # the output files against the reference's own writers on the same u (io.cpp:99-119,
+    # :198-223; cli.cpp:129-133): payload and VTK frames byte for byte; the JSON header's
+    # whitespace depends on the (unvendored) nlohmann version, so it is compared parsed
+    g = op.Grid.make(dims, h)
+    d = str(tmp_path)
+    assert ref.write_image4d(g, uo, d + "/ref.json", d + "/ref.raw") == 0
+    assert open(d + "/ref.raw", "rb").read() == open(d + "/out.raw", "rb").read()
+    assert json.load(open(d + "/ref.json")) == json.load(open(d + "/out.json"))
+    for l in range(1, dims[3] + 1):
+        assert ref.export_frame_vtk(g, uo, l, f"{d}/ref_f{l - 1}.vtk") == 0
+        assert open(f"{d}/ref_f{l - 1}.vtk", "rb").read() == open(f"{d}/out_f{l - 1}.vtk", "rb").read(), l
 
 
 @pytest.mark.gpu
@@ -152,4 +162,12 @@ def test_cli_track_matches_reference(cli, ref, tmp_path):
     assert rows[0] == "trajectory_id,frame,x,y,z"
     want = ref.track(Grid.make(dims, 1.0), u32, 0.5, 3, 5.0)
     assert rows[1:] == [f"{a},{b},{x:g},{y:g},{z:g}" for a, b, x, y, z in want]
-    assert os.path.exists(os.path.join(d, f"lab_f{dims[3] - 1}.vtk"))
+    # byte for byte against the reference's writers: write_trajectories (io.cpp:170-177) of
+    # its track() points, and the label-field VTKs of cli.cpp:174-188
+    g = Grid.make(dims, 1.0)
+    assert ref.write_trajectories(want, os.path.join(d, "ref.csv")) == 0
+    assert open(os.path.join(d, "ref.csv"), "rb").read() == open(os.path.join(d, "traj.csv"), "rb").read()
+    assert ref.export_label_vtks(g, u32, 0.5, os.path.join(d, "reflab")) == 0
+    for l in range(dims[3]):
+        a = open(os.path.join(d, f"reflab_f{l}.vtk"), "rb").read()
+        assert a == open(os.path.join(d, f"lab_f{l}.vtk"), "rb").read(), l

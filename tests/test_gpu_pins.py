@@ -14,8 +14,9 @@ and min/max of u, the sha256 of the final u's bits and the 0.5-mask voxel count.
 The device session recomputes them here and must match: iterations exactly, u bit
 for bit (so the 0.5-mask too), min/max exactly.  Residual and tolerance are
 sums of squares formed in a different order (per-slice 256-lane trees vs the
-reference's sequential sweep: ~1e-12 relative on 16.8 M doxels) and are compared to
-1e-10 relative -- equal iteration counts show no stopping decision flipped.
+reference's sequential sweep, whose own rounding error grows up to ~N eps: 2.2e-10
+relative measured on config 2's 1.3e8 doxels) and are compared to 1e-8 relative --
+equal iteration counts show that no stopping decision flipped.
 """
 import hashlib
 import json
@@ -55,9 +56,9 @@ def test_config_pinned_to_reference(gpu, name):
         u = s.get_u()
         mask = s.get_mask(0.5)
     assert [d["iterations"] for d in diags] == pin["iterations"]
-    np.testing.assert_allclose([d["residual"] for d in diags], pin["residual"], rtol=1e-10, atol=0)
+    np.testing.assert_allclose([d["residual"] for d in diags], pin["residual"], rtol=1e-8, atol=0)
     if not fixed:
-        np.testing.assert_allclose([d["tol"] for d in diags], pin["tol"], rtol=1e-10, atol=0)
+        np.testing.assert_allclose([d["tol"] for d in diags], pin["tol"], rtol=1e-8, atol=0)
     assert [d["umin"] for d in diags] == pin["umin"]
     assert [d["umax"] for d in diags] == pin["umax"]
     assert sha(u) == pin["u_sha256"], "u differs from the reference's bits"

@@ -239,3 +239,42 @@ def test_slabs_exchange_path_tma(gpu, kernel):
     for k, (its_ok, u_ok, halo_n, dims) in res.items():
         assert its_ok and u_ok, (kernel, k, res)
         assert halo_n > 0, (kernel, k, res)
+
+
+@pytest.mark.parametrize("n_slabs,pinned", [(1, True), (1, False), (3, False)])
+def test_step_host_matches_device_steps(gpu, n_slabs, pinned):
+    """ss_session_step_host (compact host interiors in and out; single slab + page-locked
+    input: chunked upload overlapped with the per-chunk assembly) == set_u + step + get_u."""
+    import torch
+    import workloads
+    wl = workloads.small((20, 14, 10, 11), seed=21)
+    g = gpu.Grid.make(wl.dims, wl.h)
+    p = gpu.seg_params(**{**wl.params, "n_steps": 6, "sor_rel_tol": 1e-8, "rescale_radius": 3.0})
+    inner = (slice(1, -1),) * 4
+    with gpu.Session(g, n_slabs=n_slabs) as a, gpu.Session(g) as b:
+        a.prepare(wl.image, wl.rows, p, wl.u0)
+        b.prepare(wl.image, wl.rows, p, wl.u0)
+        shape = a.interior_shape
+        if pinned:
+            t_in = torch.empty(shape, dtype=torch.float64).pin_memory()
+            t_out = torch.empty(shape, dtype=torch.float64).pin_memory()
+            t_in.copy_(torch.from_numpy(np.ascontiguousarray(b.get_u()[inner])))
+        else:
+            h_in = np.ascontiguousarray(b.get_u()[inner])
+            h_out = np.empty(shape)
+        for n, fixed in enumerate([0, 0, 9, 0]):
+            if pinned:
+                da = a.step_host(t_in.data_ptr(), t_out.data_ptr(), fixed)
+                got = t_out.numpy().copy()
+                t_in, t_out = t_out, t_in
+            else:
+                da = a.step_host(h_in, h_out, fixed)
+                got = h_out.copy()
+                h_in, h_out = h_out, h_in
+            db = b.step_fixed(fixed) if fixed else b.step()
+            want = b.get_u()[inner]
+            assert da == db, n
+            assert np.array_equal(got.view(np.uint64), np.ascontiguousarray(want).view(np.uint64)), n
+        # the interior copies alone
+        a.set_u_interior(want * 0.5)
+        assert np.array_equal(a.get_u_interior(), want * 0.5)
