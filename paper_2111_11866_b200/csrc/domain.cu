@@ -340,7 +340,10 @@ SorArgs Slab::sor_args(const PField B[kStateBuffers], const PField& rhs, bool he
     a.l_step = 1;
     a.dyn = 1;  // whole-slab pass launches; ranges clear it (sor.cu)
     a.wave = kernel == 2 && world == 1 && wflags.p != nullptr && wave_supported(L) ? 1 : 0;
-    if (kernel == 7 && !heat && world == 1 && wflags.p != nullptr && kwave_supported(L)) a.wave = 2;
+    if (kernel == 7 && !heat && world == 1 && wflags.p != nullptr && kwave_supported(L)) {
+        a.wave = 2;
+        a.kwj = kwave_axis_j(L);
+    }
     a.flags = wflags.p;
     a.snake = pass_snake();
     a.l2hint = pass_l2hint();

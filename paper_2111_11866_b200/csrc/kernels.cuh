@@ -66,6 +66,7 @@ struct SorArgs {
     int pdl_off;            // launch without programmatic dependent launch (side-stream launches)
     int dyn;                // TMA pass: items from the colour's atomic counter (one such launch per pass)
     int wave;               // 1: two-iteration wavefront kernel per loop body, 2: one-sweep k-wavefront
+    int kwj;                // one-sweep wavefront marches along j (1) or k (0)
     int* flags;             // wavefront item completion flags (epochs)
     int snake;              // TMA pass: black passes walk the items in reverse (L2 reuse at the turn)
     int order;              // TMA pass item order: 0 slice-major, 1 slice-fastest
@@ -120,6 +121,7 @@ size_t wave_flags(const Layout& L);
 // one-sweep k-wavefront (kernel 7, sor_tma.cu): support test, flag / partial sizes,
 // partials per slice, launch (one iteration: red + black)
 bool kwave_supported(const Layout& L);
+int kwave_axis_j(const Layout& L);  // 1: the one-sweep wavefront marches along j
 size_t kwave_flags(const Layout& L);
 size_t kwave_partials(const Layout& L);
 int kwave_bps(const Layout& L);

@@ -1060,16 +1060,27 @@ constexpr int kKwP = SSB_KWAVE_PLANES;
 #endif
 constexpr int kKwLag = SSB_KWAVE_LAG;
 constexpr int kKwPub = 4;  // publisher ring: items a consumer may finish ahead of the publisher
+// The wavefront marches along k (chunk = a plane chunk of every row group and slice) or,
+// when that cross-section is smaller, along j (chunk = a row group of every plane chunk
+// and slice: the j-wavefront) -- the u rows between a chunk's red and black items must
+// stay in L2, and the j cross-section of a wide, shallow grid (config 4: 8 MB) is a
+// quarter of the k one
 struct KwGeo {
     int nkc;        // plane chunks of kKwP planes
-    int M;          // items per chunk and colour: njg * n4
-    long long NT;   // items of the launch: (nkc + LAG) steps x 2 colours x M (empty halves skipped)
+    int axis_j;     // 1: chunks are row groups (j-wavefront), 0: plane chunks (k-wavefront)
+    int nch;        // chunks along the march axis
+    int NA;         // items per chunk and slice (row groups, or plane chunks for axis_j)
+    int M;          // items per chunk and colour: NA * n4
+    long long NT;   // items of the launch: (nch + LAG) steps x 2 colours x M (empty halves skipped)
 };
-__host__ __device__ __forceinline__ KwGeo make_kwgeo(const Layout& L, const Geo& G) {
+__host__ __device__ __forceinline__ KwGeo make_kwgeo(const Layout& L, const Geo& G, int axis_j = 0) {
     KwGeo k;
     k.nkc = (L.n3 + kKwP - 1) / kKwP;
-    k.M = G.njg * L.n4;
-    k.NT = (long long)(k.nkc + kKwLag) * 2 * k.M;
+    k.axis_j = axis_j;
+    k.nch = axis_j ? G.njg : k.nkc;
+    k.NA = axis_j ? k.nkc : G.njg;
+    k.M = k.NA * L.n4;
+    k.NT = (long long)(k.nch + kKwLag) * 2 * k.M;
     return k;
 }
 
@@ -1096,51 +1107,54 @@ __global__ void __launch_bounds__(kKwThreads, SSB_CTAS_PER_SM) sor_kwave_tma(con
     const int epoch = *(volatile const int*)&st->epoch_base + n;
     const Layout& L = a.L;
     const Geo G = make_geo(L, false);
-    const KwGeo K = make_kwgeo(L, G);
+    const KwGeo K = make_kwgeo(L, G, a.kwj);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int bin = in_buf(n), bout = out_buf(n);
     int* const flg = a.flags;  // per red item: the epoch of the launch that completed it
-    // item cursor: block blk (2 per step: red, black), row group jg, slice l0 + 1 (l fastest);
-    // advanced by gridDim.x items with additions only
+    // item cursor: block blk (2 per step: red, black), position a within the chunk (row group,
+    // or plane chunk for the j-wavefront), slice l0 + 1 (l fastest); advanced by gridDim.x
+    // items with additions only
     struct Cur {
-        int blk, jg, l0;
+        int blk, a, l0;
     };
-    const int NB = 2 * (K.nkc + kKwLag);
+    const int NB = 2 * (K.nch + kKwLag);
     const int gq = (int)(gridDim.x / (unsigned)L.n4), gr = (int)(gridDim.x % (unsigned)L.n4);
     auto first = [&]() {
         Cur c;
         const int x0 = (int)blockIdx.x % K.M;
         c.blk = (int)blockIdx.x / K.M;
-        c.jg = x0 / L.n4;
-        c.l0 = x0 - c.jg * L.n4;
+        c.a = x0 / L.n4;
+        c.l0 = x0 - c.a * L.n4;
         return c;
     };
     auto advance = [&](Cur& c) {
         c.l0 += gr;
-        c.jg += gq;
+        c.a += gq;
         if (c.l0 >= L.n4) {
             c.l0 -= L.n4;
-            ++c.jg;
+            ++c.a;
         }
-        while (c.jg >= G.njg) {
-            c.jg -= G.njg;
+        while (c.a >= K.NA) {
+            c.a -= K.NA;
             ++c.blk;
         }
     };
     // colour and Item of the cursor's item; false: empty half-step (no such chunk)
     auto item_of = [&](const Cur& c, int& C, Item& it) -> bool {
         C = c.blk & 1;
-        const int kc = (c.blk >> 1) - C * kKwLag;  // plane chunk
-        if (kc < 0 || kc >= K.nkc) return false;
+        const int ch = (c.blk >> 1) - C * kKwLag;  // chunk along the march axis
+        if (ch < 0 || ch >= K.nch) return false;
+        const int kc = K.axis_j ? c.a : ch, jg = K.axis_j ? ch : c.a;
         it.l = c.l0 + 1;
         it.s0 = 0;
-        it.j0 = c.jg * G.R + 1;
+        it.j0 = jg * G.R + 1;
         it.rows = min(G.R, L.n2 - it.j0 + 1);
         it.k0 = kc * kKwP + 1;
         it.k1 = min(it.k0 + kKwP - 1, L.n3);
         return true;
     };
-    auto chunk = [&](const Item& it) { return (it.k0 - 1) / kKwP; };
+    auto chunk = [&](const Item& it) { return (it.k0 - 1) / kKwP; };  // plane chunk
+    auto rgroup = [&](const Item& it) { return (it.j0 - 1) / G.R; };  // row group
     auto flag_of = [&](int kc, int jg, int l) -> const int* {
         return flg + ((long long)kc * G.njg + jg) * L.n4 + (l - 1);
     };
@@ -1155,7 +1169,7 @@ __global__ void __launch_bounds__(kKwThreads, SSB_CTAS_PER_SM) sor_kwave_tma(con
             mbar_wait(&doneB[ps], pph);
             if (C == 0) {
                 __threadfence();  // the consumers' stores (ordered before their arrivals) -> gpu scope
-                asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(flag_of(chunk(it), c.jg, it.l)),
+                asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(flag_of(chunk(it), rgroup(it), it.l)),
                              "r"(epoch)
                              : "memory");
             }
@@ -1174,8 +1188,8 @@ __global__ void __launch_bounds__(kKwThreads, SSB_CTAS_PER_SM) sor_kwave_tma(con
         // loaded one black item ahead (relaxed, in parallel), re-polled only if not yet set
         Cur nb{-1, 0, 0};
         int nbv[7];
-        auto deps = [&](const Cur& c, const Item& it, const int*(&q)[7]) {
-            const int kc = chunk(it), jg = c.jg, l = it.l;
+        auto deps = [&](const Item& it, const int*(&q)[7]) {
+            const int kc = chunk(it), jg = rgroup(it), l = it.l;
             const int* self = flag_of(kc, jg, l);
             q[0] = self;
             q[1] = l > 1 ? self - 1 : self;
@@ -1192,7 +1206,7 @@ __global__ void __launch_bounds__(kKwThreads, SSB_CTAS_PER_SM) sor_kwave_tma(con
                 Item it2;
                 if (item_of(c, C2, it2) && C2 == 1) {
                     const int* q[7];
-                    deps(c, it2, q);
+                    deps(it2, q);
 #pragma unroll
                     for (int u = 0; u < 7; ++u) nbv[u] = ld_relaxed(q[u]);
                     nb = c;
@@ -1206,8 +1220,8 @@ __global__ void __launch_bounds__(kKwThreads, SSB_CTAS_PER_SM) sor_kwave_tma(con
             if (!item_of(c, C, it)) continue;
             if (C == 1) {
                 const int* q[7];
-                deps(c, it, q);
-                const bool pre = nb.blk == c.blk && nb.jg == c.jg && nb.l0 == c.l0;
+                deps(it, q);
+                const bool pre = nb.blk == c.blk && nb.a == c.a && nb.l0 == c.l0;
                 int v[7];
 #pragma unroll
                 for (int u = 0; u < 7; ++u) v[u] = pre ? nbv[u] : ld_relaxed(q[u]);
@@ -1247,7 +1261,7 @@ __global__ void __launch_bounds__(kKwThreads, SSB_CTAS_PER_SM) sor_kwave_tma(con
         else
             consume_item_flat<1, false, V>(a, L, G, ft, sptr(smem), bars.fullM, bars.emptyM, bars.fullK, bars.emptyK,
                                            ms, mph, s0, ph0, it, a.U[bout][1], nullptr, nullptr, r2);
-        const long long canon = ((long long)(it.l - 1) * K.nkc + chunk(it)) * G.njg + c.jg;
+        const long long canon = ((long long)(it.l - 1) * K.nkc + chunk(it)) * G.njg + rgroup(it);
         if (lane == 0)
 #pragma unroll
             for (int k = 0; k < V; ++k) a.part[n & 3][C][canon * kWarps + warp + k * NW] = r2[k];
@@ -1438,16 +1452,24 @@ void launch_sor_wave(cudaStream_t s, const SorArgs& a, bool heat) {
     SSB_LAUNCHED();
 }
 
-bool kwave_supported(const Layout& L) {
-    // whole-row flat items, one slab; a plane of the whole grid (all i, j, l; ~60 B per
-    // doxel) must leave L2 room for the ~3 planes the wavefront keeps live
+// u rows live in L2 between a chunk's first red read and its last black read: about
+// LAG + 2 chunks of (red-new + black-old) = 8 B per doxel of a chunk (the coefficient /
+// rhs streams are evict_first).  A chunk is kKwP planes of every (j, l) (k-wavefront) or
+// R rows of every (k, l) (j-wavefront); the smaller one is used
+static double kwave_chunk_bytes(const Layout& L, const Geo& G, int axis_j) {
+    return axis_j ? (double)G.R * L.n1 * L.n3 * L.n4 * 8.0 : (double)kKwP * L.n1 * L.n2 * L.n4 * 8.0;
+}
+int kwave_axis_j(const Layout& L) {
+    const int forced = std::getenv("SSB_KWAVE_AXIS") ? std::atoi(std::getenv("SSB_KWAVE_AXIS")) : -1;
+    if (forced >= 0) return forced;
     const Geo G = make_geo(L);
-    // u rows live in L2 between a chunk's first red read and its last black read: about
-    // LAG + 2 chunks of (red-new + black-old) = 8 B per doxel of a plane (the coefficient /
-    // rhs streams are evict_first)
-    const double plane_u = (double)L.n1 * L.n2 * L.n4 * 8.0;
+    return kwave_chunk_bytes(L, G, 1) < kwave_chunk_bytes(L, G, 0) ? 1 : 0;
+}
+bool kwave_supported(const Layout& L) {
+    // whole-row flat items, one slab; the live chunks must leave L2 room
+    const Geo G = make_geo(L);
     return tma_pass_supported(L) && !G.wpr && !G.S && L.glo && L.ghi && kwave_smem(L) <= 110u * 1024u &&
-           (kKwLag + 2.0) * kKwP * plane_u <= SSB_KWAVE_L2MB * 1024.0 * 1024;
+           (kKwLag + 2.0) * kwave_chunk_bytes(L, G, kwave_axis_j(L)) <= SSB_KWAVE_L2MB * 1024.0 * 1024;
 }
 size_t kwave_flags(const Layout& L) {
     const Geo G = make_geo(L);
@@ -1465,7 +1487,7 @@ int kwave_bps(const Layout& L) {
 
 void launch_sor_kwave(cudaStream_t s, const SorArgs& a) {
     const Geo G = make_geo(a.L);
-    const KwGeo K = make_kwgeo(a.L, G);
+    const KwGeo K = make_kwgeo(a.L, G, a.kwj);
     const size_t smem = kwave_smem(a.L);
     static size_t last_smem = 0;
     static int blocks = 0;

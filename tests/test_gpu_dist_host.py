@@ -91,7 +91,10 @@ def test_distributed_domain_over_host_transport(gpu, world):
     for r in range(world):
         d = out[r][1]
         assert [x["iterations"] for x in d] == [x["iterations"] for x in ref_diags]
-        assert [x["residual"] for x in d] == [x["residual"] for x in ref_diags]  # same sums, same order
+        # the single domain runs the resident kernel on this small grid, the slabs the TMA
+        # two-pass: identical iterates; the residual's partial sums are formed differently
+        assert [x["residual"] for x in d] == pytest.approx([x["residual"] for x in ref_diags], rel=1e-12)
+        assert [x["tol"] for x in d] == [x["tol"] for x in ref_diags]
         assert [x["umin"] for x in d] == [x["umin"] for x in ref_diags]
         assert [x["umax"] for x in d] == [x["umax"] for x in ref_diags]
         # the timed (non-profiling) solves recorded their exchanges: 2 per SOR iteration

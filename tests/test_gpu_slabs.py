@@ -273,7 +273,10 @@ def test_step_host_matches_device_steps(gpu, n_slabs, pinned):
                 h_in, h_out = h_out, h_in
             db = b.step_fixed(fixed) if fixed else b.step()
             want = b.get_u()[inner]
-            assert da == db, n
+            # the single-slab session runs the resident kernel on this small grid, the slab
+            # group the TMA two-pass: same iterates, residual sums in a different order
+            assert [da[k] for k in ("iterations", "umin", "umax")] == [db[k] for k in ("iterations", "umin", "umax")], n
+            assert da["residual"] == pytest.approx(db["residual"], rel=1e-12) and da["tol"] == db["tol"], n
             assert np.array_equal(got.view(np.uint64), np.ascontiguousarray(want).view(np.uint64)), n
         # the interior copies alone
         a.set_u_interior(want * 0.5)
