@@ -147,6 +147,9 @@ def make_workload(workloads, ssd, config, rank, world):
     if config == "config3" and world < 2:
         # 2.1e9 doxels x ~130 B of device state = 280 GB: more than one B200 (BASELINE: 2/4/8 GPUs)
         raise SystemExit("config3 needs >= 2 GPUs (280 GB of device state)")
+    if config == "tiny":  # bench-path tests only (6 frames per rank)
+        lb, cnt = ssd.partition(6 * world, world)[rank]
+        return workloads.tiny(world, planes=(lb - 1, lb + cnt) if world > 1 else None)
     n4 = {"config2": 32, "config3": 64, "config4": 16 * world}[config]
     lb, cnt = ssd.partition(n4, world)[rank]
     planes = (lb - 1, lb + cnt) if world > 1 else None
@@ -249,7 +252,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="config4", choices=["config0", "config1", "config2", "config3", "config4"])
+    ap.add_argument("--config", default="config4", choices=["config0", "config1", "config2", "config3", "config4", "tiny"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--loop-mode", type=int, default=1)
     args = ap.parse_args()
@@ -264,16 +267,24 @@ def main():
     from paper_2111_11866_b200 import dist as ssd
 
     rank, world, local = env_rank()
+    # SUBSURF_DIST_TRANSPORT=host: the ranks exchange through the host (gloo + dist.HostComm),
+    # so several ranks may share one GPU -- a functional test of this multi-rank path where
+    # only one GPU exists, never a scaling measurement
+    host_tr = os.environ.get("SUBSURF_DIST_TRANSPORT") == "host"
+    local = local % max(1, torch.cuda.device_count()) if host_tr else local
     torch.cuda.set_device(local)
     uid = None
     force_dist = os.environ.get("SUBSURF_FORCE_DIST") == "1"  # exercise the NCCL path at N=1
     dist_init = world > 1 or force_dist
     if dist_init:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if host_tr:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         # each rank builds only its slab (owned planes + one halo/ghost plane per side)
         wl = make_workload(workloads, ssd, args.config, rank, world)
-        uid = ssd.broadcast_uid(ss.nccl_unique_id() if rank == 0 else None)
+        uid = ssd.HostComm() if host_tr else ssd.broadcast_uid(ss.nccl_unique_id() if rank == 0 else None)
     else:
         wl = make_workload(workloads, ssd, args.config, 0, 1)
     fixed = wl.notes.get("fixed_sweeps")
@@ -297,7 +308,7 @@ def main():
             sess.step_nodiag()
 
     def max_over_ranks(vals):
-        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        t = torch.tensor(vals, dtype=torch.float64, device="cpu" if host_tr else "cuda")
         if world > 1:
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return [float(v) for v in t.tolist()]
@@ -390,7 +401,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(wl, args.config, world),
-            "parallelism": f"t-slabs x{world} (NCCL halo exchange per colour pass)" if world > 1 else "1 GPU",
+            "parallelism": (f"t-slabs x{world} (" + ("host-staged gloo exchange, ranks sharing a GPU: "
+                                                     "functional test, not a scaling number" if host_tr else
+                                                     "NCCL halo exchange per colour pass") + ")") if world > 1 else "1 GPU",
             "sweeps_timed": int(sweeps),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n_owned * world,
                     "d2h_bytes_per_step": 8 * n_owned * world,

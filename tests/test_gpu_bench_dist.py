@@ -1,0 +1,39 @@
+"""bench.py's multi-rank path (torchrun, N = 2 and 3) on one GPU: the ranks' halo
+exchanges go through the host (SUBSURF_DIST_TRANSPORT=host -> gloo + dist.HostComm),
+so the path runs -- per-rank slab workloads, max-over-ranks timing, the halo report
+of the timed run, one JSON line from rank 0 -- without a second GPU.  A functional
+test only: ranks sharing a GPU measure nothing about scaling."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_bench_multirank_over_host_transport(gpu, n):
+    env = dict(os.environ, SUBSURF_DIST_TRANSPORT="host")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", str(n),
+           "--config", "tiny", "--steps", "2", "--warmup", "3", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 only
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == n and d["value"] > 0 and d["config"]["dims"] == [24, 20, 12, 6 * n]
+    assert d["halo"]["exchanges_timed"] > 0 and d["halo"]["exchange_ms"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 8 * 24 * 20 * 12 * 6 * n

@@ -350,3 +350,30 @@ def test_segment_step_noconvergence(gpu, oracle, kernel):
             s.step()
     assert e.value.iterations == 9
     assert e.value.last_residual > 0
+
+
+@pytest.mark.parametrize("k", [5, 12, 23])
+def test_stopping_tie_at_the_references_own_residual(gpu, ref, k):
+    """the stopping residual is a sum of squares in a different order than the
+    reference's (256-lane trees of per-slice partials vs its sequential sweep,
+    solver.cpp:306-312, :357-359), so it can differ from the reference's in the last bits.
+    With sor_tol set to the reference's own residual after k iterations the reference stops
+    at k (res <= tol); this documents how the GPU decides the tie: at k when its residual is
+    not above the tolerance, else one iteration later -- and the residuals agree to 1e-12."""
+    dims = (9, 7, 6, 5)
+    g = gpu.Grid.make(dims, 0.125)
+    og = cs.grid(dims, 0.125)
+    u = cs.rand_field(dims, 40 + k)
+    st, off, _, _ = ref.assemble_step(og, u, None, 0.2, 1e-3)
+    st, _, it, r_k = ref.redblack_sor(og, off, u, u, 1.4, 1e-300, k)
+    assert st == oracle_noconv() and it == k
+    st, u_ref, it_ref, res_ref = ref.redblack_sor(og, off, u, u, 1.4, r_k, 10 * k)
+    assert st == 0 and it_ref == k and res_ref == r_k  # the reference: res <= tol at k
+    with pytest.raises(gpu.SolverError) as e:  # the GPU's own residual after exactly k sweeps
+        gpu.redblack_sor(off, u, u, 1.4, 1e-300, k, g)
+    r_gpu = e.value.last_residual
+    assert r_gpu == pytest.approx(r_k, rel=1e-12)
+    r = gpu.redblack_sor(off, u, u, 1.4, r_k, 10 * k, g)
+    assert r.iterations == (k if r_gpu <= r_k else k + 1)
+    if r.iterations == k:
+        assert_bits(r.u, u_ref, "tie decided at k: the reference's iterate")

@@ -290,5 +290,18 @@ def small(dims=(16, 12, 10, 8), seed=7) -> Workload:
     return Workload(f"small {dims}", dims, h, image, u0, rows, _base_params(h, 3, rescale_radius=4.0), 3)
 
 
+def tiny(gpus: int = 1, planes=None) -> Workload:
+    """A small weak-scaled grid (24x20x12 x 6 frames per GPU, config-0 parameters) for
+    exercising bench.py's multi-rank path in tests; planes as in config1."""
+    dims = (24, 20, 12, 6 * gpus)
+    wl = small(dims, seed=17)
+    wl.name = f"tiny: 24x20x12x{6 * gpus} ball (bench-path test)"
+    if planes is not None:
+        p0, p1 = planes
+        wl.image = wl.image[p0:p1 + 1].copy()
+        wl.u0 = wl.u0[p0:p1 + 1].copy()
+    return wl
+
+
 CONFIGS = {"config0": config0, "config1": config1, "config2": config2, "config3": config3,
-           "config4": config4}
+           "config4": config4, "tiny": tiny}
