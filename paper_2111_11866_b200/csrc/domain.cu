@@ -898,8 +898,9 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
             SSB_CUDA(cudaEventElapsedTime(&ms, l0, l1));
             prof.loop_ms += ms;
             // passes run: red 1..it+1, black 1..it (+1 when the finalize sits in the black pass)
+            // (a fixed-sweep solve's last black pass carries only the decision: not counted)
             prof.loop_passes += a[0].wave == 2 ? 2LL * (st_host->iterations + 1)  // k-wavefront bodies
-                                               : 2LL * st_host->iterations + 1 + (a[0].fuse_final ? 1 : 0);
+                                               : 2LL * st_host->iterations + 1 + (a[0].fuse_final && !fixed ? 1 : 0);
         }
         const int bodies = wave ? st_host->iterations / WI + 1 : st_host->iterations + 1;
         const int U = graph_unroll();

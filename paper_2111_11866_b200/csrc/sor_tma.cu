@@ -794,7 +794,10 @@ __global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_
     const Geo G = make_geo(L, a.tile2d != 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nl = (a.l_hi - a.l_lo) / a.l_step + 1;  // slices l_lo, l_lo + l_step, .. l_hi
-    const long long n_items = (long long)G.nsg * G.njg * G.nkc * nl;
+    // fixed-sweep solves know their end: the black pass after the last iteration (it only
+    // carries the head's decision of that iteration) updates nothing
+    const bool idle = C == 1 && *(volatile const int*)&st->fixed && n > *(volatile const int*)&st->max_iter;
+    const long long n_items = idle ? 0 : (long long)G.nsg * G.njg * G.nkc * nl;
     // snake order: black passes walk the items backwards, so each pass starts on
     // the rows the previous pass touched last (still in L2)
     const bool rev = C == 1 && a.snake;

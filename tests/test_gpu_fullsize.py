@@ -83,3 +83,13 @@ def test_wide_rows_kernels_agree(gpu):
     for key, (its, u) in res.items():
         assert its == its0, key
         assert np.array_equal(u.view(np.uint64), u0.view(np.uint64)), key
+    # and against the unmodified reference (oracle/_ref, one worker per frame)
+    from oracle import oracle_py as op
+    if op.ref_available():
+        R = op.ref()
+        po = op.seg_params(tau=h, epsilon=1e-3, omega=1.4, sor_rel_tol=1e-8, n_steps=2, sigma=np.sqrt(2) * h,
+                           K=500.0, delta=0.5, vartheta=0.5, rescale_radius=8.0)
+        st, uref, info = R.segment(op.Grid.make(dims, h), img, rows, po, None, dims[3])
+        assert st == 0
+        assert [d["iterations"] for d in info["diags"]] == its0
+        assert np.array_equal(u0.view(np.uint64), uref.view(np.uint64))

@@ -377,3 +377,50 @@ def test_stopping_tie_at_the_references_own_residual(gpu, ref, k):
     assert r.iterations == (k if r_gpu <= r_k else k + 1)
     if r.iterations == k:
         assert_bits(r.u, u_ref, "tie decided at k: the reference's iterate")
+
+
+@pytest.mark.parametrize("mode", ["step", "step_fixed", "fixed_sweeps", "step_host"])
+def test_session_nonfinite_is_numerical_error(gpu, mode):
+    """assemble_step's NumericalError (solver.cpp:71-75) from every session step flavour --
+    decided on the device (sor_init reads the assembly flag), no host sync in between; the
+    session's u is left as it was (fixed_sweeps used to skip the check)."""
+    import workloads
+    wl = workloads.small((12, 10, 8, 6), seed=3)
+    g = gpu.Grid.make(wl.dims, wl.h)
+    with gpu.Session(g) as s:
+        s.prepare(wl.image, wl.rows, gpu.seg_params(**{**wl.params, "n_steps": 3}), wl.u0)
+        u = s.get_u()
+        u[3, 4, 5, 6] = np.nan
+        s.set_u(u)
+        with pytest.raises(gpu.NumericalError):
+            if mode == "step":
+                s.step()
+            elif mode == "step_fixed":
+                s.step_fixed(5)
+            elif mode == "fixed_sweeps":
+                s.fixed_sweeps(5)
+            else:
+                s.step_host(np.ascontiguousarray(u[1:-1, 1:-1, 1:-1, 1:-1]), None, 0)
+        after = s.get_u()
+        assert np.array_equal(np.isnan(after), np.isnan(u)) and np.array_equal(after[~np.isnan(u)], u[~np.isnan(u)])
+
+
+def test_explicit_zero_rescale_radius(gpu, oracle):
+    """rescale_radius = 0 set explicitly is the reference's r = 0 ball (<= 1 doxel: a no-op,
+    seedinit.cpp:73-88), not "each row's own radius" (ADVICE r01); NaN / None is std::nullopt."""
+    from oracle import oracle_py as op
+    dims, h = (10, 8, 7, 6), 0.125
+    g = gpu.Grid.make(dims, h)
+    og = cs.grid(dims, h)
+    u = cs.rand_field(dims, 8)
+    rows = [(f, 4.0, 3.0, 3.0, 2.5) for f in range(dims[3])]
+    assert_bits(gpu.local_rescale(u, rows, g, 0.0), u, "r = 0: no-op")
+    assert_bits(gpu.local_rescale(u, rows, g, None), oracle.local_rescale(og, u, rows, None)[1], "per row")
+    img = cs.f32_image(dims, 9)
+    for rr in (0.0, None):
+        kw = dict(tau=h, epsilon=1e-3, omega=1.4, sor_tol=1e-9, n_steps=2, sigma=0.17, K=200.0, delta=0.5,
+                  vartheta=0.5, rescale_radius=rr)
+        u_g, _ = gpu.segment(img, rows, gpu.seg_params(**kw), g)
+        st, u_o, _ = oracle.segment(op.Grid.make(dims, h), img, rows, op.seg_params(**kw))
+        assert st == 0
+        assert_bits(u_g, u_o, f"segment rescale_radius={rr}")
