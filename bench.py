@@ -100,7 +100,7 @@ class ClockSampler:
 
     def summary(self):
         lines = self.lines or getattr(self, "pre", [])
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -111,13 +111,17 @@ class ClockSampler:
                 mx = float(parts[1])
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[7]))
+            except ValueError:
+                pass
             for n, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w": statistics.median(pw) if pw else None}
 
 
 def workload_config(wl, config: str, world: int) -> dict:
