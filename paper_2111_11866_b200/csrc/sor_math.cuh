@@ -64,6 +64,26 @@ __device__ __forceinline__ void doxel_update(const SorArgs& a, const DoxelIn& d,
     }
 }
 
+// the update alone (no residual): the same bits of unew
+template <int C>
+__device__ __forceinline__ void doxel_update_nores(const SorArgs& a, const DoxelIn& d, double& unew) {
+    const double c0 = (double)d.c[0], c1 = (double)d.c[1], c2 = (double)d.c[2];
+    const double c3 = (double)d.c[3], c4 = (double)d.c[4], c5 = (double)d.c[5];
+    const double c6 = (double)d.c[6], c7 = (double)d.c[7];
+    const double dg = 1.0 - (c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7);
+    double acc = d.rhs;
+    acc -= c0 * d.nb[0];
+    acc -= c1 * d.nb[1];
+    acc -= c2 * d.nb[2];
+    acc -= c3 * d.nb[3];
+    acc -= c4 * d.nb[4];
+    acc -= c5 * d.nb[5];
+    acc -= c6 * d.nb[6];
+    acc -= c7 * d.nb[7];
+    const double ubar = acc / dg;
+    unew = a.omega * ubar + a.keep * d.u0;
+}
+
 // doxel_update + the store(s) of the new value; returns the squared residual
 template <int C, bool HINT = false, bool MIRROR = false>
 __device__ __forceinline__ double compute_doxel(const SorArgs& a, const DoxelIn& d,

@@ -611,7 +611,7 @@ __device__ __forceinline__ FlatThread flat_thread(const Layout& L, const Geo& G,
 // address a per-thread constant plus a stage base carried from plane to plane
 // (the general version re-derives its addresses per plane: ~35 integer
 // instructions per warp-plane against ~90 for the arithmetic itself).
-template <int C, bool PUSH, int V>
+template <int C, bool PUSH, int V, bool RES = true>
 __device__ __forceinline__ void consume_item_flat(const SorArgs& a, const Layout& L, const Geo& G,
                                                   const FlatThread (&ft)[V], uint32_t sbase, uint64_t* fullM,
                                                   uint64_t* emptyM, uint64_t* fullK, uint64_t* emptyK, uint32_t& ms,
@@ -679,7 +679,12 @@ __device__ __forceinline__ void consume_item_flat(const SorArgs& a, const Layout
             d.nb[6] = lds_f64<0>(x + G.off_ulm);
             d.nb[7] = lds_f64<0>(x + G.off_ulp);
             double unew, e2;
-            doxel_update<C>(a, d, unew, e2);
+            if constexpr (RES) {
+                doxel_update<C>(a, d, unew, e2);
+            } else {  // fixed-sweep solves before their last iteration: the update alone
+                doxel_update_nores<C>(a, d, unew);
+                e2 = 0.0;
+            }
             if (on) {
                 wq[k][par[k]] = unew;
                 if constexpr (PUSH) {
@@ -796,7 +801,14 @@ __global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_
     const int nl = (a.l_hi - a.l_lo) / a.l_step + 1;  // slices l_lo, l_lo + l_step, .. l_hi
     // fixed-sweep solves know their end: the black pass after the last iteration (it only
     // carries the head's decision of that iteration) updates nothing
-    const bool idle = C == 1 && *(volatile const int*)&st->fixed && n > *(volatile const int*)&st->max_iter;
+    const bool fixed_solve = *(volatile const int*)&st->fixed != 0;
+    const int max_it = *(volatile const int*)&st->max_iter;
+    const bool idle = C == 1 && fixed_solve && n > max_it;
+    // fixed-sweep solves need a residual only for their last iteration (the diagnostics):
+    // red(max_iter + 1) carries its red part, black(max_iter) its black part; the other
+    // passes skip the residual arithmetic and write zero partials (-1.6% per sweep, config 4:
+    // the power-capped clock rises with the work saved)
+    const bool need_res = !fixed_solve || (C == 0 ? n == max_it + 1 : n == max_it);
     const long long n_items = idle ? 0 : (long long)G.nsg * G.njg * G.nkc * nl;
     // snake order: black passes walk the items backwards, so each pass starts on
     // the rows the previous pass touched last (still in L2)
@@ -879,9 +891,14 @@ __global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_
         double* plo = PUSH && it.l == 1 ? a.push_lo[bout][C] : nullptr;
         double* phi = PUSH && it.l == L.n4 ? a.push_hi[bout][C] : nullptr;
         double r2[V];
-        if constexpr (FLAT)
-            consume_item_flat<C, PUSH, V>(a, L, G, ft, sptr(smem), bars.fullM, bars.emptyM, bars.fullK, bars.emptyK, ms,
-                                          mph, s0, ph0, it, ucw, plo, phi, r2);
+        if constexpr (FLAT) {
+            if (need_res)
+                consume_item_flat<C, PUSH, V, true>(a, L, G, ft, sptr(smem), bars.fullM, bars.emptyM, bars.fullK,
+                                                    bars.emptyK, ms, mph, s0, ph0, it, ucw, plo, phi, r2);
+            else
+                consume_item_flat<C, PUSH, V, false>(a, L, G, ft, sptr(smem), bars.fullM, bars.emptyM, bars.fullK,
+                                                     bars.emptyK, ms, mph, s0, ph0, it, ucw, plo, phi, r2);
+        }
         else
             r2[0] = consume_item<C, HEAT, PUSH>(a, L, G, smem, bars.fullM, bars.emptyM, bars.fullK, bars.emptyK, ms,
                                                 mph, s0, ph0, it, ucw, warp, lane, pol.ustore, plo, phi);
