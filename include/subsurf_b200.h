@@ -282,6 +282,10 @@ typedef struct {
     long long halo_n;
 } ss_profile;
 SS_API ss_status ss_session_profile(ss_session* s, ss_profile* out);
+/* self-test of the assembly kernel's rsqrt tail (assemble_tile.cu): the largest relative
+ * error of the hardware rsqrt.approx.f64 over every normal positive input high word; the
+ * tail's exactness argument needs it below 2^-11 (two Newton steps then leave a few ulps) */
+SS_API ss_status ss_selftest_rsqrt(double* eps0);
 /* algorithmic bytes of one SOR colour pass: 28 B x interior doxels (SURVEY 8(d):
  * 56 B per doxel per red+black sweep) */
 SS_API double ss_sor_pass_bytes(const ss_grid* g);

@@ -215,6 +215,7 @@ def library() -> C.CDLL:
     sig("ss_session_get_mask", [C.c_void_p, C.c_double, C.POINTER(C.c_uint8)])
     sig("ss_session_fixed_sweeps", [C.c_void_p, C.c_int, _D])
     sig("ss_session_step_fixed", [C.c_void_p, C.c_int, C.POINTER(StepDiag)])
+    sig("ss_selftest_rsqrt", [_D])
     sig("ss_session_step_host", [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(StepDiag)])
     sig("ss_session_set_u_interior", [C.c_void_p, C.c_void_p])
     sig("ss_session_get_u_interior", [C.c_void_p, C.c_void_p])

@@ -25,6 +25,10 @@
 // exponent lies in the normal float range, float(-q') == float(-q) exactly;
 // otherwise (probability ~2e-6 per face) the doxel is recomputed with the
 // reference's exact sequence.  So every coefficient is the reference's bits.
+// The error budget rests on the hardware approximation's accuracy: measured
+// exhaustively over every normal input high word (ss_selftest_rsqrt, a GPU test),
+// its relative error is eps0 = 9.3e-7 (2^-20.0); one Newton step leaves
+// 1.5 eps0^2 ~ 2^-39.4, the second the rounding of its own arithmetic (~2 ulps).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -230,6 +234,27 @@ __device__ __forceinline__ bool near_midpoint(double q) {
 // G of a tile (both colours) into L2 ahead of the tile: 3D view of a colour's G array
 // [planes][rows][W * 8 doubles], box 17 slots x 8 faces, 8 rows, 4 planes
 constexpr int kGBoxX = (kTI / 2 + 1) * 8;
+// Self-test of the assumption behind the rsqrt tail: the hardware approximation
+// (rsqrt.approx.ftz.f64 = MUFU.RSQ64H, a function of the input's high word) has a small
+// relative error eps0, so that two Newton steps bring it to a few ulps.  Exhaustive over
+// every normal positive high word, at both ends of its low word; eps0 = max |1 - x y^2| / 2.
+__global__ void rsqrt_bound_kernel(unsigned long long* worst) {
+    const unsigned total = 2046u << 20;  // exponents 1 .. 2046, 20 mantissa bits of the high word
+    double mx = 0.0;
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const unsigned hi = ((t >> 20) + 1u) << 20 | (t & 0xFFFFFu);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const double x = __hiloint2double((int)hi, q ? -1 : 0);
+            double y;
+            asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+            const double e = fabs(__fma_rn(-__dmul_rn(x, y), y, 1.0));
+            mx = fmax(mx, e);
+        }
+    }
+    atomicMax(worst, (unsigned long long)__double_as_longlong(mx));  // non-negative: order = bits
+}
+
 struct AsmTileArgs {
     Maps<1> maps;
     CUtensorMap gmap[2];
@@ -520,6 +545,20 @@ unsigned grid_for(K kernel, size_t smem, long long tiles) {
 }  // namespace
 
 static bool launch_tile(cudaStream_t s, AsmTileArgs& p, bool pow2);
+
+double rsqrt_approx_bound() {
+    unsigned long long* d = nullptr;
+    SSB_CUDA(cudaMalloc(&d, sizeof *d));
+    SSB_CUDA(cudaMemset(d, 0, sizeof *d));
+    rsqrt_bound_kernel<<<1184, 256>>>(d);
+    SSB_LAUNCHED();
+    unsigned long long h = 0;
+    SSB_CUDA(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));
+    SSB_CUDA(cudaFree(d));
+    double e;
+    std::memcpy(&e, &h, sizeof e);
+    return 0.5 * e;  // 1 - x y^2 = -(2 eps + eps^2) for y = (1 + eps) / sqrt(x)
+}
 
 bool assemble_tile_supported(const Layout& L) {
     // TMA box bounds / alignment hold for every grid (W even); off by SSB_ASM_TILE=0

@@ -673,6 +673,14 @@ ss_status ss_session_get_u_interior(ss_session* s, double* u) {
     });
 }
 
+ss_status ss_selftest_rsqrt(double* eps0) {
+    return guard([&] {
+        require(eps0 != nullptr, "null output");
+        require_device();
+        *eps0 = rsqrt_approx_bound();
+    });
+}
+
 ss_status ss_session_eoc_row(ss_session* s, int n, double omega, double sor_tol, int sor_max_iter, double* err,
                              long long* sweeps) {
     return guard([&] {

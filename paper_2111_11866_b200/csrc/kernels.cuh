@@ -186,6 +186,7 @@ struct EdgeArgs {
 void launch_face_coefficients(cudaStream_t s, const EdgeArgs& a);
 // TMA-staged tile kernels (assemble_tile.cu); false = not launched (no tensor-map encoder)
 bool assemble_tile_supported(const Layout& L);
+double rsqrt_approx_bound();  // self-test: max relative error of rsqrt.approx.f64 (exhaustive)
 bool launch_assemble_tile(cudaStream_t s, const AsmArgs& a, bool pow2);
 // the same restricted to slices [l_lo, l_hi] (the upload-overlapped assembly of step_host)
 bool launch_assemble_tile_range(cudaStream_t s, const AsmArgs& a, int l_lo, int l_hi);

@@ -424,3 +424,16 @@ def test_explicit_zero_rescale_radius(gpu, oracle):
         st, u_o, _ = oracle.segment(op.Grid.make(dims, h), img, rows, op.seg_params(**kw))
         assert st == 0
         assert_bits(u_g, u_o, f"segment rescale_radius={rr}")
+
+
+def test_rsqrt_approximation_bound(gpu):
+    """The assembly tail's exactness argument (assemble_tile.cu): q' from rsqrt.approx.f64 +
+    two Newton steps lies within ~20 double ulps of the reference's quotient, and a float
+    rounding decision is trusted only >= 512 ulps from a midpoint.  That needs the hardware
+    approximation's relative error eps0 well below 2^-11 -- checked exhaustively here over every
+    normal positive input high word (the only part MUFU.RSQ64H reads)."""
+    import ctypes as C
+    e = C.c_double(0.0)
+    assert gpu.library().ss_selftest_rsqrt(C.byref(e)) == 0
+    assert 0.0 < e.value < 2.0 ** -11, e.value
+    print("rsqrt.approx.f64 max relative error", e.value)
