@@ -3,6 +3,7 @@ that exchange halo planes and all-gather per-slice residuals must give the
 single-slab result bit for bit (same iterates, same iteration counts) -- the
 property the multi-GPU NCCL path relies on."""
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -281,3 +282,30 @@ def test_step_host_matches_device_steps(gpu, n_slabs, pinned):
         # the interior copies alone
         a.set_u_interior(want * 0.5)
         assert np.array_equal(a.get_u_interior(), want * 0.5)
+
+
+@pytest.mark.parametrize("n_slabs", [1, 3])
+def test_fixed_sweep_steps_vs_oracle(gpu, oracle, n_slabs):
+    """ss_session_step_fixed (BASELINE config 4's time step) on 1 and 3 slabs against the C
+    restatement's no-early-stop loop, which tests/test_fixed_sweeps_cpu.py pins to the
+    reference's own fixed-sweep iterate: u bit for bit, the last residual to 1e-12."""
+    import math
+    import workloads
+    from oracle import oracle_py as op
+    sys_path_tests = os.path.dirname(os.path.abspath(__file__))
+    if sys_path_tests not in sys.path:
+        sys.path.insert(0, sys_path_tests)
+    from test_fixed_sweeps_cpu import oracle_fixed_steps
+    wl = workloads.small((17, 11, 9, 7), seed=5)
+    og = op.Grid.make(wl.dims, wl.h)
+    p = op.seg_params(**{**wl.params, "n_steps": 2, "sor_rel_tol": 0.0})
+    u_or, res = oracle_fixed_steps(oracle, og, wl, p, 2, 9)
+    g = gpu.Grid.make(wl.dims, wl.h)
+    with gpu.Session(g, n_slabs=n_slabs) as s:
+        s.prepare(wl.image, wl.rows, gpu.seg_params(**{**wl.params, "n_steps": 2, "sor_rel_tol": 0.0}), wl.u0)
+        d = [s.step_fixed(9) for _ in range(2)]
+        u = s.get_u()
+    assert [x["iterations"] for x in d] == [9, 9]
+    assert np.array_equal(u.view(np.uint64), u_or.view(np.uint64))
+    for x, r in zip(d, res):
+        assert math.isclose(x["residual"], r, rel_tol=1e-12)
