@@ -269,6 +269,11 @@ __device__ __forceinline__ void prefetch_G(const AsmTileArgs& p, const Tile& x) 
     tensor3_prefetch(&p.gmap[1], x.b * (kTI / 2) * 8, x.jb * kTJ + 1, z);
 }
 
+#ifndef SSB_ASMT_L1PREF
+#define SSB_ASMT_L1PREF 0  // G pulled into L1 one plane ahead: measured neutral (0.587 vs 0.580 ms config 1)
+#endif
+constexpr bool GPREF_L1 = SSB_ASMT_L1PREF != 0;
+
 template <bool POW2, int STAGES, int MINB>
 __global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __grid_constant__ AsmTileArgs p) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -306,8 +311,26 @@ __global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __
         const int j = x.jb * kTJ + 1 + ty;
         // this thread's bases at plane kk = 0 of the brick (row ty, slot s)
         const uint32_t rb = buf + (uint32_t)(ty * kSS + s) * 8;
+        // G record (64 B, one cache line's half) of this thread's doxel at plane kk: pulled
+        // into L1 one plane ahead (ptxas would otherwise sink the loads next to their use,
+        // after the face gradients, and expose their latency)
+        auto g_rec = [&](int kk) -> const double* {
+            const int k = x.kc * kTK + 1 + kk;
+            const int e = (c + 1 + j + k + x.l + L.lpar) & 1;
+            const int i = x.b * kTI + 1 + 2 * s + e;
+            if (!a.G[c] || kk >= kTK || j > L.n2 || k > L.n3 || i > L.n1) return nullptr;
+            return a.G[c] + (L.row(j, k, x.l) * L.W + (i >> 1)) * 8;
+        };
+        if constexpr (GPREF_L1) {
+            const double* g0 = g_rec(0);
+            if (g0) asm volatile("prefetch.global.L1 [%0];" ::"l"(g0));
+        }
 #pragma unroll 1
         for (int kk = 0; kk < kTK; ++kk) {
+            if constexpr (GPREF_L1) {
+                const double* gn = g_rec(kk + 1);
+                if (gn) asm volatile("prefetch.global.L1 [%0];" ::"l"(gn));
+            }
             const int k = x.kc * kTK + 1 + kk;
             const int e = (c + 1 + j + k + x.l + L.lpar) & 1;
             const int i = x.b * kTI + 1 + 2 * s + e;
@@ -325,7 +348,7 @@ __global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __
                 const double2* gp = reinterpret_cast<const double2*>(a.G[c] + pg * 8);
 #pragma unroll
                 for (int h2 = 0; h2 < 4; ++h2) {
-                    const double2 v = __ldcs(gp + h2);
+                    const double2 v = GPREF_L1 ? __ldg(gp + h2) : __ldcs(gp + h2);
                     gv[2 * h2] = v.x;
                     gv[2 * h2 + 1] = v.y;
                 }
