@@ -38,7 +38,7 @@ def sha(a) -> str:
 def build(name):
     import workloads
     return {"config0": workloads.config0, "config1": workloads.config1, "config2": workloads.config2,
-            "config4": lambda: workloads.config4(1)}[name]()
+            "config4": lambda: workloads.config4(1), "config3s": lambda: workloads.config3_slab(4)}[name]()
 
 
 @pytest.mark.parametrize("name", sorted(PINS))

@@ -309,3 +309,29 @@ def test_fixed_sweep_steps_vs_oracle(gpu, oracle, n_slabs):
     assert np.array_equal(u.view(np.uint64), u_or.view(np.uint64))
     for x, r in zip(d, res):
         assert math.isclose(x["residual"], r, rel_tol=1e-12)
+
+
+def test_kernel_switch_within_a_session(gpu):
+    """ss_session_set_kernel between solves of ONE session (the captured CUDA
+    graph was keyed without the item shape, so a switch between the whole-row and the
+    2D-tiled TMA passes could replay the old graph): every solve runs -- and reports -- the
+    kernel asked for, and all give the same iterate."""
+    import workloads
+    wl = workloads.small((40, 12, 10, 6), seed=9)
+    g = gpu.Grid.make(wl.dims, wl.h)
+    p = gpu.seg_params(**{**wl.params, "n_steps": 8, "sor_rel_tol": 1e-8})
+    outs = {}
+    with gpu.Session(g) as s:
+        s.prepare(wl.image, wl.rows, p, wl.u0)
+        u_start = s.get_u()
+        for kernel in ("tma", "tma2d", "tma", "ldg", "tma2d", "resident", "tma"):
+            s.set_u(u_start)
+            s.set_kernel(kernel)
+            d = s.step()
+            assert s.sor_kernel() == kernel
+            outs.setdefault(kernel, []).append((d["iterations"], s.get_u()))
+    its0, u0 = outs["tma"][0]
+    for kernel, runs in outs.items():
+        for its, u in runs:
+            assert its == its0, kernel
+            assert np.array_equal(u.view(np.uint64), u0.view(np.uint64)), kernel

@@ -266,6 +266,20 @@ def config3(planes=None) -> Workload:
     return _nuclei_workload("config3: 512x512x128x64 nuclei", (512, 512, 128, 64), 2000, 1003, 10, planes)
 
 
+def config3_slab(n4: int = 4) -> Workload:
+    """The first n4 frames of config 3 (512x512x128, ~2000 nuclei) as a grid of their own:
+    config 3's full-width rows and planes on one GPU (a parity case; the whole config 3
+    needs >= 2 GPUs)."""
+    wl = config3(planes=(0, n4 + 1))
+    n1, n2, n3, _ = wl.dims
+    wl.dims = (n1, n2, n3, n4)
+    wl.image[-1] = 0.0  # the slab's upper ghost plane (the 64-frame grid's frame n4 + 1 otherwise)
+    wl.u0[-1] = 0.0
+    wl.rows = [r for r in wl.rows if r[0] < n4]
+    wl.name = f"config3 slab: 512x512x128x{n4} (config 3's first {n4} frames)"
+    return wl
+
+
 def config4(gpus: int = 1, planes=None) -> Workload:
     """Weak scaling: 256x256x128 x (16 * gpus) frames, config-2 data and solver
     settings, fixed 50 SOR sweeps per time step (no early stop)."""
