@@ -1109,20 +1109,19 @@ void Domain::prepare(const double* image, const ss_center* c, int n, const ss_se
     mark("u0 + rescale");
 
     // local_threshold, heat_smooth x2, face_coefficients (solver.cpp:419-422)
-    std::vector<std::unique_ptr<DevField>> img, th, t1, t2, t3;
+    // the heat solves' three rotating outputs are the state buffers S[1..3]: unused until
+    // the first step (which overwrites their interiors; their ghosts are reset below), so
+    // prepare's peak is 2 fields above the steady state -- config 3 fits two GPUs
+    std::vector<std::unique_ptr<DevField>> img, th;
     for (Slab* s : sp) {
         img.emplace_back(new DevField);
         th.emplace_back(new DevField);
-        t1.emplace_back(new DevField);
-        t2.emplace_back(new DevField);
-        t3.emplace_back(new DevField);
         img.back()->alloc(s->L);
         th.back()->alloc(s->L);
-        t1.back()->alloc(s->L);
-        t2.back()->alloc(s->L);
-        t3.back()->alloc(s->L);
         s->upload(host_slab(image, *s), img.back()->pf());
     }
+    sync();
+    for (Slab* s : sp) s->stage.reset();  // the upload staging buffer comes back on demand
     mark("alloc + image upload");
     {
         std::vector<std::unique_ptr<BallSet>> bsets;
@@ -1162,7 +1161,8 @@ void Domain::prepare(const double* image, const ss_center* c, int n, const ss_se
     mark("local_threshold");
 
     std::vector<Triple> b1, b2;
-    for (size_t s = 0; s < sp.size(); ++s) b1.push_back({img[s]->pf(), t1[s]->pf(), t2[s]->pf(), t3[s]->pf()});
+    for (size_t s = 0; s < sp.size(); ++s)
+        b1.push_back({img[s]->pf(), sp[s]->S[1].pf(), sp[s]->S[2].pf(), sp[s]->S[3].pf()});
     const int r1 = heat_smooth(b1, p.sigma, p.smooth_steps, p.smooth_omega, p.smooth_tol, p.smooth_max_iter);
     mark("heat_smooth(I0)");
     for (size_t s = 0; s < sp.size(); ++s)
