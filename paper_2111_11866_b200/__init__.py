@@ -491,7 +491,19 @@ def eoc_row(n: int, omega: float = 1.5, sor_tol: float = 1e-8, sor_max_iter: int
 
 
 # ----------------------------------------------------------------------------- device session
+def _nccl_of_torch_first() -> None:
+    """The library dlopens "libnccl.so.2" on first NCCL use and gets whichever copy is
+    loaded already.  Import torch first (when installed) so that copy is torch's bundled
+    NCCL: were the system library loaded first under the same soname, a later
+    `import torch` would bind libtorch_cuda to it and fail on symbols the older NCCL lacks."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
+    _nccl_of_torch_first()
     buf = (C.c_uint8 * 128)()
     _check(library().ss_nccl_unique_id(buf))
     return bytes(buf)
@@ -519,6 +531,7 @@ class Session:
                 _check(library().ss_session_create_dist_host(C.byref(g), rank, world, uid.as_abi(), device,
                                                              C.byref(h)))
             else:
+                _nccl_of_torch_first()
                 ub = (C.c_uint8 * 128).from_buffer_copy(uid)
                 _check(library().ss_session_create_dist(C.byref(g), rank, world, ub, device, C.byref(h)))
         else:

@@ -1202,6 +1202,28 @@ void Domain::set_u_interior(const double* host) {
 
 void Domain::get_u_interior(double* host) {
     const long long fr = (long long)g.n1 * g.n2 * g.n3;
+    if (single() && host_pinned(host)) {  // slice chunks: unpack chunk q+1 while chunk q moves
+        Slab& x = *sp[0];
+        const int n4 = x.L.n4, C = std::min(n4, 8);
+        while ((int)up_ev.size() < C + 1) {
+            cudaEvent_t e;
+            SSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            up_ev.push_back(e);
+        }
+        double* d = x.stage_p();
+        for (int q = 0; q < C; ++q) {
+            const int a = 1 + (int)((long long)q * n4 / C), b = (int)((long long)(q + 1) * n4 / C);
+            launch_unpack_interior(stream, x.L, x.S[cur].pf(), d, a, b);
+            SSB_CUDA(cudaEventRecord(up_ev[q], stream));
+            SSB_CUDA(cudaStreamWaitEvent(h2d, up_ev[q], 0));
+            SSB_CUDA(cudaMemcpyAsync(host + (a - 1) * fr, d + (a - 1) * fr, (size_t)(b - a + 1) * fr * sizeof(double),
+                                     cudaMemcpyDeviceToHost, h2d));
+        }
+        SSB_CUDA(cudaEventRecord(up_ev[C], h2d));
+        SSB_CUDA(cudaStreamWaitEvent(stream, up_ev[C], 0));  // later users of the staging buffer
+        SSB_CUDA(cudaStreamSynchronize(h2d));
+        return;
+    }
     for (Slab* s : sp) {
         double* d = s->stage_p();
         launch_unpack_interior(stream, s->L, s->S[cur].pf(), d);

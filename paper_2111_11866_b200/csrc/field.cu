@@ -131,10 +131,12 @@ __global__ void pack_interior_kernel(const Layout L, const double* __restrict__ 
     for (int i = 1 + lane; i <= L.n1; i += 32) dst.c[(i + par) & 1][r * L.W + (i >> 1)] = src[cq * L.n1 + i - 1];
 }
 
-__global__ void unpack_interior_kernel(const Layout L, PField src, double* __restrict__ dst, long long nrows) {
-    const long long q = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+__global__ void unpack_interior_kernel(const Layout L, PField src, double* __restrict__ dst, int l_lo,
+                                       long long nrows) {
+    const long long q0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (q >= nrows) return;
+    if (q0 >= nrows) return;
+    const long long q = q0 + (long long)(l_lo - 1) * L.n2 * L.n3;  // compact row index from slice 1
     const int j = (int)(q % L.n2) + 1;
     const long long t = q / L.n2;
     const int k = (int)(t % L.n3) + 1;
@@ -369,9 +371,11 @@ void launch_pack_interior(cudaStream_t s, const Layout& L, const double* src, PF
     SSB_LAUNCHED();
 }
 
-void launch_unpack_interior(cudaStream_t s, const Layout& L, PField src, double* dst) {
-    const long long nrows = (long long)L.n2 * L.n3 * L.n4;
-    unpack_interior_kernel<<<ceil_div(nrows * 32, 256), 256, 0, s>>>(L, src, dst, nrows);
+void launch_unpack_interior(cudaStream_t s, const Layout& L, PField src, double* dst, int l_lo, int l_hi) {
+    if (l_hi < 0) l_hi = L.n4;
+    const long long nrows = (long long)L.n2 * L.n3 * (l_hi - l_lo + 1);
+    if (nrows <= 0) return;
+    unpack_interior_kernel<<<ceil_div(nrows * 32, 256), 256, 0, s>>>(L, src, dst, l_lo, nrows);
     SSB_LAUNCHED();
 }
 

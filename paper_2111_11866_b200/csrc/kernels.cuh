@@ -211,7 +211,8 @@ void launch_unpack(cudaStream_t s, const Layout& L, PField src, double* dst);
 // compact interior arrays (n1*n2*n3*n4 doubles, i fastest, no ghosts): slices [l_lo, l_hi]
 // of src (indexed from slice 1) into dst's interior / every interior doxel of src out
 void launch_pack_interior(cudaStream_t s, const Layout& L, const double* src, PField dst, int l_lo, int l_hi);
-void launch_unpack_interior(cudaStream_t s, const Layout& L, PField src, double* dst);
+void launch_unpack_interior(cudaStream_t s, const Layout& L, PField src, double* dst, int l_lo = 1,
+                            int l_hi = -1);
 void launch_fill(cudaStream_t s, const Layout& L, PField f, double v);
 void launch_set_ghosts(cudaStream_t s, const Layout& L, PField f, double v);
 // ghost doxels of src copied into dst
