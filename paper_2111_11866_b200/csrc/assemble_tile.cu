@@ -210,6 +210,47 @@ __device__ __forceinline__ double face_sq(const SStencil& S, const double* h, co
     return g[0] * g[0] + g[1] * g[1] + g[2] * g[2] + g[3] * g[3];  // edge.cpp:53-54
 }
 
+// |grad_f u|^2 / sigma, sigma = (hinv / 4)^2, on an isotropic power-of-two grid: the face
+// gradient with every power-of-two scaling pulled out of the arithmetic.  The reference's
+// g_t = (0.25 X - 0.25 Y) hinv (X, Y the two corner sums) equals 0.25 hinv RN(X - Y), the
+// normal g_n = RN(pn - p0) hinv = (hinv / 4) RN(4 (pn - p0)), and squares and the sum of the
+// four squares commute with the common factor sigma -- exactly, as long as nothing under-
+// or overflows: guaranteed when every staged value is 0 or within [2^-400, 2^400] (the
+// per-step guard, assemble_guard_kernel) and hinv within [2^-40, 2^40] (host).  8 FP64
+// instructions per face fewer than face_sq (the 0.25 and 1/h products).
+template <int F>
+__device__ __forceinline__ double face_sq_scaled(const SStencil& S, double p0) {
+    constexpr int A = F >> 1, SG = (F & 1) ? 1 : -1;
+    constexpr int ai = A == 0 ? SG : 0, aj = A == 1 ? SG : 0, ak = A == 2 ? SG : 0, al = A == 3 ? SG : 0;
+    const double pn = S.at<ai, aj, ak, al>();
+    const double p0pn = p0 + pn;
+    double d[4];
+    d[A] = 4.0 * (pn - p0);
+#define SSB_SCALED_TANGENT(T)                                                                        \
+    if constexpr (A != T) {                                                                           \
+        constexpr int ti = T == 0, tj = T == 1, tk = T == 2, tl = T == 3;                              \
+        const double X = p0pn + S.at<ti, tj, tk, tl>() + S.at<ai + ti, aj + tj, ak + tk, al + tl>();   \
+        const double Y = p0pn + S.at<-ti, -tj, -tk, -tl>() + S.at<ai - ti, aj - tj, ak - tk, al - tl>(); \
+        d[T] = X - Y;                                                                                  \
+    }
+    SSB_SCALED_TANGENT(0)
+    SSB_SCALED_TANGENT(1)
+    SSB_SCALED_TANGENT(2)
+    SSB_SCALED_TANGENT(3)
+#undef SSB_SCALED_TANGENT
+    return d[0] * d[0] + d[1] * d[1] + d[2] * d[2] + d[3] * d[3];
+}
+
+// 1/sqrt(x) with one Newton step: relative error <= 1.5 eps0^2 + rounding ~ 1.3e-12 for the
+// measured eps0 = 9.3e-7 of the hardware approximation (used only when the per-process
+// self-test confirms eps0 < 2^-19.5, see ss_selftest_rsqrt)
+__device__ __forceinline__ double rsqrt_nr1(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = __fma_rn(-__dmul_rn(x, y), y, 1.0);
+    return __fma_rn(__dmul_rn(y, 0.5), e, y);
+}
+
 // 1/sqrt(x) to ~1 ulp for normal x: hardware approximation + two Newton steps
 __device__ __forceinline__ double rsqrt_nr(double x) {
     double y;
@@ -223,12 +264,13 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 
 // float(q') is float(q) for every q within ~20 ulps of q' unless q' sits near a float
 // rounding midpoint or outside the normal float range: then take the exact path
+template <int T = 512>
 __device__ __forceinline__ bool near_midpoint(double q) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(q);
     const int low = (int)(b & 0x1FFFFFFFull);
     const int ex = (int)((b >> 52) & 0x7FF);
     const int d = low - (1 << 28);
-    return (d < 512 && d > -512) || ex < 1023 - 120 || ex > 1023 + 120;
+    return (d < T && d > -T) || ex < 1023 - 120 || ex > 1023 + 120;
 }
 
 // G of a tile (both colours) into L2 ahead of the tile: 3D view of a colour's G array
@@ -258,7 +300,9 @@ __global__ void rsqrt_bound_kernel(unsigned long long* worst) {
 struct AsmTileArgs {
     Maps<1> maps;
     CUtensorMap gmap[2];
-    int gpref;  // G maps valid
+    int gpref;          // G maps valid
+    const int* guard;   // non-null: scaled face gradients unless *guard (a value out of range)
+    double sigma;       // (hinv / 4)^2 of the isotropic power-of-two grid (scaled mode)
     AsmArgs a;
     TileGeo g;
 };
@@ -274,7 +318,7 @@ __device__ __forceinline__ void prefetch_G(const AsmTileArgs& p, const Tile& x) 
 #endif
 constexpr bool GPREF_L1 = SSB_ASMT_L1PREF != 0;
 
-template <bool POW2, int STAGES, int MINB>
+template <bool POW2, int STAGES, int MINB, bool NR1>
 __global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __grid_constant__ AsmTileArgs p) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[STAGES], empty[STAGES];
@@ -303,6 +347,9 @@ __global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __
     int stage = 0;
     uint32_t phase = 0;
     bool bad = false;
+    // scaled face gradients: the host chose them for this grid and this step's u passed the
+    // guard (uniform over the grid: one flag written before the launch)
+    const bool scaled = POW2 && p.guard && *(volatile const int*)p.guard == 0;
     for (; t < g.tiles; t += gridDim.x) {
         const Tile x = tile_of(L, g, t);
         const uint32_t buf = sbase + stage * kFieldBytes;
@@ -358,14 +405,26 @@ __global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __
             }
             const double p0 = S.at<0, 0, 0, 0>();
             double x2[8];
-            x2[0] = a.eps + face_sq<0, POW2>(S, a.h, a.hinv, p0);  // A_f^2 = eps + |grad_f u|^2
-            x2[1] = a.eps + face_sq<1, POW2>(S, a.h, a.hinv, p0);
-            x2[2] = a.eps + face_sq<2, POW2>(S, a.h, a.hinv, p0);
-            x2[3] = a.eps + face_sq<3, POW2>(S, a.h, a.hinv, p0);
-            x2[4] = a.eps + face_sq<4, POW2>(S, a.h, a.hinv, p0);
-            x2[5] = a.eps + face_sq<5, POW2>(S, a.h, a.hinv, p0);
-            x2[6] = a.eps + face_sq<6, POW2>(S, a.h, a.hinv, p0);
-            x2[7] = a.eps + face_sq<7, POW2>(S, a.h, a.hinv, p0);
+            if (scaled) {  // A_f^2 = eps + sigma * (|grad_f u|^2 / sigma), the same bits
+                const double sg = p.sigma;
+                x2[0] = a.eps + sg * face_sq_scaled<0>(S, p0);
+                x2[1] = a.eps + sg * face_sq_scaled<1>(S, p0);
+                x2[2] = a.eps + sg * face_sq_scaled<2>(S, p0);
+                x2[3] = a.eps + sg * face_sq_scaled<3>(S, p0);
+                x2[4] = a.eps + sg * face_sq_scaled<4>(S, p0);
+                x2[5] = a.eps + sg * face_sq_scaled<5>(S, p0);
+                x2[6] = a.eps + sg * face_sq_scaled<6>(S, p0);
+                x2[7] = a.eps + sg * face_sq_scaled<7>(S, p0);
+            } else {
+                x2[0] = a.eps + face_sq<0, POW2>(S, a.h, a.hinv, p0);  // A_f^2 = eps + |grad_f u|^2
+                x2[1] = a.eps + face_sq<1, POW2>(S, a.h, a.hinv, p0);
+                x2[2] = a.eps + face_sq<2, POW2>(S, a.h, a.hinv, p0);
+                x2[3] = a.eps + face_sq<3, POW2>(S, a.h, a.hinv, p0);
+                x2[4] = a.eps + face_sq<4, POW2>(S, a.h, a.hinv, p0);
+                x2[5] = a.eps + face_sq<5, POW2>(S, a.h, a.hinv, p0);
+                x2[6] = a.eps + face_sq<6, POW2>(S, a.h, a.hinv, p0);
+                x2[7] = a.eps + face_sq<7, POW2>(S, a.h, a.hinv, p0);
+            }
             double a_sq_sum = 0.0;
 #pragma unroll
             for (int f = 0; f < 8; ++f) a_sq_sum += x2[f];  // solver.cpp:51-55, sequential f
@@ -376,10 +435,12 @@ __global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __
             for (int q = 0; q < 4; ++q) th[q] = a.t_h2[q] * abar_f;
             float cf[8];
             bool slow = false;
+            // one Newton step (NR1): q' within ~11,700 ulps of the exact quotient -> trust a
+            // float rounding decision only >= 2^14 ulps from a midpoint (slow path ~6e-5 per face)
 #pragma unroll
             for (int f = 0; f < 8; ++f) {
-                const double q = th[f >> 1] * gv[f] * rsqrt_nr(x2[f]);
-                slow |= near_midpoint(q);
+                const double q = th[f >> 1] * gv[f] * (NR1 ? rsqrt_nr1(x2[f]) : rsqrt_nr(x2[f]));
+                slow |= NR1 ? near_midpoint<16384>(q) : near_midpoint<512>(q);
                 cf[f] = __double2float_rn(-q);
             }
             if (slow) {  // the reference's exact sequence (solver.cpp:51-66)
@@ -569,6 +630,29 @@ unsigned grid_for(K kernel, size_t smem, long long tiles) {
 
 static bool launch_tile(cudaStream_t s, AsmTileArgs& p, bool pow2);
 
+// flag = 1 if some value of u (both colour arrays, ghosts and halos included) is non-zero
+// and outside [2^-400, 2^400] or not finite: the scaled face gradients' exactness range
+__global__ void assemble_guard_kernel(const unsigned long long* __restrict__ c0,
+                                      const unsigned long long* __restrict__ c1, long long n, int* flag) {
+    int bad = 0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const unsigned long long b = __ldcs(c ? c1 + e : c0 + e);
+            const unsigned ex = (unsigned)(b >> 52) & 0x7FFu;
+            bad |= (b << 1) != 0 && (ex < 1023u - 400u || ex > 1023u + 400u);
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+void launch_assemble_guard(cudaStream_t s, const Layout& L, const double* u0, const double* u1, int* flag) {
+    assemble_guard_kernel<<<kReduceBlocks * 2, 512, 0, s>>>(reinterpret_cast<const unsigned long long*>(u0),
+                                                            reinterpret_cast<const unsigned long long*>(u1), L.cs,
+                                                            flag);
+    SSB_LAUNCHED();
+}
+
 double rsqrt_approx_bound() {
     unsigned long long* d = nullptr;
     SSB_CUDA(cudaMalloc(&d, sizeof *d));
@@ -613,14 +697,31 @@ bool launch_assemble_tile(cudaStream_t s, const AsmArgs& a, bool pow2) {
     return launch_tile(s, p, pow2);
 }
 
-static bool launch_tile(cudaStream_t s, AsmTileArgs& p, bool pow2) {
-    const AsmArgs& a = p.a;
-    if (!encode_brick(&p.maps.m[0][0], a.L, a.u[0]) || !encode_brick(&p.maps.m[0][1], a.L, a.u[1])) return false;
-    static const int gpref = env_int("SSB_ASM_GPREF", 0);  // measured neutral (+12% DRAM reads): off
-    p.gpref = gpref && a.G[0] && encode_G(&p.gmap[0], a.L, a.G[0]) && encode_G(&p.gmap[1], a.L, a.G[1]) ? 1 : 0;
+// the one-Newton-step face rsqrt, once per process: the hardware approximation's error must
+// be what the exactness argument assumes (eps0 < 2^-19.5; measured 9.3e-7 = 2^-20.04)
+static bool nr1_ok() {
+    static const bool ok = env_int("SSB_ASM_NR1", 1) != 0 && rsqrt_approx_bound() < 1.0 / 741455.0;  // 2^-19.5
+    return ok;
+}
+
+// scaled face gradients: isotropic power-of-two spacing within [2^-40, 2^40]
+static bool scaled_grid(const AsmArgs& a, bool pow2, double* sigma) {
+    if (!pow2 || env_int("SSB_ASM_SCALED", 1) == 0) return false;
+    for (int q = 1; q < 4; ++q)
+        if (a.h[q] != a.h[0]) return false;
+    int e = 0;
+    std::frexp(a.h[0], &e);
+    if (e < -39 || e > 41) return false;
+    const double c = 0.25 / a.h[0];
+    *sigma = c * c;
+    return true;
+}
+
+template <bool NR1>
+static bool launch_tile_t(cudaStream_t s, AsmTileArgs& p, bool pow2) {
     constexpr int ST = SSB_ASMT_STAGES;
     const size_t smem = (size_t)ST * kFieldBytes;
-    auto k = pow2 ? assemble_tile_kernel<true, ST, SSB_ASMT_MINB> : assemble_tile_kernel<false, ST, SSB_ASMT_MINB>;
+    auto k = pow2 ? assemble_tile_kernel<true, ST, SSB_ASMT_MINB, NR1> : assemble_tile_kernel<false, ST, SSB_ASMT_MINB, NR1>;
     static bool configured[2] = {false, false};
     if (!configured[pow2]) {
         SSB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -631,6 +732,21 @@ static bool launch_tile(cudaStream_t s, AsmTileArgs& p, bool pow2) {
     k<<<(unsigned)std::min<long long>(p.g.tiles, grid[pow2]), kThreadsT, smem, s>>>(p);
     SSB_LAUNCHED();
     return true;
+}
+
+static bool launch_tile(cudaStream_t s, AsmTileArgs& p, bool pow2) {
+    const AsmArgs& a = p.a;
+    if (!encode_brick(&p.maps.m[0][0], a.L, a.u[0]) || !encode_brick(&p.maps.m[0][1], a.L, a.u[1])) return false;
+    static const int gpref = env_int("SSB_ASM_GPREF", 0);  // measured neutral (+12% DRAM reads): off
+    p.gpref = gpref && a.G[0] && encode_G(&p.gmap[0], a.L, a.G[0]) && encode_G(&p.gmap[1], a.L, a.G[1]) ? 1 : 0;
+    // the scaled face gradients need this step's u within range: one guard pass over both
+    // colour arrays (8 B per padded doxel) writes the flag the tile kernel reads
+    if (a.guard && scaled_grid(a, pow2, &p.sigma)) {
+        SSB_CUDA(cudaMemsetAsync(a.guard, 0, sizeof(int), s));
+        launch_assemble_guard(s, a.L, a.u[0], a.u[1], a.guard);
+        p.guard = a.guard;
+    }
+    return nr1_ok() ? launch_tile_t<true>(s, p, pow2) : launch_tile_t<false>(s, p, pow2);
 }
 
 bool launch_edge_tile(cudaStream_t s, const EdgeArgs& a, bool pow2) {

@@ -252,6 +252,7 @@ void Slab::assemble(PField u, bool with_G, double tau, double eps, double* off_o
     }
     a.eps = eps;
     a.bad = flags.p;
+    a.guard = flags.p + 2;  // the tile kernel's scaled-gradient guard (flags[1]: threshold)
     a.off_out = off_out;
     a.diag_out = diag_out;
     a.abar_out = abar_out;

@@ -166,6 +166,7 @@ struct AsmArgs {
     double h[4];
     double hinv[4];         // 1/h (used only when every h is a power of two)
     int* bad;               // set when a diag is non-finite (solver.cpp:71-75)
+    int* guard;             // device flag for the tile kernel's scaled gradients (null: exact path)
     // export (per-call API): padded outputs, may be null
     double* off_out;        // 8 per padded doxel
     double* diag_out;
@@ -187,6 +188,7 @@ void launch_face_coefficients(cudaStream_t s, const EdgeArgs& a);
 // TMA-staged tile kernels (assemble_tile.cu); false = not launched (no tensor-map encoder)
 bool assemble_tile_supported(const Layout& L);
 double rsqrt_approx_bound();  // self-test: max relative error of rsqrt.approx.f64 (exhaustive)
+void launch_assemble_guard(cudaStream_t s, const Layout& L, const double* u0, const double* u1, int* flag);
 bool launch_assemble_tile(cudaStream_t s, const AsmArgs& a, bool pow2);
 // the same restricted to slices [l_lo, l_hi] (the upload-overlapped assembly of step_host)
 bool launch_assemble_tile_range(cudaStream_t s, const AsmArgs& a, int l_lo, int l_hi);
