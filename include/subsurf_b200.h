@@ -282,6 +282,10 @@ typedef struct {
     long long halo_n;
 } ss_profile;
 SS_API ss_status ss_session_profile(ss_session* s, ss_profile* out);
+/* the coefficients a step would assemble at the session's current u (the tile kernel of the
+ * device-resident path, G included) as padded fp64 off-diagonals (8 * P; ghost doxels 0) --
+ * what assemble_step (solver.cpp:23-77) returns in StepCoefficients::offdiag; single slab */
+SS_API ss_status ss_session_assemble_export(ss_session* s, double* offdiag);
 /* self-test of the assembly kernel's rsqrt tail (assemble_tile.cu): the largest relative
  * error of the hardware rsqrt.approx.f64 over every normal positive input high word; the
  * tail's exactness argument needs it below 2^-11 (two Newton steps then leave a few ulps) */

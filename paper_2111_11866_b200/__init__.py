@@ -216,6 +216,7 @@ def library() -> C.CDLL:
     sig("ss_session_fixed_sweeps", [C.c_void_p, C.c_int, _D])
     sig("ss_session_step_fixed", [C.c_void_p, C.c_int, C.POINTER(StepDiag)])
     sig("ss_selftest_rsqrt", [_D])
+    sig("ss_session_assemble_export", [C.c_void_p, _D])
     sig("ss_session_step_host", [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(StepDiag)])
     sig("ss_session_set_u_interior", [C.c_void_p, C.c_void_p])
     sig("ss_session_get_u_interior", [C.c_void_p, C.c_void_p])
@@ -616,6 +617,13 @@ class Session:
                                             C.byref(d) if diag else None)
         _check(st, d.iterations, d.residual)
         return dict(iterations=d.iterations, residual=d.residual, tol=d.tol, umin=d.umin, umax=d.umax) if diag else None
+
+    def assemble_export(self) -> np.ndarray:
+        """The off-diagonals the next step would assemble at the session's u (the device
+        path's tile kernel), padded (n4+2, n3+2, n2+2, n1+2, 8) fp64."""
+        out = np.empty(self.g.shape + (8,))
+        _check(library().ss_session_assemble_export(self._h, _dp(out)))
+        return out
 
     def set_u_interior(self, u) -> None:
         a = np.ascontiguousarray(u, dtype=np.float64).reshape(self.interior_shape)

@@ -257,6 +257,22 @@ __global__ void pack_coef_kernel(const Layout L, const double* __restrict__ off,
     for (int f = 0; f < 8; ++f) dst[f] = (float)off[e * 8 + f];
 }
 
+// colour-packed fp32 rows -> padded fp64 off-diagonals (8 per doxel; ghost doxels 0)
+__global__ void unpack_coef_kernel(const Layout L, const float* __restrict__ c0, const float* __restrict__ c1,
+                                   double* off) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= L.P) return;
+    const int i = (int)(e % L.iMax);
+    long long r = e / L.iMax;
+    const int j = (int)(r % L.jMax);
+    const int k = (int)((r / L.jMax) % L.kMax);
+    const int l = (int)(r / ((long long)L.jMax * L.kMax));
+    const bool in = i >= 1 && i <= L.n1 && j >= 1 && j <= L.n2 && k >= 1 && k <= L.n3 && l >= 1 && l <= L.n4;
+    const float* src = in ? (L.colour(i, j, k, l) ? c1 : c0) + L.coef_slot(i, j, k, l) * 8 : nullptr;
+#pragma unroll
+    for (int f = 0; f < 8; ++f) off[e * 8 + f] = in ? (double)src[f] : 0.0;
+}
+
 __global__ void pack8_kernel(const Layout L, const double* __restrict__ src, double* d0,
                              double* d1) {
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -382,6 +398,11 @@ void launch_face_coefficients(cudaStream_t s, const EdgeArgs& a0) {
 
 void launch_pack_coef(cudaStream_t s, const Layout& L, const double* off, float* c0, float* c1) {
     pack_coef_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, off, c0, c1);
+    SSB_LAUNCHED();
+}
+
+void launch_unpack_coef(cudaStream_t s, const Layout& L, const float* c0, const float* c1, double* off) {
+    unpack_coef_kernel<<<ceil_div(L.P, 256), 256, 0, s>>>(L, c0, c1, off);
     SSB_LAUNCHED();
 }
 

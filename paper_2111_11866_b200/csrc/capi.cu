@@ -673,6 +673,26 @@ ss_status ss_session_get_u_interior(ss_session* s, double* u) {
     });
 }
 
+ss_status ss_session_assemble_export(ss_session* s, double* offdiag) {
+    return guard([&] {
+        require(s && offdiag, "null session / output");
+        Domain& d = *s->d;
+        require(d.prepared, "session not prepared");
+        require(d.single(), "assemble_export: single-slab sessions");
+        SSB_CUDA(cudaSetDevice(d.device));
+        Slab& x = *d.sp[0];
+        x.assemble(x.S[d.cur].pf(), x.have_G, d.prm.tau, d.prm.epsilon, nullptr, nullptr, nullptr);
+        Dev<double> off;
+        off.alloc((size_t)x.L.P * 8);
+        launch_unpack_coef(d.stream, x.L, x.coef[0].p, x.coef[1].p, off.p);
+        int bad = 0;
+        SSB_CUDA(cudaMemcpyAsync(&bad, x.flags.p, sizeof(int), cudaMemcpyDeviceToHost, d.stream));
+        copy_d2h(offdiag, off.p, (size_t)x.L.P * 8 * sizeof(double), d.stream);
+        d.sync();
+        if (bad) throw Error(SS_ERR_NONFINITE, "assemble_step: non-finite coefficient (bad input field?)");
+    });
+}
+
 ss_status ss_selftest_rsqrt(double* eps0) {
     return guard([&] {
         require(eps0 != nullptr, "null output");

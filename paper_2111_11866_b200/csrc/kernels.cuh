@@ -198,6 +198,8 @@ bool launch_edge_tile(cudaStream_t s, const EdgeArgs& a, bool pow2);
 // (pack_coefficients, solver.cpp:233-249)
 void launch_pack_coef(cudaStream_t s, const Layout& L, const double* off, float* coef0,
                       float* coef1);
+// colour-packed fp32 rows -> padded fp64 off-diagonals (the session's coefficients, for tests)
+void launch_unpack_coef(cudaStream_t s, const Layout& L, const float* c0, const float* c1, double* off);
 // padded 8-vector field -> colour-packed
 void launch_pack8(cudaStream_t s, const Layout& L, const double* src, double* d0, double* d1);
 // heat-step export (assemble_heat_step, solver.cpp:79-116)

@@ -437,3 +437,38 @@ def test_rsqrt_approximation_bound(gpu):
     assert gpu.library().ss_selftest_rsqrt(C.byref(e)) == 0
     assert 0.0 < e.value < 2.0 ** -11, e.value
     print("rsqrt.approx.f64 max relative error", e.value)
+
+
+@pytest.mark.parametrize("case", ["iso_pow2", "iso_pow2_guard", "aniso_pow2", "non_pow2"])
+def test_tile_assembly_coefficients_vs_oracle(gpu, oracle, case):
+    """The device path's assembly (assemble_tile.cu: TMA-staged bricks, the rsqrt tail with
+    its exact fallback, the scaled face gradients behind the range guard) against the oracle's
+    assemble_step off-diagonals, bit for bit, on u with a wide range of magnitudes and exact
+    zeros.  K = 0 makes the session's G exactly 1 (edge.cpp: 1 / (1 + 0)), so the oracle runs
+    with G == 1.  iso_pow2: the scaled path; iso_pow2_guard: one value of 1e-200 trips the
+    guard (reference expression); aniso_pow2 / non_pow2: the per-axis expressions."""
+    from oracle import oracle_py as op
+    dims = (37, 13, 11, 7)
+    h = {"iso_pow2": 1 / 32, "iso_pow2_guard": 1 / 32, "aniso_pow2": (1 / 32, 1 / 16, 1 / 32, 1 / 64),
+         "non_pow2": (0.1, 0.07, 0.13, 0.05)}[case]
+    g = gpu.Grid.make(dims, h)
+    og = op.Grid.make(dims, h)
+    tau, eps = 0.03, 1e-3
+    img = cs.f32_image(dims, 7)
+    rows = [(f, 18.0, 6.0, 5.0, 3.0) for f in range(dims[3])]
+    rng = np.random.default_rng(77)
+    u = np.zeros(g.shape)
+    vals = rng.normal(0.5, 0.4, size=u[1:-1, 1:-1, 1:-1, 1:-1].shape) * 10.0 ** rng.uniform(-3, 3, size=u[1:-1, 1:-1, 1:-1, 1:-1].shape)
+    vals[rng.random(vals.shape) < 0.2] = 0.0
+    u[1:-1, 1:-1, 1:-1, 1:-1] = vals
+    if case == "iso_pow2_guard":
+        u[3, 4, 5, 6] = 1e-200
+    p = gpu.seg_params(tau=tau, epsilon=eps, omega=1.4, sor_tol=1e-9, n_steps=1, sigma=0.1, K=0.0, delta=0.5,
+                       vartheta=0.5, rescale_radius=2.0)
+    with gpu.Session(g) as s:
+        s.prepare(img, rows, p, None)
+        s.set_u(u)
+        off_gpu = s.assemble_export()
+    st, off_ref, _, _ = oracle.assemble_step(og, u, None, tau, eps)
+    assert st == 0
+    assert_bits(off_gpu, off_ref, f"tile assembly, {case}")
