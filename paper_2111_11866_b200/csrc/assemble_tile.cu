@@ -16,19 +16,21 @@
 // loads; the fp32 coefficients go out as two 128-bit stores per doxel.
 //
 // Bit-exactness: the face gradients keep the reference's expression order
-// (-fmad=false).  The tail replaces the correctly rounded sqrt / div chain of
-// solver.cpp:48-66 by a reciprocal square root with two Newton steps: the
-// quotient q' = ((t_a Abar') G_f) rsqrt'(A_f^2) lies within ~20 double ulps of
-// the reference's q = ((t_a Abar) G_f) / sqrt(A_f^2), and the only output is
-// float(-q).  When q' is at least 512 double ulps away from a float rounding
-// midpoint (its low 29 mantissa bits differ from 2^28 by >= 512) and its
-// exponent lies in the normal float range, float(-q') == float(-q) exactly;
-// otherwise (probability ~2e-6 per face) the doxel is recomputed with the
-// reference's exact sequence.  So every coefficient is the reference's bits.
-// The error budget rests on the hardware approximation's accuracy: measured
-// exhaustively over every normal input high word (ss_selftest_rsqrt, a GPU test),
-// its relative error is eps0 = 9.3e-7 (2^-20.0); one Newton step leaves
-// 1.5 eps0^2 ~ 2^-39.4, the second the rounding of its own arithmetic (~2 ulps).
+// (-fmad=false), or -- on isotropic power-of-two grids whose u passed this step's
+// range guard -- the same values with every power-of-two scaling pulled out
+// (face_sq_scaled, exact by the argument there).  The tail replaces the correctly
+// rounded sqrt / div chain of solver.cpp:48-66 by a reciprocal square root: the
+// quotient q' = ((t_a Abar') G_f) rsqrt'(A_f^2) lies close to the reference's
+// q = ((t_a Abar) G_f) / sqrt(A_f^2), and the only output is float(-q).  When q' is
+// far enough from a float rounding midpoint (its low 29 mantissa bits differ from
+// 2^28 by >= T) and its exponent lies in the normal float range, float(-q') ==
+// float(-q) exactly; otherwise the doxel is recomputed with the reference's exact
+// sequence.  So every coefficient is the reference's bits.  With two Newton steps q'
+// is within ~20 ulps (T = 512, slow path ~2e-6 per face); with one (NR1, the default
+// when the self-test confirms it) within ~11,700 ulps (T = 2^14, ~6e-5 per face).  The
+// budget rests on the hardware approximation's accuracy, measured exhaustively over
+// every normal input high word (ss_selftest_rsqrt: eps0 = 9.3e-7 = 2^-20.0, re-checked
+// once per process before the first one-step launch and in the GPU tests).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
