@@ -31,6 +31,12 @@
 // budget rests on the hardware approximation's accuracy, measured exhaustively over
 // every normal input high word (ss_selftest_rsqrt: eps0 = 9.3e-7 = 2^-20.0, re-checked
 // once per process before the first one-step launch and in the GPU tests).
+// Certified face gradients (round 2, default): on isotropic power-of-two grids whose u passed
+// the range guard, |grad_f u|^2 comes from shared central differences (face_sq_cert, ~half the
+// FP64 instructions of the reference's corner sums) within a bound proven from max |u| (the
+// guard's second word); the tail's midpoint distance grows by that bound, and the doxels near a
+// midpoint take the exact sequence (exact_doxel, out of line), so the coefficients stay the
+// reference's bits.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -73,16 +79,31 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sptr(bar)) : "memory");
 }
+#ifndef SSB_ASMT_SUSPEND
+#define SSB_ASMT_SUSPEND 0  // try_wait suspend-time hint in ns (0: the hardware's default)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(sptr(bar)),
-        "r"(parity)
-        : "memory");
+    if constexpr (SSB_ASMT_SUSPEND > 0) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+            "@!p bra WAIT_%=;\n"
+            "}\n" ::"r"(sptr(bar)),
+            "r"(parity), "n"(SSB_ASMT_SUSPEND)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            "@!p bra WAIT_%=;\n"
+            "}\n" ::"r"(sptr(bar)),
+            "r"(parity)
+            : "memory");
+    }
 }
 // 3D tensor copy of the box at {x (slot), y (row j), z (plane l*kMax + k)}
 __device__ __forceinline__ void tensor3_g2s(uint32_t dst, const CUtensorMap* map, int x, int y, int z,
@@ -124,13 +145,16 @@ struct Tile {
     int l, b, jb, kc;
 };
 __device__ __forceinline__ Tile tile_of(const Layout& L, const TileGeo& g, long long t) {
+    // 32-bit divisions (inline; the 64-bit ones are subroutine calls): tile counts stay far
+    // below 2^32 (config 3's slab of a 512^2 x 128 x 64 grid: 2.1 M tiles)
+    unsigned r = (unsigned)t;
     Tile x;
-    x.l = (int)(t % g.nl) + g.l_lo;
-    long long r = t / g.nl;
-    x.b = (int)(r % g.nb);
-    r /= g.nb;
-    x.jb = (int)(r % g.njb);
-    x.kc = (int)(r / g.njb);
+    x.l = (int)(r % (unsigned)g.nl) + g.l_lo;
+    r /= (unsigned)g.nl;
+    x.b = (int)(r % (unsigned)g.nb);
+    r /= (unsigned)g.nb;
+    x.jb = (int)(r % (unsigned)g.njb);
+    x.kc = (int)(r / (unsigned)g.njb);
     return x;
 }
 
@@ -243,6 +267,55 @@ __device__ __forceinline__ double face_sq_scaled(const SStencil& S, double p0) {
     return d[0] * d[0] + d[1] * d[1] + d[2] * d[2] + d[3] * d[3];
 }
 
+// Certified face gradients (the default on isotropic power-of-two grids whose u passed the
+// guard).  The scaled tangential difference d_T = RN(X - Y) of face_sq_scaled, X and Y the two
+// rounded corner sums ((p0 + pn) + p_+T) + pn_+T and ((p0 + pn) + p_-T) + pn_-T, equals
+// (p_+T - p_-T) + (pn_+T - pn_-T) up to the sums' roundings (the common p0 + pn cancels):
+// d'_T = RN(c_T(p) + c_T(pn)) with the central differences c_T = RN(x_+T - x_-T), where c_T(p)
+// is shared by the six faces not normal to T.  With M >= every |u| and u_r = 2^-53:
+//   |d_T - d'_T| <= E = 32 M u_r      (X, Y: 7.01 M u_r each; RN(X - Y): 4.01; d': 8.02)
+// and with F = sum of the four squares (the normal term is the same bits in both),
+//   |F_ex - F'| <= 8.1 u_r F + 2 sqrt(3) E sqrt(F) + 3.1 E^2,
+// so A_f^2 = eps + sigma F moves by at most rho A_f^2 with
+//   rho = 40 u_r + 1.75 E sqrt(sigma) / sqrt(eps) + 3.1 (E sqrt(sigma) / sqrt(eps))^2
+// (max over F of sqrt(sigma F) / (eps + sigma F) is 1 / (2 sqrt(eps)); 40 u_r also covers the
+// roundings of eps + sigma F, of the mean for Abar^2 and of the fused squares).  The quotient
+// q ~ Abar / A_f then moves by at most rho relative, i.e. rho 2^53 ulps, on top of the tail's
+// own budget: the float rounding decision is trusted only >= T = 1.25 (budget + rho 2^53) ulps
+// from a midpoint, otherwise the doxel takes the exact sequence (face_sq_scaled + sqrt/div).
+// ~108 instead of ~216 FP64 instructions per doxel for the eight faces.
+template <int F>
+__device__ __forceinline__ double face_sq_cert(const SStencil& S, double p0, const double c[4]) {
+    constexpr int A = F >> 1, SG = (F & 1) ? 1 : -1;
+    constexpr int ai = A == 0 ? SG : 0, aj = A == 1 ? SG : 0, ak = A == 2 ? SG : 0, al = A == 3 ? SG : 0;
+    const double n4 = 4.0 * (S.at<ai, aj, ak, al>() - p0);
+    double acc = __dmul_rn(n4, n4);
+#define SSB_CERT_TANGENT(T)                                                                              \
+    if constexpr (A != T) {                                                                               \
+        constexpr int ti = T == 0, tj = T == 1, tk = T == 2, tl = T == 3;                                  \
+        const double d = c[T] + (S.at<ai + ti, aj + tj, ak + tk, al + tl>() - S.at<ai - ti, aj - tj, ak - tk, al - tl>()); \
+        acc = __fma_rn(d, d, acc);                                                                        \
+    }
+    SSB_CERT_TANGENT(0)
+    SSB_CERT_TANGENT(1)
+    SSB_CERT_TANGENT(2)
+    SSB_CERT_TANGENT(3)
+#undef SSB_CERT_TANGENT
+    return acc;
+}
+
+// the midpoint distance T (ulps of q) the certified gradients need, or 0 when the bound is too
+// loose to pay (T > 2^17: more than ~5e-4 of the faces would take the slow path; then the exact
+// scaled gradients run); M from the guard's high word
+__device__ __forceinline__ int cert_threshold(unsigned hmax, double sqrt_sigma, double eps, bool nr1) {
+    const double ur = 0x1p-53;
+    const double M = __hiloint2double((int)(hmax + 1u), 0);
+    const double Er = 32.0 * M * ur * sqrt_sigma / sqrt(eps);
+    const double rho = 40.0 * ur + 1.75 * Er + 3.1 * Er * Er;
+    const double t = 1.25 * ((nr1 ? 11700.0 : 20.0) + rho * 0x1p53);
+    return t < 131072.0 ? max(nr1 ? 16384 : 512, (int)t + 1) : 0;
+}
+
 // 1/sqrt(x) with one Newton step: relative error <= 1.5 eps0^2 + rounding ~ 1.3e-12 for the
 // measured eps0 = 9.3e-7 of the hardware approximation (used only when the per-process
 // self-test confirms eps0 < 2^-19.5, see ss_selftest_rsqrt)
@@ -262,17 +335,6 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
     e = __fma_rn(-__dmul_rn(x, y), y, 1.0);
     y = __fma_rn(__dmul_rn(y, 0.5), e, y);
     return y;
-}
-
-// float(q') is float(q) for every q within ~20 ulps of q' unless q' sits near a float
-// rounding midpoint or outside the normal float range: then take the exact path
-template <int T = 512>
-__device__ __forceinline__ bool near_midpoint(double q) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(q);
-    const int low = (int)(b & 0x1FFFFFFFull);
-    const int ex = (int)((b >> 52) & 0x7FF);
-    const int d = low - (1 << 28);
-    return (d < T && d > -T) || ex < 1023 - 120 || ex > 1023 + 120;
 }
 
 // G of a tile (both colours) into L2 ahead of the tile: 3D view of a colour's G array
@@ -305,6 +367,8 @@ struct AsmTileArgs {
     int gpref;          // G maps valid
     const int* guard;   // non-null: scaled face gradients unless *guard (a value out of range)
     double sigma;       // (hinv / 4)^2 of the isotropic power-of-two grid (scaled mode)
+    double sqrt_sigma;  // hinv / 4
+    int cert;           // certified face gradients: 1 on, 0 off, 2 no margin (test-only; SSB_ASM_CERT)
     AsmArgs a;
     TileGeo g;
 };
@@ -319,6 +383,49 @@ __device__ __forceinline__ void prefetch_G(const AsmTileArgs& p, const Tile& x) 
 #define SSB_ASMT_L1PREF 0  // G pulled into L1 one plane ahead: measured neutral (0.587 vs 0.580 ms config 1)
 #endif
 constexpr bool GPREF_L1 = SSB_ASMT_L1PREF != 0;
+
+// the reference's exact sequence for one doxel (solver.cpp:51-66): exact A_f^2 (scaled or the
+// reference's expression), Abar by sqrt, the quotients by sqrt / div.  Out of line: it runs for
+// ~1e-3 of the doxels, and inlined its registers would spill the main path's
+struct Coef8 {
+    float4 lo, hi;
+};
+template <bool POW2>
+__device__ __noinline__ Coef8 exact_doxel(const SStencil S, double p0, bool scaled, const AsmTileArgs& p, double g0,
+                                          double g1, double g2, double g3, double g4, double g5, double g6,
+                                          double g7) {
+    const AsmArgs& a = p.a;
+    const double gv[8] = {g0, g1, g2, g3, g4, g5, g6, g7};
+    float cf[8];
+    double x2[8];
+    if (scaled) {  // A_f^2 = eps + sigma * (|grad_f u|^2 / sigma), the same bits
+        const double sg = p.sigma;
+        x2[0] = a.eps + sg * face_sq_scaled<0>(S, p0);
+        x2[1] = a.eps + sg * face_sq_scaled<1>(S, p0);
+        x2[2] = a.eps + sg * face_sq_scaled<2>(S, p0);
+        x2[3] = a.eps + sg * face_sq_scaled<3>(S, p0);
+        x2[4] = a.eps + sg * face_sq_scaled<4>(S, p0);
+        x2[5] = a.eps + sg * face_sq_scaled<5>(S, p0);
+        x2[6] = a.eps + sg * face_sq_scaled<6>(S, p0);
+        x2[7] = a.eps + sg * face_sq_scaled<7>(S, p0);
+    } else {
+        x2[0] = a.eps + face_sq<0, POW2>(S, a.h, a.hinv, p0);
+        x2[1] = a.eps + face_sq<1, POW2>(S, a.h, a.hinv, p0);
+        x2[2] = a.eps + face_sq<2, POW2>(S, a.h, a.hinv, p0);
+        x2[3] = a.eps + face_sq<3, POW2>(S, a.h, a.hinv, p0);
+        x2[4] = a.eps + face_sq<4, POW2>(S, a.h, a.hinv, p0);
+        x2[5] = a.eps + face_sq<5, POW2>(S, a.h, a.hinv, p0);
+        x2[6] = a.eps + face_sq<6, POW2>(S, a.h, a.hinv, p0);
+        x2[7] = a.eps + face_sq<7, POW2>(S, a.h, a.hinv, p0);
+    }
+    double sq = 0.0;
+#pragma unroll
+    for (int f = 0; f < 8; ++f) sq += x2[f];  // solver.cpp:51-55, sequential f
+    const double abar = sqrt(a.eps + 0.125 * sq);
+#pragma unroll
+    for (int f = 0; f < 8; ++f) cf[f] = __double2float_rn(-(a.t_h2[f >> 1] * abar * gv[f] / sqrt(x2[f])));
+    return Coef8{make_float4(cf[0], cf[1], cf[2], cf[3]), make_float4(cf[4], cf[5], cf[6], cf[7])};
+}
 
 template <bool POW2, int STAGES, int MINB, bool NR1>
 __global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __grid_constant__ AsmTileArgs p) {
@@ -352,6 +459,11 @@ __global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __
     // scaled face gradients: the host chose them for this grid and this step's u passed the
     // guard (uniform over the grid: one flag written before the launch)
     const bool scaled = POW2 && p.guard && *(volatile const int*)p.guard == 0;
+    // certified face gradients: the midpoint distance their error bound needs at this step's
+    // max |u| (0: the bound is too loose, exact scaled gradients)
+    const int cert_T = !(scaled && p.cert) ? 0
+                       : p.cert == 2 ? 1  // test-only: no margin (shows that the tests see the bound)
+                                     : cert_threshold(((volatile const unsigned*)p.guard)[1], p.sqrt_sigma, a.eps, NR1);
     for (; t < g.tiles; t += gridDim.x) {
         const Tile x = tile_of(L, g, t);
         const uint32_t buf = sbase + stage * kFieldBytes;
@@ -407,7 +519,22 @@ __global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __
             }
             const double p0 = S.at<0, 0, 0, 0>();
             double x2[8];
-            if (scaled) {  // A_f^2 = eps + sigma * (|grad_f u|^2 / sigma), the same bits
+            if (cert_T) {  // within rho A_f^2 of the exact values (face_sq_cert)
+                double cc[4];
+                cc[0] = S.at<1, 0, 0, 0>() - S.at<-1, 0, 0, 0>();
+                cc[1] = S.at<0, 1, 0, 0>() - S.at<0, -1, 0, 0>();
+                cc[2] = S.at<0, 0, 1, 0>() - S.at<0, 0, -1, 0>();
+                cc[3] = S.at<0, 0, 0, 1>() - S.at<0, 0, 0, -1>();
+                const double sg = p.sigma;
+                x2[0] = __fma_rn(sg, face_sq_cert<0>(S, p0, cc), a.eps);
+                x2[1] = __fma_rn(sg, face_sq_cert<1>(S, p0, cc), a.eps);
+                x2[2] = __fma_rn(sg, face_sq_cert<2>(S, p0, cc), a.eps);
+                x2[3] = __fma_rn(sg, face_sq_cert<3>(S, p0, cc), a.eps);
+                x2[4] = __fma_rn(sg, face_sq_cert<4>(S, p0, cc), a.eps);
+                x2[5] = __fma_rn(sg, face_sq_cert<5>(S, p0, cc), a.eps);
+                x2[6] = __fma_rn(sg, face_sq_cert<6>(S, p0, cc), a.eps);
+                x2[7] = __fma_rn(sg, face_sq_cert<7>(S, p0, cc), a.eps);
+            } else if (scaled) {  // A_f^2 = eps + sigma * (|grad_f u|^2 / sigma), the same bits
                 const double sg = p.sigma;
                 x2[0] = a.eps + sg * face_sq_scaled<0>(S, p0);
                 x2[1] = a.eps + sg * face_sq_scaled<1>(S, p0);
@@ -438,22 +565,30 @@ __global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __
             float cf[8];
             bool slow = false;
             // one Newton step (NR1): q' within ~11,700 ulps of the exact quotient -> trust a
-            // float rounding decision only >= 2^14 ulps from a midpoint (slow path ~6e-5 per face)
+            // float rounding decision only >= 2^14 ulps from a midpoint (slow path ~6e-5 per face);
+            // certified gradients: >= cert_T ulps
+            const unsigned Tm = cert_T ? (unsigned)cert_T : NR1 ? 16384u : 512u;
 #pragma unroll
             for (int f = 0; f < 8; ++f) {
                 const double q = th[f >> 1] * gv[f] * (NR1 ? rsqrt_nr1(x2[f]) : rsqrt_nr(x2[f]));
-                slow |= NR1 ? near_midpoint<16384>(q) : near_midpoint<512>(q);
                 cf[f] = __double2float_rn(-q);
+                // q' within Tm ulps of a float rounding midpoint: its low 29 mantissa bits within
+                // Tm of 2^28 (one unsigned compare)
+                slow |= (((unsigned)__double2loint(q) & 0x1FFFFFFFu) - ((1u << 28) - Tm)) < 2u * Tm;
+                // and the result a normal float with exponent field 8 .. 246, i.e. q' within
+                // 2^-120 .. 2^120 (zero, subnormal, inf and NaN results all take the exact path)
+                slow |= ((__float_as_uint(cf[f]) & 0x7F800000u) - (8u << 23)) > (238u << 23);
             }
-            if (slow) {  // the reference's exact sequence (solver.cpp:51-66)
-                const double abar = sqrt(sbar);
+            if (slow) {  // the reference's exact sequence
+                const Coef8 e = exact_doxel<POW2>(S, p0, scaled, p, gv[0], gv[1], gv[2], gv[3], gv[4], gv[5], gv[6], gv[7]);
+                cf[0] = e.lo.x, cf[1] = e.lo.y, cf[2] = e.lo.z, cf[3] = e.lo.w;
+                cf[4] = e.hi.x, cf[5] = e.hi.y, cf[6] = e.hi.z, cf[7] = e.hi.w;
+                // diag = 1 - sum of the 8 (float-valued) doubles is non-finite iff some
+                // coefficient is (a sum of 8 finite floats cannot overflow a double),
+                // solver.cpp:68-75; the fast path's coefficients are all finite
 #pragma unroll
-                for (int f = 0; f < 8; ++f) cf[f] = __double2float_rn(-(a.t_h2[f >> 1] * abar * gv[f] / sqrt(x2[f])));
+                for (int f = 0; f < 8; ++f) bad |= (__float_as_uint(cf[f]) & 0x7F800000u) == 0x7F800000u;
             }
-            // diag = 1 - sum of the 8 (float-valued) doubles is non-finite iff some
-            // coefficient is (a sum of 8 finite floats cannot overflow a double), solver.cpp:68-75
-#pragma unroll
-            for (int f = 0; f < 8; ++f) bad |= (__float_as_uint(cf[f]) & 0x7F800000u) == 0x7F800000u;
             float4* cw = reinterpret_cast<float4*>(a.coef[c] + (row * L.Wc + ((i - 1) >> 1)) * 8);
             __stcs(cw, make_float4(cf[0], cf[1], cf[2], cf[3]));
             __stcs(cw + 1, make_float4(cf[4], cf[5], cf[6], cf[7]));
@@ -632,27 +767,43 @@ unsigned grid_for(K kernel, size_t smem, long long tiles) {
 
 static bool launch_tile(cudaStream_t s, AsmTileArgs& p, bool pow2);
 
-// flag = 1 if some value of u (both colour arrays, ghosts and halos included) is non-zero
-// and outside [2^-400, 2^400] or not finite: the scaled face gradients' exactness range
+// guard[0] = 1 if some value of u (both colour arrays, ghosts and halos included) is non-zero
+// and outside [2^-400, 2^400] or not finite: the scaled face gradients' exactness range.
+// guard[1] = the largest high word of |u| over the same elements: M = (guard[1] + 1) << 32
+// bounds every |u| from above (the certified face gradients' error bound scales with M)
 __global__ void assemble_guard_kernel(const unsigned long long* __restrict__ c0,
-                                      const unsigned long long* __restrict__ c1, long long n, int* flag) {
+                                      const unsigned long long* __restrict__ c1, long long e0, long long n,
+                                      int* guard) {
     int bad = 0;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    unsigned hmax = 0;
+    for (long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x) {
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const unsigned long long b = __ldcs(c ? c1 + e : c0 + e);
             const unsigned ex = (unsigned)(b >> 52) & 0x7FFu;
             bad |= (b << 1) != 0 && (ex < 1023u - 400u || ex > 1023u + 400u);
+            hmax = max(hmax, (unsigned)(b >> 32) & 0x7FFFFFFFu);
         }
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+    hmax = __reduce_max_sync(0xFFFFFFFFu, hmax);
+    if ((threadIdx.x & 31) == 0 && hmax) atomicMax(reinterpret_cast<unsigned*>(guard) + 1, hmax);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(guard, 1);
+}
+
+// the guard over the packed elements of slices l_lo .. l_hi (both colour arrays); the caller
+// zeroes guard[0..1] first
+static void launch_guard_range(cudaStream_t s, const Layout& L, const double* u0, const double* u1, int l_lo,
+                               int l_hi, int* guard) {
+    assemble_guard_kernel<<<kReduceBlocks * 2, 512, 0, s>>>(reinterpret_cast<const unsigned long long*>(u0),
+                                                            reinterpret_cast<const unsigned long long*>(u1),
+                                                            (long long)l_lo * L.sl, (long long)(l_hi + 1) * L.sl,
+                                                            guard);
+    SSB_LAUNCHED();
 }
 
 void launch_assemble_guard(cudaStream_t s, const Layout& L, const double* u0, const double* u1, int* flag) {
-    assemble_guard_kernel<<<kReduceBlocks * 2, 512, 0, s>>>(reinterpret_cast<const unsigned long long*>(u0),
-                                                            reinterpret_cast<const unsigned long long*>(u1), L.cs,
-                                                            flag);
-    SSB_LAUNCHED();
+    launch_guard_range(s, L, u0, u1, 0, L.lMax - 1, flag);
 }
 
 double rsqrt_approx_bound() {
@@ -723,15 +874,16 @@ template <bool NR1>
 static bool launch_tile_t(cudaStream_t s, AsmTileArgs& p, bool pow2) {
     constexpr int ST = SSB_ASMT_STAGES;
     const size_t smem = (size_t)ST * kFieldBytes;
+    const int v = pow2 ? 1 : 0;
     auto k = pow2 ? assemble_tile_kernel<true, ST, SSB_ASMT_MINB, NR1> : assemble_tile_kernel<false, ST, SSB_ASMT_MINB, NR1>;
     static bool configured[2] = {false, false};
-    if (!configured[pow2]) {
+    if (!configured[v]) {
         SSB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured[pow2] = true;
+        configured[v] = true;
     }
     static unsigned grid[2] = {0, 0};
-    if (!grid[pow2]) grid[pow2] = grid_for(k, smem, 1LL << 40);
-    k<<<(unsigned)std::min<long long>(p.g.tiles, grid[pow2]), kThreadsT, smem, s>>>(p);
+    if (!grid[v]) grid[v] = grid_for(k, smem, 1LL << 40);
+    k<<<(unsigned)std::min<long long>(p.g.tiles, grid[v]), kThreadsT, smem, s>>>(p);
     SSB_LAUNCHED();
     return true;
 }
@@ -744,9 +896,12 @@ static bool launch_tile(cudaStream_t s, AsmTileArgs& p, bool pow2) {
     // the scaled face gradients need this step's u within range: one guard pass over both
     // colour arrays (8 B per padded doxel) writes the flag the tile kernel reads
     if (a.guard && scaled_grid(a, pow2, &p.sigma)) {
-        SSB_CUDA(cudaMemsetAsync(a.guard, 0, sizeof(int), s));
-        launch_assemble_guard(s, a.L, a.u[0], a.u[1], a.guard);
+        SSB_CUDA(cudaMemsetAsync(a.guard, 0, 2 * sizeof(int), s));
+        // the slices the tiles read: l_lo - 1 .. l_hi + 1
+        launch_guard_range(s, a.L, a.u[0], a.u[1], p.g.l_lo - 1, p.g.l_lo + p.g.nl, a.guard);
         p.guard = a.guard;
+        p.sqrt_sigma = std::sqrt(p.sigma);
+        p.cert = env_int("SSB_ASM_CERT", 1);  // 0 off; 2 = no margin (test-only, wrong bits)
     }
     return nr1_ok() ? launch_tile_t<true>(s, p, pow2) : launch_tile_t<false>(s, p, pow2);
 }

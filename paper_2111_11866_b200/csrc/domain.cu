@@ -232,6 +232,7 @@ AsmArgs Slab::asm_args(PField u, bool with_G, double tau, double eps) const {
     }
     a.eps = eps;
     a.bad = flags.p;
+    a.guard = flags.p + 2;  // the tile kernel's range guard: flags[2] out of range, flags[3] max |u| high word
     return a;
 }
 
@@ -252,7 +253,7 @@ void Slab::assemble(PField u, bool with_G, double tau, double eps, double* off_o
     }
     a.eps = eps;
     a.bad = flags.p;
-    a.guard = flags.p + 2;  // the tile kernel's scaled-gradient guard (flags[1]: threshold)
+    a.guard = flags.p + 2;  // the tile kernel's range guard: flags[2] out of range, flags[3] max |u| high word (flags[1]: threshold)
     a.off_out = off_out;
     a.diag_out = diag_out;
     a.abar_out = abar_out;

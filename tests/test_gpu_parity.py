@@ -472,3 +472,57 @@ def test_tile_assembly_coefficients_vs_oracle(gpu, oracle, case):
     st, off_ref, _, _ = oracle.assemble_step(og, u, None, tau, eps)
     assert st == 0
     assert_bits(off_gpu, off_ref, f"tile assembly, {case}")
+
+
+def _cert_field(dims, seed, sharp):
+    """u in [0, 1] as segmentation iterates are: a smooth 4D profile (or, sharp, a ball with a
+    one-doxel edge: gradients ~ 1/h) plus noise, Dirichlet ghosts 0 (the reference's setting)."""
+    rng = np.random.default_rng(seed)
+    n1, n2, n3, n4 = dims
+    l, k, j, i = np.meshgrid(*[np.arange(n) for n in dims[::-1]], indexing="ij")
+    r = np.sqrt(((i - n1 / 2) / n1) ** 2 + ((j - n2 / 2) / n2) ** 2 + ((k - n3 / 2) / n3) ** 2
+                + ((l - n4 / 2) / n4) ** 2)
+    prof = (r < 0.3).astype(float) if sharp else 1.0 / (1.0 + 8.0 * r)
+    u = np.zeros(cs.shape(dims))
+    u[1:-1, 1:-1, 1:-1, 1:-1] = np.clip(prof + rng.normal(0, 0.02, prof.shape), 0.0, 1.0)
+    return u
+
+
+def _assemble_session(gpu, g, u, tau, eps):
+    dims = (g.n1, g.n2, g.n3, g.n4)
+    img = cs.f32_image(dims, 7)
+    rows = [(f, dims[0] / 2, dims[1] / 2, dims[2] / 2, 3.0) for f in range(dims[3])]
+    p = gpu.seg_params(tau=tau, epsilon=eps, omega=1.4, sor_tol=1e-9, n_steps=1, sigma=0.1, K=0.0, delta=0.5,
+                       vartheta=0.5, rescale_radius=2.0)
+    with gpu.Session(g) as s:
+        s.prepare(img, rows, p, None)
+        s.set_u(u)
+        return s.assemble_export()
+
+
+@pytest.mark.parametrize("h,sharp", [(1 / 32, False), (1 / 64, False), (1 / 32, True), (1 / 128, True)])
+def test_certified_face_gradients_vs_oracle(gpu, oracle, h, sharp, monkeypatch):
+    """The certified face gradients (assemble_tile.cu face_sq_cert: central differences instead
+    of the reference's rounded corner sums, within a proven bound of its |grad_f u|^2, the float
+    rounding decision trusted only outside that bound) give the reference's coefficients bit for
+    bit on ~0.9 M doxels (7 M faces) of u in [0, 1], smooth and with sharp edges, at h = 1/32,
+    1/64, 1/128; so do the exact scaled gradients (SSB_ASM_CERT=0).  With no margin
+    (SSB_ASM_CERT=2, test-only) some coefficients must come out wrong: the path under test is the
+    one that ran, and its margin is what keeps it exact."""
+    from oracle import oracle_py as op
+    dims = (64, 30, 24, 20)
+    g = gpu.Grid.make(dims, h)
+    tau, eps = h, 1e-3
+    u = _cert_field(dims, 11 + int(sharp), sharp)
+    st, off_ref, _, _ = oracle.assemble_step(op.Grid.make(dims, h), u, None, tau, eps)
+    assert st == 0
+    monkeypatch.setenv("SSB_ASM_CERT", "1")
+    assert_bits(_assemble_session(gpu, g, u, tau, eps), off_ref, f"certified gradients h={h} sharp={sharp}")
+    monkeypatch.setenv("SSB_ASM_CERT", "0")
+    assert_bits(_assemble_session(gpu, g, u, tau, eps), off_ref, f"exact scaled gradients h={h} sharp={sharp}")
+    if not sharp and h == 1 / 64:
+        monkeypatch.setenv("SSB_ASM_CERT", "2")
+        off_bad = _assemble_session(gpu, g, u, tau, eps)
+        wrong = int(np.count_nonzero(off_bad.view(np.uint64) != off_ref.view(np.uint64)))
+        print(f"no-margin certified gradients: {wrong} of {off_ref.size} coefficients differ")
+        assert wrong > 0
