@@ -138,16 +138,31 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sptr(bar)) : "memory");
 }
+#ifndef SSB_SOR_SUSPEND
+#define SSB_SOR_SUSPEND 0  // try_wait suspend-time hint in ns (0: the hardware's default)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(sptr(bar)),
-        "r"(parity)
-        : "memory");
+    if constexpr (SSB_SOR_SUSPEND > 0) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+            "@!p bra WAIT_%=;\n"
+            "}\n" ::"r"(sptr(bar)),
+            "r"(parity), "n"(SSB_SOR_SUSPEND)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            "@!p bra WAIT_%=;\n"
+            "}\n" ::"r"(sptr(bar)),
+            "r"(parity)
+            : "memory");
+    }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
     asm volatile(

@@ -12,6 +12,8 @@ wl = workloads.CONFIGS[cfg]()
 g = ss.Grid.make(wl.dims, wl.h)
 s = ss.Session(g)
 s.prepare(wl.image, wl.rows, ss.seg_params(**{**wl.params, "n_steps": 5}), wl.u0)
+if os.environ.get("SUBSURF_KERNEL"):
+    s.set_kernel(os.environ["SUBSURF_KERNEL"])
 st = torch.cuda.ExternalStream(s.stream)
 s.fixed_sweeps(20)
 lines = []
@@ -31,6 +33,6 @@ proc.terminate()
 ms = e0.elapsed_time(e1)
 vals = [[float(x) for x in l.split(",")] for l in lines if l.count(",") == 2]
 vals = vals[len(vals) // 4:]  # steady state
-print(json.dumps(dict(config=cfg, lib=os.environ.get("SUBSURF_B200_LIB"), us_per_sweep=1e3 * ms / N,
+print(json.dumps(dict(config=cfg, lib=os.environ.get("SUBSURF_B200_LIB"), kernel=os.environ.get("SUBSURF_KERNEL"), us_per_sweep=1e3 * ms / N,
                       sm_mhz=statistics.median(v[0] for v in vals), power_w=statistics.median(v[1] for v in vals),
                       mem_mhz=statistics.median(v[2] for v in vals), samples=len(vals))))
