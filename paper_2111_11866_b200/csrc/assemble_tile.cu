@@ -205,22 +205,22 @@ __device__ __forceinline__ double scale_h(double x, const double* h, const doubl
 
 // corner-average difference along tangent T of face F (edge.cpp:16-22, :43-45):
 // (0.25*(((p0 + pn) + p_t) + p_nt) - 0.25*(((p0 + pn) + p_-t) + p_n-t)) / h_T
-template <int F, int T, bool POW2>
-__device__ __forceinline__ double tangent(const SStencil& S, const double* h, const double* hinv, double p0pn) {
+template <int F, int T, bool POW2, class ST>
+__device__ __forceinline__ double tangent(const ST& S, const double* h, const double* hinv, double p0pn) {
     constexpr int A = F >> 1, SG = (F & 1) ? 1 : -1;
     constexpr int ai = A == 0 ? SG : 0, aj = A == 1 ? SG : 0, ak = A == 2 ? SG : 0, al = A == 3 ? SG : 0;
     constexpr int ti = T == 0, tj = T == 1, tk = T == 2, tl = T == 3;
-    const double plus = 0.25 * (p0pn + S.at<ti, tj, tk, tl>() + S.at<ai + ti, aj + tj, ak + tk, al + tl>());
-    const double minus = 0.25 * (p0pn + S.at<-ti, -tj, -tk, -tl>() + S.at<ai - ti, aj - tj, ak - tk, al - tl>());
+    const double plus = 0.25 * (p0pn + S.template at<ti, tj, tk, tl>() + S.template at<ai + ti, aj + tj, ak + tk, al + tl>());
+    const double minus = 0.25 * (p0pn + S.template at<-ti, -tj, -tk, -tl>() + S.template at<ai - ti, aj - tj, ak - tk, al - tl>());
     return scale_h<POW2>(plus - minus, h, hinv, T);
 }
 
 // face_gradient (edge.cpp:33-48) of face F
-template <int F, bool POW2>
-__device__ __forceinline__ void face_grad(const SStencil& S, const double* h, const double* hinv, double p0,
+template <int F, bool POW2, class ST>
+__device__ __forceinline__ void face_grad(const ST& S, const double* h, const double* hinv, double p0,
                                           double g[4]) {
     constexpr int A = F >> 1, SG = (F & 1) ? 1 : -1;
-    const double pn = S.at<A == 0 ? SG : 0, A == 1 ? SG : 0, A == 2 ? SG : 0, A == 3 ? SG : 0>();
+    const double pn = S.template at<A == 0 ? SG : 0, A == 1 ? SG : 0, A == 2 ? SG : 0, A == 3 ? SG : 0>();
     g[A] = scale_h<POW2>((double)SG * (pn - p0), h, hinv, A);
     const double p0pn = p0 + pn;
     if constexpr (A != 0) g[0] = tangent<F, 0, POW2>(S, h, hinv, p0pn);
@@ -229,8 +229,8 @@ __device__ __forceinline__ void face_grad(const SStencil& S, const double* h, co
     if constexpr (A != 3) g[3] = tangent<F, 3, POW2>(S, h, hinv, p0pn);
 }
 
-template <int F, bool POW2>
-__device__ __forceinline__ double face_sq(const SStencil& S, const double* h, const double* hinv, double p0) {
+template <int F, bool POW2, class ST>
+__device__ __forceinline__ double face_sq(const ST& S, const double* h, const double* hinv, double p0) {
     double g[4];
     face_grad<F, POW2>(S, h, hinv, p0, g);
     return g[0] * g[0] + g[1] * g[1] + g[2] * g[2] + g[3] * g[3];  // edge.cpp:53-54
@@ -244,19 +244,19 @@ __device__ __forceinline__ double face_sq(const SStencil& S, const double* h, co
 // or overflows: guaranteed when every staged value is 0 or within [2^-400, 2^400] (the
 // per-step guard, assemble_guard_kernel) and hinv within [2^-40, 2^40] (host).  8 FP64
 // instructions per face fewer than face_sq (the 0.25 and 1/h products).
-template <int F>
-__device__ __forceinline__ double face_sq_scaled(const SStencil& S, double p0) {
+template <int F, class ST>
+__device__ __forceinline__ double face_sq_scaled(const ST& S, double p0) {
     constexpr int A = F >> 1, SG = (F & 1) ? 1 : -1;
     constexpr int ai = A == 0 ? SG : 0, aj = A == 1 ? SG : 0, ak = A == 2 ? SG : 0, al = A == 3 ? SG : 0;
-    const double pn = S.at<ai, aj, ak, al>();
+    const double pn = S.template at<ai, aj, ak, al>();
     const double p0pn = p0 + pn;
     double d[4];
     d[A] = 4.0 * (pn - p0);
 #define SSB_SCALED_TANGENT(T)                                                                        \
     if constexpr (A != T) {                                                                           \
         constexpr int ti = T == 0, tj = T == 1, tk = T == 2, tl = T == 3;                              \
-        const double X = p0pn + S.at<ti, tj, tk, tl>() + S.at<ai + ti, aj + tj, ak + tk, al + tl>();   \
-        const double Y = p0pn + S.at<-ti, -tj, -tk, -tl>() + S.at<ai - ti, aj - tj, ak - tk, al - tl>(); \
+        const double X = p0pn + S.template at<ti, tj, tk, tl>() + S.template at<ai + ti, aj + tj, ak + tk, al + tl>();   \
+        const double Y = p0pn + S.template at<-ti, -tj, -tk, -tl>() + S.template at<ai - ti, aj - tj, ak - tk, al - tl>(); \
         d[T] = X - Y;                                                                                  \
     }
     SSB_SCALED_TANGENT(0)
@@ -284,16 +284,16 @@ __device__ __forceinline__ double face_sq_scaled(const SStencil& S, double p0) {
 // own budget: the float rounding decision is trusted only >= T = 1.25 (budget + rho 2^53) ulps
 // from a midpoint, otherwise the doxel takes the exact sequence (face_sq_scaled + sqrt/div).
 // ~108 instead of ~216 FP64 instructions per doxel for the eight faces.
-template <int F>
-__device__ __forceinline__ double face_sq_cert(const SStencil& S, double p0, const double c[4]) {
+template <int F, class ST>
+__device__ __forceinline__ double face_sq_cert(const ST& S, double p0, const double c[4]) {
     constexpr int A = F >> 1, SG = (F & 1) ? 1 : -1;
     constexpr int ai = A == 0 ? SG : 0, aj = A == 1 ? SG : 0, ak = A == 2 ? SG : 0, al = A == 3 ? SG : 0;
-    const double n4 = 4.0 * (S.at<ai, aj, ak, al>() - p0);
+    const double n4 = 4.0 * (S.template at<ai, aj, ak, al>() - p0);
     double acc = __dmul_rn(n4, n4);
 #define SSB_CERT_TANGENT(T)                                                                              \
     if constexpr (A != T) {                                                                               \
         constexpr int ti = T == 0, tj = T == 1, tk = T == 2, tl = T == 3;                                  \
-        const double d = c[T] + (S.at<ai + ti, aj + tj, ak + tk, al + tl>() - S.at<ai - ti, aj - tj, ak - tk, al - tl>()); \
+        const double d = c[T] + (S.template at<ai + ti, aj + tj, ak + tk, al + tl>() - S.template at<ai - ti, aj - tj, ak - tk, al - tl>()); \
         acc = __fma_rn(d, d, acc);                                                                        \
     }
     SSB_CERT_TANGENT(0)
@@ -390,8 +390,8 @@ constexpr bool GPREF_L1 = SSB_ASMT_L1PREF != 0;
 struct Coef8 {
     float4 lo, hi;
 };
-template <bool POW2>
-__device__ __noinline__ Coef8 exact_doxel(const SStencil S, double p0, bool scaled, const AsmTileArgs& p, double g0,
+template <bool POW2, class ST>
+__device__ __noinline__ Coef8 exact_doxel(const ST S, double p0, bool scaled, const AsmTileArgs& p, double g0,
                                           double g1, double g2, double g3, double g4, double g5, double g6,
                                           double g7) {
     const AsmArgs& a = p.a;
@@ -517,14 +517,14 @@ __global__ void __launch_bounds__(kThreadsT, MINB) assemble_tile_kernel(const __
 #pragma unroll
                 for (int f = 0; f < 8; ++f) gv[f] = 1.0;
             }
-            const double p0 = S.at<0, 0, 0, 0>();
+            const double p0 = S.template at<0, 0, 0, 0>();
             double x2[8];
             if (cert_T) {  // within rho A_f^2 of the exact values (face_sq_cert)
                 double cc[4];
-                cc[0] = S.at<1, 0, 0, 0>() - S.at<-1, 0, 0, 0>();
-                cc[1] = S.at<0, 1, 0, 0>() - S.at<0, -1, 0, 0>();
-                cc[2] = S.at<0, 0, 1, 0>() - S.at<0, 0, -1, 0>();
-                cc[3] = S.at<0, 0, 0, 1>() - S.at<0, 0, 0, -1>();
+                cc[0] = S.template at<1, 0, 0, 0>() - S.template at<-1, 0, 0, 0>();
+                cc[1] = S.template at<0, 1, 0, 0>() - S.template at<0, -1, 0, 0>();
+                cc[2] = S.template at<0, 0, 1, 0>() - S.template at<0, 0, -1, 0>();
+                cc[3] = S.template at<0, 0, 0, 1>() - S.template at<0, 0, 0, -1>();
                 const double sg = p.sigma;
                 x2[0] = __fma_rn(sg, face_sq_cert<0>(S, p0, cc), a.eps);
                 x2[1] = __fma_rn(sg, face_sq_cert<1>(S, p0, cc), a.eps);
