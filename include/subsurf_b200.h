@@ -235,6 +235,16 @@ SS_API ss_status ss_session_fixed_sweeps(ss_session* s, int n_sweeps, double* re
  * neighbour is in.  ss_session_set_u_interior / _get_u_interior: the copies alone. */
 SS_API ss_status ss_session_step_host(ss_session* s, const double* u_in, double* u_out, int n_sweeps,
                                       ss_step_diag* diag);
+/* ss_session_step_host with the result's download left in flight (ABI 6; single slab,
+ * page-locked u_in / u_out, else exactly ss_session_step_host): returns once the step is
+ * computed and its D2H enqueued; u_out is complete after ss_session_wait (or any call that
+ * reads it).  When the next call's u_in is this call's u_out, every upload chunk waits on
+ * the device for its download chunk, so the D2H of step n and the H2D of step n + 1 run
+ * concurrently in the two PCIe directions; the data still makes the full round trip. */
+SS_API ss_status ss_session_step_host_async(ss_session* s, const double* u_in, double* u_out, int n_sweeps,
+                                            ss_step_diag* diag);
+/* wait for every transfer of ss_session_step_host_async and the session's stream */
+SS_API ss_status ss_session_wait(ss_session* s);
 SS_API ss_status ss_session_set_u_interior(ss_session* s, const double* u);
 SS_API ss_status ss_session_get_u_interior(ss_session* s, double* u);
 /* one time step of BASELINE config 4 (ABI 5): ss_session_step with exactly n_sweeps

@@ -218,6 +218,8 @@ def library() -> C.CDLL:
     sig("ss_selftest_rsqrt", [_D])
     sig("ss_session_assemble_export", [C.c_void_p, _D])
     sig("ss_session_step_host", [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(StepDiag)])
+    sig("ss_session_step_host_async", [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(StepDiag)])
+    sig("ss_session_wait", [C.c_void_p])
     sig("ss_session_set_u_interior", [C.c_void_p, C.c_void_p])
     sig("ss_session_get_u_interior", [C.c_void_p, C.c_void_p])
     sig("ss_session_set_loop_mode", [C.c_void_p, C.c_int])
@@ -617,6 +619,22 @@ class Session:
                                             C.byref(d) if diag else None)
         _check(st, d.iterations, d.residual)
         return dict(iterations=d.iterations, residual=d.residual, tol=d.tol, umin=d.umin, umax=d.umax) if diag else None
+
+    def step_host_async(self, u_in=None, u_out=None, n_sweeps: int = 0, diag: bool = True):
+        """step_host with the result's download left in flight (single slab, page-locked
+        buffers given as pointers; otherwise step_host): u_out is complete after wait().  When
+        the next call's u_in is this call's u_out, each upload chunk waits on the device for its
+        download chunk -- the D2H of step n and the H2D of step n + 1 overlap."""
+        d = StepDiag()
+        p_in = None if u_in is None else C.c_void_p(int(u_in))
+        p_out = None if u_out is None else C.c_void_p(int(u_out))
+        st = library().ss_session_step_host_async(self._h, p_in, p_out, n_sweeps, C.byref(d) if diag else None)
+        _check(st, d.iterations, d.residual)
+        return dict(iterations=d.iterations, residual=d.residual, tol=d.tol, umin=d.umin, umax=d.umax) if diag else None
+
+    def wait(self) -> None:
+        """Every transfer of step_host_async done (and the session's stream idle)."""
+        _check(library().ss_session_wait(self._h))
 
     def assemble_export(self) -> np.ndarray:
         """The off-diagonals the next step would assemble at the session's u (the device

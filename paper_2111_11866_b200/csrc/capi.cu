@@ -98,7 +98,7 @@ struct ss_session {
 extern "C" {
 
 const char* ss_last_error(void) { return t_err.c_str(); }
-int ss_abi_version(void) { return 5; }
+int ss_abi_version(void) { return 6; }
 unsigned long long ss_launch_count(void) { return g_launches.load(); }
 
 int ss_device_available(void) {
@@ -656,10 +656,38 @@ ss_status ss_session_step_host(ss_session* s, const double* u_in, double* u_out,
     });
 }
 
+ss_status ss_session_step_host_async(ss_session* s, const double* u_in, double* u_out, int n_sweeps,
+                                     ss_step_diag* diag) {
+    return guard([&] {
+        require(s != nullptr, "null session");
+        require(n_sweeps >= 0, "n_sweeps must be >= 0");
+        SSB_CUDA(cudaSetDevice(s->d->device));
+        try {
+            s->d->step_host_async(u_in, u_out, n_sweeps, diag);
+        } catch (const SolverErrT& e) {
+            if (diag) {
+                diag->iterations = e.iterations;
+                diag->residual = e.residual;
+            }
+            throw;
+        }
+    });
+}
+
+ss_status ss_session_wait(ss_session* s) {
+    return guard([&] {
+        require(s != nullptr, "null session");
+        SSB_CUDA(cudaSetDevice(s->d->device));
+        s->d->wait_transfers();
+        s->d->sync();
+    });
+}
+
 ss_status ss_session_set_u_interior(ss_session* s, const double* u) {
     return guard([&] {
         require(s && u, "null session / buffer");
         SSB_CUDA(cudaSetDevice(s->d->device));
+        s->d->wait_transfers();
         s->d->set_u_interior(u);
         s->d->sync();
     });
@@ -669,6 +697,7 @@ ss_status ss_session_get_u_interior(ss_session* s, double* u) {
     return guard([&] {
         require(s && u, "null session / buffer");
         SSB_CUDA(cudaSetDevice(s->d->device));
+        s->d->wait_transfers();
         s->d->get_u_interior(u);
     });
 }

@@ -189,6 +189,11 @@ double* Slab::stage_p() {
     stage.alloc(L.P);
     return stage.p;
 }
+
+double* Slab::dstage_p() {
+    dstage.alloc(L.P);
+    return dstage.p;
+}
 double* Slab::stage8_p() {
     stage8.alloc(L.P * 8);
     return stage8.p;
@@ -417,6 +422,7 @@ void Domain::init_common() {
     SSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     SSB_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
     SSB_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    SSB_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
     // the end slices and the halo exchange run on high-priority streams: the interior
     // pass is a persistent grid that fills every CTA slot, and pending CTAs of a
     // higher-priority stream (the end slices, the NCCL exchange kernels) are scheduled
@@ -511,6 +517,9 @@ Domain::~Domain() {
     if (h2d) cudaStreamSynchronize(h2d);
     for (auto e : up_ev) cudaEventDestroy(e);
     if (h2d) cudaStreamDestroy(h2d);
+    if (d2h) cudaStreamSynchronize(d2h);
+    for (auto e : dn_ev) cudaEventDestroy(e);
+    if (d2h) cudaStreamDestroy(d2h);
     if (comm) cudaStreamDestroy(comm);
 }
 
@@ -1249,8 +1258,12 @@ void Domain::upload_assemble(const double* host) {
     SSB_CUDA(cudaEventRecord(up_ev[C], stream));  // earlier users of the staging buffer are done
     SSB_CUDA(cudaStreamWaitEvent(h2d, up_ev[C], 0));
     auto lo = [&](int q) { return 1 + (int)((long long)q * n4 / C); };
+    // this input is the previous step's result still on its way down (step_host_async): each
+    // chunk goes up as soon as it has come down (same chunks), device-ordered, no host wait
+    const bool chained = dn_host == host && (int)dn_ev.size() >= 2 * C + 1;
     for (int q = 0; q < C; ++q) {
         const int a = lo(q), b = lo(q + 1) - 1;
+        if (chained) SSB_CUDA(cudaStreamWaitEvent(h2d, dn_ev[q], 0));
         SSB_CUDA(cudaMemcpyAsync(st + (a - 1) * fr, host + (a - 1) * fr, (size_t)(b - a + 1) * fr * sizeof(double),
                                  cudaMemcpyHostToDevice, h2d));
         SSB_CUDA(cudaEventRecord(up_ev[q], h2d));
@@ -1271,8 +1284,56 @@ void Domain::upload_assemble(const double* host) {
 
 SolveOut Domain::step_host(const double* in, double* out, int fixed, ss_step_diag* diag) {
     const SolveOut o = step_impl(diag, fixed, true, in);
+    wait_transfers();
     if (out) get_u_interior(out);
     return o;
+}
+
+// the result's compact interior to page-locked `host` in slice chunks on the d2h stream: the
+// unpack of chunk q + 1 (main stream, its own staging buffer) overlaps the copy of chunk q; no
+// host wait (wait_transfers)
+void Domain::download_async(double* host) {
+    Slab& x = *sp[0];
+    const long long fr = (long long)g.n1 * g.n2 * g.n3;
+    const int n4 = x.L.n4, C = std::min(n4, 8);
+    while ((int)dn_ev.size() < 2 * C + 1) {
+        cudaEvent_t e;
+        SSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        dn_ev.push_back(e);
+    }
+    double* d = x.dstage_p();
+    for (int q = 0; q < C; ++q) {
+        const int a = 1 + (int)((long long)q * n4 / C), b = (int)((long long)(q + 1) * n4 / C);
+        SSB_CUDA(cudaStreamWaitEvent(stream, dn_ev[q], 0));  // the previous copy out of this staging chunk
+        launch_unpack_interior(stream, x.L, x.S[cur].pf(), d, a, b);
+        SSB_CUDA(cudaEventRecord(dn_ev[C + q], stream));
+        SSB_CUDA(cudaStreamWaitEvent(d2h, dn_ev[C + q], 0));
+        SSB_CUDA(cudaMemcpyAsync(host + (a - 1) * fr, d + (a - 1) * fr, (size_t)(b - a + 1) * fr * sizeof(double),
+                                 cudaMemcpyDeviceToHost, d2h));
+        SSB_CUDA(cudaEventRecord(dn_ev[q], d2h));
+    }
+    dn_host = host;
+}
+
+SolveOut Domain::step_host_async(const double* in, double* out, int fixed, ss_step_diag* diag) {
+    const bool async = single() && out && host_pinned(out) && (!in || host_pinned(in)) &&
+                       assemble_tile_supported(sp[0]->L);
+    if (!async) return step_host(in, out, fixed, diag);
+    if (dn_host && dn_host != in) wait_transfers();  // only a chained input may still be in flight
+    const SolveOut o = step_impl(diag, fixed, true, in);
+    if (dn_host) wait_transfers();  // (a chained download is complete: the upload waited for it)
+    download_async(out);
+    return o;
+}
+
+// every transfer of step_host_async complete (host), and the main stream ordered after them
+void Domain::wait_transfers() {
+    if (!dn_host) return;
+    const int C = (int)(dn_ev.size() - 1) / 2;
+    SSB_CUDA(cudaEventRecord(dn_ev[2 * C], d2h));
+    SSB_CUDA(cudaStreamWaitEvent(stream, dn_ev[2 * C], 0));
+    SSB_CUDA(cudaStreamSynchronize(d2h));
+    dn_host = nullptr;
 }
 
 SolveOut Domain::step_impl(ss_step_diag* diag, int fixed, bool rescale, const double* host_in) {

@@ -118,11 +118,13 @@ struct Slab {
     Dev<int> flags;
     Dev<double> bad_all;     // all-gathered assembly flags (world doubles; slab groups / ranks)
     Dev<double> stage, stage8;
+    Dev<double> dstage;      // step_host_async: the download staging (the upload keeps `stage`)
     BallSet rescale_balls;
 
     Slab(const ss_grid& global, int l0, int n4_local, int index, int chunk, int world,
          cudaStream_t s);
     double* stage_p();
+    double* dstage_p();
     double* stage8_p();
     void upload(const double* host_padded, PField dst, PField twin0 = PField(), PField twin1 = PField(),
                 PField twin2 = PField());
@@ -296,12 +298,23 @@ struct Domain {
     SolveOut step_host(const double* in, double* out, int fixed, ss_step_diag* diag);
     void set_u_interior(const double* host);
     void get_u_interior(double* host);
+    // step_host with the result's download left in flight (single slab, page-locked buffers;
+    // otherwise exactly step_host): out is complete after wait_transfers(), and when the next
+    // call's input is this call's output, each upload chunk waits on the device for its
+    // download chunk, so the D2H of step n and the H2D of step n + 1 run concurrently on the
+    // two copy directions (ss_session_step_host_async)
+    SolveOut step_host_async(const double* in, double* out, int fixed, ss_step_diag* diag);
+    void wait_transfers();
     // EOC verification row (eoc.cpp:83-137) on an n^4 session; returns the space-time L2 error
     double eoc_row(int n, double omega, double sor_tol, int max_iter, long long* total_sweeps);
 
 private:
     cudaStream_t h2d = nullptr;        // step_host: chunked upload of the step's input
     std::vector<cudaEvent_t> up_ev;   // ... one event per chunk (+ the staging-free event)
+    cudaStream_t d2h = nullptr;        // step_host_async: chunked download of the step's result
+    std::vector<cudaEvent_t> dn_ev;   // ... per chunk: unpacked (C + q) / copied (q); [2C]: all copied
+    const double* dn_host = nullptr;  // the host buffer the in-flight download writes (null: none)
+    void download_async(double* host);
     SolveOut step_impl(ss_step_diag* diag, int fixed, bool rescale, const double* host_in);
     void upload_assemble(const double* host);
     void init_common();

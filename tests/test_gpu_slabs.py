@@ -284,6 +284,50 @@ def test_step_host_matches_device_steps(gpu, n_slabs, pinned):
         assert np.array_equal(a.get_u_interior(), want * 0.5)
 
 
+@pytest.mark.parametrize("chunks_slices", [(20, 14, 10, 11), (16, 12, 8, 5)])
+def test_step_host_async_chain_matches_device_steps(gpu, chunks_slices):
+    """ss_session_step_host_async (ABI 6): the result's download left in flight, the next
+    step's upload of that same buffer chained to it on the device chunk by chunk -- K steps
+    through host memory == K device steps bit for bit, with a mid-run switch to a fresh input
+    buffer (not chained: waits for the download first) and the synchronous call in between."""
+    import torch
+    import workloads
+    wl = workloads.small(chunks_slices, seed=23)
+    g = gpu.Grid.make(wl.dims, wl.h)
+    p = gpu.seg_params(**{**wl.params, "n_steps": 8, "sor_rel_tol": 1e-8, "rescale_radius": 3.0})
+    inner = (slice(1, -1),) * 4
+    with gpu.Session(g) as a, gpu.Session(g) as b:
+        a.prepare(wl.image, wl.rows, p, wl.u0)
+        b.prepare(wl.image, wl.rows, p, wl.u0)
+        shape = a.interior_shape
+        bufs = [torch.empty(shape, dtype=torch.float64).pin_memory() for _ in range(3)]
+        bufs[0].copy_(torch.from_numpy(np.ascontiguousarray(b.get_u()[inner])))
+        order = [(0, 1, 0), (1, 0, 0), (0, 1, 7), (2, 0, 0), (0, 1, 0), (1, 2, 5)]
+        for n, (i, o, fixed) in enumerate(order):
+            if i == 2:  # a fresh input buffer: the host copies the last result into it
+                a.wait()
+                bufs[2].copy_(bufs[1 if order[n - 1][1] == 1 else 0])
+            if n == 3:
+                da = a.step_host(bufs[i].data_ptr(), bufs[o].data_ptr(), fixed)
+            else:
+                da = a.step_host_async(bufs[i].data_ptr(), bufs[o].data_ptr(), fixed)
+            db = b.step_fixed(fixed) if fixed else b.step()
+            assert [da[k] for k in ("iterations", "umin", "umax")] == [db[k] for k in ("iterations", "umin", "umax")], n
+            a.wait()
+            want = np.ascontiguousarray(b.get_u()[inner])
+            assert np.array_equal(bufs[o].numpy().view(np.uint64), want.view(np.uint64)), n
+        # a chain of async steps with every input still on its way down, waited for once
+        a.wait()
+        bufs[0].copy_(torch.from_numpy(np.ascontiguousarray(b.get_u()[inner])))
+        for n in range(5):
+            fixed = 6 if n == 2 else 0
+            da = a.step_host_async(bufs[n % 2].data_ptr(), bufs[(n + 1) % 2].data_ptr(), fixed)
+            db = b.step_fixed(fixed) if fixed else b.step()
+            assert da["iterations"] == db["iterations"], n
+        a.wait()
+        assert np.array_equal(bufs[1].numpy().view(np.uint64), np.ascontiguousarray(b.get_u()[inner]).view(np.uint64))
+
+
 @pytest.mark.parametrize("n_slabs", [1, 3])
 def test_fixed_sweep_steps_vs_oracle(gpu, oracle, n_slabs):
     """ss_session_step_fixed (BASELINE config 4's time step) on 1 and 3 slabs against the C
