@@ -164,6 +164,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "memory");
     }
 }
+__device__ __forceinline__ void mbar_expect_tx_u(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// bulk copy with the destination and barrier as shared-window addresses
+__device__ __forceinline__ void bulk_g2s_u(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
@@ -404,26 +415,41 @@ __device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsi
         }
         return;
     }
+    // the item's five row blocks of plane k0; every stream advances by one plane (jMax rows)
+    // per stage, so the loop only adds strides (the per-plane products were a third of the
+    // producer's instructions, and producer instructions take issue slots from the consumers)
+    const long long row0 = ((long long)it.l * L.kMax + it.k0) * L.jMax + it.j0;  // row (j0, k0, l)
+    const char* pc = reinterpret_cast<const char*>(coef + row0 * L.Wc * 8);
+    const char* pr = reinterpret_cast<const char*>(rhs + row0 * W);
+    const char* pu = reinterpret_cast<const char*>(uc + row0 * W);
+    const char* pm = reinterpret_cast<const char*>(uo + (row0 - plane_rows) * W);
+    const char* pp = reinterpret_cast<const char*>(uo + (row0 + plane_rows) * W);
+    const long long dc = (long long)L.jMax * L.Wc * 32, ds = (long long)L.jMax * W * 8;
+    const uint32_t bc = it.rows * G.coef_row_bytes, br = it.rows * rb;
+    // part 0: every stream; split producers: part 1 coef / rhs / own colour, part 2 the l +- 1 rows
+    const uint32_t b1 = (HEAT ? 0u : bc) + 2u * br, b2 = 2u * br;
+    const uint32_t tx = part == 0 ? b1 + b2 : part == 1 ? b1 : b2;
+    const uint32_t sm0 = sptr(smem), bar0 = sptr(full);
     for (int p = it.k0; p <= it.k1; ++p) {
         rg.acquire(empty);
-        unsigned char* s = smem + rg.slot * G.main_bytes;
-        uint64_t* bar = &full[rg.slot];
-        const long long row0 = ((long long)it.l * L.kMax + p) * L.jMax + it.j0;  // row (j0, p, l)
+        const uint32_t st = sm0 + rg.slot * G.main_bytes, bar = bar0 + rg.slot * 8u;
         if (issue) {
-            // part 0: every stream; split producers: part 1 coef / rhs / own colour, part 2 the l +- 1 rows
-            const uint32_t b1 = (HEAT ? 0u : it.rows * G.coef_row_bytes) + 2u * it.rows * rb, b2 = 2u * it.rows * rb;
-            mbar_expect_tx(bar, part == 0 ? b1 + b2 : part == 1 ? b1 : b2);
+            mbar_expect_tx_u(bar, tx);
             if (part != 2) {
-                if (!HEAT)
-                    bulk_g2s(s + G.off_coef, coef + row0 * L.Wc * 8, it.rows * G.coef_row_bytes, bar, pol.stream);
-                bulk_g2s(s + G.off_rhs, rhs + row0 * W, it.rows * rb, bar, pol.stream);
-                bulk_g2s(s + G.off_uc, uc + row0 * W, it.rows * rb, bar, pol.uload);
+                if (!HEAT) bulk_g2s_u(st + G.off_coef, pc, bc, bar, pol.stream);
+                bulk_g2s_u(st + G.off_rhs, pr, br, bar, pol.stream);
+                bulk_g2s_u(st + G.off_uc, pu, br, bar, pol.uload);
             }
             if (part != 1) {
-                bulk_g2s(s + G.off_ulm, uo + (row0 - plane_rows) * W, it.rows * rb, bar, pol.uload);
-                bulk_g2s(s + G.off_ulp, uo + (row0 + plane_rows) * W, it.rows * rb, bar, pol.uload);
+                bulk_g2s_u(st + G.off_ulm, pm, br, bar, pol.uload);
+                bulk_g2s_u(st + G.off_ulp, pp, br, bar, pol.uload);
             }
         }
+        pc += dc;
+        pr += ds;
+        pu += ds;
+        pm += ds;
+        pp += ds;
         rg.advance();
     }
 }
@@ -449,15 +475,20 @@ __device__ __forceinline__ void produce_uk(const Layout& L, const Geo& G, unsign
         }
         return;
     }
+    // rows j0-1 .. j0+rows of plane k0-1, advancing one plane per stage
+    const char* pk =
+        reinterpret_cast<const char*>(uo + ((((long long)it.l * L.kMax + it.k0 - 1) * L.jMax + it.j0) - 1) * W);
+    const long long ds = (long long)L.jMax * W * 8;
+    const uint32_t bytes = (it.rows + 2) * rb;
+    const uint32_t sk0 = sptr(smem) + G.off_ukring, bar0 = sptr(full);
     for (int p = it.k0 - 1; p <= it.k1 + 1; ++p) {
         rg.acquire(empty);
-        unsigned char* s = smem + G.off_ukring + rg.slot * G.uk_bytes;
-        uint64_t* bar = &full[rg.slot];
-        const long long row0 = ((long long)it.l * L.kMax + p) * L.jMax + it.j0;
+        const uint32_t bar = bar0 + rg.slot * 8u;
         if (issue) {
-            mbar_expect_tx(bar, (it.rows + 2) * rb);
-            bulk_g2s(s, uo + (row0 - 1) * W, (it.rows + 2) * rb, bar, pol.uload);
+            mbar_expect_tx_u(bar, bytes);
+            bulk_g2s_u(sk0 + rg.slot * G.uk_bytes, pk, bytes, bar, pol.uload);
         }
+        pk += ds;
         rg.advance();
     }
 }
