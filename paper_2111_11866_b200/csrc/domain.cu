@@ -1211,11 +1211,18 @@ void Domain::set_u_interior(const double* host) {
     }
 }
 
+// slice chunks of the host-buffer transfers (step_host*, get_u_interior): the chained upload
+// of step_host_async trails its download by one chunk
+#ifndef SSB_HOST_CHUNKS
+#define SSB_HOST_CHUNKS 16
+#endif
+constexpr int kHostChunks = SSB_HOST_CHUNKS;
+
 void Domain::get_u_interior(double* host) {
     const long long fr = (long long)g.n1 * g.n2 * g.n3;
     if (single() && host_pinned(host)) {  // slice chunks: unpack chunk q+1 while chunk q moves
         Slab& x = *sp[0];
-        const int n4 = x.L.n4, C = std::min(n4, 8);
+        const int n4 = x.L.n4, C = std::min(n4, kHostChunks);
         while ((int)up_ev.size() < C + 1) {
             cudaEvent_t e;
             SSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1248,7 +1255,7 @@ void Domain::get_u_interior(double* host) {
 void Domain::upload_assemble(const double* host) {
     Slab& x = *sp[0];
     const long long fr = (long long)g.n1 * g.n2 * g.n3;
-    const int n4 = x.L.n4, C = std::min(n4, 8);
+    const int n4 = x.L.n4, C = std::min(n4, kHostChunks);
     while ((int)up_ev.size() < C + 1) {
         cudaEvent_t e;
         SSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1295,7 +1302,7 @@ SolveOut Domain::step_host(const double* in, double* out, int fixed, ss_step_dia
 void Domain::download_async(double* host) {
     Slab& x = *sp[0];
     const long long fr = (long long)g.n1 * g.n2 * g.n3;
-    const int n4 = x.L.n4, C = std::min(n4, 8);
+    const int n4 = x.L.n4, C = std::min(n4, kHostChunks);
     while ((int)dn_ev.size() < 2 * C + 1) {
         cudaEvent_t e;
         SSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
