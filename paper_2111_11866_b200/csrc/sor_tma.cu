@@ -138,6 +138,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sptr(bar)) : "memory");
 }
+#ifndef SSB_SOR_FLOOR
+#define SSB_SOR_FLOOR 0
+#endif
+#ifndef SSB_SOR_NOLPM
+#define SSB_SOR_NOLPM 0  // (timing-only build, WRONG results) skip the l-1 / l+1 row copies
+#endif
 #ifndef SSB_SOR_SUSPEND
 #define SSB_SOR_SUSPEND 0  // try_wait suspend-time hint in ns (0: the hardware's default)
 #endif
@@ -427,7 +433,7 @@ __device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsi
     const long long dc = (long long)L.jMax * L.Wc * 32, ds = (long long)L.jMax * W * 8;
     const uint32_t bc = it.rows * G.coef_row_bytes, br = it.rows * rb;
     // part 0: every stream; split producers: part 1 coef / rhs / own colour, part 2 the l +- 1 rows
-    const uint32_t b1 = (HEAT ? 0u : bc) + 2u * br, b2 = 2u * br;
+    const uint32_t b1 = (HEAT ? 0u : bc) + 2u * br, b2 = SSB_SOR_NOLPM && !HEAT ? 0u : 2u * br;
     const uint32_t tx = part == 0 ? b1 + b2 : part == 1 ? b1 : b2;
     const uint32_t sm0 = sptr(smem), bar0 = sptr(full);
     for (int p = it.k0; p <= it.k1; ++p) {
@@ -440,7 +446,7 @@ __device__ __forceinline__ void produce_main(const Layout& L, const Geo& G, unsi
                 bulk_g2s_u(st + G.off_rhs, pr, br, bar, pol.stream);
                 bulk_g2s_u(st + G.off_uc, pu, br, bar, pol.uload);
             }
-            if (part != 1) {
+            if (part != 1 && !(SSB_SOR_NOLPM && !HEAT)) {
                 bulk_g2s_u(st + G.off_ulm, pm, br, bar, pol.uload);
                 bulk_g2s_u(st + G.off_ulp, pp, br, bar, pol.uload);
             }
@@ -726,9 +732,23 @@ __device__ __forceinline__ void consume_item_flat(const SorArgs& a, const Layout
             d.nb[7] = lds_f64<0>(x + G.off_ulp);
             double unew, e2;
             if constexpr (RES) {
+#if SSB_SOR_FLOOR == 2
+                unew = d.u0;
+                e2 = 0.0;
+#else
                 doxel_update<C>(a, d, unew, e2);
+#endif
             } else {  // fixed-sweep solves before their last iteration: the update alone
+#if SSB_SOR_FLOOR  // (timing-only build, WRONG results) every operand loaded, no arithmetic
+                unsigned long long x = (unsigned long long)__double_as_longlong(d.rhs) ^
+                                       (unsigned long long)__double_as_longlong(d.u0) ^ __float_as_uint(d.c[0]) ^
+                                       __float_as_uint(d.c[3]) ^ __float_as_uint(d.c[5]) ^ __float_as_uint(d.c[7]);
+#pragma unroll
+                for (int f = 0; f < 8; ++f) x ^= (unsigned long long)__double_as_longlong(d.nb[f]);
+                unew = SSB_SOR_FLOOR == 2 ? d.u0 : __longlong_as_double((long long)x);  // 2: u stays finite
+#else
                 doxel_update_nores<C>(a, d, unew);
+#endif
                 e2 = 0.0;
             }
             if (on) {
