@@ -329,6 +329,30 @@ def test_step_host_async_chain_matches_device_steps(gpu, chunks_slices):
 
 
 @pytest.mark.parametrize("n_slabs", [1, 3])
+def test_step_host_async_fallbacks(gpu, n_slabs):
+    """step_host_async with pageable numpy buffers (or on a slab group) is step_host: the result
+    is on the host when the call returns; wait() is then a no-op."""
+    import workloads
+    wl = workloads.small((18, 12, 10, 7), seed=29)
+    g = gpu.Grid.make(wl.dims, wl.h)
+    p = gpu.seg_params(**{**wl.params, "n_steps": 4, "sor_rel_tol": 1e-8, "rescale_radius": 3.0})
+    inner = (slice(1, -1),) * 4
+    with gpu.Session(g, n_slabs=n_slabs) as a, gpu.Session(g) as b:
+        a.prepare(wl.image, wl.rows, p, wl.u0)
+        b.prepare(wl.image, wl.rows, p, wl.u0)
+        h_in = np.ascontiguousarray(b.get_u()[inner])
+        h_out = np.empty_like(h_in)
+        for n, fixed in enumerate([0, 5, 0]):
+            da = a.step_host_async(h_in.ctypes.data, h_out.ctypes.data, fixed)
+            db = b.step_fixed(fixed) if fixed else b.step()
+            assert da["iterations"] == db["iterations"], n
+            want = np.ascontiguousarray(b.get_u()[inner])
+            assert np.array_equal(h_out.view(np.uint64), want.view(np.uint64)), n  # before any wait()
+            h_in, h_out = h_out, h_in
+        a.wait()
+
+
+@pytest.mark.parametrize("n_slabs", [1, 3])
 def test_fixed_sweep_steps_vs_oracle(gpu, oracle, n_slabs):
     """ss_session_step_fixed (BASELINE config 4's time step) on 1 and 3 slabs against the C
     restatement's no-early-stop loop, which tests/test_fixed_sweeps_cpu.py pins to the
