@@ -728,8 +728,13 @@ __device__ __forceinline__ void consume_item_flat(const SorArgs& a, const Layout
             d.nb[3] = lds_f64<0>(y + pwb);
             d.nb[4] = lds_f64<0>(am + ft[k].t_uk + par8);
             d.nb[5] = lds_f64<0>(ap + ft[k].t_uk + par8);
+#if SSB_SOR_NOLPM  // (timing only) the l-1 / l+1 neighbours replaced by the slice's own other-colour value
+            d.nb[6] = lds_f64<0>(y);
+            d.nb[7] = lds_f64<0>(y);
+#else
             d.nb[6] = lds_f64<0>(x + G.off_ulm);
             d.nb[7] = lds_f64<0>(x + G.off_ulp);
+#endif
             double unew, e2;
             if constexpr (RES) {
 #if SSB_SOR_FLOOR == 2
