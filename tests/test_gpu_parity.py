@@ -474,9 +474,10 @@ def test_tile_assembly_coefficients_vs_oracle(gpu, oracle, case):
     assert_bits(off_gpu, off_ref, f"tile assembly, {case}")
 
 
-def _cert_field(dims, seed, sharp):
+def _cert_field(dims, seed, sharp, scale=1.0):
     """u in [0, 1] as segmentation iterates are: a smooth 4D profile (or, sharp, a ball with a
-    one-doxel edge: gradients ~ 1/h) plus noise, Dirichlet ghosts 0 (the reference's setting)."""
+    one-doxel edge: gradients ~ 1/h) plus noise, Dirichlet ghosts 0 (the reference's setting);
+    scale != 1: affinely spread to [-scale, scale] (a larger max |u|: a wider certified margin)."""
     rng = np.random.default_rng(seed)
     n1, n2, n3, n4 = dims
     l, k, j, i = np.meshgrid(*[np.arange(n) for n in dims[::-1]], indexing="ij")
@@ -485,6 +486,8 @@ def _cert_field(dims, seed, sharp):
     prof = (r < 0.3).astype(float) if sharp else 1.0 / (1.0 + 8.0 * r)
     u = np.zeros(cs.shape(dims))
     u[1:-1, 1:-1, 1:-1, 1:-1] = np.clip(prof + rng.normal(0, 0.02, prof.shape), 0.0, 1.0)
+    if scale != 1.0:
+        u[1:-1, 1:-1, 1:-1, 1:-1] = (2.0 * u[1:-1, 1:-1, 1:-1, 1:-1] - 1.0) * scale
     return u
 
 
@@ -500,8 +503,9 @@ def _assemble_session(gpu, g, u, tau, eps):
         return s.assemble_export()
 
 
-@pytest.mark.parametrize("h,sharp", [(1 / 32, False), (1 / 64, False), (1 / 32, True), (1 / 128, True)])
-def test_certified_face_gradients_vs_oracle(gpu, oracle, h, sharp, monkeypatch):
+@pytest.mark.parametrize("h,sharp,scale", [(1 / 32, False, 1.0), (1 / 64, False, 1.0), (1 / 32, True, 1.0),
+                                           (1 / 128, True, 1.0), (1 / 32, False, 2.0), (1 / 16, True, 3.0)])
+def test_certified_face_gradients_vs_oracle(gpu, oracle, h, sharp, scale, monkeypatch):
     """The certified face gradients (assemble_tile.cu face_sq_cert: central differences instead
     of the reference's rounded corner sums, within a proven bound of its |grad_f u|^2, the float
     rounding decision trusted only outside that bound) give the reference's coefficients bit for
@@ -513,14 +517,14 @@ def test_certified_face_gradients_vs_oracle(gpu, oracle, h, sharp, monkeypatch):
     dims = (64, 30, 24, 20)
     g = gpu.Grid.make(dims, h)
     tau, eps = h, 1e-3
-    u = _cert_field(dims, 11 + int(sharp), sharp)
+    u = _cert_field(dims, 11 + int(sharp), sharp, scale)
     st, off_ref, _, _ = oracle.assemble_step(op.Grid.make(dims, h), u, None, tau, eps)
     assert st == 0
     monkeypatch.setenv("SSB_ASM_CERT", "1")
     assert_bits(_assemble_session(gpu, g, u, tau, eps), off_ref, f"certified gradients h={h} sharp={sharp}")
     monkeypatch.setenv("SSB_ASM_CERT", "0")
     assert_bits(_assemble_session(gpu, g, u, tau, eps), off_ref, f"exact scaled gradients h={h} sharp={sharp}")
-    if not sharp and h == 1 / 64:
+    if not sharp and h == 1 / 64 and scale == 1.0:
         monkeypatch.setenv("SSB_ASM_CERT", "2")
         off_bad = _assemble_session(gpu, g, u, tau, eps)
         wrong = int(np.count_nonzero(off_bad.view(np.uint64) != off_ref.view(np.uint64)))
