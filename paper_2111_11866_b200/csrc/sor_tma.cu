@@ -737,14 +737,21 @@ __device__ __forceinline__ void consume_item_flat(const SorArgs& a, const Layout
 #endif
             double unew, e2;
             if constexpr (RES) {
-#if SSB_SOR_FLOOR == 2
+#if SSB_SOR_FLOOR >= 2
                 unew = d.u0;
                 e2 = 0.0;
 #else
                 doxel_update<C>(a, d, unew, e2);
 #endif
             } else {  // fixed-sweep solves before their last iteration: the update alone
-#if SSB_SOR_FLOOR  // (timing-only build, WRONG results) every operand loaded, no arithmetic
+#if SSB_SOR_FLOOR == 3  // (timing only) the full arithmetic, but the old value written back
+                {
+                    double t;
+                    doxel_update_nores<C>(a, d, t);
+                    asm volatile("" ::"d"(t));
+                    unew = d.u0;
+                }
+#elif SSB_SOR_FLOOR  // (timing-only build, WRONG results) every operand loaded, no arithmetic
                 unsigned long long x = (unsigned long long)__double_as_longlong(d.rhs) ^
                                        (unsigned long long)__double_as_longlong(d.u0) ^ __float_as_uint(d.c[0]) ^
                                        __float_as_uint(d.c[3]) ^ __float_as_uint(d.c[5]) ^ __float_as_uint(d.c[7]);
