@@ -88,7 +88,8 @@ constexpr int kUKStages = SSB_UK_STAGES;      // other-colour planes (held for t
 #define SSB_FULL_ROWS 0
 #endif
 #ifndef SSB_PLANES_PER_ITEM
-#define SSB_PLANES_PER_ITEM 16  // measured: 8 -> 16 planes: config 2/4 -6%, config 1 -1% per sweep (fewer k-halo rows)
+#define SSB_PLANES_PER_ITEM 32  // measured: 8 -> 16 planes: config 2/4 -6%, config 1 -1% per sweep (fewer k-halo rows);
+                                // 16 -> 32 under the power cap: config 4 -1.0%, config 2 -0.5%, config 1 -1.0% (64: config 1 +4%)
 #endif
 constexpr int kPlanesPerItem = SSB_PLANES_PER_ITEM;
 #ifndef SSB_SMALL_SLICE_ITEMS

@@ -1,7 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-O=gpurun_out/power_i2d.jsonl; rm -f $O
-for rep in 1 2; do for v in i2d base; do
+O=gpurun_out/power_ppi.jsonl; rm -f $O
+for rep in 1 2; do for v in ppi32 base ppi8; do
   if [ $v = base ]; then L=; else L=variants/$v.so; fi
   SUBSURF_B200_LIB=$L timeout 300 python scripts/power_probe.py config4 2>&1 | tail -1 | sed "s/\"config\"/\"var\": \"$v\", \"config\"/" >> $O
 done; done
