@@ -182,13 +182,6 @@ __device__ __forceinline__ void bulk_g2s_u(uint32_t dst, const void* src, uint32
         "l"(src), "r"(bytes), "r"(bar), "l"(pol)
         : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            sptr(dst)),
-        "l"(src), "r"(bytes), "r"(sptr(bar)), "l"(pol)
-        : "memory");
-}
 
 // 2D tensor copy (box at coordinates {x, y}) with mbarrier completion
 __device__ __forceinline__ void tensor_g2s(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
