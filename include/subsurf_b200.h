@@ -78,7 +78,7 @@ typedef struct {
 } ss_step_diag;
 
 SS_API const char* ss_last_error(void);
-SS_API int ss_abi_version(void);
+SS_API int ss_abi_version(void); /* 6 (round 2: ss_session_step_host_async / ss_session_wait) */
 /* number of this library's kernel launches since load (process-wide) */
 SS_API unsigned long long ss_launch_count(void);
 /* 1 if a CUDA device is usable, else 0 (sets ss_last_error) */

@@ -22,8 +22,14 @@ def test_header_declares_the_reference_entry_points():
     for n in ["ss_assemble_step", "ss_assemble_heat_step", "ss_redblack_sor", "ss_face_coefficients",
               "ss_heat_smooth", "ss_local_threshold", "ss_build_initial", "ss_local_rescale",
               "ss_extract_mask", "ss_segment", "ss_session_create", "ss_session_step",
-              "ss_label_components", "ss_distance_centers", "ss_backtrack_link", "ss_track", "ss_session_track"]:
+              "ss_label_components", "ss_distance_centers", "ss_backtrack_link", "ss_track", "ss_session_track",
+              "ss_session_step_fixed", "ss_session_step_host", "ss_session_step_host_async", "ss_session_wait"]:
         assert n in names
+
+
+def test_abi_version(ss):
+    """ABI 6: ss_session_step_host_async / ss_session_wait."""
+    assert ss.library().ss_abi_version() == 6
 
 
 def test_library_exports_every_declared_symbol(ss):
