@@ -386,7 +386,8 @@ void launch_face_coefficients(cudaStream_t s, const EdgeArgs& a0) {
         p2 = p2 && pow2(a.h[q]);
         a.hinv[q] = 1.0 / a.h[q];
     }
-    if (!a.G_out && assemble_tile_supported(a.L) && launch_edge_tile(s, a, p2)) return;
+    // the TMA-staged tile kernel, also for the per-call API's padded export
+    if (assemble_tile_supported(a.L) && launch_edge_tile(s, a, p2)) return;
     if (a.G_out) {
         if (p2) { edge_launch<0, true, true>(s, a); edge_launch<1, true, true>(s, a); }
         else { edge_launch<0, true, false>(s, a); edge_launch<1, true, false>(s, a); }

@@ -616,12 +616,21 @@ struct EdgeTileArgs {
     Maps<2> maps;
     EdgeArgs a;
     TileGeo g;
+    const int* guard;  // non-null: scaled face gradients unless *guard (a value of I0s / ITs out of range)
+    double c;          // 0.25 / h of the isotropic power-of-two grid (scaled mode)
 };
 
 // face_coefficients (edge.cpp:73-99): G_f = 1 / (1 + K s^2), s = delta |grad_f I0s| +
-// vartheta |grad_f ITs|, fp64 output (exact sequence: sqrt / div as the reference)
-template <bool POW2>
-__global__ void __launch_bounds__(kThreadsT, 1) edge_tile_kernel(const __grid_constant__ EdgeTileArgs p) {
+// vartheta |grad_f ITs|, fp64 output (exact sequence: sqrt / div as the reference).
+// Scaled mode (isotropic power-of-two grid, both images within the guard's range): the
+// reference's |grad_f I|^2 = sigma * S with S = face_sq_scaled and sigma = c^2 exactly (the
+// argument at face_sq_scaled), and sqrt(c^2 S) = c sqrt(S) exactly for a power of two c (the
+// correctly rounded root commutes with scaling by 2^2m), so |grad_f I| = c * sqrt(S) bit for bit.
+// ST brick stages per CTA (each stage: both images, 2 x kFieldBytes): 2 stages at one CTA per SM,
+// or 1 stage at two CTAs per SM (twice the warps; the other CTA computes while one waits for its
+// next tile)
+template <bool POW2, int ST>
+__global__ void __launch_bounds__(kThreadsT, ST == 1 ? 2 : 1) edge_tile_kernel(const __grid_constant__ EdgeTileArgs p) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[2];
     const EdgeArgs& a = p.a;
@@ -638,12 +647,14 @@ __global__ void __launch_bounds__(kThreadsT, 1) edge_tile_kernel(const __grid_co
     __syncthreads();
     long long t = blockIdx.x;
     if (tid == 0)
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < ST; ++q) {
             const long long tq = t + (long long)q * gridDim.x;
             if (tq < g.tiles) load_tile<2>(L, p.maps, tile_of(L, g, tq), sbase + q * 2 * kFieldBytes, &bars[q]);
         }
     int stage = 0;
     uint32_t phase = 0;
+    // guard (uniform over the grid: one flag written before the launch)
+    const bool scaled = POW2 && p.guard && *(volatile const int*)p.guard == 0;
     for (; t < g.tiles; t += gridDim.x) {
         const Tile x = tile_of(L, g, t);
         const uint32_t buf = sbase + stage * 2 * kFieldBytes;
@@ -668,15 +679,21 @@ __global__ void __launch_bounds__(kThreadsT, 1) edge_tile_kernel(const __grid_co
             ST.bnce = SI.bnce + kFieldBytes;
             const double pi0 = SI.at<0, 0, 0, 0>(), pt0 = ST.at<0, 0, 0, 0>();
             double G[8];
-#define SSB_EDGE_TILE_FACE(F)                                                                   \
-    {                                                                                           \
-        double gi[4], gt[4];                                                                    \
-        face_grad<F, POW2>(SI, a.h, a.hinv, pi0, gi);                                           \
-        face_grad<F, POW2>(ST, a.h, a.hinv, pt0, gt);                                           \
-        const double ni = sqrt(gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2] + gi[3] * gi[3]);  \
-        const double nt = sqrt(gt[0] * gt[0] + gt[1] * gt[1] + gt[2] * gt[2] + gt[3] * gt[3]);  \
-        const double sv = a.delta * ni + a.vartheta * nt;                                       \
-        G[F] = 1.0 / (1.0 + a.K * sv * sv);                                                     \
+#define SSB_EDGE_TILE_FACE(F)                                                                       \
+    {                                                                                               \
+        double ni, nt;                                                                              \
+        if (scaled) {                                                                               \
+            ni = p.c * sqrt(face_sq_scaled<F>(SI, pi0));                                            \
+            nt = p.c * sqrt(face_sq_scaled<F>(ST, pt0));                                            \
+        } else {                                                                                    \
+            double gi[4], gt[4];                                                                    \
+            face_grad<F, POW2>(SI, a.h, a.hinv, pi0, gi);                                           \
+            face_grad<F, POW2>(ST, a.h, a.hinv, pt0, gt);                                           \
+            ni = sqrt(gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2] + gi[3] * gi[3]);               \
+            nt = sqrt(gt[0] * gt[0] + gt[1] * gt[1] + gt[2] * gt[2] + gt[3] * gt[3]);               \
+        }                                                                                           \
+        const double sv = a.delta * ni + a.vartheta * nt;                                           \
+        G[F] = 1.0 / (1.0 + a.K * sv * sv);                                                         \
     }
             SSB_EDGE_TILE_FACE(0)
             SSB_EDGE_TILE_FACE(1)
@@ -691,13 +708,18 @@ __global__ void __launch_bounds__(kThreadsT, 1) edge_tile_kernel(const __grid_co
             double2* gw = reinterpret_cast<double2*>(a.G[c] + pg * 8);
 #pragma unroll
             for (int h2 = 0; h2 < 4; ++h2) gw[h2] = make_double2(G[2 * h2], G[2 * h2 + 1]);
+            if (a.G_out) {  // per-call API: the reference's padded layout too
+                double2* go = reinterpret_cast<double2*>(a.G_out + L.padded(i, j, k, x.l) * 8);
+#pragma unroll
+                for (int h2 = 0; h2 < 4; ++h2) go[h2] = make_double2(G[2 * h2], G[2 * h2 + 1]);
+            }
         }
         __syncthreads();
         if (tid == 0) {
-            const long long tn = t + 2LL * gridDim.x;
+            const long long tn = t + (long long)ST * gridDim.x;
             if (tn < g.tiles) load_tile<2>(L, p.maps, tile_of(L, g, tn), buf, &bars[stage]);
         }
-        if (++stage == 2) {
+        if (++stage == ST) {
             stage = 0;
             phase ^= 1;
         }
@@ -914,8 +936,22 @@ bool launch_edge_tile(cudaStream_t s, const EdgeArgs& a, bool pow2) {
     if (!encode_brick(&p.maps.m[0][0], a.L, a.I0[0]) || !encode_brick(&p.maps.m[0][1], a.L, a.I0[1]) ||
         !encode_brick(&p.maps.m[1][0], a.L, a.IT[0]) || !encode_brick(&p.maps.m[1][1], a.L, a.IT[1]))
         return false;
-    const size_t smem = 4 * (size_t)kFieldBytes;
-    auto k = pow2 ? edge_tile_kernel<true> : edge_tile_kernel<false>;
+    // scaled face gradients: isotropic power-of-two grid and both smoothed images within the
+    // range guard (one pass over I0s and one over ITs, 16 B per padded doxel, one-off)
+    AsmArgs ga{};
+    for (int q = 0; q < 4; ++q) ga.h[q] = a.h[q];
+    double sigma = 0.0;
+    if (a.guard && env_int("SSB_EDGE_SCALED", 1) && scaled_grid(ga, pow2, &sigma)) {
+        SSB_CUDA(cudaMemsetAsync(a.guard, 0, 2 * sizeof(int), s));
+        launch_guard_range(s, a.L, a.I0[0], a.I0[1], 0, a.L.lMax - 1, a.guard);
+        launch_guard_range(s, a.L, a.IT[0], a.IT[1], 0, a.L.lMax - 1, a.guard);
+        p.guard = a.guard;
+        p.c = 0.25 / a.h[0];
+    }
+    static const int st = env_int("SSB_EDGE_STAGES", 1) == 2 ? 2 : 1;
+    const size_t smem = 2 * (size_t)st * kFieldBytes;
+    auto k = st == 1 ? (pow2 ? edge_tile_kernel<true, 1> : edge_tile_kernel<false, 1>)
+                     : (pow2 ? edge_tile_kernel<true, 2> : edge_tile_kernel<false, 2>);
     static bool configured[2] = {false, false};
     if (!configured[pow2]) {
         SSB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -286,6 +286,7 @@ void Slab::face_coefficients(PField I0s, PField ITs, double K, double delta, dou
     e.h[1] = gl.h2;
     e.h[2] = gl.h3;
     e.h[3] = gl.h4;
+    e.guard = flags.p + 2;  // the scaled gradients' range guard (reset by every assembly before use)
     launch_face_coefficients(stream, e);
     have_G = true;
 }

@@ -183,6 +183,7 @@ struct EdgeArgs {
     double K, delta, vartheta;
     double h[4];
     double hinv[4];
+    int* guard;             // 2 ints of scratch for the range guard of the scaled gradients (may be null)
 };
 void launch_face_coefficients(cudaStream_t s, const EdgeArgs& a);
 // TMA-staged tile kernels (assemble_tile.cu); false = not launched (no tensor-map encoder)

@@ -530,3 +530,40 @@ def test_certified_face_gradients_vs_oracle(gpu, oracle, h, sharp, scale, monkey
         wrong = int(np.count_nonzero(off_bad.view(np.uint64) != off_ref.view(np.uint64)))
         print(f"no-margin certified gradients: {wrong} of {off_ref.size} coefficients differ")
         assert wrong > 0
+
+
+@pytest.mark.parametrize("case", ["iso_pow2", "iso_pow2_guard", "iso_pow2_exact", "aniso_pow2", "non_pow2"])
+def test_tile_face_coefficients_vs_oracle(gpu, oracle, case, monkeypatch):
+    """The device path's edge detector (assemble_tile.cu edge_tile_kernel: TMA-staged I0s / ITs
+    bricks; on isotropic power-of-two grids the scaled face gradients |grad_f I| = c sqrt(S)
+    behind the range guard over both images) against the oracle's face_coefficients, bit for
+    bit, on images with magnitudes 1e-3..1e3 and exact zeros.  iso_pow2: the scaled path (two
+    guard launches more than with SSB_EDGE_SCALED=0, iso_pow2_exact); iso_pow2_guard: one value
+    of 1e-200 in ITs trips the guard (the reference's expression runs)."""
+    from oracle import oracle_py as op
+    dims = (37, 13, 11, 7)
+    h = {"iso_pow2": 1 / 32, "iso_pow2_guard": 1 / 32, "iso_pow2_exact": 1 / 64,
+         "aniso_pow2": (1 / 32, 1 / 16, 1 / 32, 1 / 64), "non_pow2": (0.1, 0.07, 0.13, 0.05)}[case]
+    g = gpu.Grid.make(dims, h)
+    rng = np.random.default_rng(5)
+    I0 = rng.normal(0.5, 0.3, size=g.shape) * 10.0 ** rng.uniform(-3, 3, size=g.shape)
+    I0[rng.random(g.shape) < 0.15] = 0.0
+    IT = np.clip(rng.normal(0.5, 0.4, size=g.shape), 0.0, 1.0)
+    if case == "iso_pow2_guard":
+        IT[2, 3, 4, 5] = 1e-200
+    monkeypatch.setenv("SSB_EDGE_SCALED", "0" if case == "iso_pow2_exact" else "1")
+    K, delta, vartheta = 1000.0, 0.5, 0.5
+    gpu.face_coefficients(I0, IT, K, delta, vartheta, g)  # the grid's cached domain is built here
+    n0 = gpu.launch_count()
+    G = gpu.face_coefficients(I0, IT, K, delta, vartheta, g)
+    n_scaled = gpu.launch_count() - n0
+    st, G_ref = oracle.face_coefficients(op.Grid.make(dims, h), I0, IT, K, delta, vartheta)
+    assert st == 0
+    assert_bits(G, G_ref, f"tile face_coefficients, {case}")
+    if case in ("iso_pow2", "iso_pow2_exact"):
+        monkeypatch.setenv("SSB_EDGE_SCALED", "0")
+        n0 = gpu.launch_count()
+        G0 = gpu.face_coefficients(I0, IT, K, delta, vartheta, g)
+        n_exact = gpu.launch_count() - n0
+        assert_bits(G0, G_ref, f"tile face_coefficients, {case}, exact gradients")
+        assert n_scaled - n_exact == (2 if case == "iso_pow2" else 0), (n_scaled, n_exact)
