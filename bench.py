@@ -348,8 +348,8 @@ def main():
     # memory and reads its result u^n back (compact interiors of this rank's slices; the ghost
     # layer is the session's Dirichlet data), the upload overlapped with the assembly; the
     # result's download is left in flight and the next step's upload of that same host buffer
-    # is chained to it chunk by chunk on the device (D2H and H2D overlap; multi-rank sessions
-    # fall back to the synchronous call)
+    # is chained to it chunk by chunk on the device (D2H and H2D overlap; on the ranks of a
+    # distributed run the chunked upload precedes the halo exchange and the assembly)
     n_owned = int(np.prod(sess.interior_shape))
     host_in = torch.empty(n_owned, dtype=torch.float64, pin_memory=True)
     host_out = torch.empty(n_owned, dtype=torch.float64, pin_memory=True)

@@ -235,8 +235,8 @@ SS_API ss_status ss_session_fixed_sweeps(ss_session* s, int n_sweeps, double* re
  * neighbour is in.  ss_session_set_u_interior / _get_u_interior: the copies alone. */
 SS_API ss_status ss_session_step_host(ss_session* s, const double* u_in, double* u_out, int n_sweeps,
                                       ss_step_diag* diag);
-/* ss_session_step_host with the result's download left in flight (ABI 6; single slab,
- * page-locked u_in / u_out, else exactly ss_session_step_host): returns once the step is
+/* ss_session_step_host with the result's download left in flight (ABI 6; one slab per
+ * process -- a single domain or a distributed rank -- and page-locked u_in / u_out, else exactly ss_session_step_host): returns once the step is
  * computed and its D2H enqueued; u_out is complete after ss_session_wait (or any call that
  * reads it).  When the next call's u_in is this call's u_out, every upload chunk waits on
  * the device for its download chunk, so the D2H of step n and the H2D of step n + 1 run

@@ -621,7 +621,7 @@ class Session:
         return dict(iterations=d.iterations, residual=d.residual, tol=d.tol, umin=d.umin, umax=d.umax) if diag else None
 
     def step_host_async(self, u_in=None, u_out=None, n_sweeps: int = 0, diag: bool = True):
-        """step_host with the result's download left in flight (single slab, page-locked
+        """step_host with the result's download left in flight (one slab per process, page-locked
         buffers given as pointers; otherwise step_host): u_out is complete after wait().  When
         the next call's u_in is this call's u_out, each upload chunk waits on the device for its
         download chunk -- the D2H of step n and the H2D of step n + 1 overlap."""

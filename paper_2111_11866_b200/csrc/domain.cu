@@ -1251,9 +1251,10 @@ void Domain::get_u_interior(double* host) {
     sync();
 }
 
-// single slab, page-locked input: slice chunks H2D on the copy stream; per chunk the main
-// stream packs it and assembles the slices whose l+1 neighbour is in (the last chunk: all)
-void Domain::upload_assemble(const double* host) {
+// one slab, page-locked input: slice chunks H2D on the copy stream; per chunk the main
+// stream packs it and (assemble) assembles the slices whose l+1 neighbour is in (the last
+// chunk: all)
+void Domain::upload_chunks(const double* host, bool assemble) {
     Slab& x = *sp[0];
     const long long fr = (long long)g.n1 * g.n2 * g.n3;
     const int n4 = x.L.n4, C = std::min(n4, kHostChunks);
@@ -1275,6 +1276,13 @@ void Domain::upload_assemble(const double* host) {
         SSB_CUDA(cudaMemcpyAsync(st + (a - 1) * fr, host + (a - 1) * fr, (size_t)(b - a + 1) * fr * sizeof(double),
                                  cudaMemcpyHostToDevice, h2d));
         SSB_CUDA(cudaEventRecord(up_ev[q], h2d));
+    }
+    if (!assemble) {
+        for (int q = 0; q < C; ++q) {
+            SSB_CUDA(cudaStreamWaitEvent(stream, up_ev[q], 0));
+            launch_pack_interior(stream, x.L, st, x.S[cur].pf(), lo(q), lo(q + 1) - 1);
+        }
+        return;
     }
     SSB_CUDA(cudaMemsetAsync(x.flags.p, 0, sizeof(int), stream));
     const AsmArgs args = x.asm_args(x.S[cur].pf(), x.have_G, prm.tau, prm.epsilon);
@@ -1324,7 +1332,7 @@ void Domain::download_async(double* host) {
 }
 
 SolveOut Domain::step_host_async(const double* in, double* out, int fixed, ss_step_diag* diag) {
-    const bool async = single() && out && host_pinned(out) && (!in || host_pinned(in)) &&
+    const bool async = sp.size() == 1 && out && host_pinned(out) && (!in || host_pinned(in)) &&
                        assemble_tile_supported(sp[0]->L);
     if (!async) return step_host(in, out, fixed, diag);
     if (dn_host && dn_host != in) wait_transfers();  // only a chained input may still be in flight
@@ -1348,12 +1356,16 @@ SolveOut Domain::step_impl(ss_step_diag* diag, int fixed, bool rescale, const do
     if (!prepared) throw Error(SS_ERR_STATE, "session not prepared");
     int roles[kStateBuffers];
     for (int q = 0; q < kStateBuffers; ++q) roles[q] = (cur + q) % kStateBuffers;
-    const bool overlap = host_in && single() && assemble_tile_supported(sp[0]->L) && host_pinned(host_in);
-    if (host_in && !overlap) set_u_interior(host_in);
+    // page-locked input of a one-slab process: chunked upload (chained to an in-flight download
+    // of the same buffer); a single domain also overlaps it with the assembly
+    const bool chunked = host_in && sp.size() == 1 && assemble_tile_supported(sp[0]->L) && host_pinned(host_in);
+    const bool overlap = chunked && single();
+    if (host_in && !chunked) set_u_interior(host_in);
+    if (chunked && !overlap) upload_chunks(host_in, false);
     exchange_role(cur, 3);  // u^{n-1} halos for the face gradients and the first red pass
     if (profiling) SSB_CUDA(cudaEventRecord(ev[2], stream));
     if (overlap)
-        upload_assemble(host_in);
+        upload_chunks(host_in, true);
     else
         for (Slab* s : sp) s->assemble(s->S[cur].pf(), s->have_G, prm.tau, prm.epsilon, nullptr, nullptr, nullptr);
     if (profiling) SSB_CUDA(cudaEventRecord(ev[3], stream));

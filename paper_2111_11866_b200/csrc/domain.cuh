@@ -298,8 +298,9 @@ struct Domain {
     SolveOut step_host(const double* in, double* out, int fixed, ss_step_diag* diag);
     void set_u_interior(const double* host);
     void get_u_interior(double* host);
-    // step_host with the result's download left in flight (single slab, page-locked buffers;
-    // otherwise exactly step_host): out is complete after wait_transfers(), and when the next
+    // step_host with the result's download left in flight (one slab per process -- a single
+    // domain or a rank of a distributed one -- and page-locked buffers; otherwise exactly
+    // step_host): out is complete after wait_transfers(), and when the next
     // call's input is this call's output, each upload chunk waits on the device for its
     // download chunk, so the D2H of step n and the H2D of step n + 1 run concurrently on the
     // two copy directions (ss_session_step_host_async)
@@ -316,7 +317,10 @@ private:
     const double* dn_host = nullptr;  // the host buffer the in-flight download writes (null: none)
     void download_async(double* host);
     SolveOut step_impl(ss_step_diag* diag, int fixed, bool rescale, const double* host_in);
-    void upload_assemble(const double* host);
+    // chunked upload of a page-locked input (chained to an in-flight download of the same
+    // buffer); assemble: each chunk's slices assembled as soon as their l+1 neighbour is in
+    // (single domain), else the upload alone (a rank: its halos are exchanged after it)
+    void upload_chunks(const double* host, bool assemble);
     void init_common();
     void init_rank(int rank);  // the rank's slab (distributed constructors)
     cudaEvent_t pool_event(size_t idx);

@@ -99,3 +99,65 @@ def test_distributed_domain_over_host_transport(gpu, world):
         assert [x["umax"] for x in d] == [x["umax"] for x in ref_diags]
         # the timed (non-profiling) solves recorded their exchanges: 2 per SOR iteration
         assert out[r][2] >= 2 * sum(x["iterations"] for x in ref_diags[:3]) and out[r][3] > 0.0
+
+
+def _rank_async(rank, world, port, q):
+    """A rank's chained host-buffer steps: step_host_async with page-locked buffers, each
+    step's input the previous step's output still on its way down (the per-rank chunked
+    upload, then the halo exchange)."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2111_11866_b200 as ss
+    from paper_2111_11866_b200 import dist as ssd
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        wl, params = _case()
+        g = ss.Grid.make(wl.dims, wl.h)
+        lb, cnt = ssd.partition(DIMS[3], world)[rank]
+        with ss.Session(g, dist=(rank, world, ssd.HostComm())) as s:
+            s.prepare(ssd.slab_view(wl.image, lb, cnt), wl.rows, ss.seg_params(**params),
+                      ssd.slab_view(wl.u0, lb, cnt))
+            n = int(np.prod(s.interior_shape))
+            hin = torch.empty(n, dtype=torch.float64).pin_memory()
+            hout = torch.empty(n, dtype=torch.float64).pin_memory()
+            hin.copy_(torch.from_numpy(s.get_u_interior().ravel()))
+            for fixed in (0, 7, 0):
+                s.step_host_async(hin.data_ptr(), hout.data_ptr(), fixed, diag=False)
+                hin, hout = hout, hin
+            s.wait()
+            q.put((rank, hin.numpy().reshape(s.interior_shape).copy(), None))
+    except Exception as e:  # surfaced by the parent
+        q.put((rank, None, repr(e)))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_distributed_step_host_async_over_host_transport(gpu):
+    """ss_session_step_host_async on the ranks of a distributed domain (2 processes, host-staged
+    transport): chained page-locked steps -- a segment() step, a fixed 7-sweep step, a segment()
+    step -- equal the single domain's device-resident steps bit for bit."""
+    import multiprocessing as mp
+    world = 2
+    wl, params = _case()
+    g = gpu.Grid.make(wl.dims, wl.h)
+    with gpu.Session(g) as s:
+        s.prepare(wl.image, wl.rows, gpu.seg_params(**params), wl.u0)
+        s.step()
+        s.step_fixed(7)
+        s.step()
+        u_ref = s.get_u()[1:-1, 1:-1, 1:-1, 1:-1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_async, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict((r, (u, x)) for r, u, x in (q.get(timeout=600) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(world):
+        assert out[r][0] is not None, out[r][1]
+    u = np.concatenate([out[r][0] for r in range(world)])
+    assert np.array_equal(u.view(np.uint64), u_ref.view(np.uint64))
