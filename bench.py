@@ -261,6 +261,10 @@ def main():
     ap.add_argument("--loop-mode", type=int, default=1)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    wd = float(os.environ.get("SUBSURF_BENCH_WATCHDOG", 0) or 0)
+    if wd > 0:  # a stuck rank dumps every thread's stack and exits instead of idling on the GPU
+        import faulthandler
+        faulthandler.dump_traceback_later(wd, exit=True)
 
     if args.impl == "reference":
         return run_reference(args, args.config)

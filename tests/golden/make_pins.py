@@ -40,7 +40,7 @@ sys.path.insert(0, ROOT)
 from oracle import oracle_py as op  # noqa: E402
 import workloads  # noqa: E402
 
-OUT = os.path.join(HERE, "pins.json")
+OUT = os.environ.get("PINS_OUT", os.path.join(HERE, "pins.json"))  # PINS_OUT: write elsewhere, merge later
 
 
 def sha(a) -> str:
@@ -62,6 +62,7 @@ PLAN = {  # config -> (workload builder, steps, fixed sweeps or None)
 
 def run(name: str) -> dict:
     build, steps, fixed = PLAN[name]
+    steps = int(os.environ.get("PINS_STEPS_" + name, steps))  # a shorter pin of the same run
     wl = build()
     R = op.ref()
     g = op.Grid.make(wl.dims, wl.h)

@@ -5,6 +5,7 @@ of the timed run, one JSON line from rank 0 -- without a second GPU.  A function
 test only: ranks sharing a GPU measure nothing about scaling."""
 import json
 import os
+import signal
 import socket
 import subprocess
 import sys
@@ -25,14 +26,23 @@ def _port():
 
 @pytest.mark.parametrize("n", [2, 3])
 def test_bench_multirank_over_host_transport(gpu, n):
-    env = dict(os.environ, SUBSURF_DIST_TRANSPORT="host")
+    # a stuck rank dumps its stacks and exits after 240 s (bench.py's watchdog); the launcher and
+    # whatever it left behind are killed as a process group, so nothing idles on the GPU
+    env = dict(os.environ, SUBSURF_DIST_TRANSPORT="host", SUBSURF_BENCH_WATCHDOG="240")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", str(n),
            "--config", "tiny", "--steps", "2", "--warmup", "3", "--no-cpu-baseline"]
-    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stderr[-3000:]
-    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
-    assert len(lines) == 1, r.stdout  # rank 0 only
+    proc = subprocess.Popen(cmd, cwd=ROOT, env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
+                            start_new_session=True)
+    try:
+        out, err = proc.communicate(timeout=420)
+    except subprocess.TimeoutExpired:
+        os.killpg(proc.pid, signal.SIGKILL)
+        out, err = proc.communicate()
+        pytest.fail("bench.py ranks did not finish in 420 s:\n" + err[-6000:])
+    assert proc.returncode == 0, err[-6000:]
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out  # rank 0 only
     d = json.loads(lines[0])
     assert d["n_gpus"] == n and d["value"] > 0 and d["config"]["dims"] == [24, 20, 12, 6 * n]
     assert d["halo"]["exchanges_timed"] > 0 and d["halo"]["exchange_ms"] > 0
