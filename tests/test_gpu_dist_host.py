@@ -65,6 +65,21 @@ def _rank_main(rank, world, port, q):
         tdist.destroy_process_group()
 
 
+def _collect(q, procs, world, timeout=300):
+    """One result per rank; whatever happens, no rank process outlives the test (a rank left
+    behind would keep its CUDA context and share the GPU with every later test and bench)."""
+    try:
+        res = [q.get(timeout=timeout) for _ in range(world)]
+        for p in procs:
+            p.join(timeout=60)
+        return res
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.kill()
+                p.join(timeout=10)
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_distributed_domain_over_host_transport(gpu, world):
     import multiprocessing as mp
@@ -81,9 +96,7 @@ def test_distributed_domain_over_host_transport(gpu, world):
     procs = [ctx.Process(target=_rank_main, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = dict((r, (u, d, hn, hm)) for r, u, d, hn, hm in (q.get(timeout=600) for _ in range(world)))
-    for p in procs:
-        p.join(timeout=120)
+    out = dict((r, (u, d, hn, hm)) for r, u, d, hn, hm in _collect(q, procs, world))
     for r in range(world):
         assert out[r][0] is not None, out[r][1]
     u = np.concatenate([out[r][0] for r in range(world)])
@@ -154,9 +167,7 @@ def test_distributed_step_host_async_over_host_transport(gpu):
     procs = [ctx.Process(target=_rank_async, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = dict((r, (u, x)) for r, u, x in (q.get(timeout=600) for _ in range(world)))
-    for p in procs:
-        p.join(timeout=120)
+    out = dict((r, (u, x)) for r, u, x in _collect(q, procs, world))
     for r in range(world):
         assert out[r][0] is not None, out[r][1]
     u = np.concatenate([out[r][0] for r in range(world)])
