@@ -489,6 +489,11 @@ Domain::Domain(const ss_grid& grid, int dev, int rank, int w, const unsigned cha
     tr = make_nccl_transport(uid, rank, w);
     const char* e = std::getenv("SSB_P2P");
     if (w > 1 && e && std::atoi(e) != 0) setup_peer_links(*tr, *sp[0], rank, w, chunk, g.n4, peers);
+    // ncclSend/ncclRecv are kernels: the interior launch of a pass is a persistent grid that fills
+    // every CTA slot, so it leaves a few free for them (SSB_COMM_RESERVE, default 8 of 296: measured
+    // free of charge on config 4, scripts/gpu_r02_s5i.sh); the in-kernel push needs none
+    const char* r = std::getenv("SSB_COMM_RESERVE");
+    comm_reserve = w > 1 && !peers.on ? (r ? std::max(0, std::atoi(r)) : 8) : 0;
     sync();
 }
 
@@ -751,7 +756,10 @@ void Domain::body_multi(const std::vector<SorArgs>& a, const std::vector<Triple>
         if (xe) SSB_CUDA(cudaEventRecord(xe[0], comm));
         tr->exchange(sp, F, colour == 0 ? 1 : 2, comm);
         SSB_CUDA(cudaEventRecord(xe ? xe[1] : ev_xchg, comm));
-        for (const SorArgs& x : a) launch_sor_pass_range(stream, x, colour, heat, 2, x.L.n4 - 1, true);
+        for (SorArgs x : a) {
+            x.grid_short = comm_reserve;
+            launch_sor_pass_range(stream, x, colour, heat, 2, x.L.n4 - 1, true);
+        }
         if (xe) SSB_CUDA(cudaEventRecord(xe[2], stream));
         SSB_CUDA(cudaStreamWaitEvent(stream, xe ? xe[1] : ev_xchg, 0));
     };

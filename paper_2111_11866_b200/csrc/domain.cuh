@@ -216,6 +216,7 @@ struct Domain {
     int device = 0;
     bool distributed = false;  // NCCL: slabs.size() == 1 < world
     PeerLinks peers;           // NVLink halo push between ranks (SSB_P2P=1)
+    int comm_reserve = 0;      // CTA slots a pass's interior launch leaves free for NCCL's send/recv kernels
     cudaStream_t stream = nullptr, cap_stream = nullptr;
     cudaStream_t comm = nullptr;  // halo exchanges (overlapped with interior slices)
     cudaStream_t bnd = nullptr;   // high priority: a colour pass's end slices, concurrent with its interior

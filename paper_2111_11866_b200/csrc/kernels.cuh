@@ -64,6 +64,7 @@ struct SorArgs {
     int l_lo, l_hi;         // slices (local, 1-based) a pass launch covers (default 1 .. n4)
     int l_step;             // ... every l_step-th of them (TMA pass; 1: all, n4 - 1: the two end slices)
     int pdl_off;            // launch without programmatic dependent launch (side-stream launches)
+    int grid_short;         // TMA pass: CTA slots this launch leaves free (0: the full persistent grid)
     int dyn;                // TMA pass: items from the colour's atomic counter (one such launch per pass)
     int wave;               // 1: two-iteration wavefront kernel per loop body, 2: one-sweep k-wavefront
     int kwj;                // one-sweep wavefront marches along j (1) or k (0)
@@ -116,6 +117,7 @@ int pass_l2hint();  // SorArgs::l2hint default (env SSB_L2HINT)
 int pass_order();   // SorArgs::order default (env SSB_ORDER)
 int pass_fuse_final();  // SorArgs::fuse_final allowed (env SSB_FUSE_FINAL)
 int pass_pdl();         // programmatic dependent launch of the TMA passes (env SSB_PDL)
+int pass_grid_short();  // CTA slots every TMA pass launch leaves free (env SSB_GRID_SHORT, default 0)
 bool wave_supported(const Layout& L);
 size_t wave_flags(const Layout& L);
 // one-sweep k-wavefront (kernel 7, sor_tma.cu): support test, flag / partial sizes,

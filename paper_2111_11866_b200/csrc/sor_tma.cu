@@ -1416,6 +1416,13 @@ int pass_pdl() {
     }();
     return v;
 }
+int pass_grid_short() {
+    static const int v = [] {
+        const char* e = std::getenv("SSB_GRID_SHORT");
+        return e ? std::max(0, std::atoi(e)) : 0;
+    }();
+    return v;
+}
 int pass_fuse_final() {
     static const int v = [] {
         const char* e = std::getenv("SSB_FUSE_FINAL");
@@ -1617,7 +1624,10 @@ void launch_sor_pass_tma(cudaStream_t s, const SorArgs& a, int colour, bool heat
     }
     const bool flat = !heat && !G.S && !G.wpr;
     const long long items = (long long)G.nsg * G.njg * G.nkc * ((a.l_hi - a.l_lo) / a.l_step + 1);
-    const unsigned grid = (unsigned)std::min<long long>(items, blocks[flat]);
+    // CTA slots left free for kernels of other streams (NCCL's send/recv beside the interior
+    // launch of a distributed pass): the grid is persistent, so nothing else frees one mid-pass
+    const int room = std::max(1, blocks[flat] - std::max(a.grid_short, pass_grid_short()));
+    const unsigned grid = (unsigned)std::min<long long>(items, room);
     SorArgs b = a;
     if (b.order < 0) b.order = 2LL * G.nsg * G.njg * G.nkc <= blocks[flat] ? 0 : 1;
     const bool push = a.push_lo[0][0] != nullptr || a.push_hi[0][0] != nullptr;

@@ -63,3 +63,39 @@ def test_config_pinned_to_reference(gpu, name):
     assert [d["umax"] for d in diags] == pin["umax"]
     assert sha(u) == pin["u_sha256"], "u differs from the reference's bits"
     assert int(mask.sum()) == pin["mask_voxels"]
+
+
+_SHORT_GRID = r"""
+import hashlib, json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2111_11866_b200 as ss
+import workloads
+wl = workloads.config1()
+g = ss.Grid.make(wl.dims, wl.h)
+with ss.Session(g) as s:
+    s.set_kernel("tma")
+    s.prepare(wl.image, wl.rows, ss.seg_params(**{**wl.params, "n_steps": 3}), wl.u0)
+    its = [s.step()["iterations"] for _ in range(2)] + [s.step_fixed(9)["iterations"]]
+    u = s.get_u()
+print(json.dumps({"its": its, "sha": hashlib.sha256(np.ascontiguousarray(u).tobytes()).hexdigest()}))
+"""
+
+
+@pytest.mark.parametrize("short", [8, 37, 295])
+def test_short_persistent_grid_is_bit_identical(gpu, short):
+    """The TMA pass is a persistent grid handing out items from a counter; a distributed rank's
+    interior launch leaves CTA slots free for NCCL's send/recv kernels (Domain::comm_reserve).
+    SSB_GRID_SHORT applies the same shortening to every launch (read once per process, hence
+    the subprocess): iteration counts and u must not depend on the grid size, down to one CTA."""
+    import subprocess
+    import sys
+    root = os.path.dirname(HERE)
+    res = []
+    for env in ({}, {"SSB_GRID_SHORT": str(short)}):
+        r = subprocess.run([sys.executable, "-c", _SHORT_GRID, root], env={**os.environ, **env},
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert res[0] == res[1]
+    assert res[0]["its"][:2] == PINS["config1"]["iterations"][:2]
