@@ -252,7 +252,8 @@ SS_API ss_status ss_session_get_u_interior(ss_session* s, double* u);
  * n_sweeps red+black sweeps, local_rescale).  The reference has no such mode: its
  * redblack_sor throws SolverError at max_iter and drops the iterate (solver.cpp:391-395);
  * this is that iterate (tests pin it against the reference, tests/golden/pins.json).
- * diag: iterations = n_sweeps, residual = the last residual, tol = 1. */
+ * diag: iterations = n_sweeps, residual = the last residual, tol = 1.  diag == NULL (here
+ * and in the host-buffer calls with n_sweeps > 0): no residual is evaluated at all. */
 SS_API ss_status ss_session_step_fixed(ss_session* s, int n_sweeps, ss_step_diag* diag);
 /* run_levelset_row (eoc.cpp:83-137): the EOC verification row n (10/20/40/80/160) on a
  * session created for the grid n^4 with h = 2.5/n; *err = space-time L2 error,

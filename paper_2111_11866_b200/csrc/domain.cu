@@ -809,7 +809,7 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
     for (size_t s = 0; s < sp.size(); ++s) {
         Slab& x = *sp[s];
         const double* ns = use_norm ? (world == 1 ? x.norm_loc.p : x.norm_all.p) : nullptr;
-        launch_sor_init(stream, x.st.p, tol_abs, ns, g.n4, rel, max_iter, fixed ? 1 : 0, epoch_base,
+        launch_sor_init(stream, x.st.p, tol_abs, ns, g.n4, rel, max_iter, fixed ? fixed_mode : 0, epoch_base,
                         check_assembly && world == 1 ? x.flags.p : nullptr,
                         check_assembly && world > 1 ? x.bad_all.p : nullptr, world);
         a.push_back(x.sor_args(B[s].data(), rhs[s], heat, omega, hc, world, kern));
@@ -920,7 +920,8 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
             // passes run: red 1..it+1, black 1..it (+1 when the finalize sits in the black pass)
             // (a fixed-sweep solve's last black pass carries only the decision: not counted)
             prof.loop_passes += a[0].wave == 2 ? 2LL * (st_host->iterations + 1)  // k-wavefront bodies
-                                               : 2LL * st_host->iterations + 1 + (a[0].fuse_final && !fixed ? 1 : 0);
+                                               : 2LL * st_host->iterations + (fixed && fixed_mode == 2 ? 0 : 1) +
+                                                     (a[0].fuse_final && !fixed ? 1 : 0);
         }
         const int bodies = wave ? st_host->iterations / WI + 1 : st_host->iterations + 1;
         const int U = graph_unroll();
@@ -983,7 +984,8 @@ SolveOut Domain::solve(const std::vector<Triple>& B, const std::vector<PField>& 
             for (size_t b = 0; b < body_ev.size(); ++b) {
                 float ms = 0.f;
                 const size_t base = body_ev[b];
-                if (profiling && (int)b <= it) {  // red(b+1) did real work (b+1 <= it+1)
+                // red(b+1) did real work (b+1 <= it+1; a fixed-sweep solve without diagnostics: <= it)
+                if (profiling && (int)b < it + (fixed && fixed_mode == 2 ? 0 : 1)) {
                     SSB_CUDA(cudaEventElapsedTime(&ms, ev_pool[base], ev_pool[base + 1]));
                     prof.red_ms += ms;
                     prof.red_n++;
@@ -1391,6 +1393,9 @@ SolveOut Domain::step_impl(ss_step_diag* diag, int fixed, bool rescale, const do
     std::vector<PField> rhs;
     for (const Triple& t : B) rhs.push_back(t[0]);  // rhs = guess = u^{n-1} (solver.cpp:430)
     int rr = 0;
+    // without a diag struct nobody reads a fixed-sweep solve's residual (ss_session_fixed_sweeps returns it
+    // and asks for it): the pass that would only evaluate it stays idle
+    fixed_mode = diag || want_residual ? 1 : 2;
     const SolveOut o = fixed ? solve(B, rhs, false, prm.omega, nullptr, 1.0, false, 0.0, fixed, true, &rr, true)
                              : solve(B, rhs, false, prm.omega, nullptr, prm.sor_tol, rel, prm.sor_rel_tol,
                                      prm.sor_max_iter, false, &rr, true);
@@ -1443,6 +1448,13 @@ SolveOut Domain::step_impl(ss_step_diag* diag, int fixed, bool rescale, const do
 
 // fixed-sweep mode without the rescale (ss_session_fixed_sweeps): assemble + exactly
 // n_sweeps sweeps; non-finite coefficients are reported like step()'s
-double Domain::fixed_sweeps(int n_sweeps) { return step(nullptr, n_sweeps, false).residual; }
+double Domain::fixed_sweeps(int n_sweeps) {
+    struct Want {
+        bool& w;
+        explicit Want(bool& x) : w(x) { w = true; }
+        ~Want() { w = false; }
+    } want(want_residual);
+    return step(nullptr, n_sweeps, false).residual;
+}
 
 }  // namespace ssb

@@ -216,6 +216,10 @@ struct Domain {
     int device = 0;
     bool distributed = false;  // NCCL: slabs.size() == 1 < world
     PeerLinks peers;           // NVLink halo push between ranks (SSB_P2P=1)
+    // fixed-sweep solves: 1 = the last iteration's residual is evaluated (diagnostics, ss_session_fixed_sweeps),
+    // 2 = no residual (step_fixed / step_host* without a diag struct): SorState::fixed
+    int fixed_mode = 1;
+    bool want_residual = false;  // set around ss_session_fixed_sweeps
     int comm_reserve = 0;      // CTA slots a pass's interior launch leaves free for NCCL's send/recv kernels
     cudaStream_t stream = nullptr, cap_stream = nullptr;
     cudaStream_t comm = nullptr;  // halo exchanges (overlapped with interior slices)

@@ -17,7 +17,8 @@ struct SorState {
     int n_red, n_black;
     int done, converged;
     int iterations, max_iter;
-    int fixed;
+    int fixed;      // 0: to tolerance; 1: exactly max_iter sweeps, the last iteration's residual evaluated;
+                    // 2: exactly max_iter sweeps and no residual at all (nobody asked for diagnostics)
     int nonfinite;  // assemble_step found a non-finite coefficient (solver.cpp:71-75): no solve
     unsigned int counter;
     unsigned int item_ctr[2];  // dynamic item counters of the TMA colour passes (zeroed by the other pass)

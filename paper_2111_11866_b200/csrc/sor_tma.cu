@@ -873,14 +873,16 @@ __global__ void __launch_bounds__(pass_threads(FLAT), SSB_CTAS_PER_SM) sor_pass_
     const int nl = (a.l_hi - a.l_lo) / a.l_step + 1;  // slices l_lo, l_lo + l_step, .. l_hi
     // fixed-sweep solves know their end: the black pass after the last iteration (it only
     // carries the head's decision of that iteration) updates nothing
-    const bool fixed_solve = *(volatile const int*)&st->fixed != 0;
+    const int fixed_mode = *(volatile const int*)&st->fixed;
+    const bool fixed_solve = fixed_mode != 0;
     const int max_it = *(volatile const int*)&st->max_iter;
-    const bool idle = C == 1 && fixed_solve && n > max_it;
+    // (mode 2, no diagnostics wanted: red(max_iter + 1) would only evaluate that residual -- idle too)
+    const bool idle = fixed_solve && n > max_it && (C == 1 || fixed_mode == 2);
     // fixed-sweep solves need a residual only for their last iteration (the diagnostics):
     // red(max_iter + 1) carries its red part, black(max_iter) its black part; the other
     // passes skip the residual arithmetic and write zero partials (-1.6% per sweep, config 4:
     // the power-capped clock rises with the work saved)
-    const bool need_res = !fixed_solve || (C == 0 ? n == max_it + 1 : n == max_it);
+    const bool need_res = !fixed_solve || (fixed_mode == 1 && (C == 0 ? n == max_it + 1 : n == max_it));
     const long long n_items = idle ? 0 : (long long)G.nsg * G.njg * G.nkc * nl;
     // snake order: black passes walk the items backwards, so each pass starts on
     // the rows the previous pass touched last (still in L2)

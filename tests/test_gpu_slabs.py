@@ -379,6 +379,43 @@ def test_fixed_sweep_steps_vs_oracle(gpu, oracle, n_slabs):
         assert math.isclose(x["residual"], r, rel_tol=1e-12)
 
 
+@pytest.mark.parametrize("n_slabs,kernel", [(1, "tma"), (1, "auto"), (3, "tma"), (1, "ldg")])
+def test_fixed_sweep_steps_without_diagnostics(gpu, oracle, n_slabs, kernel):
+    """step_fixed(diag=False): nobody reads the residual, so the solve runs in SorState::fixed
+    mode 2 -- no residual arithmetic and the red pass that would only evaluate the last residual
+    stays idle.  u after mixed no-diag / diag steps is the oracle's bit for bit, the diag step
+    still reports its own residual, and ss_session_fixed_sweeps (which returns the residual)
+    still evaluates it."""
+    import math
+    import workloads
+    from oracle import oracle_py as op
+    sys_path_tests = os.path.dirname(os.path.abspath(__file__))
+    if sys_path_tests not in sys.path:
+        sys.path.insert(0, sys_path_tests)
+    from test_fixed_sweeps_cpu import oracle_fixed_steps
+    # 40 x 24 rows: enough items for the TMA pass's counter hand-out on one slab
+    wl = workloads.small((40, 24, 9, 7), seed=6)
+    og = op.Grid.make(wl.dims, wl.h)
+    prm = {**wl.params, "n_steps": 3, "sor_rel_tol": 0.0}
+    u_or, res = oracle_fixed_steps(oracle, og, wl, op.seg_params(**prm), 3, 9)
+    g = gpu.Grid.make(wl.dims, wl.h)
+    with gpu.Session(g, n_slabs=n_slabs) as s:
+        s.set_kernel(kernel)
+        s.prepare(wl.image, wl.rows, gpu.seg_params(**prm), wl.u0)
+        assert s.step_fixed(9, diag=False) is None
+        assert s.step_fixed(9, diag=False) is None
+        d = s.step_fixed(9)
+        u = s.get_u()
+        r_fs = s.fixed_sweeps(4)  # assemble + 4 sweeps, returns the 4th iteration's residual
+        s.profile()
+        s.step_fixed(5, diag=False)
+        sweeps = s.profile()["sweeps"]
+    assert np.array_equal(u.view(np.uint64), u_or.view(np.uint64))
+    assert d["iterations"] == 9 and math.isclose(d["residual"], res[2], rel_tol=1e-12)
+    assert r_fs > 0.0 and math.isfinite(r_fs)
+    assert sweeps == 5
+
+
 def test_kernel_switch_within_a_session(gpu):
     """ss_session_set_kernel between solves of ONE session (the captured CUDA
     graph was keyed without the item shape, so a switch between the whole-row and the
