@@ -14,7 +14,7 @@ through its public calls on the seeded synthetic workloads of bench.py
   config1  64^4, all 20 steps
   config2  256x256x64x32, all 30 steps
   config3s 512x512x128x4 (config 3's first 4 frames as a grid), steps 1-5
-  config4  256x256x128x16 (N = 1), 5 steps of exactly 50 sweeps each: the reference
+  config4  256x256x128x16 (N = 1), 10 steps of exactly 50 sweeps each: the reference
            throws SolverError at max_iter; ref_segment_fixed recovers the reference's
            own iterate by re-running with sor_tol = the thrown residual (oracle/ref_shim.cpp)
 
@@ -56,7 +56,7 @@ PLAN = {  # config -> (workload builder, steps, fixed sweeps or None)
     "config0": (lambda: workloads.config0(), 10, None),
     "config1": (lambda: workloads.config1(), 20, None),
     "config2": (lambda: workloads.config2(), 30, None),
-    "config4": (lambda: workloads.config4(1), 5, 50),
+    "config4": (lambda: workloads.config4(1), 10, 50),
     "config3s": (lambda: workloads.config3_slab(4), 5, None),  # config 3's 512x512x128 frames
 }
 

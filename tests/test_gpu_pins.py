@@ -8,7 +8,7 @@ and min/max of u, the sha256 of the final u's bits and the 0.5-mask voxel count.
   config0  32^4            all 10 segment() steps
   config1  64^4            all 20 steps
   config2  256x256x64x32   all 30 steps
-  config4  256x256x128x16  5 steps of exactly 50 sweeps (the reference's own iterate,
+  config4  256x256x128x16  10 steps of exactly 50 sweeps (the reference's own iterate,
                            recovered past its SolverError, oracle/ref_shim.cpp)
 
 The device session recomputes them here and must match: iterations exactly, u bit
